@@ -1,0 +1,172 @@
+/*
+ * nolf.h -- C ABI of the B200-native i-NOLF render path (libnolf_b200.so).
+ *
+ * Plain C types only: host pointers for asset creation, device pointers for
+ * per-frame buffers, an opaque cudaStream_t passed as void*.  Every entry
+ * point returns 0 on success or a negative NOLF_E* status; nolf_last_error()
+ * returns a thread-local message for the last failure on the calling thread.
+ *
+ * Each entry point replaces one reference (radfarm, pure numpy) interface;
+ * the Python host mirror paper_2303_04086_b200/ binds these via ctypes and
+ * keeps the reference signatures:
+ *
+ *   nolf_asset_create   <- LightFieldAsset construction / assetio.read_asset
+ *                          (lightfield.py:217-248, assetio.py:174-255): uploads
+ *                          density atlas, PSH (Phi narrowed to u32), features,
+ *                          MLPs, diffuse atlas or hash grid, march params.
+ *   nolf_render_rays    <- lightfield.render_rays(asset, origins, dirs, counters)
+ *                          (lightfield.py:400-456)
+ *   nolf_render_rect    <- renderer.render_range(asset, RayRange, counters)
+ *                          (renderer.py:63-93), camera_dirs fused on device
+ *   nolf_render_scene   <- renderer.render_frame + farm.compose
+ *                          (renderer.py:96-107, farm.py:129-172) fused: march,
+ *                          shade and depth-composite every asset of a scene
+ *                          over a list of screen tiles of one or more cameras
+ *   nolf_compose        <- farm.compose(frames, alpha_vis) (farm.py:129-172)
+ *   nolf_counters layout = RenderCounters {fs_evals, fd_evals, hit_pixels,
+ *                          march_samples} (lightfield.py:113-126)
+ *
+ * Error mapping in the host mirror (errors.py of the reference):
+ *   NOLF_EINVAL -> DomainError, NOLF_ESTATE -> StateError,
+ *   NOLF_EDATA -> DataError, NOLF_ECUDA / NOLF_ENOMEM -> RuntimeError.
+ */
+#ifndef NOLF_H_
+#define NOLF_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define NOLF_ABI_VERSION 1
+
+#define NOLF_OK 0
+#define NOLF_EINVAL -1
+#define NOLF_ESTATE -2
+#define NOLF_EDATA -3
+#define NOLF_ECUDA -4
+#define NOLF_ENOMEM -5
+
+#define NOLF_HEAD_IDENTITY 0
+#define NOLF_HEAD_SIGMOID 1
+#define NOLF_HEAD_EXP 2
+
+/* MLP execution mode for the specular network (lightfield.py:632-637). */
+#define NOLF_MLP_FP32 0   /* CUDA-core fp32, tolerance 1e-3 vs reference */
+#define NOLF_MLP_BF16 1   /* tcgen05 bf16 x bf16 -> fp32 TMEM, tolerance 2/255 */
+
+typedef struct NolfAtlasDesc {        /* CubeAtlas, atlas.py:25-51 */
+    int32_t b, r, channels;
+    int64_t n_cubes;
+    const int32_t *index;             /* (b,b,b), -1 = empty */
+    const float *cubes;               /* (n_cubes, r+1, r+1, r+1, channels) */
+} NolfAtlasDesc;
+
+typedef struct NolfMlpDesc {          /* Mlp, neural.py:29-86 */
+    int32_t n_layers;                 /* number of weight matrices */
+    int32_t widths[5];                /* widths[0] = input width */
+    const float *w[4];                /* (out, in) row-major */
+    const float *b[4];
+    int32_t n_heads;
+    int32_t head_act[8];              /* NOLF_HEAD_* */
+    int32_t head_w[8];
+} NolfMlpDesc;
+
+typedef struct NolfAssetDesc {        /* LightFieldAsset, lightfield.py:217-248 */
+    NolfAtlasDesc density;
+    int32_t has_diffuse_atlas;
+    NolfAtlasDesc diffuse;
+    /* PshTable, encoding.py:109-140 */
+    int32_t psh_resolution;
+    int64_t psh_table_size;           /* m */
+    int64_t psh_offset_size;          /* m_phi */
+    const int64_t *psh_offsets;       /* (m_phi,) */
+    uint64_t primes_h0[3], primes_h1[3];
+    const float *psh_features;        /* (m, F) */
+    int32_t psh_features_dim;         /* F */
+    /* HashGridEncoder, encoding.py:405-459 (live diffuse path) */
+    int32_t hg_levels, hg_features;
+    int64_t hg_table_size;
+    int32_t hg_resolution[16];
+    int32_t hg_dense[16];
+    int64_t hg_rows[16];
+    const float *hg_feat[16];
+    NolfMlpDesc specular, diffuse_mlp;
+    /* MarchParams, lightfield.py:85-90 */
+    double step, t_stop, alpha_floor;
+    double proxy_min[3], proxy_max[3]; /* Aabb proxy */
+    /* ModelWiring, lightfield.py:59-67 */
+    int32_t use_hit_point, use_opacity, refine_opacity, use_tint, use_diffuse_color;
+} NolfAssetDesc;
+
+typedef struct NolfAsset *nolf_asset_t;
+
+/* One placed asset: the scene transform replaces object_to_world
+ * (renderer.py:110-113, farm.py:118-122).  w2o = inv(object_to_world) and
+ * scale = uniform_scale_of(w2o) are computed on the host exactly as the
+ * reference does (lightfield.py:408-409). */
+typedef struct NolfInstance {
+    nolf_asset_t asset;
+    double w2o[16];
+    double scale;
+} NolfInstance;
+
+typedef struct NolfCamera {            /* Camera, core.py:90-126 */
+    double pose[16];                   /* camera-to-world, row-major */
+    double fx, fy, cx, cy;
+    int32_t width, height;
+} NolfCamera;
+
+typedef struct NolfTile {              /* RayRange rect of one camera */
+    int32_t cam, x0, y0, x1, y1;
+} NolfTile;
+
+/* Scene output.  Pixels are written in TILE-PACKED order: tile t (in the
+ * order given) owns pixels [t*tile_stride, t*tile_stride + w_t*h_t), row-major
+ * inside the tile.  Any pointer may be NULL to skip that output. */
+typedef struct NolfSceneOut {
+    float *rgba;                       /* (.., 4) f32, farm.compose Frame.rgba */
+    float *depth;                      /* f32, inf = miss */
+    uint8_t *rgba8;                    /* protocol.encode_frame RAW rgba8 */
+    uint16_t *depth16;                 /* protocol.encode_frame RAW depth u16 */
+    int64_t tile_stride;               /* pixels per tile slot (>= max w*h) */
+    double depth_far;                  /* encode_frame far plane */
+} NolfSceneOut;
+
+int nolf_abi_version(void);
+const char *nolf_last_error(void);
+
+int nolf_asset_create(const NolfAssetDesc *desc, int device, nolf_asset_t *out);
+int nolf_asset_destroy(nolf_asset_t asset);
+int nolf_asset_set_mlp_mode(nolf_asset_t asset, int mode);
+int64_t nolf_asset_device_bytes(nolf_asset_t asset);
+
+/* Workspace bytes needed for up to n_rays rays x n_inst placed assets. */
+size_t nolf_workspace_bytes(int32_t n_inst, int64_t n_rays);
+
+/* counters: device uint64[4] accumulated (not reset). */
+int nolf_render_rays(const NolfInstance *inst, const double *origins, int32_t origin_stride,
+                     const double *dirs, int64_t n, float *rgba, float *depth,
+                     unsigned long long *counters, void *workspace, size_t ws_bytes,
+                     void *stream);
+
+int nolf_render_rect(const NolfInstance *inst, const NolfCamera *cam, int32_t x0, int32_t y0,
+                     int32_t x1, int32_t y1, float *rgba, float *depth,
+                     unsigned long long *counters, void *workspace, size_t ws_bytes,
+                     void *stream);
+
+int nolf_render_scene(const NolfInstance *inst, int32_t n_inst, const NolfCamera *cams,
+                      int32_t n_cams, const NolfTile *tiles, int32_t n_tiles,
+                      const NolfSceneOut *out, double alpha_vis, unsigned long long *counters,
+                      void *workspace, size_t ws_bytes, void *stream);
+
+/* frames: rgba (K, P, 4) f32, depth (K, P) f32, all device pointers. */
+int nolf_compose(int32_t K, int64_t P, const float *rgba, const float *depth, double alpha_vis,
+                 float *out_rgba, float *out_depth, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NOLF_H_ */

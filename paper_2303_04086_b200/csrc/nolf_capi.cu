@@ -1,0 +1,552 @@
+// nolf_capi.cu -- C ABI (include/nolf.h): asset upload, workspace layout and
+// the launch sequence of the i-NOLF hot path on sm_100a.
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/nolf.h"
+#include "nolf_kernels.cuh"
+
+using namespace nolf;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char *fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define CUDA_TRY(x)                                                                     \
+  do {                                                                                  \
+    cudaError_t e_ = (x);                                                               \
+    if (e_ != cudaSuccess) return fail(NOLF_ECUDA, "%s: %s", #x, cudaGetErrorString(e_)); \
+  } while (0)
+
+constexpr int kMaxInst = 64;
+constexpr int kMaxCams = 32;
+
+}  // namespace
+
+struct NolfAsset {
+  int device = 0;
+  DevAsset host{};             // host copy with device pointers
+  DevAsset *dev = nullptr;     // device copy
+  std::vector<void *> allocs;
+  int64_t bytes = 0;
+
+  template <class T>
+  int upload(const T *src, size_t count, T **dst) {
+    *dst = nullptr;
+    if (count == 0) return 0;
+    void *p = nullptr;
+    cudaError_t e = cudaMalloc(&p, count * sizeof(T));
+    if (e != cudaSuccess) return fail(NOLF_ENOMEM, "cudaMalloc(%zu): %s", count * sizeof(T), cudaGetErrorString(e));
+    allocs.push_back(p);
+    bytes += (int64_t)(count * sizeof(T));
+    e = cudaMemcpy(p, src, count * sizeof(T), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return fail(NOLF_ECUDA, "cudaMemcpy: %s", cudaGetErrorString(e));
+    *dst = static_cast<T *>(p);
+    return 0;
+  }
+  ~NolfAsset() {
+    for (void *p : allocs) cudaFree(p);
+    if (dev) cudaFree(dev);
+  }
+};
+
+namespace {
+
+int upload_atlas(NolfAsset *A, const NolfAtlasDesc &d, int channels, DevAtlas *out, const char *what) {
+  if (d.b < 1 || d.r < 1 || d.channels != channels || !d.index)
+    return fail(NOLF_EINVAL, "%s atlas: bad shape (b=%d r=%d C=%d)", what, d.b, d.r, d.channels);
+  const int b = d.b, s = d.r + 1;
+  const int64_t ncell = (int64_t)b * b * b;
+  for (int64_t i = 0; i < ncell; ++i)
+    if (d.index[i] < -1 || d.index[i] >= d.n_cubes)
+      return fail(NOLF_EINVAL, "%s atlas: index entries must reference valid cubes", what);
+  out->b = b;
+  out->r = d.r;
+  out->C = channels;
+  out->s = s;
+  out->mb = (b + kMacro - 1) / kMacro;
+  std::vector<uint8_t> macro((size_t)out->mb * out->mb * out->mb, 0);
+  for (int x = 0; x < b; ++x)
+    for (int y = 0; y < b; ++y)
+      for (int z = 0; z < b; ++z)
+        if (d.index[((int64_t)x * b + y) * b + z] != -1)
+          macro[((size_t)(x / kMacro) * out->mb + y / kMacro) * out->mb + z / kMacro] = 1;
+  int32_t *idx;
+  uint8_t *mac;
+  float *cubes;
+  int rc;
+  if ((rc = A->upload(d.index, (size_t)ncell, &idx))) return rc;
+  if ((rc = A->upload(macro.data(), macro.size(), &mac))) return rc;
+  const size_t nc = (size_t)d.n_cubes * s * s * s * channels;
+  if (nc == 0) {               // keep a valid pointer for empty atlases
+    float z4[4] = {0, 0, 0, 0};
+    if ((rc = A->upload(z4, 4, &cubes))) return rc;
+  } else if ((rc = A->upload(d.cubes, nc, &cubes))) {
+    return rc;
+  }
+  out->index = idx;
+  out->macro = mac;
+  out->cubes = cubes;
+  return 0;
+}
+
+int pack_mlp(NolfAsset *A, const NolfMlpDesc &m, DevMlp *out, const char *what) {
+  if (m.n_layers != 2 && m.n_layers != 3)
+    return fail(NOLF_EINVAL, "%s MLP: %d layers unsupported (need 2 or 3)", what, m.n_layers);
+  if (m.widths[0] < 1 || m.widths[0] > kInp)
+    return fail(NOLF_EINVAL, "%s MLP: input width %d > %d", what, m.widths[0], kInp);
+  for (int l = 1; l < m.n_layers; ++l)
+    if (m.widths[l] != kHid) return fail(NOLF_EINVAL, "%s MLP: hidden width %d != %d", what, m.widths[l], kHid);
+  if (m.widths[m.n_layers] != 4) return fail(NOLF_EINVAL, "%s MLP: output width must be 4", what);
+  std::vector<float> P(MlpOff::total, 0.f);
+  const int in = m.widths[0];
+  for (int o = 0; o < kHid; ++o) {
+    for (int i = 0; i < in; ++i) P[MlpOff::w0t + i * kHid + o] = m.w[0][o * in + i];
+    P[MlpOff::b0 + o] = m.b[0][o];
+  }
+  if (m.n_layers == 3) {
+    for (int o = 0; o < kHid; ++o) {
+      for (int i = 0; i < kHid; ++i) P[MlpOff::w1 + o * kHid + i] = m.w[1][o * kHid + i];
+      P[MlpOff::b1 + o] = m.b[1][o];
+    }
+  }
+  const int L = m.n_layers - 1;
+  for (int j = 0; j < 4; ++j) {
+    for (int i = 0; i < kHid; ++i) P[MlpOff::wl + j * kHid + i] = m.w[L][j * kHid + i];
+    P[MlpOff::bl + j] = m.b[L][j];
+  }
+  int j = 0;
+  for (int h = 0; h < m.n_heads; ++h)
+    for (int k = 0; k < m.head_w[h]; ++k, ++j) {
+      if (j >= 4) return fail(NOLF_EINVAL, "%s MLP: head widths exceed output width", what);
+      out->act[j] = m.head_act[h];
+    }
+  if (j != 4) return fail(NOLF_EINVAL, "%s MLP: head widths must sum to the output width", what);
+  out->n_layers = m.n_layers;
+  out->in = in;
+  float *p;
+  int rc = A->upload(P.data(), P.size(), &p);
+  out->params = p;
+  return rc;
+}
+
+int g_num_sms = 0;
+
+int num_sms() {
+  if (!g_num_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_num_sms <= 0) g_num_sms = 148;
+  }
+  return g_num_sms;
+}
+
+constexpr size_t kShadeSmem = (size_t)(2 * MlpOff::total + kInp * kShadeThreads) * sizeof(float);
+
+int ensure_attrs() {
+  static bool done = false;
+  if (!done) {
+    CUDA_TRY(cudaFuncSetAttribute(k_shade, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kShadeSmem));
+    done = true;
+  }
+  return 0;
+}
+
+size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+struct Workspace {
+  unsigned int *counts;
+  HitRec *queue;
+  long long cap;
+  uint8_t *nhit;
+  float *lrgba, *ldepth;
+};
+
+size_t ws_layout(int n_inst, int64_t n_rays, char *base, Workspace *w) {
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off = align_up(off + bytes, 256);
+    return base ? base + o : nullptr;
+  };
+  const size_t n = (size_t)(n_rays > 0 ? n_rays : 1);
+  char *counts = take(sizeof(unsigned) * (size_t)(n_inst > 0 ? n_inst : 1));
+  char *queue = take(sizeof(HitRec) * n * (size_t)n_inst);
+  char *nhit = take(n);
+  char *lrgba = take(sizeof(float) * 4 * n * (size_t)n_inst);
+  char *ldepth = take(sizeof(float) * n * (size_t)n_inst);
+  if (w) {
+    w->counts = reinterpret_cast<unsigned *>(counts);
+    w->queue = reinterpret_cast<HitRec *>(queue);
+    w->cap = (long long)n;
+    w->nhit = reinterpret_cast<uint8_t *>(nhit);
+    w->lrgba = reinterpret_cast<float *>(lrgba);
+    w->ldepth = reinterpret_cast<float *>(ldepth);
+  }
+  return off;
+}
+
+int fill_inst(const NolfInstance *in, DevInst *out) {
+  if (!in || !in->asset) return fail(NOLF_EINVAL, "null asset instance");
+  if (!(in->scale > 0.0)) return fail(NOLF_EINVAL, "instance scale must be positive");
+  out->a = in->asset->dev;
+  for (int r = 0; r < 3; ++r)
+    for (int c = 0; c < 4; ++c) out->w2o[r * 4 + c] = in->w2o[r * 4 + c];
+  out->scale = in->scale;
+  return 0;
+}
+
+int run_shade(const DevInst *inst, int n_inst, const Workspace &w, int mode, float *rgba, float *depth,
+              long long layer_stride, unsigned long long *counters, cudaStream_t st);
+
+}  // namespace
+
+// Per-launch instance / camera tables live in a device-side parameter block.
+namespace {
+struct ParamBlock {
+  DevInst inst[kMaxInst];
+  CamParams cams[kMaxCams];
+  TileParams rect;
+};
+}  // namespace
+
+extern "C" {
+
+int nolf_abi_version(void) { return NOLF_ABI_VERSION; }
+const char *nolf_last_error(void) { return g_err.c_str(); }
+
+int nolf_asset_create(const NolfAssetDesc *d, int device, nolf_asset_t *out) {
+  if (!d || !out) return fail(NOLF_EINVAL, "null argument");
+  *out = nullptr;
+  CUDA_TRY(cudaSetDevice(device));
+  NolfAsset *A = new NolfAsset();
+  A->device = device;
+  DevAsset &H = A->host;
+  int rc = 0;
+  auto bail = [&](int code) { delete A; return code; };
+  if ((rc = upload_atlas(A, d->density, 1, &H.den, "density"))) return bail(rc);
+  H.has_dif = d->has_diffuse_atlas ? 1 : 0;
+  if (H.has_dif && (rc = upload_atlas(A, d->diffuse, 4, &H.dif, "diffuse"))) return bail(rc);
+  // PSH
+  if (d->psh_resolution < 1 || d->psh_table_size < 1 || d->psh_offset_size < 1 || !d->psh_offsets ||
+      !d->psh_features)
+    return bail(fail(NOLF_EINVAL, "psh: missing table"));
+  if (d->psh_table_size >= (1ll << 30) || d->psh_offset_size >= (1ll << 30))
+    return bail(fail(NOLF_EINVAL, "psh: table too large for u32 slot arithmetic"));
+  if (d->psh_features_dim < 1 || d->psh_features_dim > 4)
+    return bail(fail(NOLF_EINVAL, "psh: feature dim %d unsupported (1..4)", d->psh_features_dim));
+  H.N = d->psh_resolution;
+  H.m = (uint32_t)d->psh_table_size;
+  H.mphi = (uint32_t)d->psh_offset_size;
+  H.F = d->psh_features_dim;
+  {
+    std::vector<uint32_t> phi((size_t)d->psh_offset_size);
+    for (int64_t i = 0; i < d->psh_offset_size; ++i) {
+      int64_t v = d->psh_offsets[i];
+      if (v < 0 || v >= d->psh_table_size) return bail(fail(NOLF_EINVAL, "psh: offset out of range"));
+      phi[(size_t)i] = (uint32_t)v;
+    }
+    const int s = H.N + 1;
+    std::vector<uint32_t> tab((size_t)6 * s);
+    for (int a = 0; a < 3; ++a)
+      for (int x = 0; x < s; ++x) {
+        tab[(size_t)a * s + x] = (uint32_t)(((uint64_t)x * d->primes_h0[a]) % (uint64_t)H.m);
+        tab[(size_t)(3 + a) * s + x] = (uint32_t)(((uint64_t)x * d->primes_h1[a]) % (uint64_t)H.mphi);
+      }
+    uint32_t *pp, *tp;
+    float *fp;
+    if ((rc = A->upload(phi.data(), phi.size(), &pp))) return bail(rc);
+    if ((rc = A->upload(tab.data(), tab.size(), &tp))) return bail(rc);
+    if ((rc = A->upload(d->psh_features, (size_t)d->psh_table_size * H.F, &fp))) return bail(rc);
+    H.phi = pp;
+    H.tab = tp;
+    H.feat = fp;
+  }
+  // hash grid (live diffuse)
+  H.hg_levels = d->hg_levels;
+  H.hg_F = d->hg_features;
+  H.hg_table = (unsigned long long)d->hg_table_size;
+  if (H.hg_levels < 0 || H.hg_levels > kMaxLevels) return bail(fail(NOLF_EINVAL, "hash grid: bad level count"));
+  for (int l = 0; l < H.hg_levels; ++l) {
+    H.hg_res[l] = d->hg_resolution[l];
+    H.hg_dense[l] = d->hg_dense[l];
+    float *fp;
+    if ((rc = A->upload(d->hg_feat[l], (size_t)d->hg_rows[l] * H.hg_F, &fp))) return bail(rc);
+    H.hg_feat[l] = fp;
+  }
+  if ((rc = pack_mlp(A, d->specular, &H.fs, "specular"))) return bail(rc);
+  if (d->diffuse_mlp.n_layers) {
+    if ((rc = pack_mlp(A, d->diffuse_mlp, &H.fd, "diffuse"))) return bail(rc);
+  } else {
+    H.fd.params = nullptr;
+  }
+  const int expect_in = H.F + 16 + (d->refine_opacity ? 1 : 0);
+  if (H.fs.in != expect_in)
+    return bail(fail(NOLF_EINVAL, "specular MLP input %d != F+16+refine %d", H.fs.in, expect_in));
+  if (!H.has_dif && d->use_diffuse_color) {
+    if (!H.fd.params) return bail(fail(NOLF_EINVAL, "no diffuse atlas and no diffuse MLP"));
+    if (H.fd.in != H.hg_levels * H.hg_F || H.hg_F > 4)
+      return bail(fail(NOLF_EINVAL, "diffuse MLP input %d != levels*F %d", H.fd.in, H.hg_levels * H.hg_F));
+  }
+  H.step = d->step;
+  H.t_stop = d->t_stop;
+  H.alpha_floor = d->alpha_floor;
+  if (!(H.step > 0.0)) return bail(fail(NOLF_EINVAL, "march step must be positive"));
+  for (int k = 0; k < 3; ++k) {
+    H.pmin[k] = d->proxy_min[k];
+    H.pmax[k] = d->proxy_max[k];
+  }
+  H.use_hit_point = d->use_hit_point;
+  H.use_opacity = d->use_opacity;
+  H.refine_opacity = d->refine_opacity;
+  H.use_tint = d->use_tint;
+  H.use_diffuse_color = d->use_diffuse_color;
+  H.mlp_mode = NOLF_MLP_FP32;
+  cudaError_t e = cudaMalloc(&A->dev, sizeof(DevAsset));
+  if (e != cudaSuccess) return bail(fail(NOLF_ENOMEM, "cudaMalloc asset: %s", cudaGetErrorString(e)));
+  e = cudaMemcpy(A->dev, &H, sizeof(DevAsset), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) return bail(fail(NOLF_ECUDA, "cudaMemcpy asset: %s", cudaGetErrorString(e)));
+  A->bytes += sizeof(DevAsset);
+  *out = A;
+  return 0;
+}
+
+int nolf_asset_destroy(nolf_asset_t a) {
+  if (!a) return 0;
+  cudaSetDevice(a->device);
+  delete a;
+  return 0;
+}
+
+int nolf_asset_set_mlp_mode(nolf_asset_t a, int mode) {
+  if (!a) return fail(NOLF_EINVAL, "null asset");
+  if (mode != NOLF_MLP_FP32) return fail(NOLF_EINVAL, "MLP mode %d not available in this build", mode);
+  a->host.mlp_mode = mode;
+  CUDA_TRY(cudaMemcpy(a->dev, &a->host, sizeof(DevAsset), cudaMemcpyHostToDevice));
+  return 0;
+}
+
+int64_t nolf_asset_device_bytes(nolf_asset_t a) { return a ? a->bytes : 0; }
+
+size_t nolf_workspace_bytes(int32_t n_inst, int64_t n_rays) { return ws_layout(n_inst, n_rays, nullptr, nullptr); }
+
+}  // extern "C"
+
+namespace {
+
+int run_shade(const DevInst *inst, int n_inst, const Workspace &w, int mode, float *rgba, float *depth,
+              long long layer_stride, unsigned long long *counters, cudaStream_t st) {
+  ShadeArgs sa{};
+  sa.inst = inst;
+  sa.n_inst = n_inst;
+  sa.queue = w.queue;
+  sa.cap = w.cap;
+  sa.counts = w.counts;
+  sa.mode = mode;
+  sa.rgba = rgba;
+  sa.depth = depth;
+  sa.layer_stride = layer_stride;
+  sa.counters = counters;
+  const int blocks = num_sms() * 3;
+  k_shade<<<blocks, kShadeThreads, kShadeSmem, st>>>(sa);
+  CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+// Device-resident copies of the per-launch instance / camera tables.  They
+// are written with cudaMemcpyAsync from pinned staging on the caller's
+// stream, so consecutive launches on one stream never race.
+struct ParamRing {
+  ParamBlock *host = nullptr;
+  ParamBlock *dev = nullptr;
+  int slots = 0, next = 0;
+  cudaEvent_t *done = nullptr;
+};
+thread_local ParamRing g_ring;
+
+int ring_acquire(ParamBlock **h, ParamBlock **d, int *slot) {
+  ParamRing &R = g_ring;
+  if (!R.host) {
+    R.slots = 8;
+    CUDA_TRY(cudaMallocHost(&R.host, sizeof(ParamBlock) * R.slots));
+    CUDA_TRY(cudaMalloc(&R.dev, sizeof(ParamBlock) * R.slots));
+    R.done = new cudaEvent_t[R.slots];
+    for (int i = 0; i < R.slots; ++i) {
+      CUDA_TRY(cudaEventCreateWithFlags(&R.done[i], cudaEventDisableTiming));
+      CUDA_TRY(cudaEventRecord(R.done[i], 0));
+    }
+  }
+  int s = R.next;
+  R.next = (R.next + 1) % R.slots;
+  CUDA_TRY(cudaEventSynchronize(R.done[s]));   // host staging slot free again
+  *h = R.host + s;
+  *d = R.dev + s;
+  *slot = s;
+  return 0;
+}
+
+int ring_release(int slot, cudaStream_t st) {
+  CUDA_TRY(cudaEventRecord(g_ring.done[slot], st));
+  return 0;
+}
+
+int launch_march_shade(int mode, const NolfInstance *ins, int n_inst, const NolfCamera *cams, int n_cams,
+                       const NolfTile *tiles_dev, int n_tiles, TileParams rect, long long n_rays,
+                       long long tile_stride, const double *origins, int origin_stride, const double *dirs,
+                       float *rgba, float *depth, const NolfSceneOut *sout, double alpha_vis,
+                       unsigned long long *counters, void *workspace, size_t ws_bytes, cudaStream_t st) {
+  if (n_inst < 1 || n_inst > kMaxInst) return fail(NOLF_EINVAL, "instance count %d outside 1..%d", n_inst, kMaxInst);
+  if (n_cams > kMaxCams) return fail(NOLF_EINVAL, "camera count %d > %d", n_cams, kMaxCams);
+  if (!counters) return fail(NOLF_EINVAL, "counters pointer required");
+  if (mode == kModeScene && n_inst > 255) return fail(NOLF_EINVAL, "too many layers");
+  const size_t need = ws_layout(n_inst, n_rays, nullptr, nullptr);
+  if (!workspace || ws_bytes < need) return fail(NOLF_EINVAL, "workspace too small: %zu < %zu", ws_bytes, need);
+  int rc;
+  if ((rc = ensure_attrs())) return rc;
+  Workspace w;
+  ws_layout(n_inst, n_rays, static_cast<char *>(workspace), &w);
+  ParamBlock *hp, *dp;
+  int slot;
+  if ((rc = ring_acquire(&hp, &dp, &slot))) return rc;
+  for (int k = 0; k < n_inst; ++k)
+    if ((rc = fill_inst(ins + k, hp->inst + k))) return rc;
+  for (int c = 0; c < n_cams; ++c) {
+    const NolfCamera &C = cams[c];
+    for (int q = 0; q < 16; ++q) hp->cams[c].pose[q] = C.pose[q];
+    hp->cams[c].fx = C.fx;
+    hp->cams[c].fy = C.fy;
+    hp->cams[c].cx = C.cx;
+    hp->cams[c].cy = C.cy;
+  }
+  hp->rect = rect;
+  CUDA_TRY(cudaMemcpyAsync(dp, hp, sizeof(ParamBlock), cudaMemcpyHostToDevice, st));
+  if ((rc = ring_release(slot, st))) return rc;
+  if (n_rays == 0) return 0;
+  CUDA_TRY(cudaMemsetAsync(w.counts, 0, sizeof(unsigned) * n_inst, st));
+
+  MarchArgs ma{};
+  ma.inst = dp->inst;
+  ma.n_inst = n_inst;
+  ma.origins = origins;
+  ma.origin_stride = origin_stride;
+  ma.dirs = dirs;
+  ma.n_rays = n_rays;
+  ma.cams = dp->cams;
+  ma.tiles = mode == kModeScene ? reinterpret_cast<const TileParams *>(tiles_dev) : &dp->rect;
+  ma.tile_stride = tile_stride;
+  ma.queue = w.queue;
+  ma.cap = w.cap;
+  ma.counts = w.counts;
+  ma.rgba = rgba;
+  ma.depth = depth;
+  ma.nhit = w.nhit;
+  ma.counters = counters;
+  const unsigned grid = (unsigned)((n_rays + 127) / 128);
+  if (mode == kModeRays) k_march<kModeRays><<<grid, 128, 0, st>>>(ma);
+  else if (mode == kModeRect) k_march<kModeRect><<<grid, 128, 0, st>>>(ma);
+  else k_march<kModeScene><<<grid, 128, 0, st>>>(ma);
+  CUDA_TRY(cudaGetLastError());
+  if (mode == kModeScene) {
+    if ((rc = run_shade(dp->inst, n_inst, w, mode, w.lrgba, w.ldepth, (long long)w.cap, counters, st))) return rc;
+    ComposeArgs ca{};
+    ca.n_pix = n_rays;
+    ca.nhit = w.nhit;
+    ca.K = 0;
+    ca.rgba = w.lrgba;
+    ca.depth = w.ldepth;
+    ca.layer_stride = w.cap;
+    ca.tiles = reinterpret_cast<const TileParams *>(tiles_dev);
+    ca.tile_stride = tile_stride;
+    ca.alpha_vis = (float)alpha_vis;
+    ca.out_rgba = sout->rgba;
+    ca.out_depth = sout->depth;
+    ca.out_rgba8 = sout->rgba8;
+    ca.out_depth16 = sout->depth16;
+    ca.depth_far = (float)sout->depth_far;
+    k_compose<<<(unsigned)((n_rays + 255) / 256), 256, 0, st>>>(ca);
+    CUDA_TRY(cudaGetLastError());
+  } else {
+    if ((rc = run_shade(dp->inst, n_inst, w, mode, rgba, depth, 0, counters, st))) return rc;
+  }
+  return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+int nolf_render_rays(const NolfInstance *inst, const double *origins, int32_t origin_stride, const double *dirs,
+                     int64_t n, float *rgba, float *depth, unsigned long long *counters, void *workspace,
+                     size_t ws_bytes, void *stream) {
+  if (n < 0) return fail(NOLF_EINVAL, "negative ray count");
+  if (n > 0 && (!origins || !dirs || !rgba || !depth)) return fail(NOLF_EINVAL, "null buffer");
+  if (n >= (1ll << 32)) return fail(NOLF_EINVAL, "too many rays for one launch");
+  TileParams rect{0, 0, 0, 0, 0};
+  return launch_march_shade(kModeRays, inst, 1, nullptr, 0, nullptr, 0, rect, n, 0, origins,
+                            origin_stride ? 1 : 0, dirs, rgba, depth, nullptr, 0.5, counters, workspace,
+                            ws_bytes, static_cast<cudaStream_t>(stream));
+}
+
+int nolf_render_rect(const NolfInstance *inst, const NolfCamera *cam, int32_t x0, int32_t y0, int32_t x1,
+                     int32_t y1, float *rgba, float *depth, unsigned long long *counters, void *workspace,
+                     size_t ws_bytes, void *stream) {
+  if (!cam) return fail(NOLF_EINVAL, "null camera");
+  if (!(0 <= x0 && x0 < x1 && x1 <= cam->width)) return fail(NOLF_EINVAL, "ray range x bounds outside frame");
+  if (!(0 <= y0 && y0 < y1 && y1 <= cam->height)) return fail(NOLF_EINVAL, "ray range y bounds outside frame");
+  TileParams rect{0, x0, y0, x1, y1};
+  const long long n = (long long)(x1 - x0) * (y1 - y0);
+  return launch_march_shade(kModeRect, inst, 1, cam, 1, nullptr, 0, rect, n, 0, nullptr, 0, nullptr, rgba,
+                            depth, nullptr, 0.5, counters, workspace, ws_bytes, static_cast<cudaStream_t>(stream));
+}
+
+int nolf_render_scene(const NolfInstance *inst, int32_t n_inst, const NolfCamera *cams, int32_t n_cams,
+                      const NolfTile *tiles, int32_t n_tiles, const NolfSceneOut *out, double alpha_vis,
+                      unsigned long long *counters, void *workspace, size_t ws_bytes, void *stream) {
+  if (!out || !cams || n_cams < 1) return fail(NOLF_EINVAL, "null scene argument");
+  if (n_tiles < 0 || (n_tiles > 0 && !tiles)) return fail(NOLF_EINVAL, "bad tile list");
+  if (out->tile_stride < 1) return fail(NOLF_EINVAL, "tile_stride must be positive");
+  const long long n = (long long)n_tiles * out->tile_stride;
+  if (n >= (1ll << 32)) return fail(NOLF_EINVAL, "too many pixels for one launch");
+  TileParams rect{0, 0, 0, 0, 0};
+  return launch_march_shade(kModeScene, inst, n_inst, cams, n_cams, tiles, n_tiles, rect, n, out->tile_stride,
+                            nullptr, 0, nullptr, nullptr, nullptr, out, alpha_vis, counters, workspace, ws_bytes,
+                            static_cast<cudaStream_t>(stream));
+}
+
+int nolf_compose(int32_t K, int64_t P, const float *rgba, const float *depth, double alpha_vis, float *out_rgba,
+                 float *out_depth, void *stream) {
+  if (K < 1) return fail(NOLF_EINVAL, "compose needs at least one frame");
+  if (K > kMaxLayers) return fail(NOLF_EINVAL, "compose: %d frames > %d", K, kMaxLayers);
+  if (P == 0) return 0;
+  if (!rgba || !depth || !out_rgba || !out_depth) return fail(NOLF_EINVAL, "null buffer");
+  ComposeArgs ca{};
+  ca.n_pix = P;
+  ca.nhit = nullptr;
+  ca.K = K;
+  ca.rgba = rgba;
+  ca.depth = depth;
+  ca.layer_stride = P;
+  ca.tiles = nullptr;
+  ca.alpha_vis = (float)alpha_vis;
+  ca.out_rgba = out_rgba;
+  ca.out_depth = out_depth;
+  k_compose<<<(unsigned)((P + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(ca);
+  CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,570 @@
+// nolf_kernels.cuh -- the i-NOLF hot path as three sm_100a kernels:
+//
+//   k_march    per ray (x placed asset): proxy slab test + fixed-step
+//              transmittance march with EXACT empty-space skipping; emits one
+//              HitRec per hit into a per-instance queue (lightfield.py:400-445,
+//              129-186).
+//   k_shade    per hit record: PSH slots + trilinear features, SH(d_obj),
+//              fused fp32 MLP (weights staged in shared memory), diffuse atlas
+//              or live hash-grid diffuse, combine (lightfield.py:267-336,
+//              446-455).
+//   k_compose  per pixel: stable depth sort of its hit layers + front-to-back
+//              over in f64 + encode_frame RAW quantisation (farm.py:129-172,
+//              protocol.py:256-266).
+#pragma once
+#include "nolf_device.cuh"
+
+namespace nolf {
+
+enum RayMode { kModeRays = 0, kModeRect = 1, kModeScene = 2 };
+
+struct CamParams {             // NolfCamera with pose rows
+  double pose[16];
+  double fx, fy, cx, cy;
+};
+
+struct TileParams { int cam, x0, y0, x1, y1; };
+
+struct MarchArgs {
+  const DevInst *inst;         // n_inst instances (device)
+  int n_inst;
+  // ray source
+  const double *origins;       // kModeRays
+  int origin_stride;           // 0 => shared origin
+  const double *dirs;          // kModeRays
+  long long n_rays;            // total ray slots
+  const CamParams *cams;       // kModeRect / kModeScene (device)
+  const TileParams *tiles;     // kModeScene (device) ; kModeRect: tiles[0] is the rect
+  long long tile_stride;       // kModeScene: pixel slots per tile
+  // outputs
+  HitRec *queue;               // n_inst * cap records
+  long long cap;               // per-instance capacity
+  unsigned int *counts;        // n_inst
+  float *rgba;                 // kModeRays/kModeRect: miss init (n, 4)
+  float *depth;
+  uint8_t *nhit;               // kModeScene: per pixel layer count
+  unsigned long long *counters;
+};
+
+// Exit parameter of an axis-aligned box [lo, hi] (object coords) along the
+// ray, with faces on the unit-cube boundary pushed to infinity because march
+// positions are clipped to [0,1] (lightfield.py:166).
+__device__ __forceinline__ double box_exit(const double o[3], const double d[3], const double lo[3],
+                                           const double hi[3]) {
+  const double INF = __longlong_as_double(0x7ff0000000000000ll);
+  double t = INF;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    if (d[k] > 0.0 && hi[k] < 1.0) t = fmin(t, (hi[k] - o[k]) / d[k]);
+    else if (d[k] < 0.0 && lo[k] > 0.0) t = fmin(t, (lo[k] - o[k]) / d[k]);
+  }
+  return t;
+}
+
+// Sample i's clipped position and index cell, exactly as march_rays computes
+// them (t_mid = t_near + (i+0.5)*step ; pos = clip(o + t_mid*d, 0, 1)).
+__device__ __forceinline__ double sample_cell(const double o[3], const double d[3], double t_near, double delta,
+                                              long long i, int b, double pos[3], int cell[3]) {
+  double t_mid = __dadd_rn(t_near, __dmul_rn((double)i + 0.5, delta));
+  const double bd = (double)b;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    pos[k] = clamp01(__dadd_rn(o[k], __dmul_rn(t_mid, d[k])));
+    cell[k] = clampi((int)floor(__dmul_rn(pos[k], bd)), 0, b - 1);
+  }
+  return t_mid;
+}
+
+// march_rays (lightfield.py:129-186) for one ray.
+//
+// Exact empty-space skipping: an empty sample has sigma = 0, so absorb = 1,
+// w = 0 (never "better", best_w starts at 0), alpha_c and T are unchanged and
+// it is not counted; skipping it is bitwise neutral.  From an empty sample
+// i in an empty box B (a macro cell, else an index cell) we jump to a guess j
+// (the last sample before B's analytic exit) and VERIFY sample j's cell is in
+// B.  Each computed cell coordinate is a monotone function of i (fl() is
+// monotone, t_mid is monotone in i, clip/floor are monotone), so cells of all
+// samples between i and j lie between cell(i) and cell(j), i.e. inside B:
+// every skipped sample is provably empty, whatever the rounding.
+struct MarchOut {
+  double alpha_c, t_hit;
+  long long samples;
+  bool hit;
+};
+
+__device__ __forceinline__ MarchOut march_ray(const DevAsset &A, const double o[3], const double d[3],
+                                              double t_near, double t_far) {
+  MarchOut r;
+  r.alpha_c = 0.0;
+  r.t_hit = __longlong_as_double(0x7ff0000000000000ll);
+  r.samples = 0;
+  r.hit = false;
+  if (!(t_near < t_far)) return r;
+  const DevAtlas &at = A.den;
+  const double delta = A.step;
+  const int b = at.b, mb = at.mb;
+  const double inv_b = 1.0 / (double)b;
+  double best_w = 0.0, trans = 1.0, alpha_c = 0.0, t_hit = r.t_hit;
+  long long samples = 0;
+  long long i = 0;
+  for (;;) {
+    double pos[3];
+    int cell[3];
+    const double t_mid = sample_cell(o, d, t_near, delta, i, b, pos, cell);
+    if (!(t_mid < t_far)) break;
+    int lo_c[3], hi_c[3];
+    bool empty = false;
+    const int m0 = cell[0] / kMacro, m1 = cell[1] / kMacro, m2 = cell[2] / kMacro;
+    int cid = -1;
+    if (!__ldg(at.macro + (m0 * mb + m1) * mb + m2)) {
+      empty = true;
+      lo_c[0] = m0 * kMacro; lo_c[1] = m1 * kMacro; lo_c[2] = m2 * kMacro;
+#pragma unroll
+      for (int k = 0; k < 3; ++k) hi_c[k] = min(lo_c[k] + kMacro, b) - 1;
+    } else {
+      cid = __ldg(at.index + (cell[0] * b + cell[1]) * b + cell[2]);
+      if (cid < 0) {
+        empty = true;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) lo_c[k] = hi_c[k] = cell[k];
+      }
+    }
+    if (empty) {
+      double lo[3], hi[3];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        lo[k] = lo_c[k] * inv_b;
+        hi[k] = (hi_c[k] + 1) * inv_b;
+      }
+      double te = box_exit(o, d, lo, hi);
+      double tl = fmin(te, t_far);
+      double jf = floor((tl - t_near) / delta - 0.5);
+      long long j = jf > 9.0e15 ? (long long)9.0e15 : (long long)jf;
+      long long next = i + 1;
+      for (int attempt = 0; attempt < 2 && j > i; ++attempt, --j) {
+        double pj[3];
+        int cj[3];
+        double tj = sample_cell(o, d, t_near, delta, j, b, pj, cj);
+        bool inside = tj < t_far;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) inside = inside && cj[k] >= lo_c[k] && cj[k] <= hi_c[k];
+        if (inside) { next = j + 1; break; }
+      }
+      i = next;
+      continue;
+    }
+    float s;
+    atlas_trilinear<1>(at, cid, pos, &s);
+    const double sigma = (double)s;
+    ++samples;
+    const double absorb = exp(__dmul_rn(-sigma, delta));
+    const double w = __dmul_rn(trans, __dsub_rn(1.0, absorb));
+    if (w > best_w) { best_w = w; t_hit = t_mid; }
+    alpha_c = __dadd_rn(alpha_c, w);
+    trans = __dmul_rn(trans, absorb);
+    if (!(trans > A.t_stop)) break;
+    ++i;
+  }
+  r.alpha_c = alpha_c;
+  r.samples = samples;
+  r.hit = alpha_c > A.alpha_floor;
+  r.t_hit = r.hit ? t_hit : __longlong_as_double(0x7ff0000000000000ll);
+  return r;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(128) k_march(MarchArgs args) {
+  const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const unsigned lane = threadIdx.x & 31;
+  bool valid = gid < args.n_rays;
+  double ow[3] = {0, 0, 0}, dw[3] = {0, 0, 1};
+  if (valid) {
+    if (MODE == kModeRays) {
+      const double *op = args.origins + (args.origin_stride ? 3 * gid : 0);
+      ow[0] = op[0]; ow[1] = op[1]; ow[2] = op[2];
+      dw[0] = args.dirs[3 * gid]; dw[1] = args.dirs[3 * gid + 1]; dw[2] = args.dirs[3 * gid + 2];
+    } else {
+      long long t = MODE == kModeRect ? 0 : gid / args.tile_stride;
+      long long local = MODE == kModeRect ? gid : gid % args.tile_stride;
+      const TileParams tp = args.tiles[t];
+      const int w = tp.x1 - tp.x0, h = tp.y1 - tp.y0;
+      if (local >= (long long)w * h) {
+        valid = false;
+      } else {
+        const CamParams &cp = args.cams[tp.cam];
+        double px = (double)(tp.x0 + (int)(local % w)), py = (double)(tp.y0 + (int)(local / w));
+        camera_dir(cp.pose, cp.fx, cp.fy, cp.cx, cp.cy, px, py, dw);
+        ow[0] = cp.pose[3]; ow[1] = cp.pose[7]; ow[2] = cp.pose[11];
+      }
+    }
+    if (MODE != kModeScene && valid) {   // miss defaults (lightfield.py:415-416)
+      reinterpret_cast<float4 *>(args.rgba)[gid] = make_float4(0.f, 0.f, 0.f, 0.f);
+      args.depth[gid] = __int_as_float(0x7f800000);
+    }
+  }
+  unsigned long long samples_total = 0;
+  unsigned ordinal = 0;
+  for (int k = 0; k < args.n_inst; ++k) {
+    const DevInst &I = args.inst[k];
+    const DevAsset &A = *I.a;
+    bool hit = false;
+    double o[3], d[3], t_near = 0, t_far = 0;
+    MarchOut mr;
+    if (valid) {
+      to_object(I.w2o, ow, dw, o, d);
+      bool boxhit = slab(A.pmin, A.pmax, o, d, t_near, t_far);
+      if (boxhit) {
+        mr = march_ray(A, o, d, t_near, t_far);
+        samples_total += (unsigned long long)mr.samples;
+        hit = mr.hit;
+      }
+    }
+    // warp-aggregated queue append (one atomic per warp per instance)
+    const unsigned ballot = __ballot_sync(0xffffffffu, hit);
+    if (ballot) {
+      unsigned base = 0;
+      if (lane == __ffs(ballot) - 1) base = atomicAdd(args.counts + k, (unsigned)__popc(ballot));
+      base = __shfl_sync(0xffffffffu, base, __ffs(ballot) - 1);
+      if (hit) {
+        const unsigned pos = base + __popc(ballot & ((1u << lane) - 1u));
+        HitRec rec;
+        double t_obj = mr.t_hit;
+        double p[3];
+        if (A.use_hit_point) {
+#pragma unroll
+          for (int q = 0; q < 3; ++q) p[q] = clamp01(__dadd_rn(o[q], __dmul_rn(t_obj, d[q])));
+        } else {           // ablation: shade at the proxy entry (lightfield.py:438-445)
+          t_obj = t_near;
+#pragma unroll
+          for (int q = 0; q < 3; ++q) p[q] = clamp01(__dadd_rn(o[q], __dmul_rn(t_near, d[q])));
+        }
+        rec.p[0] = p[0]; rec.p[1] = p[1]; rec.p[2] = p[2];
+        rec.alpha_c = mr.alpha_c;
+        rec.t_obj = t_obj;
+        rec.d[0] = d[0]; rec.d[1] = d[1]; rec.d[2] = d[2];
+        rec.out_idx = (uint32_t)gid;
+        rec.ordinal = ordinal;
+        if ((long long)pos < args.cap) args.queue[(long long)k * args.cap + pos] = rec;
+        ++ordinal;
+      }
+    }
+  }
+  if (MODE == kModeScene && valid) args.nhit[gid] = (uint8_t)ordinal;
+  // march_samples counter (lightfield.py:430-431)
+#pragma unroll
+  for (int off = 16; off; off >>= 1) samples_total += __shfl_xor_sync(0xffffffffu, samples_total, off);
+  if (lane == 0 && samples_total) atomicAdd(args.counters + 3, samples_total);
+}
+
+// ---------------------------------------------------------------- shading
+struct ShadeArgs {
+  const DevInst *inst;
+  int n_inst;
+  const HitRec *queue;
+  long long cap;
+  const unsigned int *counts;
+  int mode;                    // RayMode
+  float *rgba;                 // rays/rect: (n,4); scene: layers (L, P, 4)
+  float *depth;                // rays/rect: (n,);  scene: layers (L, P)
+  long long layer_stride;      // scene: P
+  unsigned long long *counters;
+};
+
+constexpr int kShadeThreads = 128;
+
+// Fully fused MLP forward for one row (neural.py:89-108), fp32 with
+// sequential FMA accumulation.  Layer 0 is computed input-major from a
+// per-thread input column in shared memory so every weight read is a
+// warp-uniform broadcast; layers 1 and 2 are fused output-by-output so only
+// one hidden vector lives in registers.
+__device__ __forceinline__ void mlp_row(const float *__restrict__ P, int n_layers, int in, const int act[4],
+                                        const float *xcol, float out[4]) {
+  float h[kHid];
+#pragma unroll
+  for (int o = 0; o < kHid; ++o) h[o] = 0.f;
+  for (int i = 0; i < in; ++i) {
+    const float xi = xcol[i * kShadeThreads];
+    const float4 *wr = reinterpret_cast<const float4 *>(P + MlpOff::w0t + i * kHid);
+#pragma unroll
+    for (int q = 0; q < kHid / 4; ++q) {
+      const float4 wv = wr[q];
+      h[4 * q + 0] = fmaf(xi, wv.x, h[4 * q + 0]);
+      h[4 * q + 1] = fmaf(xi, wv.y, h[4 * q + 1]);
+      h[4 * q + 2] = fmaf(xi, wv.z, h[4 * q + 2]);
+      h[4 * q + 3] = fmaf(xi, wv.w, h[4 * q + 3]);
+    }
+  }
+#pragma unroll
+  for (int o = 0; o < kHid; ++o) {
+    const float z = h[o] + P[MlpOff::b0 + o];
+    h[o] = z > 0.f ? z : 0.f;
+  }
+  float acc4[4] = {0.f, 0.f, 0.f, 0.f};
+  if (n_layers == 3) {
+    for (int o = 0; o < kHid; ++o) {
+      const float4 *wr = reinterpret_cast<const float4 *>(P + MlpOff::w1 + o * kHid);
+      float acc = 0.f;
+#pragma unroll
+      for (int q = 0; q < kHid / 4; ++q) {
+        const float4 wv = wr[q];
+        acc = fmaf(h[4 * q + 0], wv.x, acc);
+        acc = fmaf(h[4 * q + 1], wv.y, acc);
+        acc = fmaf(h[4 * q + 2], wv.z, acc);
+        acc = fmaf(h[4 * q + 3], wv.w, acc);
+      }
+      float z = acc + P[MlpOff::b1 + o];
+      z = z > 0.f ? z : 0.f;
+      // last layer accumulates this hidden unit (index o) into all 4 outputs
+      // -- sequential in o, matching a row-major dot product
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc4[j] = fmaf(z, P[MlpOff::wl + j * kHid + o], acc4[j]);
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      float acc = 0.f;
+#pragma unroll
+      for (int o = 0; o < kHid; ++o) acc = fmaf(h[o], P[MlpOff::wl + j * kHid + o], acc);
+      acc4[j] = acc;
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const float z = acc4[j] + P[MlpOff::bl + j];
+    out[j] = act[j] == 0 ? z : (act[j] == 1 ? sigmoidf_np(z) : expf(z));
+  }
+}
+
+__global__ void __launch_bounds__(kShadeThreads) k_shade(ShadeArgs args) {
+  extern __shared__ __align__(16) float smem[];
+  float *s_fs = smem;                               // MlpOff::total
+  float *s_fd = smem + MlpOff::total;               // MlpOff::total
+  float *s_x = smem + 2 * MlpOff::total;            // kInp * kShadeThreads
+  const int tid = threadIdx.x;
+  int cur = -1;
+  unsigned long long n_fs = 0, n_fd = 0;
+  for (long long tile = blockIdx.x;; tile += gridDim.x) {
+    // map the global tile id onto (instance, first record)
+    int k = 0;
+    long long t = tile;
+    unsigned cnt = 0;
+    for (; k < args.n_inst; ++k) {
+      cnt = min((long long)args.counts[k], args.cap);
+      long long nt = (cnt + kShadeThreads - 1) / kShadeThreads;
+      if (t < nt) break;
+      t -= nt;
+    }
+    if (k >= args.n_inst) break;
+    const DevInst &I = args.inst[k];
+    const DevAsset &A = *I.a;
+    if (k != cur) {
+      __syncthreads();
+      for (int q = tid; q < MlpOff::total; q += kShadeThreads) {
+        s_fs[q] = A.fs.params[q];
+        s_fd[q] = A.fd.params ? A.fd.params[q] : 0.f;
+      }
+      __syncthreads();
+      cur = k;
+    }
+    const long long r = t * kShadeThreads + tid;
+    if (r >= cnt) continue;
+    const HitRec rec = args.queue[(long long)k * args.cap + r];
+    float *xcol = s_x + tid;
+    // PSH encode (encoding.py:390-394)
+    int base[3];
+    double w8[8];
+    base_weights(rec.p, A.N, base, w8);
+    double es0 = 0.0, es1 = 0.0, es_rest[2] = {0.0, 0.0};
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const uint32_t slot = psh_slot(A.tab, A.phi, A.N, A.m, A.mphi, base[0] + (c & 1),
+                                     base[1] + ((c >> 1) & 1), base[2] + ((c >> 2) & 1));
+      if (A.F == 2) {
+        const float2 f = __ldg(reinterpret_cast<const float2 *>(A.feat) + slot);
+        es0 = __dadd_rn(es0, __dmul_rn((double)f.x, w8[c]));
+        es1 = __dadd_rn(es1, __dmul_rn((double)f.y, w8[c]));
+      } else {
+        const float *f = A.feat + (size_t)slot * A.F;
+        es0 = __dadd_rn(es0, __dmul_rn((double)__ldg(f), w8[c]));
+        if (A.F > 1) es1 = __dadd_rn(es1, __dmul_rn((double)__ldg(f + 1), w8[c]));
+        if (A.F > 2) es_rest[0] = __dadd_rn(es_rest[0], __dmul_rn((double)__ldg(f + 2), w8[c]));
+        if (A.F > 3) es_rest[1] = __dadd_rn(es_rest[1], __dmul_rn((double)__ldg(f + 3), w8[c]));
+      }
+    }
+    int nin = 0;
+    xcol[(nin++) * kShadeThreads] = (float)es0;
+    if (A.F > 1) xcol[(nin++) * kShadeThreads] = (float)es1;
+    if (A.F > 2) xcol[(nin++) * kShadeThreads] = (float)es_rest[0];
+    if (A.F > 3) xcol[(nin++) * kShadeThreads] = (float)es_rest[1];
+    double sh[16];
+    sh_encode(rec.d, sh);
+#pragma unroll
+    for (int q = 0; q < 16; ++q) xcol[(nin + q) * kShadeThreads] = (float)sh[q];
+    nin += 16;
+    const double ac = clampd(rec.alpha_c, 1e-4, 1.0 - 1e-4);
+    if (A.refine_opacity) xcol[(nin++) * kShadeThreads] = (float)ac;
+    float fs_out[4];
+    mlp_row(s_fs, A.fs.n_layers, A.fs.in, A.fs.act, xcol, fs_out);
+    ++n_fs;
+    double alpha;
+    const double z = (double)fs_out[3];
+    if (!A.use_opacity) alpha = clampd(rec.alpha_c, 0.0, 1.0);
+    else if (A.refine_opacity) alpha = sigmoid_np(z + log(ac / (1.0 - ac)));
+    else alpha = sigmoid_np(z);
+    double cd[3], tint;
+    if (!A.use_diffuse_color) {
+      cd[0] = cd[1] = cd[2] = 0.0;
+      tint = 1.0;
+    } else if (A.has_dif) {
+      float dv[4];
+      atlas_query<4>(A.dif, rec.p, dv);
+      cd[0] = dv[0]; cd[1] = dv[1]; cd[2] = dv[2];
+      tint = dv[3];
+    } else {
+      // live diffuse: hash grid (encoding.py:467-478) + diffuse MLP
+      int ni = 0;
+      for (int l = 0; l < A.hg_levels; ++l) {
+        const int n = A.hg_res[l];
+        int bl[3];
+        double wl[8];
+        base_weights(rec.p, n, bl, wl);
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+        for (int c = 0; c < 8; ++c) {
+          const int cx = c & 1, cy = (c >> 1) & 1, cz = (c >> 2) & 1;
+          long long idx;
+          if (A.hg_dense[l]) {
+            const long long side = n + 1;
+            idx = ((bl[0] * side + bl[1]) * side + bl[2]) + ((cx * side + cy) * side + cz);
+          } else {
+            // PRIMES_H0 (encoding.py:30), xor hash (encoding.py:454-459)
+            unsigned long long h = ((unsigned long long)(bl[0] + cx) * 1ull) ^
+                                   ((unsigned long long)(bl[1] + cy) * 2654435761ull) ^
+                                   ((unsigned long long)(bl[2] + cz) * 805459861ull);
+            idx = (long long)(h % A.hg_table);
+          }
+          const float *row = A.hg_feat[l] + idx * A.hg_F;
+          for (int f = 0; f < A.hg_F && f < 4; ++f)
+            acc[f] = __dadd_rn(acc[f], __dmul_rn((double)__ldg(row + f), wl[c]));
+        }
+        for (int f = 0; f < A.hg_F && f < 4; ++f) xcol[(ni++) * kShadeThreads] = (float)acc[f];
+      }
+      float dv[4];
+      mlp_row(s_fd, A.fd.n_layers, A.fd.in, A.fd.act, xcol, dv);
+      ++n_fd;
+      cd[0] = dv[0]; cd[1] = dv[1]; cd[2] = dv[2];
+      tint = dv[3];
+    }
+    if (!A.use_tint) tint = 0.5;
+    float4 out;
+    out.x = (float)clampd(__dadd_rn(cd[0], __dmul_rn(tint, (double)fs_out[0])), 0.0, 1.0);
+    out.y = (float)clampd(__dadd_rn(cd[1], __dmul_rn(tint, (double)fs_out[1])), 0.0, 1.0);
+    out.z = (float)clampd(__dadd_rn(cd[2], __dmul_rn(tint, (double)fs_out[2])), 0.0, 1.0);
+    out.w = (float)alpha;
+    float dep = (float)__ddiv_rn(rec.t_obj, I.scale);
+    if (out.w <= 0.f) {        // lightfield.py:453-455
+      out = make_float4(0.f, 0.f, 0.f, 0.f);
+      dep = __int_as_float(0x7f800000);
+    }
+    const long long o = args.mode == kModeScene ? (long long)rec.ordinal * args.layer_stride + rec.out_idx
+                                                : (long long)rec.out_idx;
+    reinterpret_cast<float4 *>(args.rgba)[o] = out;
+    args.depth[o] = dep;
+  }
+  // fs_evals, fd_evals, hit_pixels (lightfield.py:299-301, 324-325)
+  const unsigned lane = tid & 31;
+#pragma unroll
+  for (int off = 16; off; off >>= 1) {
+    n_fs += __shfl_xor_sync(0xffffffffu, n_fs, off);
+    n_fd += __shfl_xor_sync(0xffffffffu, n_fd, off);
+  }
+  if (lane == 0) {
+    if (n_fs) { atomicAdd(args.counters + 0, n_fs); atomicAdd(args.counters + 2, n_fs); }
+    if (n_fd) atomicAdd(args.counters + 1, n_fd);
+  }
+}
+
+// ---------------------------------------------------------------- compose
+struct ComposeArgs {
+  long long n_pix;             // total pixel slots
+  const uint8_t *nhit;         // scene mode: per-pixel layer count (NULL => K layers)
+  int K;                       // layers when nhit == NULL
+  const float *rgba;           // (L, P, 4)
+  const float *depth;          // (L, P)
+  long long layer_stride;      // P
+  const TileParams *tiles;     // scene mode: skip padding slots (NULL => none)
+  long long tile_stride;
+  float alpha_vis;             // compared in f32 (numpy 2 weak scalar)
+  float *out_rgba;
+  float *out_depth;
+  uint8_t *out_rgba8;
+  uint16_t *out_depth16;
+  float depth_far;
+};
+
+constexpr int kMaxLayers = 64;
+
+// farm.compose (farm.py:129-172) for one pixel; frames whose pixel is a miss
+// (rgba 0, depth inf) sort last and leave out_c and T unchanged, so
+// compositing only the hit layers is bitwise equal to compositing all K.
+__global__ void __launch_bounds__(256) k_compose(ComposeArgs a) {
+  const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= a.n_pix) return;
+  if (a.tiles) {
+    const TileParams tp = a.tiles[p / a.tile_stride];
+    if (p % a.tile_stride >= (long long)(tp.x1 - tp.x0) * (tp.y1 - tp.y0)) return;
+  }
+  const int n = a.nhit ? (int)a.nhit[p] : a.K;
+  float dk[kMaxLayers];
+  unsigned char ord[kMaxLayers];
+  // stable insertion sort by depth (np.argsort kind="stable")
+  for (int k = 0; k < n; ++k) {
+    const float dv = a.depth[(long long)k * a.layer_stride + p];
+    int j = k;
+    while (j > 0 && dk[j - 1] > dv) { dk[j] = dk[j - 1]; ord[j] = ord[j - 1]; --j; }
+    dk[j] = dv;
+    ord[j] = (unsigned char)k;
+  }
+  double oc0 = 0.0, oc1 = 0.0, oc2 = 0.0, trans = 1.0;
+  float od = __int_as_float(0x7f800000);
+  bool set = false;
+  for (int r = 0; r < n; ++r) {
+    const int k = ord[r];
+    const float4 c = reinterpret_cast<const float4 *>(a.rgba)[(long long)k * a.layer_stride + p];
+    oc0 = __dadd_rn(oc0, __dmul_rn(trans, (double)c.x));
+    oc1 = __dadd_rn(oc1, __dmul_rn(trans, (double)c.y));
+    oc2 = __dadd_rn(oc2, __dmul_rn(trans, (double)c.z));
+    if (!set && c.w > a.alpha_vis) { od = dk[r]; set = true; }
+    trans = __dmul_rn(trans, (double)(1.0f - c.w));
+  }
+  float4 o;
+  o.x = (float)clampd(oc0, 0.0, 1.0);
+  o.y = (float)clampd(oc1, 0.0, 1.0);
+  o.z = (float)clampd(oc2, 0.0, 1.0);
+  o.w = (float)clampd(__dsub_rn(1.0, trans), 0.0, 1.0);
+  if (o.w <= 0.f) {
+    o = make_float4(0.f, 0.f, 0.f, 0.f);
+    od = __int_as_float(0x7f800000);
+  }
+  if (a.out_rgba) reinterpret_cast<float4 *>(a.out_rgba)[p] = o;
+  if (a.out_depth) a.out_depth[p] = od;
+  if (a.out_rgba8) {           // encode_frame (protocol.py:256-266): clip(round(x*255))
+    const float q[4] = {o.x, o.y, o.z, o.w};
+    uchar4 u;
+    unsigned char uu[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      float v = rintf(q[c] * 255.0f);
+      v = v < 0.f ? 0.f : (v > 255.f ? 255.f : v);
+      uu[c] = (unsigned char)v;
+    }
+    u.x = uu[0]; u.y = uu[1]; u.z = uu[2]; u.w = uu[3];
+    reinterpret_cast<uchar4 *>(a.out_rgba8)[p] = u;
+  }
+  if (a.out_depth16) {
+    uint16_t qd = 65535;
+    if (isfinite(od)) qd = (uint16_t)rintf(fminf(od, a.depth_far) / a.depth_far * 65534.0f);
+    a.out_depth16[p] = qd;
+  }
+}
+
+}  // namespace nolf

@@ -1,0 +1,367 @@
+"""Reference-signature render entry points backed by libnolf_b200.so.
+
+  render_rays(asset, origins, dirs, counters=None)   lightfield.py:400-456
+  render_ray(asset, ray, counters=None)              lightfield.py:459-463
+  render_range(asset, ray_range, counters=None)      renderer.py:63-93
+  render_frame(scene, camera, counters=None)         renderer.py:96-107
+  compose(frames, asset_order=None, alpha_vis=0.5)   farm.py:129-172
+  SceneRenderer / render_scene                       fused march+shade+compose
+                                                     over screen tiles (fast path)
+
+Host arrays in, host arrays out for the reference signatures (the copies are
+part of the call, as a drop-in must); ``SceneRenderer`` keeps everything on
+the device.  Per-asset device state is uploaded once and cached by the
+identity of the asset's arrays (plus a checksum of its MLP parameters, which
+the reference's own tests mutate in place); ``invalidate()`` drops it.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import time
+import zlib
+from collections import OrderedDict
+
+import numpy as np
+
+from . import _native as N
+from . import errors
+from .model import Frame, RayRange, RenderCounters, Tile, uniform_scale_of
+
+_torch = None
+
+
+def torch():
+    global _torch
+    if _torch is None:
+        import torch as t
+        _torch = t
+    return _torch
+
+
+def _device():
+    t = torch()
+    if not t.cuda.is_available():
+        raise RuntimeError("CUDA device required: the i-NOLF path has no CPU fallback")
+    return t.device("cuda", t.cuda.current_device())
+
+
+def _stream_ptr():
+    return torch().cuda.current_stream().cuda_stream
+
+
+# ------------------------------------------------------------------ assets
+class DeviceAsset:
+    """Owns one nolf_asset_t (device copy of every table of an asset)."""
+
+    def __init__(self, asset, device_index: int):
+        desc, keep = N.asset_desc(asset)
+        h = C.c_void_p()
+        N.check(N.lib().nolf_asset_create(C.byref(desc), int(device_index), C.byref(h)))
+        del keep
+        self.handle = h
+        self.device_index = device_index
+        self.nbytes = int(N.lib().nolf_asset_device_bytes(h))
+
+    def set_mlp_mode(self, mode: int) -> None:
+        N.check(N.lib().nolf_asset_set_mlp_mode(self.handle, int(mode)))
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h and N._lib is not None:
+            N._lib.nolf_asset_destroy(h)
+            self.handle = None
+
+
+_CACHE: "OrderedDict[tuple, tuple]" = OrderedDict()
+_CACHE_MAX = 64
+
+
+def _fingerprint(asset, device_index):
+    if getattr(asset, "analytic_color", None) is not None or (
+            asset.density_atlas is None and getattr(asset, "analytic_density", None) is not None):
+        raise errors.DomainError(
+            "analytic (closed-form) assets are a CPU test bypass and are not supported by the "
+            "B200 render path; bake them into cube atlases first")
+    if asset.density_atlas is None:
+        raise errors.StateError("asset is not baked; no density cache to march")
+    arrays = [asset.density_atlas.index, asset.density_atlas.cubes, asset.psh.offsets,
+              asset.psh_features]
+    if asset.diffuse_atlas is not None:
+        arrays += [asset.diffuse_atlas.index, asset.diffuse_atlas.cubes]
+    if asset.diffuse_features is not None:
+        arrays += list(asset.diffuse_features)
+    crc = 0
+    for m in (asset.specular_mlp, asset.diffuse_mlp):
+        if m is not None:
+            for a in list(m.weights) + list(m.biases):
+                crc = zlib.crc32(np.ascontiguousarray(a).view(np.uint8), crc)
+    w = asset.wiring
+    key = (device_index, tuple(id(a) for a in arrays), crc,
+           (asset.march.step, asset.march.t_stop, asset.march.alpha_floor),
+           tuple(np.asarray(asset.proxy.min, float)), tuple(np.asarray(asset.proxy.max, float)),
+           (w.use_hit_point, w.use_opacity, w.use_tint, w.refine_opacity, w.use_diffuse_color),
+           tuple(m.heads) if (m := asset.specular_mlp) is not None else None)
+    return key, arrays
+
+
+def device_asset(asset, device_index: int | None = None) -> DeviceAsset:
+    """Upload (or fetch the cached upload of) an asset on a CUDA device."""
+    if device_index is None:
+        _device()
+        device_index = torch().cuda.current_device()
+    key, arrays = _fingerprint(asset, device_index)
+    hit = _CACHE.get(key)
+    if hit is not None:
+        _CACHE.move_to_end(key)
+        return hit[0]
+    dev = DeviceAsset(asset, device_index)
+    _CACHE[key] = (dev, arrays)       # arrays pinned so their ids stay unique
+    while len(_CACHE) > _CACHE_MAX:
+        _CACHE.popitem(last=False)
+    return dev
+
+
+def invalidate() -> None:
+    """Forget every cached device asset (call after in-place array edits)."""
+    _CACHE.clear()
+
+
+# ------------------------------------------------------------------ workspace
+_WS = {}
+
+
+def workspace(nbytes: int):
+    t = torch()
+    dev = _device()
+    cur = _WS.get(dev.index)
+    if cur is None or cur.numel() < nbytes:
+        _WS[dev.index] = None
+        cur = t.empty(max(int(nbytes), 1), dtype=t.uint8, device=dev)
+        _WS[dev.index] = cur
+    return cur
+
+
+def _instance(asset, transform=None) -> N.Instance:
+    o2w = np.asarray(asset.object_to_world if transform is None else transform, np.float64)
+    w2o = np.linalg.inv(o2w)                      # lightfield.py:408
+    scale = uniform_scale_of(w2o)                 # lightfield.py:409
+    dev = device_asset(asset)
+    inst = N.Instance()
+    inst.asset = dev.handle
+    flat = w2o.reshape(16)
+    for i in range(16):
+        inst.w2o[i] = float(flat[i])
+    inst.scale = float(scale)
+    inst._dev = dev                               # keep the handle alive
+    return inst
+
+
+def _merge(counters, cnt_dev):
+    if counters is None:
+        return
+    c = cnt_dev.cpu().numpy()
+    counters.fs_evals += int(c[0])
+    counters.fd_evals += int(c[1])
+    counters.hit_pixels += int(c[2])
+    counters.march_samples += int(c[3])
+
+
+# ------------------------------------------------------------------ reference API
+def render_rays(asset, origins, dirs, counters=None):
+    """World-space rays -> (rgba (B,4) f32, depth (B,) f32); lightfield.py:400-456."""
+    t = torch()
+    origins = np.asarray(origins, dtype=np.float64)
+    dirs = np.asarray(dirs, dtype=np.float64)
+    if origins.ndim != 2 or origins.shape[1] != 3 or dirs.shape != origins.shape:
+        raise errors.DomainError("origins and dirs must both be (B,3)")
+    n = len(origins)
+    inst = _instance(asset)
+    dev = _device()
+    shared = n > 0 and origins.strides[0] == 0
+    o_host = np.ascontiguousarray(origins[:1] if shared else origins)
+    o = t.from_numpy(o_host).to(dev)
+    d = t.from_numpy(np.ascontiguousarray(dirs)).to(dev)
+    rgba = t.empty((n, 4), dtype=t.float32, device=dev)
+    depth = t.empty((n,), dtype=t.float32, device=dev)
+    cnt = t.zeros(4, dtype=t.int64, device=dev)
+    need = int(N.lib().nolf_workspace_bytes(1, n))
+    ws = workspace(need)
+    N.check(N.lib().nolf_render_rays(C.byref(inst), o.data_ptr(), 0 if shared else 1, d.data_ptr(), n,
+                                     rgba.data_ptr(), depth.data_ptr(), cnt.data_ptr(), ws.data_ptr(),
+                                     ws.numel(), _stream_ptr()))
+    out = rgba.cpu().numpy(), depth.cpu().numpy()
+    _merge(counters, cnt)
+    return out
+
+
+def render_ray(asset, ray, counters=None):
+    rgba, depth = render_rays(asset, np.asarray(ray.origin)[None, :],
+                              np.asarray(ray.direction)[None, :], counters)
+    return rgba[0], float(depth[0])
+
+
+def render_range(asset, ray_range, counters=None):
+    """Render a RayRange rectangle -> (Tile, instr); renderer.py:63-93."""
+    t = torch()
+    counters = counters if counters is not None else RenderCounters()
+    start = time.perf_counter()
+    inst = _instance(asset)
+    cam = ray_range.camera
+    x0, y0, x1, y1 = ray_range.x0, ray_range.y0, ray_range.x1, ray_range.y1
+    h, w = y1 - y0, x1 - x0
+    dev = _device()
+    rgba = t.empty((h, w, 4), dtype=t.float32, device=dev)
+    depth = t.empty((h, w), dtype=t.float32, device=dev)
+    cnt = t.zeros(4, dtype=t.int64, device=dev)
+    ws = workspace(int(N.lib().nolf_workspace_bytes(1, h * w)))
+    cs = N.camera_struct(cam)
+    N.check(N.lib().nolf_render_rect(C.byref(inst), C.byref(cs), x0, y0, x1, y1, rgba.data_ptr(),
+                                     depth.data_ptr(), cnt.data_ptr(), ws.data_ptr(), ws.numel(),
+                                     _stream_ptr()))
+    tile = Tile(x0=x0, y0=y0, rgba=rgba.cpu().numpy(), depth=depth.cpu().numpy())
+    c = cnt.cpu().numpy()
+    before_fs, before_hits = counters.fs_evals, counters.hit_pixels
+    _merge(counters, cnt)
+    instr = {"wall_time_s": time.perf_counter() - start, "rays": int(h * w),
+             "hits": counters.hit_pixels - before_hits, "fs_evals": counters.fs_evals - before_fs}
+    del c
+    return tile, instr
+
+
+def render_frame(scene, camera, counters=None):
+    """Per-asset full frames for depth composition; renderer.py:96-107."""
+    frames = []
+    for asset, transform in scene:
+        placed = asset
+        if transform is not None:
+            import dataclasses
+            placed = dataclasses.replace(asset, object_to_world=np.asarray(transform, np.float64))
+        tile, _ = render_range(placed, RayRange(camera, 0, 0, camera.width, camera.height,
+                                                getattr(asset, "name", "asset")), counters)
+        frames.append(Frame(width=camera.width, height=camera.height, rgba=tile.rgba,
+                            depth=tile.depth))
+    return frames
+
+
+def compose(frames, asset_order=None, alpha_vis: float = 0.5):
+    """Depth-sorted front-to-back over of per-asset frames; farm.py:129-172."""
+    if not frames:
+        raise errors.ProtocolError("compose needs at least one frame")
+    t = torch()
+    h, w = frames[0].height, frames[0].width
+    dev = _device()
+    rgba = t.from_numpy(np.ascontiguousarray(np.stack([f.rgba for f in frames]), np.float32)).to(dev)
+    depth = t.from_numpy(np.ascontiguousarray(np.stack([f.depth for f in frames]), np.float32)).to(dev)
+    orgba, odepth = compose_device(rgba.reshape(len(frames), h * w, 4), depth.reshape(len(frames), h * w),
+                                   alpha_vis)
+    return Frame(width=w, height=h, rgba=orgba.reshape(h, w, 4).cpu().numpy(),
+                 depth=odepth.reshape(h, w).cpu().numpy())
+
+
+def compose_device(rgba, depth, alpha_vis: float = 0.5):
+    """compose on device tensors: rgba (K,P,4) f32, depth (K,P) f32."""
+    t = torch()
+    K, P = depth.shape
+    out_rgba = t.empty((P, 4), dtype=t.float32, device=rgba.device)
+    out_depth = t.empty((P,), dtype=t.float32, device=rgba.device)
+    N.check(N.lib().nolf_compose(K, P, rgba.contiguous().data_ptr(), depth.contiguous().data_ptr(),
+                                 float(alpha_vis), out_rgba.data_ptr(), out_depth.data_ptr(),
+                                 _stream_ptr()))
+    return out_rgba, out_depth
+
+
+# ------------------------------------------------------------------ fast path
+def frame_tiles(width: int, height: int, tile: int = 32, cam: int = 0) -> np.ndarray:
+    """tile_ranges (renderer.py:176-187) as an (n,5) int32 [cam,x0,y0,x1,y1] table."""
+    out = [(cam, tx, ty, min(tx + tile, width), min(ty + tile, height))
+           for ty in range(0, height, tile) for tx in range(0, width, tile)]
+    return np.asarray(out, dtype=np.int32).reshape(-1, 5)
+
+
+class SceneRenderer:
+    """Fused multi-asset renderer: march + shade + depth compose of every
+    placed asset over a tile list, all resident on one device.
+
+    ``scene`` is a list of (asset, transform) like render_frame's; each tile
+    row is (camera index, x0, y0, x1, y1); pixels come back tile-packed with
+    ``tile_stride`` slots per tile.
+    """
+
+    def __init__(self, scene, alpha_vis: float = 0.5, depth_far: float = 10.0):
+        self.insts = [_instance(a, tr) for a, tr in scene]
+        arr = (N.Instance * len(self.insts))()
+        for i, inst in enumerate(self.insts):
+            C.memmove(C.byref(arr[i]), C.byref(inst), C.sizeof(N.Instance))
+        self._inst_arr = arr
+        self.alpha_vis = float(alpha_vis)
+        self.depth_far = float(depth_far)
+        self.device = _device()
+        self._ws = None
+
+    def mlp_mode(self, mode: int) -> None:
+        for inst in self.insts:
+            inst._dev.set_mlp_mode(mode)
+
+    def alloc(self, n_tiles: int, tile_stride: int, want_f32=True, want_u8=True):
+        t = torch()
+        P = n_tiles * tile_stride
+        out = {}
+        if want_f32:
+            out["rgba"] = t.empty((P, 4), dtype=t.float32, device=self.device)
+            out["depth"] = t.empty((P,), dtype=t.float32, device=self.device)
+        if want_u8:
+            out["rgba8"] = t.empty((P, 4), dtype=t.uint8, device=self.device)
+            out["depth16"] = t.empty((P,), dtype=t.int16, device=self.device)
+        out["counters"] = t.zeros(4, dtype=t.int64, device=self.device)
+        need = int(N.lib().nolf_workspace_bytes(len(self.insts), P))
+        if self._ws is None or self._ws.numel() < need:
+            self._ws = None
+            self._ws = t.empty(need, dtype=t.uint8, device=self.device)
+        return out
+
+    def render(self, cameras, tiles_dev, n_tiles: int, tile_stride: int, out: dict, stream=None):
+        cams = (N.Camera * len(cameras))()
+        for i, c in enumerate(cameras):
+            cams[i] = N.camera_struct(c)
+        so = N.SceneOut()
+        so.rgba = out["rgba"].data_ptr() if "rgba" in out else None
+        so.depth = out["depth"].data_ptr() if "depth" in out else None
+        so.rgba8 = out["rgba8"].data_ptr() if "rgba8" in out else None
+        so.depth16 = out["depth16"].data_ptr() if "depth16" in out else None
+        so.tile_stride = int(tile_stride)
+        so.depth_far = self.depth_far
+        st = stream if stream is not None else _stream_ptr()
+        N.check(N.lib().nolf_render_scene(self._inst_arr, len(self.insts), cams, len(cameras),
+                                          tiles_dev.data_ptr(), int(n_tiles), C.byref(so),
+                                          self.alpha_vis, out["counters"].data_ptr(),
+                                          self._ws.data_ptr(), self._ws.numel(), st))
+
+
+def unpack_index(tiles: np.ndarray, tile_stride: int, width: int, height: int, cam: int = 0):
+    """Packed-slot index of every pixel of camera ``cam`` (row-major H*W), -1 if absent."""
+    idx = np.full(height * width, -1, dtype=np.int64)
+    for t, (c, x0, y0, x1, y1) in enumerate(tiles):
+        if c != cam:
+            continue
+        w = x1 - x0
+        ys, xs = np.mgrid[y0:y1, x0:x1]
+        idx[(ys * width + xs).reshape(-1)] = t * tile_stride + (
+            (ys - y0) * w + (xs - x0)).reshape(-1)
+    return idx
+
+
+def render_scene(scene, camera, counters=None, tile: int = 32):
+    """Composed Frame of a scene in one fused launch sequence (== compose(render_frame(...)))."""
+    t = torch()
+    r = SceneRenderer(scene)
+    tiles = frame_tiles(camera.width, camera.height, tile)
+    tiles_dev = t.from_numpy(tiles).to(r.device)
+    out = r.alloc(len(tiles), tile * tile, want_f32=True, want_u8=False)
+    r.render([camera], tiles_dev, len(tiles), tile * tile, out)
+    idx = t.from_numpy(unpack_index(tiles, tile * tile, camera.width, camera.height)).to(r.device)
+    rgba = out["rgba"].index_select(0, idx).reshape(camera.height, camera.width, 4)
+    depth = out["depth"].index_select(0, idx).reshape(camera.height, camera.width)
+    _merge(counters, out["counters"])
+    return Frame(width=camera.width, height=camera.height, rgba=rgba.cpu().numpy(),
+                 depth=depth.cpu().numpy())
