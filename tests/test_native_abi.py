@@ -1,0 +1,42 @@
+"""The C-ABI library loads without a GPU and exports every entry point that
+include/nolf.h declares (no compute calls here)."""
+
+import ctypes
+import os
+import re
+
+from paper_2303_04086_b200 import _native
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared():
+    src = open(os.path.join(ROOT, "include", "nolf.h")).read()
+    return sorted(set(re.findall(r"\b(nolf_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_header_declares_entry_points():
+    names = declared()
+    for n in ("nolf_asset_create", "nolf_render_rays", "nolf_render_rect", "nolf_render_scene",
+              "nolf_compose", "nolf_last_error"):
+        assert n in names
+
+
+def test_library_exports_every_declared_symbol():
+    lib = _native.lib()
+    missing = [n for n in declared() if not hasattr(lib, n)]
+    assert not missing, missing
+    assert lib.nolf_abi_version() == 1
+
+
+def test_workspace_size_is_monotone():
+    lib = _native.lib()
+    assert lib.nolf_workspace_bytes(1, 1000) < lib.nolf_workspace_bytes(2, 1000)
+    assert lib.nolf_workspace_bytes(1, 1000) < lib.nolf_workspace_bytes(1, 2000)
+
+
+def test_invalid_arguments_fail_loudly_without_gpu():
+    lib = _native.lib()
+    rc = lib.nolf_compose(0, 10, None, None, 0.5, None, None, None)
+    assert rc == _native.NOLF_EINVAL
+    assert b"at least one frame" in lib.nolf_last_error()
