@@ -23,6 +23,9 @@
  *                          shade and depth-composite every asset of a scene
  *                          over a list of screen tiles of one or more cameras
  *   nolf_compose        <- farm.compose(frames, alpha_vis) (farm.py:129-172)
+ *   nolf_march_rays     <- lightfield.march_rays (lightfield.py:129-186)
+ *   nolf_eval_diffuse   <- hashgrid_encode + mlp_forward(diffuse_mlp)
+ *                          (encoding.py:467-478, lightfield.py:319-327)
  *   nolf_counters layout = RenderCounters {fs_evals, fd_evals, hit_pixels,
  *                          march_samples} (lightfield.py:113-126)
  *
@@ -157,10 +160,23 @@ int nolf_render_rect(const NolfInstance *inst, const NolfCamera *cam, int32_t x0
                      unsigned long long *counters, void *workspace, size_t ws_bytes,
                      void *stream);
 
+/* tiles: DEVICE pointer to n_tiles NolfTile (uploaded once per tiling). */
 int nolf_render_scene(const NolfInstance *inst, int32_t n_inst, const NolfCamera *cams,
                       int32_t n_cams, const NolfTile *tiles, int32_t n_tiles,
                       const NolfSceneOut *out, double alpha_vis, unsigned long long *counters,
                       void *workspace, size_t ws_bytes, void *stream);
+
+/* march_rays (lightfield.py:129-186) on object-space rays (no transform, no
+ * renormalisation), slab against the asset proxy: per-ray MarchResult
+ * fields.  Used e.g. for hit-shell collection (lightfield.py:475-512). */
+int nolf_march_rays(nolf_asset_t asset, const double *origins, int32_t origin_stride, const double *dirs,
+                    int64_t n, uint8_t *hit, double *t_hit, double *alpha_c, int64_t *samples, double *p_h,
+                    void *workspace, size_t ws_bytes, void *stream);
+
+/* Live diffuse network (hash grid + diffuse MLP, encoding.py:467-478,
+ * neural.py:89-108) at n object-space points -> (n, 4) post-activation
+ * (c_d, t); what bake_diffuse_cubes caches (lightfield.py:547-576). */
+int nolf_eval_diffuse(nolf_asset_t asset, const double *points, int64_t n, float *out, void *stream);
 
 /* frames: rgba (K, P, 4) f32, depth (K, P) f32, all device pointers. */
 int nolf_compose(int32_t K, int64_t P, const float *rgba, const float *depth, double alpha_vis,

@@ -94,6 +94,8 @@ def lib():
         "nolf_render_scene": ([C.POINTER(Instance), i32, C.POINTER(Camera), i32, vp, i32,
                                C.POINTER(SceneOut), dbl, vp, vp, C.c_size_t, vp], C.c_int),
         "nolf_compose": ([i32, i64, vp, vp, dbl, vp, vp, vp], C.c_int),
+        "nolf_march_rays": ([vp, vp, i32, vp, i64, vp, vp, vp, vp, vp, vp, C.c_size_t, vp], C.c_int),
+        "nolf_eval_diffuse": ([vp, vp, i64, vp, vp], C.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)

@@ -2,6 +2,7 @@
 // the launch sequence of the i-NOLF hot path on sm_100a.
 #include <cstdarg>
 #include <cstdio>
+#include <algorithm>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -161,6 +162,7 @@ int ensure_attrs() {
   static bool done = false;
   if (!done) {
     CUDA_TRY(cudaFuncSetAttribute(k_shade, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kShadeSmem));
+    CUDA_TRY(cudaFuncSetAttribute(k_eval_diffuse, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kShadeSmem));
     done = true;
   }
   return 0;
@@ -525,6 +527,61 @@ int nolf_render_scene(const NolfInstance *inst, int32_t n_inst, const NolfCamera
   return launch_march_shade(kModeScene, inst, n_inst, cams, n_cams, tiles, n_tiles, rect, n, out->tile_stride,
                             nullptr, 0, nullptr, nullptr, nullptr, out, alpha_vis, counters, workspace, ws_bytes,
                             static_cast<cudaStream_t>(stream));
+}
+
+int nolf_march_rays(nolf_asset_t asset, const double *origins, int32_t origin_stride, const double *dirs, int64_t n,
+                    uint8_t *hit, double *t_hit, double *alpha_c, int64_t *samples, double *p_h, void *workspace,
+                    size_t ws_bytes, void *stream) {
+  if (!asset) return fail(NOLF_EINVAL, "null asset");
+  if (n < 0 || n >= (1ll << 32)) return fail(NOLF_EINVAL, "bad ray count");
+  if (n == 0) return 0;
+  if (!origins || !dirs || !hit || !t_hit || !alpha_c || !samples || !p_h) return fail(NOLF_EINVAL, "null buffer");
+  (void)workspace;
+  (void)ws_bytes;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  ParamBlock *hp, *dp;
+  int slot, rc;
+  if ((rc = ring_acquire(&hp, &dp, &slot))) return rc;
+  memset(&hp->inst[0], 0, sizeof(DevInst));
+  hp->inst[0].a = asset->dev;
+  hp->inst[0].scale = 1.0;
+  CUDA_TRY(cudaMemcpyAsync(dp, hp, sizeof(ParamBlock), cudaMemcpyHostToDevice, st));
+  if ((rc = ring_release(slot, st))) return rc;
+  MarchArgs ma{};
+  ma.inst = dp->inst;
+  ma.n_inst = 1;
+  ma.origins = origins;
+  ma.origin_stride = origin_stride ? 1 : 0;
+  ma.dirs = dirs;
+  ma.n_rays = n;
+  ma.raw_rays = 1;
+  ma.out_hit = hit;
+  ma.out_t_hit = t_hit;
+  ma.out_alpha_c = alpha_c;
+  ma.out_samples = reinterpret_cast<long long *>(samples);
+  ma.out_p_h = p_h;
+  unsigned long long *dummy = nullptr;
+  ma.counters = dummy;
+  k_march<kModeRays><<<(unsigned)((n + 127) / 128), 128, 0, st>>>(ma);
+  CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+int nolf_eval_diffuse(nolf_asset_t asset, const double *points, int64_t n, float *out, void *stream) {
+  if (!asset) return fail(NOLF_EINVAL, "null asset");
+  if (!asset->host.fd.params || asset->host.hg_levels < 1) return fail(NOLF_ESTATE, "asset has no diffuse network");
+  if (asset->host.fd.in != asset->host.hg_levels * asset->host.hg_F)
+    return fail(NOLF_EINVAL, "diffuse MLP input width mismatch");
+  if (n < 0) return fail(NOLF_EINVAL, "negative point count");
+  if (n == 0) return 0;
+  if (!points || !out) return fail(NOLF_EINVAL, "null buffer");
+  int rc;
+  if ((rc = ensure_attrs())) return rc;
+  const long long blocks = std::min<long long>((n + kShadeThreads - 1) / kShadeThreads, (long long)num_sms() * 8);
+  k_eval_diffuse<<<(unsigned)blocks, kShadeThreads, kShadeSmem, static_cast<cudaStream_t>(stream)>>>(asset->dev, points,
+                                                                                                    n, out);
+  CUDA_TRY(cudaGetLastError());
+  return 0;
 }
 
 int nolf_compose(int32_t K, int64_t P, const float *rgba, const float *depth, double alpha_vis, float *out_rgba,

@@ -44,6 +44,11 @@ struct MarchArgs {
   float *depth;
   uint8_t *nhit;               // kModeScene: per pixel layer count
   unsigned long long *counters;
+  // march_rays mode (lightfield.py:129-186 outputs per ray, no queue)
+  int raw_rays;                // 1: rays are already in object space (no w2o, no renormalise)
+  uint8_t *out_hit;
+  double *out_t_hit, *out_alpha_c, *out_p_h;
+  long long *out_samples;
 };
 
 // Exit parameter of an axis-aligned box [lo, hi] (object coords) along the
@@ -209,15 +214,32 @@ __global__ void __launch_bounds__(128) k_march(MarchArgs args) {
     const DevAsset &A = *I.a;
     bool hit = false;
     double o[3], d[3], t_near = 0, t_far = 0;
-    MarchOut mr;
+    MarchOut mr{0.0, __longlong_as_double(0x7ff0000000000000ll), 0, false};
     if (valid) {
-      to_object(I.w2o, ow, dw, o, d);
+      if (args.raw_rays) {
+#pragma unroll
+        for (int q = 0; q < 3; ++q) { o[q] = ow[q]; d[q] = dw[q]; }
+      } else {
+        to_object(I.w2o, ow, dw, o, d);
+      }
       bool boxhit = slab(A.pmin, A.pmax, o, d, t_near, t_far);
       if (boxhit) {
         mr = march_ray(A, o, d, t_near, t_far);
         samples_total += (unsigned long long)mr.samples;
         hit = mr.hit;
       }
+    }
+    if (args.out_hit) {        // march_rays outputs (MarchResult, lightfield.py:101-110)
+      if (valid) {
+        args.out_hit[gid] = hit ? 1 : 0;
+        args.out_t_hit[gid] = mr.t_hit;
+        args.out_alpha_c[gid] = mr.alpha_c;
+        args.out_samples[gid] = mr.samples;
+#pragma unroll
+        for (int q = 0; q < 3; ++q)
+          args.out_p_h[3 * gid + q] = hit ? clamp01(__dadd_rn(o[q], __dmul_rn(mr.t_hit, d[q]))) : 0.0;
+      }
+      continue;
     }
     // warp-aggregated queue append (one atomic per warp per instance)
     const unsigned ballot = __ballot_sync(0xffffffffu, hit);
@@ -253,7 +275,7 @@ __global__ void __launch_bounds__(128) k_march(MarchArgs args) {
   // march_samples counter (lightfield.py:430-431)
 #pragma unroll
   for (int off = 16; off; off >>= 1) samples_total += __shfl_xor_sync(0xffffffffu, samples_total, off);
-  if (lane == 0 && samples_total) atomicAdd(args.counters + 3, samples_total);
+  if (lane == 0 && samples_total && args.counters) atomicAdd(args.counters + 3, samples_total);
 }
 
 // ---------------------------------------------------------------- shading
@@ -334,6 +356,8 @@ __device__ __forceinline__ void mlp_row(const float *__restrict__ P, int n_layer
     out[j] = act[j] == 0 ? z : (act[j] == 1 ? sigmoidf_np(z) : expf(z));
   }
 }
+
+__device__ __forceinline__ int hashgrid_encode_col(const DevAsset &A, const double p[3], float *xcol);
 
 __global__ void __launch_bounds__(kShadeThreads) k_shade(ShadeArgs args) {
   extern __shared__ __align__(16) float smem[];
@@ -422,32 +446,7 @@ __global__ void __launch_bounds__(kShadeThreads) k_shade(ShadeArgs args) {
       tint = dv[3];
     } else {
       // live diffuse: hash grid (encoding.py:467-478) + diffuse MLP
-      int ni = 0;
-      for (int l = 0; l < A.hg_levels; ++l) {
-        const int n = A.hg_res[l];
-        int bl[3];
-        double wl[8];
-        base_weights(rec.p, n, bl, wl);
-        double acc[4] = {0.0, 0.0, 0.0, 0.0};
-        for (int c = 0; c < 8; ++c) {
-          const int cx = c & 1, cy = (c >> 1) & 1, cz = (c >> 2) & 1;
-          long long idx;
-          if (A.hg_dense[l]) {
-            const long long side = n + 1;
-            idx = ((bl[0] * side + bl[1]) * side + bl[2]) + ((cx * side + cy) * side + cz);
-          } else {
-            // PRIMES_H0 (encoding.py:30), xor hash (encoding.py:454-459)
-            unsigned long long h = ((unsigned long long)(bl[0] + cx) * 1ull) ^
-                                   ((unsigned long long)(bl[1] + cy) * 2654435761ull) ^
-                                   ((unsigned long long)(bl[2] + cz) * 805459861ull);
-            idx = (long long)(h % A.hg_table);
-          }
-          const float *row = A.hg_feat[l] + idx * A.hg_F;
-          for (int f = 0; f < A.hg_F && f < 4; ++f)
-            acc[f] = __dadd_rn(acc[f], __dmul_rn((double)__ldg(row + f), wl[c]));
-        }
-        for (int f = 0; f < A.hg_F && f < 4; ++f) xcol[(ni++) * kShadeThreads] = (float)acc[f];
-      }
+      hashgrid_encode_col(A, rec.p, xcol);
       float dv[4];
       mlp_row(s_fd, A.fd.n_layers, A.fd.in, A.fd.act, xcol, dv);
       ++n_fd;
@@ -480,6 +479,60 @@ __global__ void __launch_bounds__(kShadeThreads) k_shade(ShadeArgs args) {
   if (lane == 0) {
     if (n_fs) { atomicAdd(args.counters + 0, n_fs); atomicAdd(args.counters + 2, n_fs); }
     if (n_fd) atomicAdd(args.counters + 1, n_fd);
+  }
+}
+
+// ---------------------------------------------------------------- live diffuse
+// Hash-grid encode (encoding.py:467-478) of one point into a per-thread smem
+// column; returns the encoded width.
+__device__ __forceinline__ int hashgrid_encode_col(const DevAsset &A, const double p[3], float *xcol) {
+  int ni = 0;
+  for (int l = 0; l < A.hg_levels; ++l) {
+    const int n = A.hg_res[l];
+    int bl[3];
+    double wl[8];
+    base_weights(p, n, bl, wl);
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int c = 0; c < 8; ++c) {
+      const int cx = c & 1, cy = (c >> 1) & 1, cz = (c >> 2) & 1;
+      long long idx;
+      if (A.hg_dense[l]) {     // dense levels (encoding.py:449-453)
+        const long long side = n + 1;
+        idx = ((bl[0] * side + bl[1]) * side + bl[2]) + ((cx * side + cy) * side + cz);
+      } else {                 // xor-prime hashed levels (encoding.py:454-459)
+        unsigned long long h = ((unsigned long long)(bl[0] + cx) * 1ull) ^
+                               ((unsigned long long)(bl[1] + cy) * 2654435761ull) ^
+                               ((unsigned long long)(bl[2] + cz) * 805459861ull);
+        idx = (long long)(h % A.hg_table);
+      }
+      const float *row = A.hg_feat[l] + idx * A.hg_F;
+      for (int f = 0; f < A.hg_F && f < 4; ++f)
+        acc[f] = __dadd_rn(acc[f], __dmul_rn((double)__ldg(row + f), wl[c]));
+    }
+    for (int f = 0; f < A.hg_F && f < 4; ++f) xcol[(ni++) * kShadeThreads] = (float)acc[f];
+  }
+  return ni;
+}
+
+// Diffuse network at arbitrary points: (c_d, t) post-activation, i.e. what
+// bake_diffuse_cubes caches (lightfield.py:547-576) and what the live path
+// returns (lightfield.py:319-327).
+__global__ void __launch_bounds__(kShadeThreads) k_eval_diffuse(const DevAsset *Ap, const double *pts, long long n,
+                                                                float *out) {
+  extern __shared__ __align__(16) float smem[];
+  float *s_fd = smem;
+  float *s_x = smem + MlpOff::total;
+  const DevAsset &A = *Ap;
+  for (int q = threadIdx.x; q < MlpOff::total; q += kShadeThreads) s_fd[q] = A.fd.params[q];
+  __syncthreads();
+  for (long long i = (long long)blockIdx.x * kShadeThreads + threadIdx.x; i < n;
+       i += (long long)gridDim.x * kShadeThreads) {
+    const double p[3] = {pts[3 * i], pts[3 * i + 1], pts[3 * i + 2]};
+    float *xcol = s_x + threadIdx.x;
+    hashgrid_encode_col(A, p, xcol);
+    float dv[4];
+    mlp_row(s_fd, A.fd.n_layers, A.fd.in, A.fd.act, xcol, dv);
+    reinterpret_cast<float4 *>(out)[i] = make_float4(dv[0], dv[1], dv[2], dv[3]);
   }
 }
 

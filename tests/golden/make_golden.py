@@ -47,6 +47,7 @@ from radfarm.encoding import _base_weights, psh_encode_with_cache, hashgrid_enco
 from radfarm.farm import compose  # noqa: E402
 from radfarm.lightfield import (  # noqa: E402
     LightFieldTrainConfig,
+    collect_hit_points,
     MarchParams,
     RenderCounters,
     ablation_variant,
@@ -268,6 +269,15 @@ def main():
 
     savez("rays_sphere.npz", rays_case(sph, rng))
     savez("rays_sphere_xform.npz", rays_case(placed(sph, m), rng))
+
+    # ---- hit shells the toy assets were built from (synth restatement pins) ----
+    sh = {}
+    for kind in ("sphere", "box", "two"):
+        a = assets[kind]
+        src = AtlasSource(a.density_atlas)
+        sh[f"{kind}_psh"] = collect_hit_points(src, a.march, n_cameras=12, image_size=16)
+        sh[f"{kind}_dif"] = collect_hit_points(src, a.march, n_cameras=8, image_size=8)
+    savez("shells.npz", sh)
 
     # ---- compose goldens (farm.py:129-172) ----
     comp = {}

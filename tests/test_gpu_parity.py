@@ -143,3 +143,16 @@ def test_mutated_mlp_is_reuploaded():
     a2.specular_mlp.biases[-1][:3] += 2.0
     t2, _ = R.render_range(a2, RayRange(cam, 0, 0, 32, 32))
     assert np.abs(t1.rgba - t2.rgba).max() > 1e-3
+
+
+def test_live_diffuse_eval_vs_reference():
+    g = load("render_live_far.npz")
+    a = case_asset("live", g)
+    import torch
+    from paper_2303_04086_b200 import _native as N
+    dev = R.device_asset(a)
+    p = torch.from_numpy(np.ascontiguousarray(g["shade_p"])).cuda()
+    out = torch.empty((len(p), 4), dtype=torch.float32, device="cuda")
+    N.check(N.lib().nolf_eval_diffuse(dev.handle, p.data_ptr(), len(p), out.data_ptr(),
+                                      R._stream_ptr()))
+    np.testing.assert_allclose(out.cpu().numpy(), g["diffuse"], rtol=0, atol=2e-6)
