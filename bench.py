@@ -1,0 +1,413 @@
+#!/usr/bin/env python
+"""i-NOLF render benchmark: BASELINE.json's metric on BASELINE config 4.
+
+Workload (config 4): a 12-asset "zodiac" scene (synthetic assets built like
+the reference builds them: analytic densities baked at b=32, r=8, PSH N=64,
+random-init networks from default_rng(i), baked diffuse atlas) rendered at
+3840x2160 from a camera at distance 4 looking at the ring centre.  One step =
+one full 4K frame: march + shade + depth-compose of all 12 assets over every
+32x32 tile, plus encode_frame's rgba8 + u16 quantisation.  With N GPUs the
+tiles are interleaved over the ranks (tile t -> rank t mod N, strong scaling)
+and the encoded tiles are gathered to rank 0 with NCCL (the frame composer).
+
+  python bench.py [--gpus N --steps K --warmup W]      # our arm
+  python bench.py --impl reference ...                  # CPU reference arm
+
+Prints ONE JSON line on rank 0.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Mrays/s and fps at 4K for multi-asset i-NOLF scene at 1/2/4/8 B200 vs CPU ref"
+UNIT = "Mrays/s"
+CACHE_DIR = os.environ.get("NOLF_BENCH_CACHE", "/tmp/nolf_bench_assets")
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=200)
+    p.add_argument("--warmup", type=int, default=10)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--width", type=int, default=3840)
+    p.add_argument("--height", type=int, default=2160)
+    p.add_argument("--assets", type=int, default=12)
+    p.add_argument("--tile", type=int, default=32)
+    p.add_argument("--mlp", default="fp32", choices=["fp32", "bf16"])
+    p.add_argument("--cpu-seconds", type=float, default=12.0)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    return p.parse_args()
+
+
+# ------------------------------------------------------------------ scene
+def build_scene(n_assets):
+    """Config-4 scene; cached as .nolf files so repeated runs on a box reuse it."""
+    from paper_2303_04086_b200 import nolf_io, synth
+    os.makedirs(CACHE_DIR, exist_ok=True)
+    cache, assets = {}, []
+    for i in range(n_assets):
+        kind = synth.ZODIAC_KINDS[i % 3]
+        path = os.path.join(CACHE_DIR, f"zodiac_{kind}_{i}_b32r8n64.nolf")
+        if os.path.exists(path):
+            a = nolf_io.read_asset(path)
+        else:
+            a = synth.make_asset(kind, seed=i, cache=cache)
+            tmp = f"{path}.{os.getpid()}.tmp"
+            nolf_io.write_asset(a, tmp)
+            os.replace(tmp, path)
+        assets.append(a)
+    return list(zip(assets, synth.zodiac_transforms(n_assets)))
+
+
+def camera_for_step(k, width, height):
+    from paper_2303_04086_b200 import synth
+    return synth.zodiac_camera(width, height, azimuth=0.3 + 0.005 * k)
+
+
+# ------------------------------------------------------------------ clocks
+class Clocks:
+    """nvidia-smi sampling of the local GPU during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []            # (host time, fields)
+        self.proc = None
+        self.window = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "20"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append((time.perf_counter(), parts))
+
+    def wait_first(self, timeout=10.0):
+        t0 = time.perf_counter()
+        while self.proc is not None and not self.rows and time.perf_counter() - t0 < timeout:
+            time.sleep(0.01)
+
+    def mark(self, t0, t1):
+        self.window = (t0, t1)
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        rows = [r for t, r in self.rows if self.window and self.window[0] <= t <= self.window[1]]
+        in_window = bool(rows)
+        if not rows and self.rows and self.window:   # timed region shorter than one sample
+            mid = 0.5 * (self.window[0] + self.window[1])
+            rows = [min(self.rows, key=lambda tr: abs(tr[0] - mid))[1]]
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        load = [v for v in sm if v > 600] or sm
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[2 + i] == "Active"})
+        return {"sm_mhz": statistics.median(load) if load else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(rows), "in_timed_window": in_window}
+
+
+# ------------------------------------------------------------------ CPU reference (oracle port)
+def cpu_sample(scene, cam, tiles, seconds, seed=0, max_tiles=None):
+    """Render + compose random 32x32 tiles with the C oracle (the reference's
+    algorithm restated, every fixed march step evaluated) on all host cores
+    until ``seconds`` elapse; returns (rays, elapsed, tiles used)."""
+    from oracle import oracle as O
+    oas = [(O.Asset(a), tr) for a, tr in scene]
+    rng = np.random.default_rng(seed)
+    order = rng.permutation(len(tiles))
+    rays, t0, used = 0, time.perf_counter(), 0
+    for t in order:
+        _, x0, y0, x1, y1 = (int(v) for v in tiles[t])
+        rg, dp = [], []
+        for oa, tr in oas:
+            r, d = O.render_rect(oa, cam, (x0, y0, x1, y1), transform=tr)
+            rg.append(r)
+            dp.append(d)
+        O.compose(np.stack(rg), np.stack(dp))
+        rays += (x1 - x0) * (y1 - y0)
+        used += 1
+        if time.perf_counter() - t0 >= seconds or (max_tiles and used >= max_tiles):
+            break
+    return rays, time.perf_counter() - t0, used
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from oracle import oracle as O
+    from paper_2303_04086_b200.render import frame_tiles
+    O.build()
+    scene = build_scene(args.assets)
+    tiles = frame_tiles(args.width, args.height, args.tile)
+    cores = os.cpu_count()
+    cam = camera_for_step(0, args.width, args.height)
+    per_step_tiles = 24
+    for w in range(args.warmup):
+        cpu_sample(scene, cam, tiles, 1e9, seed=1000 + w, max_tiles=4)
+    rays = 0
+    el = 0.0
+    for k in range(args.steps):
+        r, e, _ = cpu_sample(scene, camera_for_step(k, args.width, args.height), tiles, 1e9,
+                             seed=k, max_tiles=per_step_tiles)
+        rays += r
+        el += e
+    value = rays / el / 1e6
+    npix = args.width * args.height
+    sample = (f"{args.steps} steps x {per_step_tiles} random 32x32 tiles of the 4K frame "
+              f"(12 assets each, oracle render + compose), extrapolated to Mrays/s")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": el / args.steps * 1e3, "fps": value * 1e6 / npix,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": workload_config(args),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def workload_config(args):
+    return {"workload": (f"BASELINE config 4: {args.assets}-asset zodiac scene at "
+                         f"{args.width}x{args.height}, {args.tile}x{args.tile} ray tiles "
+                         f"interleaved over ranks, NCCL gather of rgba8+u16 to rank 0"),
+            "assets": args.assets, "width": args.width, "height": args.height,
+            "atlas_b": 32, "atlas_r": 8, "psh_resolution": 64, "mlp": args.mlp,
+            "parallelism": f"ray-tile x{args.gpus}",
+            "l2": "flushed between timed steps (256 MiB write)"}
+
+
+# ------------------------------------------------------------------ our arm
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+
+    from paper_2303_04086_b200 import _native as N
+    from paper_2303_04086_b200 import build as B
+    from paper_2303_04086_b200.render import SceneRenderer, frame_tiles, unpack_index
+    B.build()
+
+    scene = build_scene(args.assets)
+    R = SceneRenderer(scene)
+    if args.mlp == "bf16":
+        R.mlp_mode(N.MLP_BF16)
+    W, H, T = args.width, args.height, args.tile
+    stride = T * T
+    tiles = frame_tiles(W, H, T)
+    n_tiles = len(tiles)
+    n_max = math.ceil(n_tiles / world)
+    mine = tiles[rank::world]
+    pad = np.zeros((n_max - len(mine), 5), np.int32)      # empty tiles: no pixels
+    my_tiles = torch.from_numpy(np.concatenate([mine, pad]).astype(np.int32)).to(dev)
+    P = n_max * stride
+    buf = torch.empty(P * 6, dtype=torch.uint8, device=dev)   # rgba8 | depth16 (encode_frame RAW)
+    rgba8 = buf[:P * 4]
+    depth16 = buf[P * 4:]
+    out = R.alloc(n_max, stride, want_f32=False, want_u8=False)
+    out["rgba8"] = rgba8
+    out["depth16"] = depth16
+    gather = [torch.empty_like(buf) for _ in range(world)] if (world > 1 and rank == 0) else None
+    # packed (rank-major) slot of every frame pixel, for the final frame on rank 0
+    slot_of_tile = np.zeros(n_tiles, np.int64)
+    for t in range(n_tiles):
+        slot_of_tile[t] = (t % world) * n_max + t // world
+    perm_tiles = np.zeros((world * n_max, 5), np.int32)
+    perm_tiles[slot_of_tile] = tiles
+    pix_idx = torch.from_numpy(unpack_index(perm_tiles, stride, W, H)).to(dev)
+    frame = torch.empty((H * W, 4), dtype=torch.uint8, device=dev)
+    frame_d = torch.empty((H * W,), dtype=torch.int16, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    n_cam = args.warmup + args.steps + 4
+    cam_arrays = [R.camera_array([camera_for_step(k, W, H)]) for k in range(n_cam)]
+
+    def step(k):
+        R.render(cam_arrays[k % n_cam], my_tiles, n_max, stride, out)
+        if world > 1:
+            dist.gather(buf, gather, dst=0)
+        if rank == 0:
+            if world > 1:
+                rg = torch.cat([g[:P * 4] for g in gather]).view(-1, 4)
+                dp = torch.cat([g[P * 4:] for g in gather]).view(torch.int16)
+            else:
+                rg, dp = rgba8.view(-1, 4), depth16.view(torch.int16)
+            torch.index_select(rg, 0, pix_idx, out=frame)
+            torch.index_select(dp, 0, pix_idx, out=frame_d)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    clk = Clocks(local).__enter__()
+    clk.wait_first()
+    for k in range(args.warmup):
+        step(k)
+    barrier()
+    out["counters"].zero_()
+    N.check(N.lib().nolf_profile(1))
+    import ctypes
+    kms = (ctypes.c_float * 3)()
+    kern = np.zeros(3)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    barrier()
+    h0 = time.perf_counter()
+    for k in range(args.steps):
+        flush.fill_(k & 0xFF)                              # evict L2 (untimed)
+        ev[k][0].record()
+        step(args.warmup + k)
+        ev[k][1].record()
+        ev[k][1].synchronize()
+        N.check(N.lib().nolf_profile_read(kms))
+        kern += np.array(kms[:3], dtype=np.float64)
+    barrier()
+    clk.mark(h0, time.perf_counter())
+    clk.__exit__()
+    N.check(N.lib().nolf_profile(0))
+    t_local = sum(a.elapsed_time(b) for a, b in ev) / 1e3
+    t = torch.tensor([t_local], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    t_max = float(t.item())
+    cnt = out["counters"].cpu().numpy().astype(np.float64) / args.steps
+    npix = W * H
+    value = args.steps * npix / t_max / 1e6
+
+    # ---- end to end: camera in (H2D param block), encoded frame out (D2H) to pinned host
+    e2e = None
+    if not args.no_e2e:
+        host = torch.empty((H * W * 6,), dtype=torch.uint8, pin_memory=True)
+        host_rgba = host[:H * W * 4].view(H * W, 4)
+        host_d = host[H * W * 4:].view(torch.int16)
+        for k in range(2):
+            step(k)
+        barrier()
+        e_ev = []
+        for k in range(args.steps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            step(k)
+            if rank == 0:
+                host_rgba.copy_(frame, non_blocking=True)
+                host_d.copy_(frame_d, non_blocking=True)
+            b.record()
+            b.synchronize()
+            e_ev.append((a, b))
+        barrier()
+        te = torch.tensor([sum(a.elapsed_time(b) for a, b in e_ev) / 1e3], dtype=torch.float64,
+                          device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": args.steps * npix / float(te.item()) / 1e6, "unit": UNIT,
+               "h2d_bytes_per_step": int(N.lib().nolf_launch_param_bytes()),
+               "d2h_bytes_per_step": int(npix * 6)}
+
+    # ---- roofline of the dominant kernel (per-launch algorithmic bytes / event time)
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except OSError:
+        pass
+    hbm = float(peaks.get("hbm_gbs", 6650.0))
+    names = ["k_march", "k_shade", "k_compose"]
+    ms = kern / args.steps
+    S, Hh = cnt[3], cnt[2]
+    npx = n_max * stride
+    alg = {"k_march": 36.0 * S + 80.0 * Hh,
+           "k_shade": (80.0 + 228.0 + 20.0) * Hh,
+           "k_compose": 20.0 * Hh + 7.0 * npx}
+    top = names[int(np.argmax(ms))]
+    ach = alg[top] / (ms[names.index(top)] / 1e3) / 1e9
+    roof = {"bound": "hbm", "kernel": top, "achieved": ach, "peak": hbm, "unit": "GB/s",
+            "frac": ach / hbm, "traffic": None,
+            "algorithmic_bytes_per_launch": alg[top],
+            "kernel_ms": dict(zip(names, [float(x) for x in ms])),
+            "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            rays, el, used = cpu_sample(scene, camera_for_step(0, W, H), tiles, args.cpu_seconds)
+            cpu = {"value": rays / el / 1e6, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
+                   "sample": f"{used} random 32x32 tiles of the 4K frame, 12 assets each, oracle "
+                             f"render + compose on {os.cpu_count()} OpenMP threads, "
+                             f"{el:.1f} s, extrapolated"}
+        except Exception as e:  # noqa: BLE001
+            cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
+                   "sample": f"failed: {e}"}
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t_max / args.steps * 1e3,
+            "fps": args.steps / t_max, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference-pipeline assets, "
+            "random-init networks)", "config": workload_config(args),
+            "e2e": e2e, "gpu_launches": 3 * args.steps, "roofline": roof, "cpu_baseline": cpu,
+            "clocks": clk.summary(),
+            "per_frame": {"march_samples": S, "hits": Hh, "pixels": npix},
+        }
+        line["config"]["parallelism"] = f"ray-tile x{world}"
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

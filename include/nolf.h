@@ -178,6 +178,14 @@ int nolf_march_rays(nolf_asset_t asset, const double *origins, int32_t origin_st
  * (c_d, t); what bake_diffuse_cubes caches (lightfield.py:547-576). */
 int nolf_eval_diffuse(nolf_asset_t asset, const double *points, int64_t n, float *out, void *stream);
 
+/* Per-kernel timing of the calling thread's most recent render call: CUDA
+ * events on the launching stream around k_march, k_shade, k_compose.
+ * nolf_profile_read synchronises and returns 3 durations in ms. */
+int nolf_profile(int enable);
+int nolf_profile_read(float *ms);
+/* Host->device bytes every render call copies (instance + camera table). */
+size_t nolf_launch_param_bytes(void);
+
 /* frames: rgba (K, P, 4) f32, depth (K, P) f32, all device pointers. */
 int nolf_compose(int32_t K, int64_t P, const float *rgba, const float *depth, double alpha_vis,
                  float *out_rgba, float *out_depth, void *stream);

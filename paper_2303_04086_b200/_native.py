@@ -96,6 +96,9 @@ def lib():
         "nolf_compose": ([i32, i64, vp, vp, dbl, vp, vp, vp], C.c_int),
         "nolf_march_rays": ([vp, vp, i32, vp, i64, vp, vp, vp, vp, vp, vp, C.c_size_t, vp], C.c_int),
         "nolf_eval_diffuse": ([vp, vp, i64, vp, vp], C.c_int),
+        "nolf_profile": ([C.c_int], C.c_int),
+        "nolf_profile_read": ([C.POINTER(C.c_float)], C.c_int),
+        "nolf_launch_param_bytes": ([], C.c_size_t),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)

@@ -406,6 +406,21 @@ int ring_release(int slot, cudaStream_t st) {
   return 0;
 }
 
+// Optional per-kernel timing: CUDA events recorded on the launching stream
+// around k_march / k_shade / k_compose of the most recent render call.
+struct Prof {
+  bool on = false;
+  bool created = false;
+  cudaEvent_t ev[4];
+};
+thread_local Prof g_prof;
+
+int prof_mark(int i, cudaStream_t st) {
+  if (!g_prof.on) return 0;
+  CUDA_TRY(cudaEventRecord(g_prof.ev[i], st));
+  return 0;
+}
+
 int launch_march_shade(int mode, const NolfInstance *ins, int n_inst, const NolfCamera *cams, int n_cams,
                        const NolfTile *tiles_dev, int n_tiles, TileParams rect, long long n_rays,
                        long long tile_stride, const double *origins, int origin_stride, const double *dirs,
@@ -458,12 +473,15 @@ int launch_march_shade(int mode, const NolfInstance *ins, int n_inst, const Nolf
   ma.nhit = w.nhit;
   ma.counters = counters;
   const unsigned grid = (unsigned)((n_rays + 127) / 128);
+  if ((rc = prof_mark(0, st))) return rc;
   if (mode == kModeRays) k_march<kModeRays><<<grid, 128, 0, st>>>(ma);
   else if (mode == kModeRect) k_march<kModeRect><<<grid, 128, 0, st>>>(ma);
   else k_march<kModeScene><<<grid, 128, 0, st>>>(ma);
   CUDA_TRY(cudaGetLastError());
+  if ((rc = prof_mark(1, st))) return rc;
   if (mode == kModeScene) {
     if ((rc = run_shade(dp->inst, n_inst, w, mode, w.lrgba, w.ldepth, (long long)w.cap, counters, st))) return rc;
+    if ((rc = prof_mark(2, st))) return rc;
     ComposeArgs ca{};
     ca.n_pix = n_rays;
     ca.nhit = w.nhit;
@@ -481,8 +499,11 @@ int launch_march_shade(int mode, const NolfInstance *ins, int n_inst, const Nolf
     ca.depth_far = (float)sout->depth_far;
     k_compose<<<(unsigned)((n_rays + 255) / 256), 256, 0, st>>>(ca);
     CUDA_TRY(cudaGetLastError());
+    if ((rc = prof_mark(3, st))) return rc;
   } else {
     if ((rc = run_shade(dp->inst, n_inst, w, mode, rgba, depth, 0, counters, st))) return rc;
+    if ((rc = prof_mark(2, st))) return rc;
+    if ((rc = prof_mark(3, st))) return rc;
   }
   return 0;
 }
@@ -583,6 +604,24 @@ int nolf_eval_diffuse(nolf_asset_t asset, const double *points, int64_t n, float
   CUDA_TRY(cudaGetLastError());
   return 0;
 }
+
+int nolf_profile(int enable) {
+  if (enable && !g_prof.created) {
+    for (int i = 0; i < 4; ++i) CUDA_TRY(cudaEventCreate(&g_prof.ev[i]));
+    g_prof.created = true;
+  }
+  g_prof.on = enable != 0;
+  return 0;
+}
+
+int nolf_profile_read(float *ms) {
+  if (!g_prof.created) return fail(NOLF_ESTATE, "profiling was never enabled");
+  CUDA_TRY(cudaEventSynchronize(g_prof.ev[3]));
+  for (int i = 0; i < 3; ++i) CUDA_TRY(cudaEventElapsedTime(ms + i, g_prof.ev[i], g_prof.ev[i + 1]));
+  return 0;
+}
+
+size_t nolf_launch_param_bytes(void) { return sizeof(ParamBlock); }
 
 int nolf_compose(int32_t K, int64_t P, const float *rgba, const float *depth, double alpha_vis, float *out_rgba,
                  float *out_depth, void *stream) {

@@ -202,7 +202,7 @@ __global__ void __launch_bounds__(128) k_march(MarchArgs args) {
         ow[0] = cp.pose[3]; ow[1] = cp.pose[7]; ow[2] = cp.pose[11];
       }
     }
-    if (MODE != kModeScene && valid) {   // miss defaults (lightfield.py:415-416)
+    if (MODE != kModeScene && valid && args.rgba) {   // miss defaults (lightfield.py:415-416)
       reinterpret_cast<float4 *>(args.rgba)[gid] = make_float4(0.f, 0.f, 0.f, 0.f);
       args.depth[gid] = __int_as_float(0x7f800000);
     }

@@ -320,10 +320,15 @@ class SceneRenderer:
             self._ws = t.empty(need, dtype=t.uint8, device=self.device)
         return out
 
-    def render(self, cameras, tiles_dev, n_tiles: int, tile_stride: int, out: dict, stream=None):
+    @staticmethod
+    def camera_array(cameras):
         cams = (N.Camera * len(cameras))()
         for i, c in enumerate(cameras):
             cams[i] = N.camera_struct(c)
+        return cams
+
+    def render(self, cameras, tiles_dev, n_tiles: int, tile_stride: int, out: dict, stream=None):
+        cams = cameras if isinstance(cameras, C.Array) else self.camera_array(cameras)
         so = N.SceneOut()
         so.rgba = out["rgba"].data_ptr() if "rgba" in out else None
         so.depth = out["depth"].data_ptr() if "depth" in out else None
