@@ -253,33 +253,31 @@ def run_ours(args):
     out = R.alloc(n_max, stride, want_f32=False, want_u8=False)
     out["rgba8"] = rgba8
     out["depth16"] = depth16
-    gather = [torch.empty_like(buf) for _ in range(world)] if (world > 1 and rank == 0) else None
-    # packed (rank-major) slot of every frame pixel, for the final frame on rank 0
-    slot_of_tile = np.zeros(n_tiles, np.int64)
+    gathered = torch.empty(world * P * 6, dtype=torch.uint8, device=dev) if world > 1 else None
+    # tile of every (rank, slot) in rank-major gather order, for frame assembly
+    slot_tiles = np.zeros((world * n_max, 5), np.int32)
     for t in range(n_tiles):
-        slot_of_tile[t] = (t % world) * n_max + t // world
-    perm_tiles = np.zeros((world * n_max, 5), np.int32)
-    perm_tiles[slot_of_tile] = tiles
-    pix_idx = torch.from_numpy(unpack_index(perm_tiles, stride, W, H)).to(dev)
+        slot_tiles[(t % world) * n_max + t // world] = tiles[t]
+    slot_tiles_dev = torch.from_numpy(slot_tiles).to(dev)
     frame = torch.empty((H * W, 4), dtype=torch.uint8, device=dev)
     frame_d = torch.empty((H * W,), dtype=torch.int16, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
-
     n_cam = args.warmup + args.steps + 4
     cam_arrays = [R.camera_array([camera_for_step(k, W, H)]) for k in range(n_cam)]
+    if world == 1:                 # single GPU: compose writes the frame directly
+        out["rgba8"], out["depth16"] = frame, frame_d
+    stream = torch.cuda.current_stream().cuda_stream
 
     def step(k):
-        R.render(cam_arrays[k % n_cam], my_tiles, n_max, stride, out)
+        R.render(cam_arrays[k % n_cam], my_tiles, n_max, stride, out, frame_layout=(world == 1))
         if world > 1:
-            dist.gather(buf, gather, dst=0)
-        if rank == 0:
-            if world > 1:
-                rg = torch.cat([g[:P * 4] for g in gather]).view(-1, 4)
-                dp = torch.cat([g[P * 4:] for g in gather]).view(torch.int16)
-            else:
-                rg, dp = rgba8.view(-1, 4), depth16.view(torch.int16)
-            torch.index_select(rg, 0, pix_idx, out=frame)
-            torch.index_select(dp, 0, pix_idx, out=frame_d)
+            # frame composer: NCCL gather of every rank's encoded tiles, then
+            # one unpack kernel writes the row-major frame on rank 0
+            dist.gather(buf, list(gathered.chunk(world)) if rank == 0 else None, dst=0)
+            if rank == 0:
+                N.check(N.lib().nolf_unpack_gathered(gathered.data_ptr(), world, n_max, stride,
+                                                     slot_tiles_dev.data_ptr(), W, H,
+                                                     frame.data_ptr(), frame_d.data_ptr(), stream))
 
     def barrier():
         if world > 1:
@@ -347,7 +345,7 @@ def run_ours(args):
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e2e = {"value": args.steps * npix / float(te.item()) / 1e6, "unit": UNIT,
-               "h2d_bytes_per_step": int(N.lib().nolf_launch_param_bytes()),
+               "h2d_bytes_per_step": int(N.lib().nolf_launch_param_bytes(args.assets, 1)),
                "d2h_bytes_per_step": int(npix * 6)}
 
     # ---- roofline of the dominant kernel (per-launch algorithmic bytes / event time)
@@ -390,7 +388,7 @@ def run_ours(args):
             "fps": args.steps / t_max, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference-pipeline assets, "
             "random-init networks)", "config": workload_config(args),
-            "e2e": e2e, "gpu_launches": 3 * args.steps, "roofline": roof, "cpu_baseline": cpu,
+            "e2e": e2e, "gpu_launches": (3 + (1 if world > 1 else 0)) * args.steps, "roofline": roof, "cpu_baseline": cpu,
             "clocks": clk.summary(),
             "per_frame": {"march_samples": S, "hits": Hh, "pixels": npix},
         }

@@ -126,9 +126,10 @@ typedef struct NolfTile {              /* RayRange rect of one camera */
     int32_t cam, x0, y0, x1, y1;
 } NolfTile;
 
-/* Scene output.  Pixels are written in TILE-PACKED order: tile t (in the
+/* Scene output.  layout 0 writes pixels in TILE-PACKED order: tile t (in the
  * order given) owns pixels [t*tile_stride, t*tile_stride + w_t*h_t), row-major
- * inside the tile.  Any pointer may be NULL to skip that output. */
+ * inside the tile (the unit the multi-GPU gather moves); layout 1 writes the
+ * row-major frame of each camera.  Any pointer may be NULL to skip it. */
 typedef struct NolfSceneOut {
     float *rgba;                       /* (.., 4) f32, farm.compose Frame.rgba */
     float *depth;                      /* f32, inf = miss */
@@ -136,6 +137,8 @@ typedef struct NolfSceneOut {
     uint16_t *depth16;                 /* protocol.encode_frame RAW depth u16 */
     int64_t tile_stride;               /* pixels per tile slot (>= max w*h) */
     double depth_far;                  /* encode_frame far plane */
+    int32_t layout;                    /* 0: tile-packed (above); 1: row-major frame per
+                                          camera, cameras concatenated in order */
 } NolfSceneOut;
 
 int nolf_abi_version(void);
@@ -183,8 +186,16 @@ int nolf_eval_diffuse(nolf_asset_t asset, const double *points, int64_t n, float
  * nolf_profile_read synchronises and returns 3 durations in ms. */
 int nolf_profile(int enable);
 int nolf_profile_read(float *ms);
-/* Host->device bytes every render call copies (instance + camera table). */
-size_t nolf_launch_param_bytes(void);
+/* Host->device bytes a render call copies (instance, camera, cull tables). */
+size_t nolf_launch_param_bytes(int32_t n_inst, int32_t n_cams);
+
+/* Frame assembly after gathering every rank's tile-packed encode_frame
+ * output (rank r: n_per_rank slots of rgba8, then their depth16) into one
+ * buffer: slot_tiles (DEVICE, world*n_per_rank, rank-major) gives each slot's
+ * tile; writes the row-major rgba8 (H,W,4) and depth16 (H,W) frame. */
+int nolf_unpack_gathered(const uint8_t *gathered, int32_t world, int32_t n_per_rank, int64_t tile_stride,
+                         const NolfTile *slot_tiles, int32_t width, int32_t height, uint8_t *rgba8,
+                         uint16_t *depth16, void *stream);
 
 /* frames: rgba (K, P, 4) f32, depth (K, P) f32, all device pointers. */
 int nolf_compose(int32_t K, int64_t P, const float *rgba, const float *depth, double alpha_vis,

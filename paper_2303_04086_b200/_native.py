@@ -63,7 +63,8 @@ class Camera(C.Structure):
 
 class SceneOut(C.Structure):
     _fields_ = [("rgba", C.c_void_p), ("depth", C.c_void_p), ("rgba8", C.c_void_p),
-                ("depth16", C.c_void_p), ("tile_stride", C.c_int64), ("depth_far", C.c_double)]
+                ("depth16", C.c_void_p), ("tile_stride", C.c_int64), ("depth_far", C.c_double),
+                ("layout", C.c_int32)]
 
 
 _lib = None
@@ -98,7 +99,8 @@ def lib():
         "nolf_eval_diffuse": ([vp, vp, i64, vp, vp], C.c_int),
         "nolf_profile": ([C.c_int], C.c_int),
         "nolf_profile_read": ([C.POINTER(C.c_float)], C.c_int),
-        "nolf_launch_param_bytes": ([], C.c_size_t),
+        "nolf_launch_param_bytes": ([i32, i32], C.c_size_t),
+        "nolf_unpack_gathered": ([vp, i32, i32, i64, vp, i32, i32, vp, vp, vp], C.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)

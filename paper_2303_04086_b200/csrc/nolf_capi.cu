@@ -3,6 +3,8 @@
 #include <cstdarg>
 #include <cstdio>
 #include <algorithm>
+#include <cmath>
+#include <cstddef>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -223,7 +225,59 @@ struct ParamBlock {
   DevInst inst[kMaxInst];
   CamParams cams[kMaxCams];
   TileParams rect;
+  ScreenBox cull[kMaxInst * kMaxCams];   // only the used prefix is copied
 };
+
+size_t param_bytes(int n_inst, int n_cams) {
+  return offsetof(ParamBlock, cull) + sizeof(ScreenBox) * (size_t)n_inst * (size_t)(n_cams > 0 ? n_cams : 1);
+}
+
+// Conservative image rectangle of an instance's proxy box for one camera.
+// All 8 world corners strictly in front of the camera: the projection of the
+// (convex) box is the hull of the projected corners, so pixels outside their
+// bounding rectangle (plus a 2-pixel margin for rounding) cannot hit it.
+// Corners behind/on the camera plane: no culling (or none visible when all
+// are behind, since every pixel ray goes forward from the camera).
+ScreenBox screen_box(const NolfInstance &in, const DevAsset &H, const CamParams &c) {
+  const ScreenBox full{-(1 << 29), -(1 << 29), 1 << 29, 1 << 29};
+  const double *w = in.w2o;
+  const double a00 = w[0], a01 = w[1], a02 = w[2], a10 = w[4], a11 = w[5], a12 = w[6], a20 = w[8], a21 = w[9],
+               a22 = w[10];
+  const double det = a00 * (a11 * a22 - a12 * a21) - a01 * (a10 * a22 - a12 * a20) + a02 * (a10 * a21 - a11 * a20);
+  if (!(det != 0.0) || det != det) return full;
+  const double id = 1.0 / det;
+  const double Ai[9] = {(a11 * a22 - a12 * a21) * id, (a02 * a21 - a01 * a22) * id, (a01 * a12 - a02 * a11) * id,
+                        (a12 * a20 - a10 * a22) * id, (a00 * a22 - a02 * a20) * id, (a02 * a10 - a00 * a12) * id,
+                        (a10 * a21 - a11 * a20) * id, (a01 * a20 - a00 * a21) * id, (a00 * a11 - a01 * a10) * id};
+  double xmin = 1e300, xmax = -1e300, ymin = 1e300, ymax = -1e300;
+  int behind = 0, near = 0;
+  for (int cnr = 0; cnr < 8; ++cnr) {
+    const double po[3] = {(cnr & 1) ? H.pmax[0] : H.pmin[0], (cnr & 2) ? H.pmax[1] : H.pmin[1],
+                          (cnr & 4) ? H.pmax[2] : H.pmin[2]};
+    const double q[3] = {po[0] - w[3], po[1] - w[7], po[2] - w[11]};
+    double pw[3];
+    for (int r = 0; r < 3; ++r) pw[r] = Ai[3 * r] * q[0] + Ai[3 * r + 1] * q[1] + Ai[3 * r + 2] * q[2];
+    const double v[3] = {pw[0] - c.pose[3], pw[1] - c.pose[7], pw[2] - c.pose[11]};
+    double cc[3];
+    for (int j = 0; j < 3; ++j) cc[j] = c.pose[j] * v[0] + c.pose[4 + j] * v[1] + c.pose[8 + j] * v[2];
+    const double depth = -cc[2];
+    const double vn = fabs(v[0]) + fabs(v[1]) + fabs(v[2]);
+    if (depth <= 1e-7 * (1.0 + vn)) {
+      ++near;
+      if (depth < 0.0) ++behind;
+      continue;
+    }
+    const double px = cc[0] / depth * c.fx + c.cx - 0.5;
+    const double py = -cc[1] / depth * c.fy + c.cy - 0.5;
+    xmin = fmin(xmin, px); xmax = fmax(xmax, px);
+    ymin = fmin(ymin, py); ymax = fmax(ymax, py);
+  }
+  if (behind == 8) return ScreenBox{1, 1, 0, 0};
+  if (near) return full;
+  auto clampi64 = [](double v) { return v < -(1 << 29) ? -(1 << 29) : (v > (1 << 29) ? (1 << 29) : (int)v); };
+  return ScreenBox{clampi64(floor(xmin) - 2), clampi64(floor(ymin) - 2), clampi64(ceil(xmax) + 2),
+                   clampi64(ceil(ymax) + 2)};
+}
 }  // namespace
 
 extern "C" {
@@ -441,6 +495,7 @@ int launch_march_shade(int mode, const NolfInstance *ins, int n_inst, const Nolf
   if ((rc = ring_acquire(&hp, &dp, &slot))) return rc;
   for (int k = 0; k < n_inst; ++k)
     if ((rc = fill_inst(ins + k, hp->inst + k))) return rc;
+  long long pix_base = 0;
   for (int c = 0; c < n_cams; ++c) {
     const NolfCamera &C = cams[c];
     for (int q = 0; q < 16; ++q) hp->cams[c].pose[q] = C.pose[q];
@@ -448,9 +503,15 @@ int launch_march_shade(int mode, const NolfInstance *ins, int n_inst, const Nolf
     hp->cams[c].fy = C.fy;
     hp->cams[c].cx = C.cx;
     hp->cams[c].cy = C.cy;
+    hp->cams[c].width = C.width;
+    hp->cams[c].height = C.height;
+    hp->cams[c].pix_base = pix_base;
+    pix_base += (long long)C.width * C.height;
   }
   hp->rect = rect;
-  CUDA_TRY(cudaMemcpyAsync(dp, hp, sizeof(ParamBlock), cudaMemcpyHostToDevice, st));
+  for (int k = 0; k < n_inst && n_cams > 0; ++k)
+    for (int c = 0; c < n_cams; ++c) hp->cull[k * n_cams + c] = screen_box(ins[k], ins[k].asset->host, hp->cams[c]);
+  CUDA_TRY(cudaMemcpyAsync(dp, hp, param_bytes(n_inst, n_cams), cudaMemcpyHostToDevice, st));
   if ((rc = ring_release(slot, st))) return rc;
   if (n_rays == 0) return 0;
   CUDA_TRY(cudaMemsetAsync(w.counts, 0, sizeof(unsigned) * n_inst, st));
@@ -465,6 +526,8 @@ int launch_march_shade(int mode, const NolfInstance *ins, int n_inst, const Nolf
   ma.cams = dp->cams;
   ma.tiles = mode == kModeScene ? reinterpret_cast<const TileParams *>(tiles_dev) : &dp->rect;
   ma.tile_stride = tile_stride;
+  ma.cull = n_cams > 0 ? dp->cull : nullptr;
+  ma.n_cams = n_cams > 0 ? n_cams : 1;
   ma.queue = w.queue;
   ma.cap = w.cap;
   ma.counts = w.counts;
@@ -491,6 +554,8 @@ int launch_march_shade(int mode, const NolfInstance *ins, int n_inst, const Nolf
     ca.layer_stride = w.cap;
     ca.tiles = reinterpret_cast<const TileParams *>(tiles_dev);
     ca.tile_stride = tile_stride;
+    ca.cams = dp->cams;
+    ca.frame_layout = sout->layout;
     ca.alpha_vis = (float)alpha_vis;
     ca.out_rgba = sout->rgba;
     ca.out_depth = sout->depth;
@@ -566,7 +631,7 @@ int nolf_march_rays(nolf_asset_t asset, const double *origins, int32_t origin_st
   memset(&hp->inst[0], 0, sizeof(DevInst));
   hp->inst[0].a = asset->dev;
   hp->inst[0].scale = 1.0;
-  CUDA_TRY(cudaMemcpyAsync(dp, hp, sizeof(ParamBlock), cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemcpyAsync(dp, hp, param_bytes(1, 0), cudaMemcpyHostToDevice, st));
   if ((rc = ring_release(slot, st))) return rc;
   MarchArgs ma{};
   ma.inst = dp->inst;
@@ -621,7 +686,24 @@ int nolf_profile_read(float *ms) {
   return 0;
 }
 
-size_t nolf_launch_param_bytes(void) { return sizeof(ParamBlock); }
+size_t nolf_launch_param_bytes(int32_t n_inst, int32_t n_cams) { return param_bytes(n_inst, n_cams); }
+
+int nolf_unpack_gathered(const uint8_t *gathered, int32_t world, int32_t n_per_rank, int64_t tile_stride,
+                         const NolfTile *slot_tiles, int32_t width, int32_t height, uint8_t *rgba8, uint16_t *depth16,
+                         void *stream) {
+  if (world < 1 || n_per_rank < 0 || tile_stride < 1 || width < 1 || height < 1)
+    return fail(NOLF_EINVAL, "bad unpack geometry");
+  const long long n_slots = (long long)world * n_per_rank;
+  const long long n = n_slots * tile_stride;
+  if (n == 0) return 0;
+  if (!gathered || !slot_tiles || !rgba8 || !depth16) return fail(NOLF_EINVAL, "null buffer");
+  const long long rank_bytes = (long long)n_per_rank * tile_stride * 6;
+  k_unpack<<<(unsigned)((n + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      gathered, rank_bytes, n_per_rank, tile_stride, reinterpret_cast<const TileParams *>(slot_tiles), n_slots,
+      width, reinterpret_cast<uchar4 *>(rgba8), depth16);
+  CUDA_TRY(cudaGetLastError());
+  return 0;
+}
 
 int nolf_compose(int32_t K, int64_t P, const float *rgba, const float *depth, double alpha_vis, float *out_rgba,
                  float *out_depth, void *stream) {

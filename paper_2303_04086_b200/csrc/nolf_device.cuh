@@ -138,29 +138,38 @@ __device__ __forceinline__ void to_object(const double *w2o12, const double ow[3
 }
 
 // aabb_intersect_batch (core.py:206-223), t_min = 0, t_max = inf.
+// numpy's minimum/maximum propagate NaN; a NaN slab value can only come from
+// 0*inf (d subnormal, o on a face) and makes t_near/t_far NaN, i.e. a miss.
+// Tracking it with one flag instead of NaN-aware selects is observably
+// identical (every non-NaN value is computed with the same comparisons).
+// inv[] returns 1/d (inf for d == 0) for reuse by the march.
 __device__ __forceinline__ bool slab(const double pmin[3], const double pmax[3], const double o[3],
-                                     const double d[3], double &t_near, double &t_far) {
+                                     const double d[3], double &t_near, double &t_far, double inv[3]) {
   const double INF = __longlong_as_double(0x7ff0000000000000ll);
   double lo_max = 0, hi_min = 0;
+  bool nan = false;
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
     double lo, hi;
     if (d[k] == 0.0) {
-      bool inside = (o[k] >= pmin[k]) && (o[k] <= pmax[k]);
+      const bool inside = (o[k] >= pmin[k]) && (o[k] <= pmax[k]);
       lo = inside ? -INF : INF;
       hi = inside ? INF : -INF;
+      inv[k] = INF;
     } else {
-      double inv = __ddiv_rn(1.0, d[k]);
-      double t0 = __dmul_rn(__dsub_rn(pmin[k], o[k]), inv);
-      double t1 = __dmul_rn(__dsub_rn(pmax[k], o[k]), inv);
-      lo = np_min(t0, t1);
-      hi = np_max(t0, t1);
+      inv[k] = __ddiv_rn(1.0, d[k]);
+      const double t0 = __dmul_rn(__dsub_rn(pmin[k], o[k]), inv[k]);
+      const double t1 = __dmul_rn(__dsub_rn(pmax[k], o[k]), inv[k]);
+      nan |= (t0 != t0) | (t1 != t1);
+      lo = t0 < t1 ? t0 : t1;
+      hi = t0 > t1 ? t0 : t1;
     }
     if (k == 0) { lo_max = lo; hi_min = hi; }
-    else { lo_max = np_max(lo_max, lo); hi_min = np_min(hi_min, hi); }
+    else { lo_max = lo_max > lo ? lo_max : lo; hi_min = hi_min < hi ? hi_min : hi; }
   }
-  t_near = np_max(lo_max, 0.0);
-  t_far = np_min(hi_min, INF);
+  t_near = lo_max > 0.0 ? lo_max : 0.0;
+  t_far = hi_min < INF ? hi_min : INF;
+  if (nan) t_near = t_far = __longlong_as_double(0x7ff8000000000000ll);
   return t_near <= t_far;
 }
 

@@ -21,7 +21,14 @@ enum RayMode { kModeRays = 0, kModeRect = 1, kModeScene = 2 };
 struct CamParams {             // NolfCamera with pose rows
   double pose[16];
   double fx, fy, cx, cy;
+  int width, height;
+  long long pix_base;          // frame-layout output offset of this camera
 };
+
+// Conservative screen rectangle (inclusive pixel indices) outside which a
+// pixel's ray cannot meet an instance's proxy box: the box lies in front of
+// the camera, so its image is the convex hull of its projected corners.
+struct ScreenBox { int x0, y0, x1, y1; };
 
 struct TileParams { int cam, x0, y0, x1, y1; };
 
@@ -36,6 +43,8 @@ struct MarchArgs {
   const CamParams *cams;       // kModeRect / kModeScene (device)
   const TileParams *tiles;     // kModeScene (device) ; kModeRect: tiles[0] is the rect
   long long tile_stride;       // kModeScene: pixel slots per tile
+  const ScreenBox *cull;       // [n_inst * n_cams] (NULL: no culling)
+  int n_cams;
   // outputs
   HitRec *queue;               // n_inst * cap records
   long long cap;               // per-instance capacity
@@ -54,14 +63,15 @@ struct MarchArgs {
 // Exit parameter of an axis-aligned box [lo, hi] (object coords) along the
 // ray, with faces on the unit-cube boundary pushed to infinity because march
 // positions are clipped to [0,1] (lightfield.py:166).
-__device__ __forceinline__ double box_exit(const double o[3], const double d[3], const double lo[3],
-                                           const double hi[3]) {
+// (An estimate only: the skip target is verified exactly, so 1/d is fine.)
+__device__ __forceinline__ double box_exit(const double o[3], const double d[3], const double inv[3],
+                                           const double lo[3], const double hi[3]) {
   const double INF = __longlong_as_double(0x7ff0000000000000ll);
   double t = INF;
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
-    if (d[k] > 0.0 && hi[k] < 1.0) t = fmin(t, (hi[k] - o[k]) / d[k]);
-    else if (d[k] < 0.0 && lo[k] > 0.0) t = fmin(t, (lo[k] - o[k]) / d[k]);
+    if (d[k] > 0.0 && hi[k] < 1.0) t = fmin(t, (hi[k] - o[k]) * inv[k]);
+    else if (d[k] < 0.0 && lo[k] > 0.0) t = fmin(t, (lo[k] - o[k]) * inv[k]);
   }
   return t;
 }
@@ -98,7 +108,7 @@ struct MarchOut {
 };
 
 __device__ __forceinline__ MarchOut march_ray(const DevAsset &A, const double o[3], const double d[3],
-                                              double t_near, double t_far) {
+                                              const double inv[3], double t_near, double t_far) {
   MarchOut r;
   r.alpha_c = 0.0;
   r.t_hit = __longlong_as_double(0x7ff0000000000000ll);
@@ -141,7 +151,7 @@ __device__ __forceinline__ MarchOut march_ray(const DevAsset &A, const double o[
         lo[k] = lo_c[k] * inv_b;
         hi[k] = (hi_c[k] + 1) * inv_b;
       }
-      double te = box_exit(o, d, lo, hi);
+      double te = box_exit(o, d, inv, lo, hi);
       double tl = fmin(te, t_far);
       double jf = floor((tl - t_near) / delta - 0.5);
       long long j = jf > 9.0e15 ? (long long)9.0e15 : (long long)jf;
@@ -183,6 +193,7 @@ __global__ void __launch_bounds__(128) k_march(MarchArgs args) {
   const unsigned lane = threadIdx.x & 31;
   bool valid = gid < args.n_rays;
   double ow[3] = {0, 0, 0}, dw[3] = {0, 0, 1};
+  int pix_x = 0, pix_y = 0, cam = 0;
   if (valid) {
     if (MODE == kModeRays) {
       const double *op = args.origins + (args.origin_stride ? 3 * gid : 0);
@@ -197,7 +208,10 @@ __global__ void __launch_bounds__(128) k_march(MarchArgs args) {
         valid = false;
       } else {
         const CamParams &cp = args.cams[tp.cam];
-        double px = (double)(tp.x0 + (int)(local % w)), py = (double)(tp.y0 + (int)(local / w));
+        cam = tp.cam;
+        pix_x = tp.x0 + (int)(local % w);
+        pix_y = tp.y0 + (int)(local / w);
+        double px = (double)pix_x, py = (double)pix_y;
         camera_dir(cp.pose, cp.fx, cp.fy, cp.cx, cp.cy, px, py, dw);
         ow[0] = cp.pose[3]; ow[1] = cp.pose[7]; ow[2] = cp.pose[11];
       }
@@ -213,24 +227,29 @@ __global__ void __launch_bounds__(128) k_march(MarchArgs args) {
     const DevInst &I = args.inst[k];
     const DevAsset &A = *I.a;
     bool hit = false;
-    double o[3], d[3], t_near = 0, t_far = 0;
+    double o[3], d[3], inv[3], t_near = 0, t_far = 0;
     MarchOut mr{0.0, __longlong_as_double(0x7ff0000000000000ll), 0, false};
-    if (valid) {
+    bool live = valid;
+    if (MODE != kModeRays && live && args.cull) {
+      const ScreenBox bb = args.cull[k * args.n_cams + cam];
+      live = pix_x >= bb.x0 && pix_x <= bb.x1 && pix_y >= bb.y0 && pix_y <= bb.y1;
+    }
+    if (live) {
       if (args.raw_rays) {
 #pragma unroll
         for (int q = 0; q < 3; ++q) { o[q] = ow[q]; d[q] = dw[q]; }
       } else {
         to_object(I.w2o, ow, dw, o, d);
       }
-      bool boxhit = slab(A.pmin, A.pmax, o, d, t_near, t_far);
+      bool boxhit = slab(A.pmin, A.pmax, o, d, t_near, t_far, inv);
       if (boxhit) {
-        mr = march_ray(A, o, d, t_near, t_far);
+        mr = march_ray(A, o, d, inv, t_near, t_far);
         samples_total += (unsigned long long)mr.samples;
         hit = mr.hit;
       }
     }
     if (args.out_hit) {        // march_rays outputs (MarchResult, lightfield.py:101-110)
-      if (valid) {
+      if (live) {
         args.out_hit[gid] = hit ? 1 : 0;
         args.out_t_hit[gid] = mr.t_hit;
         args.out_alpha_c[gid] = mr.alpha_c;
@@ -546,6 +565,8 @@ struct ComposeArgs {
   long long layer_stride;      // P
   const TileParams *tiles;     // scene mode: skip padding slots (NULL => none)
   long long tile_stride;
+  const CamParams *cams;       // frame layout: camera sizes / output bases
+  int frame_layout;            // 0: outputs tile-packed at p ; 1: row-major frame per camera
   float alpha_vis;             // compared in f32 (numpy 2 weak scalar)
   float *out_rgba;
   float *out_depth;
@@ -562,9 +583,16 @@ constexpr int kMaxLayers = 64;
 __global__ void __launch_bounds__(256) k_compose(ComposeArgs a) {
   const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= a.n_pix) return;
+  long long q = p;             // output index
   if (a.tiles) {
     const TileParams tp = a.tiles[p / a.tile_stride];
-    if (p % a.tile_stride >= (long long)(tp.x1 - tp.x0) * (tp.y1 - tp.y0)) return;
+    const long long local = p % a.tile_stride;
+    const int w = tp.x1 - tp.x0;
+    if (local >= (long long)w * (tp.y1 - tp.y0)) return;
+    if (a.frame_layout) {
+      const CamParams &cp = a.cams[tp.cam];
+      q = cp.pix_base + (long long)(tp.y0 + (int)(local / w)) * cp.width + (tp.x0 + (int)(local % w));
+    }
   }
   const int n = a.nhit ? (int)a.nhit[p] : a.K;
   float dk[kMaxLayers];
@@ -598,26 +626,46 @@ __global__ void __launch_bounds__(256) k_compose(ComposeArgs a) {
     o = make_float4(0.f, 0.f, 0.f, 0.f);
     od = __int_as_float(0x7f800000);
   }
-  if (a.out_rgba) reinterpret_cast<float4 *>(a.out_rgba)[p] = o;
-  if (a.out_depth) a.out_depth[p] = od;
+  if (a.out_rgba) reinterpret_cast<float4 *>(a.out_rgba)[q] = o;
+  if (a.out_depth) a.out_depth[q] = od;
   if (a.out_rgba8) {           // encode_frame (protocol.py:256-266): clip(round(x*255))
-    const float q[4] = {o.x, o.y, o.z, o.w};
+    const float qv[4] = {o.x, o.y, o.z, o.w};
     uchar4 u;
     unsigned char uu[4];
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
-      float v = rintf(q[c] * 255.0f);
+      float v = rintf(qv[c] * 255.0f);
       v = v < 0.f ? 0.f : (v > 255.f ? 255.f : v);
       uu[c] = (unsigned char)v;
     }
     u.x = uu[0]; u.y = uu[1]; u.z = uu[2]; u.w = uu[3];
-    reinterpret_cast<uchar4 *>(a.out_rgba8)[p] = u;
+    reinterpret_cast<uchar4 *>(a.out_rgba8)[q] = u;
   }
   if (a.out_depth16) {
     uint16_t qd = 65535;
     if (isfinite(od)) qd = (uint16_t)rintf(fminf(od, a.depth_far) / a.depth_far * 65534.0f);
-    a.out_depth16[p] = qd;
+    a.out_depth16[q] = qd;
   }
+}
+
+// Frame assembly after an all-rank gather: rank r's buffer holds n_per_rank
+// tile slots of rgba8 (stride*4 B each) followed by their depth16; slot_tiles
+// lists the tile of every (rank, slot) in rank-major order.
+__global__ void __launch_bounds__(256) k_unpack(const uint8_t *gathered, long long rank_bytes, int n_per_rank,
+                                                long long tile_stride, const TileParams *slot_tiles,
+                                                long long n_slots, int width, uchar4 *rgba8, uint16_t *depth16) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long s = i / tile_stride, local = i % tile_stride;
+  if (s >= n_slots) return;
+  const TileParams tp = slot_tiles[s];
+  const int w = tp.x1 - tp.x0;
+  if (local >= (long long)w * (tp.y1 - tp.y0)) return;
+  const long long r = s / n_per_rank, j = s % n_per_rank;
+  const uint8_t *base = gathered + r * rank_bytes;
+  const long long src = j * tile_stride + local;
+  const long long dst = (long long)(tp.y0 + (int)(local / w)) * width + (tp.x0 + (int)(local % w));
+  rgba8[dst] = reinterpret_cast<const uchar4 *>(base)[src];
+  depth16[dst] = reinterpret_cast<const uint16_t *>(base + (long long)n_per_rank * tile_stride * 4)[src];
 }
 
 }  // namespace nolf

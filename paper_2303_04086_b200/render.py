@@ -327,7 +327,8 @@ class SceneRenderer:
             cams[i] = N.camera_struct(c)
         return cams
 
-    def render(self, cameras, tiles_dev, n_tiles: int, tile_stride: int, out: dict, stream=None):
+    def render(self, cameras, tiles_dev, n_tiles: int, tile_stride: int, out: dict, stream=None,
+               frame_layout: bool = False):
         cams = cameras if isinstance(cameras, C.Array) else self.camera_array(cameras)
         so = N.SceneOut()
         so.rgba = out["rgba"].data_ptr() if "rgba" in out else None
@@ -336,6 +337,7 @@ class SceneRenderer:
         so.depth16 = out["depth16"].data_ptr() if "depth16" in out else None
         so.tile_stride = int(tile_stride)
         so.depth_far = self.depth_far
+        so.layout = 1 if frame_layout else 0
         st = stream if stream is not None else _stream_ptr()
         N.check(N.lib().nolf_render_scene(self._inst_arr, len(self.insts), cams, len(cameras),
                                           tiles_dev.data_ptr(), int(n_tiles), C.byref(so),
@@ -363,10 +365,10 @@ def render_scene(scene, camera, counters=None, tile: int = 32):
     tiles = frame_tiles(camera.width, camera.height, tile)
     tiles_dev = t.from_numpy(tiles).to(r.device)
     out = r.alloc(len(tiles), tile * tile, want_f32=True, want_u8=False)
-    r.render([camera], tiles_dev, len(tiles), tile * tile, out)
-    idx = t.from_numpy(unpack_index(tiles, tile * tile, camera.width, camera.height)).to(r.device)
-    rgba = out["rgba"].index_select(0, idx).reshape(camera.height, camera.width, 4)
-    depth = out["depth"].index_select(0, idx).reshape(camera.height, camera.width)
+    r.render([camera], tiles_dev, len(tiles), tile * tile, out, frame_layout=True)
+    npx = camera.width * camera.height
+    rgba = out["rgba"][:npx].reshape(camera.height, camera.width, 4)
+    depth = out["depth"][:npx].reshape(camera.height, camera.width)
     _merge(counters, out["counters"])
     return Frame(width=camera.width, height=camera.height, rgba=rgba.cpu().numpy(),
                  depth=depth.cpu().numpy())
