@@ -30,6 +30,10 @@ from .model import Frame, RayRange, RenderCounters, Tile, uniform_scale_of
 
 _torch = None
 
+# Result types; shim.install() swaps in the reference's own Tile / Frame.
+OWN_TYPES = {"Frame": Frame, "Tile": Tile}
+TYPES = dict(OWN_TYPES)
+
 
 def torch():
     global _torch
@@ -219,7 +223,7 @@ def render_range(asset, ray_range, counters=None):
     N.check(N.lib().nolf_render_rect(C.byref(inst), C.byref(cs), x0, y0, x1, y1, rgba.data_ptr(),
                                      depth.data_ptr(), cnt.data_ptr(), ws.data_ptr(), ws.numel(),
                                      _stream_ptr()))
-    tile = Tile(x0=x0, y0=y0, rgba=rgba.cpu().numpy(), depth=depth.cpu().numpy())
+    tile = TYPES["Tile"](x0=x0, y0=y0, rgba=rgba.cpu().numpy(), depth=depth.cpu().numpy())
     c = cnt.cpu().numpy()
     before_fs, before_hits = counters.fs_evals, counters.hit_pixels
     _merge(counters, cnt)
@@ -227,6 +231,13 @@ def render_range(asset, ray_range, counters=None):
              "hits": counters.hit_pixels - before_hits, "fs_evals": counters.fs_evals - before_fs}
     del c
     return tile, instr
+
+
+class _Rect:
+    """Full-frame RayRange without re-validating (bounds are the frame's)."""
+
+    def __init__(self, camera, x0, y0, x1, y1):
+        self.camera, self.x0, self.y0, self.x1, self.y1 = camera, x0, y0, x1, y1
 
 
 def render_frame(scene, camera, counters=None):
@@ -237,10 +248,9 @@ def render_frame(scene, camera, counters=None):
         if transform is not None:
             import dataclasses
             placed = dataclasses.replace(asset, object_to_world=np.asarray(transform, np.float64))
-        tile, _ = render_range(placed, RayRange(camera, 0, 0, camera.width, camera.height,
-                                                getattr(asset, "name", "asset")), counters)
-        frames.append(Frame(width=camera.width, height=camera.height, rgba=tile.rgba,
-                            depth=tile.depth))
+        tile, _ = render_range(placed, _Rect(camera, 0, 0, camera.width, camera.height), counters)
+        frames.append(TYPES["Frame"](width=camera.width, height=camera.height, rgba=tile.rgba,
+                                     depth=tile.depth))
     return frames
 
 
@@ -255,8 +265,8 @@ def compose(frames, asset_order=None, alpha_vis: float = 0.5):
     depth = t.from_numpy(np.ascontiguousarray(np.stack([f.depth for f in frames]), np.float32)).to(dev)
     orgba, odepth = compose_device(rgba.reshape(len(frames), h * w, 4), depth.reshape(len(frames), h * w),
                                    alpha_vis)
-    return Frame(width=w, height=h, rgba=orgba.reshape(h, w, 4).cpu().numpy(),
-                 depth=odepth.reshape(h, w).cpu().numpy())
+    return TYPES["Frame"](width=w, height=h, rgba=orgba.reshape(h, w, 4).cpu().numpy(),
+                          depth=odepth.reshape(h, w).cpu().numpy())
 
 
 def compose_device(rgba, depth, alpha_vis: float = 0.5):
