@@ -80,19 +80,46 @@ int upload_atlas(NolfAsset *A, const NolfAtlasDesc &d, int channels, DevAtlas *o
   out->r = d.r;
   out->C = channels;
   out->s = s;
-  out->mb = (b + kMacro - 1) / kMacro;
-  std::vector<uint8_t> macro((size_t)out->mb * out->mb * out->mb, 0);
-  for (int x = 0; x < b; ++x)
-    for (int y = 0; y < b; ++y)
-      for (int z = 0; z < b; ++z)
-        if (d.index[((int64_t)x * b + y) * b + z] != -1)
-          macro[((size_t)(x / kMacro) * out->mb + y / kMacro) * out->mb + z / kMacro] = 1;
+  // Chebyshev (L-inf) distance transform of the occupancy, separable:
+  // f1 = 1-D distance along x; f2 = min_y' max(|y-y'|, f1); f3 likewise in z.
+  const int INF = 1 << 20;
+  std::vector<int> f((size_t)ncell), g((size_t)ncell);
+  auto at3 = [b](int x, int y, int z) { return ((size_t)x * b + y) * b + z; };
+  for (int y = 0; y < b; ++y)
+    for (int z = 0; z < b; ++z) {
+      int last = -INF;
+      for (int x = 0; x < b; ++x) {
+        if (d.index[at3(x, y, z)] != -1) last = x;
+        f[at3(x, y, z)] = last == -INF ? INF : x - last;
+      }
+      last = INF;
+      for (int x = b - 1; x >= 0; --x) {
+        if (d.index[at3(x, y, z)] != -1) last = x;
+        if (last != INF) f[at3(x, y, z)] = std::min(f[at3(x, y, z)], last - x);
+      }
+    }
+  for (int pass = 0; pass < 2; ++pass) {      // pass 0: along y, pass 1: along z
+    for (int x = 0; x < b; ++x)
+      for (int u = 0; u < b; ++u)
+        for (int v = 0; v < b; ++v) {
+          int best = INF;
+          for (int w = 0; w < b; ++w) {
+            const size_t src = pass == 0 ? at3(x, w, u) : at3(x, u, w);
+            const int dv = std::max(std::abs(v - w), f[src]);
+            best = std::min(best, dv);
+          }
+          g[pass == 0 ? at3(x, v, u) : at3(x, u, v)] = best;
+        }
+    f.swap(g);
+  }
+  std::vector<uint8_t> dist((size_t)ncell);
+  for (int64_t i = 0; i < ncell; ++i) dist[(size_t)i] = (uint8_t)std::min(f[(size_t)i], 255);
   int32_t *idx;
   uint8_t *mac;
   float *cubes;
   int rc;
   if ((rc = A->upload(d.index, (size_t)ncell, &idx))) return rc;
-  if ((rc = A->upload(macro.data(), macro.size(), &mac))) return rc;
+  if ((rc = A->upload(dist.data(), dist.size(), &mac))) return rc;
   const size_t nc = (size_t)d.n_cubes * s * s * s * channels;
   if (nc == 0) {               // keep a valid pointer for empty atlases
     float z4[4] = {0, 0, 0, 0};
@@ -101,7 +128,7 @@ int upload_atlas(NolfAsset *A, const NolfAtlasDesc &d, int channels, DevAtlas *o
     return rc;
   }
   out->index = idx;
-  out->macro = mac;
+  out->dist = mac;
   out->cubes = cubes;
   return 0;
 }

@@ -9,17 +9,16 @@
 
 namespace nolf {
 
-constexpr int kMacro = 4;      // index cells per macro cell edge (skip level 1)
 constexpr int kHid = 64;       // MLP hidden width (lightfield.py:594 hidden=64)
 constexpr int kInp = 24;       // padded MLP input width (fs: 19, fd: 12)
 constexpr int kMaxLevels = 16;
 
 struct DevAtlas {              // CubeAtlas (atlas.py:25-51)
   int b, r, C, s;              // s = r + 1
-  int mb;                      // macro grid resolution ceil(b / kMacro)
   const int32_t *index;        // b^3, -1 empty
   const float *cubes;          // n * s^3 * C
-  const uint8_t *macro;        // mb^3: 1 if any cell of the macro is occupied
+  const uint8_t *dist;         // b^3: Chebyshev distance (cells) to the nearest
+                               // occupied cell, 0 = occupied, capped at 255
 };
 
 // Fully fused MLP parameter block (neural.py:29-108), fp32, padded:

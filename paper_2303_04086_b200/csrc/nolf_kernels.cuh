@@ -117,10 +117,11 @@ __device__ __forceinline__ MarchOut march_ray(const DevAsset &A, const double o[
   if (!(t_near < t_far)) return r;
   const DevAtlas &at = A.den;
   const double delta = A.step;
-  const int b = at.b, mb = at.mb;
+  const int b = at.b;
   const double inv_b = 1.0 / (double)b;
+  const double inv_delta = 1.0 / delta;
   double best_w = 0.0, trans = 1.0, alpha_c = 0.0, t_hit = r.t_hit;
-  long long samples = 0;
+  int samples = 0;
   long long i = 0;
   for (;;) {
     double pos[3];
@@ -129,31 +130,29 @@ __device__ __forceinline__ MarchOut march_ray(const DevAsset &A, const double o[
     if (!(t_mid < t_far)) break;
     int lo_c[3], hi_c[3];
     bool empty = false;
-    const int m0 = cell[0] / kMacro, m1 = cell[1] / kMacro, m2 = cell[2] / kMacro;
     int cid = -1;
-    if (!__ldg(at.macro + (m0 * mb + m1) * mb + m2)) {
+    const int ci = (cell[0] * b + cell[1]) * b + cell[2];
+    const int dist = __ldg(at.dist + ci);
+    if (dist > 0) {            // every cell within Chebyshev radius dist-1 is empty
       empty = true;
-      lo_c[0] = m0 * kMacro; lo_c[1] = m1 * kMacro; lo_c[2] = m2 * kMacro;
 #pragma unroll
-      for (int k = 0; k < 3; ++k) hi_c[k] = min(lo_c[k] + kMacro, b) - 1;
-    } else {
-      cid = __ldg(at.index + (cell[0] * b + cell[1]) * b + cell[2]);
-      if (cid < 0) {
-        empty = true;
-#pragma unroll
-        for (int k = 0; k < 3; ++k) lo_c[k] = hi_c[k] = cell[k];
+      for (int k = 0; k < 3; ++k) {
+        lo_c[k] = max(cell[k] - (dist - 1), 0);
+        hi_c[k] = min(cell[k] + (dist - 1), b - 1);
       }
+    } else {
+      cid = __ldg(at.index + ci);
     }
     if (empty) {
       double lo[3], hi[3];
 #pragma unroll
       for (int k = 0; k < 3; ++k) {
-        lo[k] = lo_c[k] * inv_b;
-        hi[k] = (hi_c[k] + 1) * inv_b;
+        lo[k] = lo_c[k] > 0 ? lo_c[k] * inv_b : -1.0;       // grid faces: clipped
+        hi[k] = hi_c[k] < b - 1 ? (hi_c[k] + 1) * inv_b : 2.0;  // positions never leave
       }
       double te = box_exit(o, d, inv, lo, hi);
       double tl = fmin(te, t_far);
-      double jf = floor((tl - t_near) / delta - 0.5);
+      double jf = floor((tl - t_near) * inv_delta - 0.5);
       long long j = jf > 9.0e15 ? (long long)9.0e15 : (long long)jf;
       long long next = i + 1;
       for (int attempt = 0; attempt < 2 && j > i; ++attempt, --j) {
@@ -223,17 +222,31 @@ __global__ void __launch_bounds__(128) k_march(MarchArgs args) {
   }
   unsigned long long samples_total = 0;
   unsigned ordinal = 0;
-  for (int k = 0; k < args.n_inst; ++k) {
+  // Instances whose conservative screen box covers this lane's pixel, then
+  // OR-ed over the warp so the instance loop below is warp-uniform and only
+  // visits candidates (ascending = scene order, so layer ordinals match).
+  unsigned long long lane_mask = 0;
+  if (valid) {
+    if (MODE == kModeRays || !args.cull) {
+      lane_mask = args.n_inst >= 64 ? ~0ull : ((1ull << args.n_inst) - 1ull);
+    } else {
+      for (int k = 0; k < args.n_inst; ++k) {
+        const ScreenBox bb = args.cull[k * args.n_cams + cam];
+        if (pix_x >= bb.x0 && pix_x <= bb.x1 && pix_y >= bb.y0 && pix_y <= bb.y1) lane_mask |= 1ull << k;
+      }
+    }
+  }
+  unsigned long long wmask = ((unsigned long long)__reduce_or_sync(0xffffffffu, (unsigned)(lane_mask >> 32)) << 32) |
+                             __reduce_or_sync(0xffffffffu, (unsigned)lane_mask);
+  while (wmask) {
+    const int k = __ffsll((long long)wmask) - 1;
+    wmask &= wmask - 1;
     const DevInst &I = args.inst[k];
     const DevAsset &A = *I.a;
     bool hit = false;
     double o[3], d[3], inv[3], t_near = 0, t_far = 0;
     MarchOut mr{0.0, __longlong_as_double(0x7ff0000000000000ll), 0, false};
-    bool live = valid;
-    if (MODE != kModeRays && live && args.cull) {
-      const ScreenBox bb = args.cull[k * args.n_cams + cam];
-      live = pix_x >= bb.x0 && pix_x <= bb.x1 && pix_y >= bb.y0 && pix_y <= bb.y1;
-    }
+    const bool live = (lane_mask >> k) & 1ull;
     if (live) {
       if (args.raw_rays) {
 #pragma unroll
