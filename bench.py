@@ -48,7 +48,7 @@ def parse():
     p.add_argument("--height", type=int, default=2160)
     p.add_argument("--assets", type=int, default=12)
     p.add_argument("--tile", type=int, default=32)
-    p.add_argument("--mlp", default="fp32", choices=["fp32", "bf16"])
+    p.add_argument("--mlp", default="bf16", choices=["fp32", "bf16"])
     p.add_argument("--cpu-seconds", type=float, default=12.0)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")

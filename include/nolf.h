@@ -197,6 +197,11 @@ int nolf_unpack_gathered(const uint8_t *gathered, int32_t world, int32_t n_per_r
                          const NolfTile *slot_tiles, int32_t width, int32_t height, uint8_t *rgba8,
                          uint16_t *depth16, void *stream);
 
+/* The specular network alone (numerics tests / microbench): x (n, in) f32
+ * device rows -> out (n, 4) f32 post-head, via the tcgen05 bf16 path
+ * (NOLF_MLP_BF16) or the fp32 CUDA-core path (NOLF_MLP_FP32). */
+int nolf_mlp_eval(nolf_asset_t asset, int mode, const float *x, int64_t n, float *out, void *stream);
+
 /* frames: rgba (K, P, 4) f32, depth (K, P) f32, all device pointers. */
 int nolf_compose(int32_t K, int64_t P, const float *rgba, const float *depth, double alpha_vis,
                  float *out_rgba, float *out_depth, void *stream);

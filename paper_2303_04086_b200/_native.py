@@ -98,6 +98,7 @@ def lib():
         "nolf_march_rays": ([vp, vp, i32, vp, i64, vp, vp, vp, vp, vp, vp, C.c_size_t, vp], C.c_int),
         "nolf_eval_diffuse": ([vp, vp, i64, vp, vp], C.c_int),
         "nolf_profile": ([C.c_int], C.c_int),
+        "nolf_mlp_eval": ([vp, C.c_int, vp, i64, vp, vp], C.c_int),
         "nolf_profile_read": ([C.POINTER(C.c_float)], C.c_int),
         "nolf_launch_param_bytes": ([i32, i32], C.c_size_t),
         "nolf_unpack_gathered": ([vp, i32, i32, i64, vp, i32, i32, vp, vp, vp], C.c_int),

@@ -11,6 +11,7 @@
 
 #include "../../include/nolf.h"
 #include "nolf_kernels.cuh"
+#include "nolf_shade_tc.cuh"
 
 using namespace nolf;
 
@@ -192,6 +193,9 @@ int ensure_attrs() {
   if (!done) {
     CUDA_TRY(cudaFuncSetAttribute(k_shade, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kShadeSmem));
     CUDA_TRY(cudaFuncSetAttribute(k_eval_diffuse, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kShadeSmem));
+    CUDA_TRY(cudaFuncSetAttribute(k_shade_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTcSmem));
+    CUDA_TRY(cudaFuncSetAttribute(k_mlp_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTcSmem));
+    CUDA_TRY(cudaFuncSetAttribute(k_mlp_fp32, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kShadeSmem));
     done = true;
   }
   return 0;
@@ -242,7 +246,7 @@ int fill_inst(const NolfInstance *in, DevInst *out) {
 }
 
 int run_shade(const DevInst *inst, int n_inst, const Workspace &w, int mode, float *rgba, float *depth,
-              long long layer_stride, unsigned long long *counters, cudaStream_t st);
+              long long layer_stride, unsigned long long *counters, cudaStream_t st, bool use_tc);
 
 }  // namespace
 
@@ -377,6 +381,38 @@ int nolf_asset_create(const NolfAssetDesc *d, int device, nolf_asset_t *out) {
   } else {
     H.fd.params = nullptr;
   }
+  // tensor-core tables: bf16 specular weights in the UMMA K-major layout
+  // (core matrix (row group g, K chunk c) at c*(rows/8)*128 + g*128) + u16 Phi
+  if (d->specular.n_layers == 3 && d->specular.widths[0] <= kTcK0) {
+    std::vector<uint16_t> wt(kTcWBytes / 2, 0);
+    auto bf16 = [](float f) {
+      uint32_t u;
+      memcpy(&u, &f, 4);
+      u += 0x7FFFu + ((u >> 16) & 1u);            // round to nearest even
+      return (uint16_t)(u >> 16);
+    };
+    auto put = [&](size_t base_elems, int row, int k, float v) {
+      const size_t off = (size_t)(k >> 3) * (64 / 8) * 128 + (size_t)(row >> 3) * 128 + (row & 7) * 16 + (k & 7) * 2;
+      wt[base_elems + off / 2] = bf16(v);
+    };
+    const int in = d->specular.widths[0];
+    for (int o = 0; o < 64; ++o)
+      for (int i = 0; i < in; ++i) put(0, o, i, d->specular.w[0][o * in + i]);
+    for (int o = 0; o < 64; ++o)
+      for (int i = 0; i < 64; ++i) put(kTcW0 / 2, o, i, d->specular.w[1][o * 64 + i]);
+    uint16_t *tw;
+    if ((rc = A->upload(wt.data(), wt.size(), &tw))) return bail(rc);
+    H.tc_w = reinterpret_cast<const uint8_t *>(tw);
+  }
+  if (d->psh_table_size <= 65536) {
+    const size_t n16 = ((size_t)d->psh_offset_size + 7) / 8 * 8;
+    std::vector<uint16_t> p16(n16, 0);
+    for (int64_t i = 0; i < d->psh_offset_size; ++i) p16[(size_t)i] = (uint16_t)d->psh_offsets[i];
+    uint16_t *pp16;
+    if ((rc = A->upload(p16.data(), p16.size(), &pp16))) return bail(rc);
+    H.phi16 = pp16;
+    H.phi16_bytes = (uint32_t)(n16 * 2);
+  }
   const int expect_in = H.F + 16 + (d->refine_opacity ? 1 : 0);
   if (H.fs.in != expect_in)
     return bail(fail(NOLF_EINVAL, "specular MLP input %d != F+16+refine %d", H.fs.in, expect_in));
@@ -417,7 +453,12 @@ int nolf_asset_destroy(nolf_asset_t a) {
 
 int nolf_asset_set_mlp_mode(nolf_asset_t a, int mode) {
   if (!a) return fail(NOLF_EINVAL, "null asset");
-  if (mode != NOLF_MLP_FP32) return fail(NOLF_EINVAL, "MLP mode %d not available in this build", mode);
+  if (mode != NOLF_MLP_FP32 && mode != NOLF_MLP_BF16) return fail(NOLF_EINVAL, "unknown MLP mode %d", mode);
+  if (mode == NOLF_MLP_BF16) {
+    if (!a->host.tc_w) return fail(NOLF_EINVAL, "bf16 tensor-core MLP needs a 3-layer specular net with <= 32 inputs");
+    if (a->host.use_diffuse_color && !a->host.has_dif)
+      return fail(NOLF_EINVAL, "bf16 tensor-core shading needs a baked diffuse atlas (live diffuse runs in fp32)");
+  }
   a->host.mlp_mode = mode;
   CUDA_TRY(cudaMemcpy(a->dev, &a->host, sizeof(DevAsset), cudaMemcpyHostToDevice));
   return 0;
@@ -432,7 +473,7 @@ size_t nolf_workspace_bytes(int32_t n_inst, int64_t n_rays) { return ws_layout(n
 namespace {
 
 int run_shade(const DevInst *inst, int n_inst, const Workspace &w, int mode, float *rgba, float *depth,
-              long long layer_stride, unsigned long long *counters, cudaStream_t st) {
+              long long layer_stride, unsigned long long *counters, cudaStream_t st, bool use_tc) {
   ShadeArgs sa{};
   sa.inst = inst;
   sa.n_inst = n_inst;
@@ -444,8 +485,11 @@ int run_shade(const DevInst *inst, int n_inst, const Workspace &w, int mode, flo
   sa.depth = depth;
   sa.layer_stride = layer_stride;
   sa.counters = counters;
-  const int blocks = num_sms() * 3;
-  k_shade<<<blocks, kShadeThreads, kShadeSmem, st>>>(sa);
+  if (use_tc) {
+    k_shade_tc<<<num_sms() * 2, kTcThreads, kTcSmem, st>>>(sa);
+  } else {
+    k_shade<<<num_sms() * 3, kShadeThreads, kShadeSmem, st>>>(sa);
+  }
   CUDA_TRY(cudaGetLastError());
   return 0;
 }
@@ -520,8 +564,11 @@ int launch_march_shade(int mode, const NolfInstance *ins, int n_inst, const Nolf
   ParamBlock *hp, *dp;
   int slot;
   if ((rc = ring_acquire(&hp, &dp, &slot))) return rc;
-  for (int k = 0; k < n_inst; ++k)
+  bool use_tc = true;
+  for (int k = 0; k < n_inst; ++k) {
     if ((rc = fill_inst(ins + k, hp->inst + k))) return rc;
+    use_tc = use_tc && ins[k].asset->host.mlp_mode == NOLF_MLP_BF16;
+  }
   long long pix_base = 0;
   for (int c = 0; c < n_cams; ++c) {
     const NolfCamera &C = cams[c];
@@ -570,7 +617,8 @@ int launch_march_shade(int mode, const NolfInstance *ins, int n_inst, const Nolf
   CUDA_TRY(cudaGetLastError());
   if ((rc = prof_mark(1, st))) return rc;
   if (mode == kModeScene) {
-    if ((rc = run_shade(dp->inst, n_inst, w, mode, w.lrgba, w.ldepth, (long long)w.cap, counters, st))) return rc;
+    if ((rc = run_shade(dp->inst, n_inst, w, mode, w.lrgba, w.ldepth, (long long)w.cap, counters, st, use_tc)))
+      return rc;
     if ((rc = prof_mark(2, st))) return rc;
     ComposeArgs ca{};
     ca.n_pix = n_rays;
@@ -593,7 +641,7 @@ int launch_march_shade(int mode, const NolfInstance *ins, int n_inst, const Nolf
     CUDA_TRY(cudaGetLastError());
     if ((rc = prof_mark(3, st))) return rc;
   } else {
-    if ((rc = run_shade(dp->inst, n_inst, w, mode, rgba, depth, 0, counters, st))) return rc;
+    if ((rc = run_shade(dp->inst, n_inst, w, mode, rgba, depth, 0, counters, st, use_tc))) return rc;
     if ((rc = prof_mark(2, st))) return rc;
     if ((rc = prof_mark(3, st))) return rc;
   }
@@ -693,6 +741,28 @@ int nolf_eval_diffuse(nolf_asset_t asset, const double *points, int64_t n, float
   const long long blocks = std::min<long long>((n + kShadeThreads - 1) / kShadeThreads, (long long)num_sms() * 8);
   k_eval_diffuse<<<(unsigned)blocks, kShadeThreads, kShadeSmem, static_cast<cudaStream_t>(stream)>>>(asset->dev, points,
                                                                                                     n, out);
+  CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+int nolf_mlp_eval(nolf_asset_t asset, int mode, const float *x, int64_t n, float *out, void *stream) {
+  if (!asset) return fail(NOLF_EINVAL, "null asset");
+  if (n < 0) return fail(NOLF_EINVAL, "negative row count");
+  if (n == 0) return 0;
+  if (!x || !out) return fail(NOLF_EINVAL, "null buffer");
+  int rc;
+  if ((rc = ensure_attrs())) return rc;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (mode == NOLF_MLP_BF16) {
+    if (!asset->host.tc_w) return fail(NOLF_EINVAL, "asset has no tensor-core weights");
+    const long long blocks = std::min<long long>((n + kTcThreads - 1) / kTcThreads, (long long)num_sms() * 2);
+    k_mlp_tc<<<(unsigned)blocks, kTcThreads, kTcSmem, st>>>(asset->dev, x, n, out);
+  } else if (mode == NOLF_MLP_FP32) {
+    const long long blocks = std::min<long long>((n + kShadeThreads - 1) / kShadeThreads, (long long)num_sms() * 4);
+    k_mlp_fp32<<<(unsigned)blocks, kShadeThreads, kShadeSmem, st>>>(asset->dev, x, n, out);
+  } else {
+    return fail(NOLF_EINVAL, "unknown MLP mode %d", mode);
+  }
   CUDA_TRY(cudaGetLastError());
   return 0;
 }

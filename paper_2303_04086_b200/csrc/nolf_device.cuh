@@ -66,6 +66,10 @@ struct DevAsset {              // LightFieldAsset (lightfield.py:217-248)
   double pmin[3], pmax[3];
   int use_hit_point, use_opacity, refine_opacity, use_tint, use_diffuse_color;
   int mlp_mode;
+  // tensor-core shading tables (NOLF_MLP_BF16)
+  const uint8_t *tc_w;         // bf16 W0 [64 x 32] then W1 [64 x 64], UMMA K-major layout
+  const uint16_t *phi16;       // Phi narrowed to u16 (m <= 65536), else null
+  uint32_t phi16_bytes;        // padded to 16 B for the TMA bulk copy
 };
 
 // One placed asset for a launch (NolfInstance minus the host handle).

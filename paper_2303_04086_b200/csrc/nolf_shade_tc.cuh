@@ -1,0 +1,371 @@
+// nolf_shade_tc.cuh -- fused shading kernel on the 5th-generation tensor cores.
+//
+// Per CTA: tiles of 128 hit records of ONE placed asset (thread t owns row t).
+//   * Phi (the PSH offset table, narrowed to u16 when m <= 65536) and the bf16
+//     specular weights are staged into shared memory with TMA bulk copies
+//     (cp.async.bulk -> mbarrier complete_tx) whenever the asset changes.
+//   * Each thread gathers its PSH corners (Phi from smem), SH(d_obj), the
+//     clamped coarse opacity and the diffuse atlas, and writes its 19-wide
+//     input row as bf16 into a K-major UMMA operand tile.
+//   * Layer 0 [19->64] and layer 1 [64->64] run as tcgen05.mma kind::f16
+//     (M=128, N=64, K=16 steps) into a 64-column TMEM accumulator issued by
+//     one thread; tcgen05.commit arrives on an mbarrier; the 4 warps read
+//     their 32 TMEM lanes back with tcgen05.ld (bias + ReLU in fp32, H1
+//     re-quantised to bf16 as the next A operand).
+//   * Layer 2 [64->4] + heads + the c = c_d + t*c_s combine run in fp32 on
+//     CUDA cores in the epilogue (N=4 is too narrow for an MMA).
+// Numerics: bf16 inputs/weights, fp32 accumulation -> north-star tolerance
+// 2/255 (lightfield.py:632-637 network, lightfield.py:291-336 combine).
+#pragma once
+#include "nolf_kernels.cuh"
+#include "nolf_tc.cuh"
+
+namespace nolf {
+
+constexpr int kTcThreads = 128;
+constexpr int kTcK0 = 32;                    // layer-0 K padded (inputs <= 32)
+constexpr uint32_t kTcA = 16384;             // A tile: 128 x 64 bf16
+constexpr uint32_t kTcW0 = 64 * kTcK0 * 2;   // 4 KB
+constexpr uint32_t kTcW1 = 64 * 64 * 2;      // 8 KB
+constexpr uint32_t kTcWBytes = kTcW0 + kTcW1;
+constexpr int kTcF32 = 64 + 64 + 4 * 64 + 4; // b0, b1, W2, b2
+constexpr uint32_t kTcPhiMax = 64 * 1024;    // Phi bytes staged in smem
+constexpr uint32_t kTcTabMax = 776;          // residue tables 6*(N+1) for N <= 128 (16-B multiple)
+constexpr uint32_t kTcSmem = 1024 + kTcA + kTcWBytes + kTcF32 * 4 + kTcTabMax * 4 + 64 + kTcPhiMax;
+
+// Two layers on tcgen05 for the 128 rows already written to A (layer-0 input,
+// bf16, K-major); returns this thread's 4 pre-head outputs (fp32).
+__device__ __forceinline__ void tc_mlp_rows(uint8_t *A, const uint8_t *W, const float *fp, uint32_t tmem,
+                                            uint64_t *bar, uint32_t &phase, int tid, float out4[4]) {
+  const uint32_t aA = tc::smem_u32(A), aW0 = tc::smem_u32(W), aW1 = aW0 + kTcW0;
+  constexpr uint32_t idesc = tc::idesc_bf16_f32(128, 64);
+  const int warp = tid >> 5;
+  const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
+  // ---- layer 0: D = X[128x32] * W0[64x32]^T
+  tc::fence_async_smem();
+  __syncthreads();
+  if (tid == 0) {
+    tc::tc_fence_after();
+#pragma unroll
+    for (int s = 0; s < kTcK0 / 16; ++s)
+      tc::umma_bf16(tmem, tc::smem_desc(aA + s * 2 * 2048, 2048, 128), tc::smem_desc(aW0 + s * 2 * 1024, 1024, 128),
+                    idesc, s > 0);
+    tc::umma_commit(bar);
+  }
+  tc::mbar_wait(bar, phase);
+  phase ^= 1;
+  tc::tc_fence_after();
+  float h[64];
+  tc::tmem_ld32(trow + 0, h);
+  tc::tmem_ld32(trow + 32, h + 32);
+  // bias + ReLU, re-quantise as the layer-1 A operand (K=64)
+  uint8_t *rowp = A + (tid >> 3) * 128 + (tid & 7) * 16;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    float v[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const float z = h[8 * c + e] + fp[8 * c + e];
+      v[e] = z > 0.f ? z : 0.f;
+    }
+    uint4 q;
+    q.x = tc::pack_bf16(v[0], v[1]);
+    q.y = tc::pack_bf16(v[2], v[3]);
+    q.z = tc::pack_bf16(v[4], v[5]);
+    q.w = tc::pack_bf16(v[6], v[7]);
+    *reinterpret_cast<uint4 *>(rowp + c * 2048) = q;
+  }
+  tc::tc_fence_before();
+  tc::fence_async_smem();
+  __syncthreads();
+  // ---- layer 1: D = H1[128x64] * W1[64x64]^T (reuses the TMEM columns)
+  if (tid == 0) {
+    tc::tc_fence_after();
+#pragma unroll
+    for (int s = 0; s < 4; ++s)
+      tc::umma_bf16(tmem, tc::smem_desc(aA + s * 2 * 2048, 2048, 128), tc::smem_desc(aW1 + s * 2 * 1024, 1024, 128),
+                    idesc, s > 0);
+    tc::umma_commit(bar);
+  }
+  tc::mbar_wait(bar, phase);
+  phase ^= 1;
+  tc::tc_fence_after();
+  tc::tmem_ld32(trow + 0, h);
+  tc::tmem_ld32(trow + 32, h + 32);
+  tc::tc_fence_before();
+  // ---- layer 2 (fp32, CUDA cores): 64 -> 4, sequential in the hidden index
+  const float *b1 = fp + 64, *w2 = fp + 128, *b2 = fp + 128 + 256;
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+  for (int o = 0; o < 64; ++o) {
+    float z = h[o] + b1[o];
+    z = z > 0.f ? z : 0.f;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[j] = fmaf(z, w2[j * 64 + o], acc[j]);
+  }
+#pragma unroll
+  for (int j = 0; j < 4; ++j) out4[j] = acc[j] + b2[j];
+}
+
+// Write one bf16 input row (n values of x, zero padded to kTcK0) to A.
+__device__ __forceinline__ void tc_write_x(uint8_t *A, int tid, const float *x, int n) {
+  uint8_t *rowp = A + (tid >> 3) * 128 + (tid & 7) * 16;
+#pragma unroll
+  for (int c = 0; c < kTcK0 / 8; ++c) {
+    float v[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) v[e] = (8 * c + e < n) ? x[8 * c + e] : 0.f;
+    uint4 q;
+    q.x = tc::pack_bf16(v[0], v[1]);
+    q.y = tc::pack_bf16(v[2], v[3]);
+    q.z = tc::pack_bf16(v[4], v[5]);
+    q.w = tc::pack_bf16(v[6], v[7]);
+    *reinterpret_cast<uint4 *>(rowp + c * 2048) = q;
+  }
+}
+
+struct TcSmemPtrs {
+  uint8_t *A, *W;
+  float *fp;
+  uint32_t *tab;
+  uint64_t *bar_mma, *bar_tma;
+  uint32_t *tmem_slot;
+  uint8_t *phi;
+};
+
+__device__ __forceinline__ TcSmemPtrs tc_carve(uint8_t *raw) {
+  uint8_t *base = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
+  TcSmemPtrs p;
+  p.A = base;
+  p.W = p.A + kTcA;
+  p.fp = reinterpret_cast<float *>(p.W + kTcWBytes);
+  p.tab = reinterpret_cast<uint32_t *>(p.fp + kTcF32);
+  p.bar_mma = reinterpret_cast<uint64_t *>(p.tab + kTcTabMax);
+  p.bar_tma = p.bar_mma + 1;
+  p.tmem_slot = reinterpret_cast<uint32_t *>(p.bar_tma + 1);
+  p.phi = reinterpret_cast<uint8_t *>(p.bar_mma) + 64;
+  return p;
+}
+
+// Stage an asset's specular tables: TMA for the bf16 weights and Phi,
+// ordinary loads for the small fp32 block and the PSH residue tables.
+__device__ __forceinline__ void tc_stage_asset(const DevAsset &A, const TcSmemPtrs &S, uint32_t &tma_phase,
+                                               int tid, bool &phi_smem) {
+  phi_smem = A.phi16 != nullptr && A.phi16_bytes <= kTcPhiMax;
+  if (tid == 0) {
+    const uint32_t bytes = kTcWBytes + (phi_smem ? A.phi16_bytes : 0u);
+    tc::mbar_arrive_expect_tx(S.bar_tma, bytes);
+    tc::bulk_g2s(S.W, A.tc_w, kTcWBytes, S.bar_tma);
+    if (phi_smem) tc::bulk_g2s(S.phi, A.phi16, A.phi16_bytes, S.bar_tma);
+  }
+  const float *P = A.fs.params;
+  for (int q = tid; q < kTcF32; q += kTcThreads) {
+    float v;
+    if (q < 64) v = P[MlpOff::b0 + q];
+    else if (q < 128) v = P[MlpOff::b1 + q - 64];
+    else if (q < 128 + 256) v = P[MlpOff::wl + q - 128];
+    else v = P[MlpOff::bl + q - 384];
+    S.fp[q] = v;
+  }
+  const int nt = 6 * (A.N + 1);
+  if (nt <= (int)kTcTabMax)
+    for (int q = tid; q < nt; q += kTcThreads) S.tab[q] = A.tab[q];
+  tc::mbar_wait(S.bar_tma, tma_phase);
+  tma_phase ^= 1;
+}
+
+__global__ void __launch_bounds__(kTcThreads) k_shade_tc(ShadeArgs args) {
+  extern __shared__ uint8_t smem_raw[];
+  const TcSmemPtrs S = tc_carve(smem_raw);
+  const int tid = threadIdx.x, warp = tid >> 5;
+  if (warp == 0) tc::tmem_alloc<64>(S.tmem_slot);
+  if (tid == 0) {
+    tc::mbar_init(S.bar_mma, 1);
+    tc::mbar_init(S.bar_tma, 1);
+    tc::mbar_fence_init();
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = *S.tmem_slot;
+  uint32_t mma_phase = 0, tma_phase = 0;
+  int cur = -1;
+  bool phi_smem = false, tab_smem = false;
+  unsigned long long n_fs = 0;
+  for (long long tile = blockIdx.x;; tile += gridDim.x) {
+    int k = 0;
+    long long t = tile;
+    unsigned cnt = 0;
+    for (; k < args.n_inst; ++k) {
+      cnt = min((long long)args.counts[k], args.cap);
+      const long long nt = (cnt + kTcThreads - 1) / kTcThreads;
+      if (t < nt) break;
+      t -= nt;
+    }
+    if (k >= args.n_inst) break;
+    const DevInst &I = args.inst[k];
+    const DevAsset &A = *I.a;
+    if (k != cur) {
+      __syncthreads();
+      tc_stage_asset(A, S, tma_phase, tid, phi_smem);
+      tab_smem = 6 * (A.N + 1) <= (int)kTcTabMax;
+      __syncthreads();
+      cur = k;
+    }
+    const long long r = t * kTcThreads + tid;
+    const bool valid = r < cnt;
+    float x[kTcK0];
+    int nin = 0;
+    double cd[3] = {0.0, 0.0, 0.0}, tint = 1.0, alpha_c = 0.0, t_obj = 0.0;
+    uint32_t out_idx = 0, ordinal = 0;
+    if (valid) {
+      const HitRec rec = args.queue[(long long)k * args.cap + r];
+      alpha_c = rec.alpha_c;
+      t_obj = rec.t_obj;
+      out_idx = rec.out_idx;
+      ordinal = rec.ordinal;
+      int base[3];
+      double w8[8];
+      base_weights(rec.p, A.N, base, w8);
+      double es[4] = {0.0, 0.0, 0.0, 0.0};
+      const uint32_t *tab = tab_smem ? S.tab : A.tab;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const int xx = base[0] + (c & 1), yy = base[1] + ((c >> 1) & 1), zz = base[2] + ((c >> 2) & 1);
+        const int s1 = A.N + 1;
+        uint32_t h0 = tab[xx] + tab[s1 + yy];
+        h0 = h0 >= A.m ? h0 - A.m : h0;
+        h0 += tab[2 * s1 + zz];
+        h0 = h0 >= A.m ? h0 - A.m : h0;
+        uint32_t h1 = tab[3 * s1 + xx] + tab[4 * s1 + yy];
+        h1 = h1 >= A.mphi ? h1 - A.mphi : h1;
+        h1 += tab[5 * s1 + zz];
+        h1 = h1 >= A.mphi ? h1 - A.mphi : h1;
+        const uint32_t off = phi_smem ? (uint32_t)reinterpret_cast<const uint16_t *>(S.phi)[h1] : __ldg(A.phi + h1);
+        uint32_t slot = h0 + off;
+        slot = slot >= A.m ? slot - A.m : slot;
+        if (A.F == 2) {
+          const float2 f = __ldg(reinterpret_cast<const float2 *>(A.feat) + slot);
+          es[0] = __dadd_rn(es[0], __dmul_rn((double)f.x, w8[c]));
+          es[1] = __dadd_rn(es[1], __dmul_rn((double)f.y, w8[c]));
+        } else {
+          for (int f = 0; f < A.F; ++f)
+            es[f] = __dadd_rn(es[f], __dmul_rn((double)__ldg(A.feat + (size_t)slot * A.F + f), w8[c]));
+        }
+      }
+      for (int f = 0; f < A.F; ++f) x[nin++] = (float)es[f];
+      double sh[16];
+      sh_encode(rec.d, sh);
+#pragma unroll
+      for (int q = 0; q < 16; ++q) x[nin + q] = (float)sh[q];
+      nin += 16;
+      if (A.refine_opacity) x[nin++] = (float)clampd(alpha_c, 1e-4, 1.0 - 1e-4);
+      if (A.use_diffuse_color && A.has_dif) {
+        float dv[4];
+        atlas_query<4>(A.dif, rec.p, dv);
+        cd[0] = dv[0]; cd[1] = dv[1]; cd[2] = dv[2];
+        tint = dv[3];
+      }
+      if (!A.use_tint) tint = 0.5;
+      ++n_fs;
+    }
+    tc_write_x(S.A, tid, x, valid ? nin : 0);
+    float z4[4];
+    tc_mlp_rows(S.A, S.W, S.fp, tmem, S.bar_mma, mma_phase, tid, z4);
+    if (valid) {
+      float fs_out[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        fs_out[j] = A.fs.act[j] == 0 ? z4[j] : (A.fs.act[j] == 1 ? sigmoidf_np(z4[j]) : expf(z4[j]));
+      const double ac = clampd(alpha_c, 1e-4, 1.0 - 1e-4);
+      const double z = (double)fs_out[3];
+      double alpha;
+      if (!A.use_opacity) alpha = clampd(alpha_c, 0.0, 1.0);
+      else if (A.refine_opacity) alpha = sigmoid_np(z + log(ac / (1.0 - ac)));
+      else alpha = sigmoid_np(z);
+      float4 o;
+      o.x = (float)clampd(__dadd_rn(cd[0], __dmul_rn(tint, (double)fs_out[0])), 0.0, 1.0);
+      o.y = (float)clampd(__dadd_rn(cd[1], __dmul_rn(tint, (double)fs_out[1])), 0.0, 1.0);
+      o.z = (float)clampd(__dadd_rn(cd[2], __dmul_rn(tint, (double)fs_out[2])), 0.0, 1.0);
+      o.w = (float)alpha;
+      float dep = (float)__ddiv_rn(t_obj, I.scale);
+      if (o.w <= 0.f) {
+        o = make_float4(0.f, 0.f, 0.f, 0.f);
+        dep = __int_as_float(0x7f800000);
+      }
+      const long long q = args.mode == kModeScene ? (long long)ordinal * args.layer_stride + out_idx
+                                                  : (long long)out_idx;
+      reinterpret_cast<float4 *>(args.rgba)[q] = o;
+      args.depth[q] = dep;
+    }
+  }
+  const unsigned lane = tid & 31;
+#pragma unroll
+  for (int off = 16; off; off >>= 1) n_fs += __shfl_xor_sync(0xffffffffu, n_fs, off);
+  if (lane == 0 && n_fs) {
+    atomicAdd(args.counters + 0, n_fs);
+    atomicAdd(args.counters + 2, n_fs);
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tc::tmem_free<64>(tmem);
+}
+
+// The specular MLP alone on n input rows (numerics tests): X (n, in) f32 ->
+// out (n, 4) post-head, via the same tcgen05 routine (mode BF16) or the fp32
+// CUDA-core routine (mode FP32).
+__global__ void __launch_bounds__(kTcThreads) k_mlp_tc(const DevAsset *Ap, const float *X, long long n, float *out) {
+  extern __shared__ uint8_t smem_raw[];
+  const TcSmemPtrs S = tc_carve(smem_raw);
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const DevAsset &A = *Ap;
+  if (warp == 0) tc::tmem_alloc<64>(S.tmem_slot);
+  if (tid == 0) {
+    tc::mbar_init(S.bar_mma, 1);
+    tc::mbar_init(S.bar_tma, 1);
+    tc::mbar_fence_init();
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = *S.tmem_slot;
+  uint32_t mma_phase = 0, tma_phase = 0;
+  bool phi_smem;
+  tc_stage_asset(A, S, tma_phase, tid, phi_smem);
+  __syncthreads();
+  const int in = A.fs.in;
+  for (long long row0 = (long long)blockIdx.x * kTcThreads; row0 < n; row0 += (long long)gridDim.x * kTcThreads) {
+    const long long r = row0 + tid;
+    float x[kTcK0];
+    for (int i = 0; i < in; ++i) x[i] = r < n ? X[r * in + i] : 0.f;
+    tc_write_x(S.A, tid, x, r < n ? in : 0);
+    float z4[4];
+    tc_mlp_rows(S.A, S.W, S.fp, tmem, S.bar_mma, mma_phase, tid, z4);
+    if (r < n)
+      for (int j = 0; j < 4; ++j)
+        out[r * 4 + j] = A.fs.act[j] == 0 ? z4[j] : (A.fs.act[j] == 1 ? sigmoidf_np(z4[j]) : expf(z4[j]));
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tc::tmem_free<64>(tmem);
+}
+
+__global__ void __launch_bounds__(kShadeThreads) k_mlp_fp32(const DevAsset *Ap, const float *X, long long n,
+                                                            float *out) {
+  extern __shared__ __align__(16) float smem[];
+  float *s_fs = smem;
+  float *s_x = smem + MlpOff::total;
+  const DevAsset &A = *Ap;
+  for (int q = threadIdx.x; q < MlpOff::total; q += kShadeThreads) s_fs[q] = A.fs.params[q];
+  __syncthreads();
+  for (long long r = (long long)blockIdx.x * kShadeThreads + threadIdx.x; r < n;
+       r += (long long)gridDim.x * kShadeThreads) {
+    float *xcol = s_x + threadIdx.x;
+    for (int i = 0; i < A.fs.in; ++i) xcol[i * kShadeThreads] = X[r * A.fs.in + i];
+    float o[4];
+    mlp_row(s_fs, A.fs.n_layers, A.fs.in, A.fs.act, xcol, o);
+    for (int j = 0; j < 4; ++j) out[r * 4 + j] = o[j];
+  }
+}
+
+}  // namespace nolf

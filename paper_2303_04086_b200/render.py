@@ -55,6 +55,26 @@ def _stream_ptr():
 
 
 # ------------------------------------------------------------------ assets
+MLP_MODES = {"fp32": N.MLP_FP32, "bf16": N.MLP_BF16}
+_MLP_MODE = N.MLP_FP32
+
+
+def set_mlp_mode(mode: str) -> None:
+    """Specular-MLP arithmetic for subsequent renders: "fp32" (CUDA cores,
+    tolerance 1e-3) or "bf16" (tcgen05 tensor cores, tolerance 2/255).
+    Assets that need the live diffuse network always shade in fp32."""
+    global _MLP_MODE
+    if mode not in MLP_MODES:
+        raise errors.ConfigError(f"unknown MLP mode {mode!r}; have {sorted(MLP_MODES)}")
+    _MLP_MODE = MLP_MODES[mode]
+
+
+def bf16_capable(asset) -> bool:
+    m = asset.specular_mlp
+    return (m is not None and len(m.weights) == 3 and m.weights[0].shape[1] <= 32
+            and (asset.diffuse_atlas is not None or not asset.wiring.use_diffuse_color))
+
+
 class DeviceAsset:
     """Owns one nolf_asset_t (device copy of every table of an asset)."""
 
@@ -66,9 +86,13 @@ class DeviceAsset:
         self.handle = h
         self.device_index = device_index
         self.nbytes = int(N.lib().nolf_asset_device_bytes(h))
+        self.mode = N.MLP_FP32
+        self.bf16_ok = bf16_capable(asset)
 
     def set_mlp_mode(self, mode: int) -> None:
-        N.check(N.lib().nolf_asset_set_mlp_mode(self.handle, int(mode)))
+        if mode != self.mode:
+            N.check(N.lib().nolf_asset_set_mlp_mode(self.handle, int(mode)))
+            self.mode = mode
 
     def __del__(self):
         h = getattr(self, "handle", None)
@@ -151,6 +175,7 @@ def _instance(asset, transform=None) -> N.Instance:
     w2o = np.linalg.inv(o2w)                      # lightfield.py:408
     scale = uniform_scale_of(w2o)                 # lightfield.py:409
     dev = device_asset(asset)
+    dev.set_mlp_mode(_MLP_MODE if dev.bf16_ok else N.MLP_FP32)
     inst = N.Instance()
     inst.asset = dev.handle
     flat = w2o.reshape(16)
@@ -172,6 +197,18 @@ def _merge(counters, cnt_dev):
 
 
 # ------------------------------------------------------------------ reference API
+def mlp_eval(asset, x, mode: str = "fp32"):
+    """The specular network alone on rows x (n, in) -> (n, 4) post-head
+    (nolf_mlp_eval; used by the numerics tests)."""
+    t = torch()
+    dev = _device()
+    xa = t.as_tensor(np.ascontiguousarray(x, np.float32)).to(dev)
+    out = t.empty((len(xa), 4), dtype=t.float32, device=dev)
+    N.check(N.lib().nolf_mlp_eval(device_asset(asset).handle, MLP_MODES[mode], xa.data_ptr(), len(xa),
+                                  out.data_ptr(), _stream_ptr()))
+    return out.cpu().numpy()
+
+
 def render_rays(asset, origins, dirs, counters=None):
     """World-space rays -> (rgba (B,4) f32, depth (B,) f32); lightfield.py:400-456."""
     t = torch()
@@ -311,7 +348,7 @@ class SceneRenderer:
 
     def mlp_mode(self, mode: int) -> None:
         for inst in self.insts:
-            inst._dev.set_mlp_mode(mode)
+            inst._dev.set_mlp_mode(mode if inst._dev.bf16_ok else N.MLP_FP32)
 
     def alloc(self, n_tiles: int, tile_stride: int, want_f32=True, want_u8=True):
         t = torch()
