@@ -231,7 +231,9 @@ def run_ours(args):
 
     from paper_2303_04086_b200 import _native as N
     from paper_2303_04086_b200 import build as B
-    from paper_2303_04086_b200.render import SceneRenderer, frame_tiles, unpack_index
+    from paper_2303_04086_b200.dist import (gather_to_root, rank_buffer_bytes, shard_tiles,
+                                            slot_tile_table)
+    from paper_2303_04086_b200.render import SceneRenderer, frame_tiles
     B.build()
 
     scene = build_scene(args.assets)
@@ -242,12 +244,10 @@ def run_ours(args):
     stride = T * T
     tiles = frame_tiles(W, H, T)
     n_tiles = len(tiles)
-    n_max = math.ceil(n_tiles / world)
-    mine = tiles[rank::world]
-    pad = np.zeros((n_max - len(mine), 5), np.int32)      # empty tiles: no pixels
-    my_tiles = torch.from_numpy(np.concatenate([mine, pad]).astype(np.int32)).to(dev)
+    mine, n_max = shard_tiles(tiles, world, rank)         # tile t -> rank t mod N
+    my_tiles = torch.from_numpy(mine).to(dev)
     P = n_max * stride
-    buf = torch.empty(P * 6, dtype=torch.uint8, device=dev)   # rgba8 | depth16 (encode_frame RAW)
+    buf = torch.empty(rank_buffer_bytes(n_max, stride), dtype=torch.uint8, device=dev)  # rgba8 | depth16
     rgba8 = buf[:P * 4]
     depth16 = buf[P * 4:]
     out = R.alloc(n_max, stride, want_f32=False, want_u8=False)
@@ -255,25 +255,25 @@ def run_ours(args):
     out["depth16"] = depth16
     gathered = torch.empty(world * P * 6, dtype=torch.uint8, device=dev) if world > 1 else None
     # tile of every (rank, slot) in rank-major gather order, for frame assembly
-    slot_tiles = np.zeros((world * n_max, 5), np.int32)
-    for t in range(n_tiles):
-        slot_tiles[(t % world) * n_max + t // world] = tiles[t]
-    slot_tiles_dev = torch.from_numpy(slot_tiles).to(dev)
-    frame = torch.empty((H * W, 4), dtype=torch.uint8, device=dev)
-    frame_d = torch.empty((H * W,), dtype=torch.int16, device=dev)
+    slot_tiles_dev = torch.from_numpy(slot_tile_table(tiles, world)).to(dev)
+    # two frame buffers so the end-to-end loop can download frame k while
+    # frame k+1 renders
+    frames = [(torch.empty((H * W, 4), dtype=torch.uint8, device=dev),
+               torch.empty((H * W,), dtype=torch.int16, device=dev)) for _ in range(2)]
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     n_cam = args.warmup + args.steps + 4
     cam_arrays = [R.camera_array([camera_for_step(k, W, H)]) for k in range(n_cam)]
-    if world == 1:                 # single GPU: compose writes the frame directly
-        out["rgba8"], out["depth16"] = frame, frame_d
     stream = torch.cuda.current_stream().cuda_stream
 
-    def step(k):
+    def step(k, fb=0):
+        frame, frame_d = frames[fb]
+        if world == 1:             # single GPU: compose writes the frame directly
+            out["rgba8"], out["depth16"] = frame, frame_d
         R.render(cam_arrays[k % n_cam], my_tiles, n_max, stride, out, frame_layout=(world == 1))
         if world > 1:
             # frame composer: NCCL gather of every rank's encoded tiles, then
             # one unpack kernel writes the row-major frame on rank 0
-            dist.gather(buf, list(gathered.chunk(world)) if rank == 0 else None, dst=0)
+            gather_to_root(buf, gathered, world, rank)
             if rank == 0:
                 N.check(N.lib().nolf_unpack_gathered(gathered.data_ptr(), world, n_max, stride,
                                                      slot_tiles_dev.data_ptr(), W, H,
@@ -322,26 +322,40 @@ def run_ours(args):
     # ---- end to end: camera in (H2D param block), encoded frame out (D2H) to pinned host
     e2e = None
     if not args.no_e2e:
-        host = torch.empty((H * W * 6,), dtype=torch.uint8, pin_memory=True)
-        host_rgba = host[:H * W * 4].view(H * W, 4)
-        host_d = host[H * W * 4:].view(torch.int16)
+        # Pipelined: step k renders into frame buffer k%2 on the compute
+        # stream; a copy stream downloads it to pinned host memory while
+        # step k+1 renders.  Timed from the first render to the last byte on
+        # the host (device events on both streams).
+        hosts = [torch.empty((H * W * 6,), dtype=torch.uint8, pin_memory=True) for _ in range(2)]
+        copy_stream = torch.cuda.Stream(device=dev)
+        comp = torch.cuda.current_stream()
         for k in range(2):
-            step(k)
+            step(k, k % 2)
         barrier()
-        e_ev = []
+        done_copy = [None, None]
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record(comp)
         for k in range(args.steps):
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record()
-            step(k)
+            fb = k % 2
+            if done_copy[fb] is not None:
+                comp.wait_event(done_copy[fb])       # buffer free again
+            step(k, fb)
             if rank == 0:
-                host_rgba.copy_(frame, non_blocking=True)
-                host_d.copy_(frame_d, non_blocking=True)
-            b.record()
-            b.synchronize()
-            e_ev.append((a, b))
+                rendered = torch.cuda.Event()
+                rendered.record(comp)
+                copy_stream.wait_event(rendered)
+                with torch.cuda.stream(copy_stream):
+                    hosts[fb][:H * W * 4].view(H * W, 4).copy_(frames[fb][0], non_blocking=True)
+                    hosts[fb][H * W * 4:].view(torch.int16).copy_(frames[fb][1], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(copy_stream)
+                done_copy[fb] = ev
+        comp.wait_stream(copy_stream)
+        t1.record(comp)
+        t1.synchronize()
         barrier()
-        te = torch.tensor([sum(a.elapsed_time(b) for a, b in e_ev) / 1e3], dtype=torch.float64,
-                          device=dev)
+        te = torch.tensor([t0.elapsed_time(t1) / 1e3], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e2e = {"value": args.steps * npix / float(te.item()) / 1e6, "unit": UNIT,

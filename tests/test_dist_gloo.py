@@ -1,0 +1,85 @@
+"""World-size-2 (gloo, CPU) test of the multi-GPU frame composer's host
+logic: tile sharding, the single gather of every rank's encoded tiles, and
+the rank-major slot table rank 0 uses to assemble the frame."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2303_04086_b200.dist import (gather_to_root, rank_buffer_bytes, shard_tiles,
+                                        slot_tile_table)
+from paper_2303_04086_b200.render import frame_tiles
+
+W, H, T = 70, 45, 16
+STRIDE = T * T
+
+
+def pixel_code(x, y):
+    return ((x * 7 + y * 13) % 251).astype(np.uint8)
+
+
+def worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        tiles = frame_tiles(W, H, T)
+        mine, n_max = shard_tiles(tiles, world, rank)
+        P = n_max * STRIDE
+        buf = np.zeros(rank_buffer_bytes(n_max, STRIDE), np.uint8)
+        rgba = buf[:P * 4].reshape(P, 4)
+        depth = buf[P * 4:].view(np.uint16)
+        for j, (c, x0, y0, x1, y1) in enumerate(mine):   # "render": encode pixel coordinates
+            w = x1 - x0
+            for l in range((x1 - x0) * (y1 - y0)):
+                x, y = x0 + l % w, y0 + l // w
+                rgba[j * STRIDE + l] = [pixel_code(np.int64(x), np.int64(y)), rank + 1, 0, 255]
+                depth[j * STRIDE + l] = y * W + x
+        t = torch.from_numpy(buf)
+        gathered = torch.empty(world * t.numel(), dtype=torch.uint8) if rank == 0 else None
+        out = gather_to_root(t, gathered, world, rank)
+        if rank == 0:
+            g = out.numpy()
+            table = slot_tile_table(tiles, world)
+            frame = np.zeros((H * W, 4), np.uint8)
+            fdepth = np.zeros(H * W, np.uint16)
+            per = rank_buffer_bytes(n_max, STRIDE)
+            for s, (c, x0, y0, x1, y1) in enumerate(table):   # what k_unpack does
+                r, j = divmod(s, n_max)
+                base = g[r * per:(r + 1) * per]
+                w = x1 - x0
+                for l in range(w * (y1 - y0)):
+                    dst = (y0 + l // w) * W + x0 + l % w
+                    frame[dst] = base[(j * STRIDE + l) * 4:(j * STRIDE + l) * 4 + 4]
+                    fdepth[dst] = base[P * 4:].view(np.uint16)[j * STRIDE + l]
+            q.put((frame, fdepth))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_gather_assembles_the_frame():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    procs = [ctx.Process(target=worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    frame, fdepth = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    ys, xs = np.mgrid[0:H, 0:W]
+    assert np.array_equal(fdepth.reshape(H, W), (ys * W + xs).astype(np.uint16))
+    assert np.array_equal(frame[:, 0].reshape(H, W), pixel_code(xs, ys))
+    tiles = frame_tiles(W, H, T)
+    owner = np.zeros((H, W), np.uint8)
+    for t, (c, x0, y0, x1, y1) in enumerate(tiles):
+        owner[y0:y1, x0:x1] = t % 2 + 1
+    assert np.array_equal(frame[:, 1].reshape(H, W), owner)   # tile t rendered by rank t mod 2
