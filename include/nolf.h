@@ -149,8 +149,14 @@ int nolf_asset_destroy(nolf_asset_t asset);
 int nolf_asset_set_mlp_mode(nolf_asset_t asset, int mode);
 int64_t nolf_asset_device_bytes(nolf_asset_t asset);
 
-/* Workspace bytes needed for up to n_rays rays x n_inst placed assets. */
+/* Workspace bytes sufficient for any call with up to n_rays rays x n_inst
+ * placed assets (upper bound). */
 size_t nolf_workspace_bytes(int32_t n_inst, int64_t n_rays);
+/* Tight workspace bytes for nolf_render_scene with these instances and
+ * cameras over n_rays pixel slots (hit queues sized by each instance's
+ * screen box, compose layers by the maximum box overlap); 0 on bad input. */
+size_t nolf_scene_workspace_bytes(const NolfInstance *inst, int32_t n_inst, const NolfCamera *cams,
+                                  int32_t n_cams, int64_t n_rays);
 
 /* counters: device uint64[4] accumulated (not reset). */
 int nolf_render_rays(const NolfInstance *inst, const double *origins, int32_t origin_stride,

@@ -88,6 +88,7 @@ def lib():
         "nolf_asset_set_mlp_mode": ([vp, C.c_int], C.c_int),
         "nolf_asset_device_bytes": ([vp], i64),
         "nolf_workspace_bytes": ([i32, i64], C.c_size_t),
+        "nolf_scene_workspace_bytes": ([C.POINTER(Instance), i32, C.POINTER(Camera), i32, i64], C.c_size_t),
         "nolf_render_rays": ([C.POINTER(Instance), vp, i32, vp, i64, vp, vp, vp, vp, C.c_size_t, vp],
                              C.c_int),
         "nolf_render_rect": ([C.POINTER(Instance), C.POINTER(Camera), i32, i32, i32, i32, vp, vp, vp,

@@ -206,31 +206,33 @@ size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 struct Workspace {
   unsigned int *counts;
   HitRec *queue;
-  long long cap;
   uint8_t *nhit;
   float *lrgba, *ldepth;
+  long long P;                 // pixel slots (layer stride)
 };
 
-size_t ws_layout(int n_inst, int64_t n_rays, char *base, Workspace *w) {
+// queue_recs: total hit-record capacity over instances; layers: compose
+// layers per pixel slot (scene mode), P: pixel slots.
+size_t ws_layout(int n_inst, long long queue_recs, int layers, long long P, char *base, Workspace *w) {
   size_t off = 0;
   auto take = [&](size_t bytes) {
     size_t o = off;
     off = align_up(off + bytes, 256);
     return base ? base + o : nullptr;
   };
-  const size_t n = (size_t)(n_rays > 0 ? n_rays : 1);
+  const size_t n = (size_t)(P > 0 ? P : 1);
   char *counts = take(sizeof(unsigned) * (size_t)(n_inst > 0 ? n_inst : 1));
-  char *queue = take(sizeof(HitRec) * n * (size_t)n_inst);
-  char *nhit = take(n);
-  char *lrgba = take(sizeof(float) * 4 * n * (size_t)n_inst);
-  char *ldepth = take(sizeof(float) * n * (size_t)n_inst);
+  char *queue = take(sizeof(HitRec) * (size_t)(queue_recs > 0 ? queue_recs : 1));
+  char *nhit = take(layers > 0 ? n : 1);
+  char *lrgba = take(sizeof(float) * 4 * n * (size_t)layers);
+  char *ldepth = take(sizeof(float) * n * (size_t)layers);
   if (w) {
     w->counts = reinterpret_cast<unsigned *>(counts);
     w->queue = reinterpret_cast<HitRec *>(queue);
-    w->cap = (long long)n;
     w->nhit = reinterpret_cast<uint8_t *>(nhit);
     w->lrgba = reinterpret_cast<float *>(lrgba);
     w->ldepth = reinterpret_cast<float *>(ldepth);
+    w->P = (long long)n;
   }
   return off;
 }
@@ -245,8 +247,8 @@ int fill_inst(const NolfInstance *in, DevInst *out) {
   return 0;
 }
 
-int run_shade(const DevInst *inst, int n_inst, const Workspace &w, int mode, float *rgba, float *depth,
-              long long layer_stride, unsigned long long *counters, cudaStream_t st, bool use_tc);
+int run_shade(const DevInst *inst, const long long *qoff, int n_inst, const Workspace &w, int mode, float *rgba,
+              float *depth, long long layer_stride, unsigned long long *counters, cudaStream_t st, bool use_tc);
 
 }  // namespace
 
@@ -256,10 +258,11 @@ struct ParamBlock {
   DevInst inst[kMaxInst];
   CamParams cams[kMaxCams];
   TileParams rect;
+  long long qoff[kMaxInst + 1];          // hit-queue offset of every instance
   ScreenBox cull[kMaxInst * kMaxCams];   // only the used prefix is copied
 };
 
-size_t param_bytes(int n_inst, int n_cams) {
+size_t param_bytes(int n_inst, int n_cams) {   // cull tail is n_inst x n_cams
   return offsetof(ParamBlock, cull) + sizeof(ScreenBox) * (size_t)n_inst * (size_t)(n_cams > 0 ? n_cams : 1);
 }
 
@@ -309,6 +312,80 @@ ScreenBox screen_box(const NolfInstance &in, const DevAsset &H, const CamParams 
   return ScreenBox{clampi64(floor(xmin) - 2), clampi64(floor(ymin) - 2), clampi64(ceil(xmax) + 2),
                    clampi64(ceil(ymax) + 2)};
 }
+// Per-launch memory plan.  A pixel yields at most one hit per instance and
+// only inside the instance's screen box, so the box area (clipped to the
+// frame, or to the rect) bounds the instance's hit queue; the number of
+// boxes overlapping any pixel bounds its compose layers.
+struct Plan {
+  std::vector<ScreenBox> cull;   // [n_inst * n_cams]
+  std::vector<long long> qoff;   // n_inst + 1
+  int layers = 0;
+  size_t bytes = 0;
+};
+
+long long box_area(const ScreenBox &b, int x0, int y0, int x1, int y1) {   // [x0,x1) x [y0,y1)
+  const long long w = (long long)std::min(b.x1 + 1, x1) - std::max(b.x0, x0);
+  const long long h = (long long)std::min(b.y1 + 1, y1) - std::max(b.y0, y0);
+  return (w > 0 && h > 0) ? w * h : 0;
+}
+
+void make_plan(int mode, const NolfInstance *ins, int n_inst, const CamParams *cams, int n_cams, TileParams rect,
+               long long n_rays, Plan &pl) {
+  pl.qoff.assign((size_t)n_inst + 1, 0);
+  pl.cull.clear();
+  if (mode == kModeRays || n_cams == 0) {
+    for (int k = 0; k < n_inst; ++k) pl.qoff[(size_t)k + 1] = pl.qoff[(size_t)k] + n_rays;
+    pl.layers = mode == kModeScene ? n_inst : 0;
+  } else {
+    pl.cull.resize((size_t)n_inst * n_cams);
+    for (int k = 0; k < n_inst; ++k)
+      for (int c = 0; c < n_cams; ++c) pl.cull[(size_t)k * n_cams + c] = screen_box(ins[k], ins[k].asset->host, cams[c]);
+    for (int k = 0; k < n_inst; ++k) {
+      long long cap = 0;
+      for (int c = 0; c < n_cams; ++c) {
+        const ScreenBox &b = pl.cull[(size_t)k * n_cams + c];
+        cap += mode == kModeRect ? box_area(b, rect.x0, rect.y0, rect.x1, rect.y1)
+                                 : box_area(b, 0, 0, cams[c].width, cams[c].height);
+      }
+      pl.qoff[(size_t)k + 1] = pl.qoff[(size_t)k] + std::min(cap, n_rays);
+    }
+    int L = 1;
+    if (mode == kModeScene) {
+      for (int c = 0; c < n_cams; ++c)
+        for (int i = 0; i < n_inst; ++i)
+          for (int j = 0; j < n_inst; ++j) {
+            const ScreenBox &bi = pl.cull[(size_t)i * n_cams + c], &bj = pl.cull[(size_t)j * n_cams + c];
+            const int px = std::max(bi.x0, 0), py = std::max(bj.y0, 0);
+            if (px >= cams[c].width || py >= cams[c].height) continue;
+            int cnt = 0;
+            for (int k = 0; k < n_inst; ++k) {
+              const ScreenBox &b = pl.cull[(size_t)k * n_cams + c];
+              cnt += px >= b.x0 && px <= b.x1 && py >= b.y0 && py <= b.y1;
+            }
+            L = std::max(L, cnt);
+          }
+    }
+    pl.layers = mode == kModeScene ? L : 0;
+  }
+  pl.bytes = ws_layout(n_inst, pl.qoff[(size_t)n_inst], pl.layers, n_rays, nullptr, nullptr);
+}
+
+void fill_cams(const NolfCamera *cams, int n_cams, CamParams *out) {
+  long long pix_base = 0;
+  for (int c = 0; c < n_cams; ++c) {
+    const NolfCamera &C = cams[c];
+    for (int q = 0; q < 16; ++q) out[c].pose[q] = C.pose[q];
+    out[c].fx = C.fx;
+    out[c].fy = C.fy;
+    out[c].cx = C.cx;
+    out[c].cy = C.cy;
+    out[c].width = C.width;
+    out[c].height = C.height;
+    out[c].pix_base = pix_base;
+    pix_base += (long long)C.width * C.height;
+  }
+}
+
 }  // namespace
 
 extern "C" {
@@ -466,19 +543,33 @@ int nolf_asset_set_mlp_mode(nolf_asset_t a, int mode) {
 
 int64_t nolf_asset_device_bytes(nolf_asset_t a) { return a ? a->bytes : 0; }
 
-size_t nolf_workspace_bytes(int32_t n_inst, int64_t n_rays) { return ws_layout(n_inst, n_rays, nullptr, nullptr); }
+size_t nolf_workspace_bytes(int32_t n_inst, int64_t n_rays) {
+  return ws_layout(n_inst, (long long)n_inst * n_rays, n_inst, n_rays, nullptr, nullptr);
+}
+
+size_t nolf_scene_workspace_bytes(const NolfInstance *inst, int32_t n_inst, const NolfCamera *cams, int32_t n_cams,
+                                  int64_t n_rays) {
+  if (!inst || !cams || n_inst < 1 || n_inst > kMaxInst || n_cams < 1 || n_cams > kMaxCams) return 0;
+  for (int k = 0; k < n_inst; ++k)
+    if (!inst[k].asset) return 0;
+  std::vector<CamParams> cp((size_t)n_cams);
+  fill_cams(cams, n_cams, cp.data());
+  Plan pl;
+  make_plan(kModeScene, inst, n_inst, cp.data(), n_cams, TileParams{0, 0, 0, 0, 0}, n_rays, pl);
+  return pl.bytes;
+}
 
 }  // extern "C"
 
 namespace {
 
-int run_shade(const DevInst *inst, int n_inst, const Workspace &w, int mode, float *rgba, float *depth,
-              long long layer_stride, unsigned long long *counters, cudaStream_t st, bool use_tc) {
+int run_shade(const DevInst *inst, const long long *qoff, int n_inst, const Workspace &w, int mode, float *rgba,
+              float *depth, long long layer_stride, unsigned long long *counters, cudaStream_t st, bool use_tc) {
   ShadeArgs sa{};
   sa.inst = inst;
   sa.n_inst = n_inst;
   sa.queue = w.queue;
-  sa.cap = w.cap;
+  sa.qoff = qoff;
   sa.counts = w.counts;
   sa.mode = mode;
   sa.rgba = rgba;
@@ -555,12 +646,17 @@ int launch_march_shade(int mode, const NolfInstance *ins, int n_inst, const Nolf
   if (n_cams > kMaxCams) return fail(NOLF_EINVAL, "camera count %d > %d", n_cams, kMaxCams);
   if (!counters) return fail(NOLF_EINVAL, "counters pointer required");
   if (mode == kModeScene && n_inst > 255) return fail(NOLF_EINVAL, "too many layers");
-  const size_t need = ws_layout(n_inst, n_rays, nullptr, nullptr);
-  if (!workspace || ws_bytes < need) return fail(NOLF_EINVAL, "workspace too small: %zu < %zu", ws_bytes, need);
+  for (int k = 0; k < n_inst; ++k)
+    if (!ins[k].asset) return fail(NOLF_EINVAL, "null asset instance");
+  std::vector<CamParams> hcams((size_t)std::max(n_cams, 1));
+  fill_cams(cams, n_cams, hcams.data());
+  thread_local Plan pl;
+  make_plan(mode, ins, n_inst, hcams.data(), n_cams, rect, n_rays, pl);
+  if (!workspace || ws_bytes < pl.bytes) return fail(NOLF_EINVAL, "workspace too small: %zu < %zu", ws_bytes, pl.bytes);
   int rc;
   if ((rc = ensure_attrs())) return rc;
   Workspace w;
-  ws_layout(n_inst, n_rays, static_cast<char *>(workspace), &w);
+  ws_layout(n_inst, pl.qoff[(size_t)n_inst], pl.layers, n_rays, static_cast<char *>(workspace), &w);
   ParamBlock *hp, *dp;
   int slot;
   if ((rc = ring_acquire(&hp, &dp, &slot))) return rc;
@@ -569,22 +665,10 @@ int launch_march_shade(int mode, const NolfInstance *ins, int n_inst, const Nolf
     if ((rc = fill_inst(ins + k, hp->inst + k))) return rc;
     use_tc = use_tc && ins[k].asset->host.mlp_mode == NOLF_MLP_BF16;
   }
-  long long pix_base = 0;
-  for (int c = 0; c < n_cams; ++c) {
-    const NolfCamera &C = cams[c];
-    for (int q = 0; q < 16; ++q) hp->cams[c].pose[q] = C.pose[q];
-    hp->cams[c].fx = C.fx;
-    hp->cams[c].fy = C.fy;
-    hp->cams[c].cx = C.cx;
-    hp->cams[c].cy = C.cy;
-    hp->cams[c].width = C.width;
-    hp->cams[c].height = C.height;
-    hp->cams[c].pix_base = pix_base;
-    pix_base += (long long)C.width * C.height;
-  }
+  for (int c = 0; c < n_cams; ++c) hp->cams[c] = hcams[(size_t)c];
   hp->rect = rect;
-  for (int k = 0; k < n_inst && n_cams > 0; ++k)
-    for (int c = 0; c < n_cams; ++c) hp->cull[k * n_cams + c] = screen_box(ins[k], ins[k].asset->host, hp->cams[c]);
+  for (int k = 0; k <= n_inst; ++k) hp->qoff[k] = pl.qoff[(size_t)k];
+  for (size_t i = 0; i < pl.cull.size(); ++i) hp->cull[i] = pl.cull[i];
   CUDA_TRY(cudaMemcpyAsync(dp, hp, param_bytes(n_inst, n_cams), cudaMemcpyHostToDevice, st));
   if ((rc = ring_release(slot, st))) return rc;
   if (n_rays == 0) return 0;
@@ -603,7 +687,7 @@ int launch_march_shade(int mode, const NolfInstance *ins, int n_inst, const Nolf
   ma.cull = n_cams > 0 ? dp->cull : nullptr;
   ma.n_cams = n_cams > 0 ? n_cams : 1;
   ma.queue = w.queue;
-  ma.cap = w.cap;
+  ma.qoff = dp->qoff;
   ma.counts = w.counts;
   ma.rgba = rgba;
   ma.depth = depth;
@@ -617,7 +701,7 @@ int launch_march_shade(int mode, const NolfInstance *ins, int n_inst, const Nolf
   CUDA_TRY(cudaGetLastError());
   if ((rc = prof_mark(1, st))) return rc;
   if (mode == kModeScene) {
-    if ((rc = run_shade(dp->inst, n_inst, w, mode, w.lrgba, w.ldepth, (long long)w.cap, counters, st, use_tc)))
+    if ((rc = run_shade(dp->inst, dp->qoff, n_inst, w, mode, w.lrgba, w.ldepth, w.P, counters, st, use_tc)))
       return rc;
     if ((rc = prof_mark(2, st))) return rc;
     ComposeArgs ca{};
@@ -626,7 +710,7 @@ int launch_march_shade(int mode, const NolfInstance *ins, int n_inst, const Nolf
     ca.K = 0;
     ca.rgba = w.lrgba;
     ca.depth = w.ldepth;
-    ca.layer_stride = w.cap;
+    ca.layer_stride = w.P;
     ca.tiles = reinterpret_cast<const TileParams *>(tiles_dev);
     ca.tile_stride = tile_stride;
     ca.cams = dp->cams;
@@ -641,7 +725,7 @@ int launch_march_shade(int mode, const NolfInstance *ins, int n_inst, const Nolf
     CUDA_TRY(cudaGetLastError());
     if ((rc = prof_mark(3, st))) return rc;
   } else {
-    if ((rc = run_shade(dp->inst, n_inst, w, mode, rgba, depth, 0, counters, st, use_tc))) return rc;
+    if ((rc = run_shade(dp->inst, dp->qoff, n_inst, w, mode, rgba, depth, 0, counters, st, use_tc))) return rc;
     if ((rc = prof_mark(2, st))) return rc;
     if ((rc = prof_mark(3, st))) return rc;
   }
@@ -706,6 +790,8 @@ int nolf_march_rays(nolf_asset_t asset, const double *origins, int32_t origin_st
   memset(&hp->inst[0], 0, sizeof(DevInst));
   hp->inst[0].a = asset->dev;
   hp->inst[0].scale = 1.0;
+  hp->qoff[0] = 0;
+  hp->qoff[1] = 0;
   CUDA_TRY(cudaMemcpyAsync(dp, hp, param_bytes(1, 0), cudaMemcpyHostToDevice, st));
   if ((rc = ring_release(slot, st))) return rc;
   MarchArgs ma{};

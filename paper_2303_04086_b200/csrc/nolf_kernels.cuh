@@ -46,8 +46,8 @@ struct MarchArgs {
   const ScreenBox *cull;       // [n_inst * n_cams] (NULL: no culling)
   int n_cams;
   // outputs
-  HitRec *queue;               // n_inst * cap records
-  long long cap;               // per-instance capacity
+  HitRec *queue;               // per-instance queues at qoff[k] .. qoff[k+1]
+  const long long *qoff;
   unsigned int *counts;        // n_inst
   float *rgba;                 // kModeRays/kModeRect: miss init (n, 4)
   float *depth;
@@ -206,13 +206,9 @@ __global__ void __launch_bounds__(128) k_march(MarchArgs args) {
       if (local >= (long long)w * h) {
         valid = false;
       } else {
-        const CamParams &cp = args.cams[tp.cam];
         cam = tp.cam;
         pix_x = tp.x0 + (int)(local % w);
         pix_y = tp.y0 + (int)(local / w);
-        double px = (double)pix_x, py = (double)pix_y;
-        camera_dir(cp.pose, cp.fx, cp.fy, cp.cx, cp.cy, px, py, dw);
-        ow[0] = cp.pose[3]; ow[1] = cp.pose[7]; ow[2] = cp.pose[11];
       }
     }
     if (MODE != kModeScene && valid && args.rgba) {   // miss defaults (lightfield.py:415-416)
@@ -238,6 +234,12 @@ __global__ void __launch_bounds__(128) k_march(MarchArgs args) {
   }
   unsigned long long wmask = ((unsigned long long)__reduce_or_sync(0xffffffffu, (unsigned)(lane_mask >> 32)) << 32) |
                              __reduce_or_sync(0xffffffffu, (unsigned)lane_mask);
+  // camera ray (core.py:162-170) only for pixels some instance may cover
+  if (MODE != kModeRays && lane_mask) {
+    const CamParams &cp = args.cams[cam];
+    camera_dir(cp.pose, cp.fx, cp.fy, cp.cx, cp.cy, (double)pix_x, (double)pix_y, dw);
+    ow[0] = cp.pose[3]; ow[1] = cp.pose[7]; ow[2] = cp.pose[11];
+  }
   while (wmask) {
     const int k = __ffsll((long long)wmask) - 1;
     wmask &= wmask - 1;
@@ -298,7 +300,7 @@ __global__ void __launch_bounds__(128) k_march(MarchArgs args) {
         rec.d[0] = d[0]; rec.d[1] = d[1]; rec.d[2] = d[2];
         rec.out_idx = (uint32_t)gid;
         rec.ordinal = ordinal;
-        if ((long long)pos < args.cap) args.queue[(long long)k * args.cap + pos] = rec;
+        if ((long long)pos < args.qoff[k + 1] - args.qoff[k]) args.queue[args.qoff[k] + pos] = rec;
         ++ordinal;
       }
     }
@@ -315,7 +317,7 @@ struct ShadeArgs {
   const DevInst *inst;
   int n_inst;
   const HitRec *queue;
-  long long cap;
+  const long long *qoff;
   const unsigned int *counts;
   int mode;                    // RayMode
   float *rgba;                 // rays/rect: (n,4); scene: layers (L, P, 4)
@@ -405,7 +407,7 @@ __global__ void __launch_bounds__(kShadeThreads) k_shade(ShadeArgs args) {
     long long t = tile;
     unsigned cnt = 0;
     for (; k < args.n_inst; ++k) {
-      cnt = min((long long)args.counts[k], args.cap);
+      cnt = min((long long)args.counts[k], args.qoff[k + 1] - args.qoff[k]);
       long long nt = (cnt + kShadeThreads - 1) / kShadeThreads;
       if (t < nt) break;
       t -= nt;
@@ -424,7 +426,7 @@ __global__ void __launch_bounds__(kShadeThreads) k_shade(ShadeArgs args) {
     }
     const long long r = t * kShadeThreads + tid;
     if (r >= cnt) continue;
-    const HitRec rec = args.queue[(long long)k * args.cap + r];
+    const HitRec rec = args.queue[args.qoff[k] + r];
     float *xcol = s_x + tid;
     // PSH encode (encoding.py:390-394)
     int base[3];

@@ -197,7 +197,7 @@ __global__ void __launch_bounds__(kTcThreads) k_shade_tc(ShadeArgs args) {
     long long t = tile;
     unsigned cnt = 0;
     for (; k < args.n_inst; ++k) {
-      cnt = min((long long)args.counts[k], args.cap);
+      cnt = min((long long)args.counts[k], args.qoff[k + 1] - args.qoff[k]);
       const long long nt = (cnt + kTcThreads - 1) / kTcThreads;
       if (t < nt) break;
       t -= nt;
@@ -219,7 +219,7 @@ __global__ void __launch_bounds__(kTcThreads) k_shade_tc(ShadeArgs args) {
     double cd[3] = {0.0, 0.0, 0.0}, tint = 1.0, alpha_c = 0.0, t_obj = 0.0;
     uint32_t out_idx = 0, ordinal = 0;
     if (valid) {
-      const HitRec rec = args.queue[(long long)k * args.cap + r];
+      const HitRec rec = args.queue[args.qoff[k] + r];
       alpha_c = rec.alpha_c;
       t_obj = rec.t_obj;
       out_idx = rec.out_idx;

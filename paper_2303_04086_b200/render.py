@@ -361,11 +361,20 @@ class SceneRenderer:
             out["rgba8"] = t.empty((P, 4), dtype=t.uint8, device=self.device)
             out["depth16"] = t.empty((P,), dtype=t.int16, device=self.device)
         out["counters"] = t.zeros(4, dtype=t.int64, device=self.device)
-        need = int(N.lib().nolf_workspace_bytes(len(self.insts), P))
+        return out
+
+    def _workspace(self, cams, P: int):
+        """Tight per-launch workspace (hit queues sized by the instances'
+        screen boxes, compose layers by their maximum overlap)."""
+        t = torch()
+        need = int(N.lib().nolf_scene_workspace_bytes(self._inst_arr, len(self.insts), cams,
+                                                      len(cams), int(P)))
+        if need == 0:
+            raise errors.DomainError("bad scene for workspace sizing")
         if self._ws is None or self._ws.numel() < need:
             self._ws = None
             self._ws = t.empty(need, dtype=t.uint8, device=self.device)
-        return out
+        return self._ws
 
     @staticmethod
     def camera_array(cameras):
@@ -386,10 +395,11 @@ class SceneRenderer:
         so.depth_far = self.depth_far
         so.layout = 1 if frame_layout else 0
         st = stream if stream is not None else _stream_ptr()
-        N.check(N.lib().nolf_render_scene(self._inst_arr, len(self.insts), cams, len(cameras),
+        ws = self._workspace(cams, int(n_tiles) * int(tile_stride))
+        N.check(N.lib().nolf_render_scene(self._inst_arr, len(self.insts), cams, len(cams),
                                           tiles_dev.data_ptr(), int(n_tiles), C.byref(so),
                                           self.alpha_vis, out["counters"].data_ptr(),
-                                          self._ws.data_ptr(), self._ws.numel(), st))
+                                          ws.data_ptr(), ws.numel(), st))
 
 
 def unpack_index(tiles: np.ndarray, tile_stride: int, width: int, height: int, cam: int = 0):
