@@ -187,9 +187,11 @@ int nolf_march_rays(nolf_asset_t asset, const double *origins, int32_t origin_st
  * (c_d, t); what bake_diffuse_cubes caches (lightfield.py:547-576). */
 int nolf_eval_diffuse(nolf_asset_t asset, const double *points, int64_t n, float *out, void *stream);
 
-/* Per-kernel timing of the calling thread's most recent render call: CUDA
- * events on the launching stream around k_march, k_shade, k_compose.
- * nolf_profile_read synchronises and returns 3 durations in ms. */
+/* Per-kernel timing: while enabled, every render call of the calling thread
+ * records CUDA events on its stream around k_march, k_shade, k_compose (up to
+ * 4096 calls).  nolf_profile_read synchronises and returns, in ms[0..2], the
+ * summed durations over all recorded calls; its return value is the call
+ * count (negative on error). */
 int nolf_profile(int enable);
 int nolf_profile_read(float *ms);
 /* Host->device bytes a render call copies (instance, camera, cull tables). */

@@ -623,17 +623,22 @@ int ring_release(int slot, cudaStream_t st) {
 }
 
 // Optional per-kernel timing: CUDA events recorded on the launching stream
-// around k_march / k_shade / k_compose of the most recent render call.
+// around k_march / k_shade / k_compose of every render call, kept in a ring
+// so a whole timed region can be read back after it ends.
+constexpr int kProfRing = 4096;
 struct Prof {
   bool on = false;
   bool created = false;
-  cudaEvent_t ev[4];
+  int calls = 0;               // render calls recorded since nolf_profile(1)
+  cudaEvent_t ev[kProfRing][4];
 };
-thread_local Prof g_prof;
+thread_local Prof *g_prof = nullptr;
 
 int prof_mark(int i, cudaStream_t st) {
-  if (!g_prof.on) return 0;
-  CUDA_TRY(cudaEventRecord(g_prof.ev[i], st));
+  if (!g_prof || !g_prof->on) return 0;
+  if (g_prof->calls >= kProfRing) return 0;
+  CUDA_TRY(cudaEventRecord(g_prof->ev[g_prof->calls][i], st));
+  if (i == 3) ++g_prof->calls;
   return 0;
 }
 
@@ -854,19 +859,34 @@ int nolf_mlp_eval(nolf_asset_t asset, int mode, const float *x, int64_t n, float
 }
 
 int nolf_profile(int enable) {
-  if (enable && !g_prof.created) {
-    for (int i = 0; i < 4; ++i) CUDA_TRY(cudaEventCreate(&g_prof.ev[i]));
-    g_prof.created = true;
+  if (enable && !g_prof) {
+    g_prof = new Prof();
+    for (int c = 0; c < kProfRing; ++c)
+      for (int i = 0; i < 4; ++i) CUDA_TRY(cudaEventCreate(&g_prof->ev[c][i]));
+    g_prof->created = true;
   }
-  g_prof.on = enable != 0;
+  if (g_prof) {
+    g_prof->on = enable != 0;
+    if (enable) g_prof->calls = 0;
+  }
   return 0;
 }
 
+// Sum of per-kernel durations over every render call recorded since
+// nolf_profile(1): ms[0..2] = k_march, k_shade, k_compose; returns calls.
 int nolf_profile_read(float *ms) {
-  if (!g_prof.created) return fail(NOLF_ESTATE, "profiling was never enabled");
-  CUDA_TRY(cudaEventSynchronize(g_prof.ev[3]));
-  for (int i = 0; i < 3; ++i) CUDA_TRY(cudaEventElapsedTime(ms + i, g_prof.ev[i], g_prof.ev[i + 1]));
-  return 0;
+  if (!g_prof) return fail(NOLF_ESTATE, "profiling was never enabled");
+  ms[0] = ms[1] = ms[2] = 0.f;
+  const int n = g_prof->calls;
+  if (n == 0) return 0;
+  CUDA_TRY(cudaEventSynchronize(g_prof->ev[n - 1][3]));
+  for (int c = 0; c < n; ++c)
+    for (int i = 0; i < 3; ++i) {
+      float t = 0.f;
+      CUDA_TRY(cudaEventElapsedTime(&t, g_prof->ev[c][i], g_prof->ev[c][i + 1]));
+      ms[i] += t;
+    }
+  return n;
 }
 
 size_t nolf_launch_param_bytes(int32_t n_inst, int32_t n_cams) { return param_bytes(n_inst, n_cams); }
