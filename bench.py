@@ -44,6 +44,7 @@ def parse():
     p.add_argument("--steps", type=int, default=200)
     p.add_argument("--warmup", type=int, default=10)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--config", type=int, default=4, choices=[1, 3, 4, 5])
     p.add_argument("--width", type=int, default=3840)
     p.add_argument("--height", type=int, default=2160)
     p.add_argument("--assets", type=int, default=12)
@@ -78,6 +79,51 @@ def build_scene(n_assets):
 def camera_for_step(k, width, height):
     from paper_2303_04086_b200 import synth
     return synth.zodiac_camera(width, height, azimuth=0.3 + 0.005 * k)
+
+
+def workload(args):
+    """(scene, views(k) -> [Camera], W, H, description) of a BASELINE config.
+
+    1: single asset, one 256x256 view           (orbit_camera(0.8, 0.3, 2.0))
+    3: single asset, 16 viewpoints at 3840x2160  (orbit azimuth 2 pi v/16, radius 1.5)
+    4: 12-asset zodiac scene at 3840x2160         (the metric's configuration)
+    5: 12-asset scene, 8 users x 2 eyes at 2160x2160 (eyes +-0.032 along camera right)
+    Each step moves the viewpoints slightly (azimuth + 0.005 k)."""
+    import math as m
+
+    from paper_2303_04086_b200 import synth
+    from paper_2303_04086_b200.model import Camera, orbit_camera
+    c = args.config
+    if c in (1, 3):
+        scene = build_scene(1)[:1]
+        scene = [(scene[0][0], np.eye(4))]
+        if c == 1:
+            W = H = 256
+            return scene, (lambda k: [orbit_camera(0.8 + 0.005 * k, 0.3, radius=2.0, size=256)]), W, H, \
+                "BASELINE config 1: single asset (sphere, random-init PSH + MLP), one 256x256 view"
+        W, H = 3840, 2160
+        return scene, (lambda k: [orbit_camera(2 * m.pi * v / 16 + 0.005 * k, 0.3, radius=1.5, width=W,
+                                               height=H) for v in range(16)]), W, H, \
+            "BASELINE config 3: single asset at 3840x2160, 16 simultaneous viewpoints"
+    scene = build_scene(args.assets)
+    if c == 5:
+        W = H = 2160
+
+        def views(k):
+            out = []
+            for u in range(8):
+                base = synth.zodiac_camera(W, H, azimuth=2 * m.pi * u / 8 + 0.005 * k)
+                for eye in (-0.032, 0.032):
+                    pose = base.pose.copy()
+                    pose[:3, 3] += eye * pose[:3, 0]
+                    out.append(Camera(pose=pose, fx=base.fx, fy=base.fy, cx=base.cx, cy=base.cy,
+                                      width=W, height=H))
+            return out
+        return scene, views, W, H, (f"BASELINE config 5: {args.assets}-asset scene, 8 users x 2 eyes "
+                                    f"at 2160x2160")
+    W, H = args.width, args.height
+    return scene, (lambda k: [camera_for_step(k, W, H)]), W, H, (
+        f"BASELINE config 4: {args.assets}-asset zodiac scene at {W}x{H}")
 
 
 # ------------------------------------------------------------------ clocks
@@ -145,7 +191,7 @@ class Clocks:
 
 
 # ------------------------------------------------------------------ CPU reference (oracle port)
-def cpu_sample(scene, cam, tiles, seconds, seed=0, max_tiles=None):
+def cpu_sample(scene, cams, tiles, seconds, seed=0, max_tiles=None):
     """Render + compose random 32x32 tiles with the C oracle (the reference's
     algorithm restated, every fixed march step evaluated) on all host cores
     until ``seconds`` elapse; returns (rays, elapsed, tiles used)."""
@@ -155,10 +201,10 @@ def cpu_sample(scene, cam, tiles, seconds, seed=0, max_tiles=None):
     order = rng.permutation(len(tiles))
     rays, t0, used = 0, time.perf_counter(), 0
     for t in order:
-        _, x0, y0, x1, y1 = (int(v) for v in tiles[t])
+        c, x0, y0, x1, y1 = (int(v) for v in tiles[t])
         rg, dp = [], []
         for oa, tr in oas:
-            r, d = O.render_rect(oa, cam, (x0, y0, x1, y1), transform=tr)
+            r, d = O.render_rect(oa, cams[c], (x0, y0, x1, y1), transform=tr)
             rg.append(r)
             dp.append(d)
         O.compose(np.stack(rg), np.stack(dp))
@@ -176,41 +222,43 @@ def run_reference(args):
     from oracle import oracle as O
     from paper_2303_04086_b200.render import frame_tiles
     O.build()
-    scene = build_scene(args.assets)
-    tiles = frame_tiles(args.width, args.height, args.tile)
+    import torch
+    if torch.cuda.is_available():
+        torch.cuda.set_device(0)        # asset synthesis only; the timed path is CPU
+    scene, views, W, H, desc = workload(args)
+    n_views = len(views(0))
+    tiles = np.concatenate([frame_tiles(W, H, args.tile, cam=v) for v in range(n_views)])
     cores = os.cpu_count()
-    cam = camera_for_step(0, args.width, args.height)
     per_step_tiles = 24
     for w in range(args.warmup):
-        cpu_sample(scene, cam, tiles, 1e9, seed=1000 + w, max_tiles=4)
+        cpu_sample(scene, views(0), tiles, 1e9, seed=1000 + w, max_tiles=4)
     rays = 0
     el = 0.0
     for k in range(args.steps):
-        r, e, _ = cpu_sample(scene, camera_for_step(k, args.width, args.height), tiles, 1e9,
-                             seed=k, max_tiles=per_step_tiles)
+        r, e, _ = cpu_sample(scene, views(k), tiles, 1e9, seed=k, max_tiles=per_step_tiles)
         rays += r
         el += e
     value = rays / el / 1e6
-    npix = args.width * args.height
-    sample = (f"{args.steps} steps x {per_step_tiles} random 32x32 tiles of the 4K frame "
-              f"(12 assets each, oracle render + compose), extrapolated to Mrays/s")
+    npix = n_views * W * H
+    sample = (f"{args.steps} steps x {per_step_tiles} random {args.tile}x{args.tile} tiles of "
+              f"{desc} ({len(scene)} assets each, oracle render + compose on {cores} threads), "
+              f"extrapolated to Mrays/s")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": el / args.steps * 1e3, "fps": value * 1e6 / npix,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": workload_config(args),
+        "data": "synthetic", "config": workload_config(args, desc, W, H, len(scene)),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
                          "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
 
 
-def workload_config(args):
-    return {"workload": (f"BASELINE config 4: {args.assets}-asset zodiac scene at "
-                         f"{args.width}x{args.height}, {args.tile}x{args.tile} ray tiles "
-                         f"interleaved over ranks, NCCL gather of rgba8+u16 to rank 0"),
-            "assets": args.assets, "width": args.width, "height": args.height,
+def workload_config(args, desc, W, H, n_assets):
+    return {"workload": (f"{desc}, {args.tile}x{args.tile} ray tiles interleaved over ranks, "
+                         f"NCCL gather of rgba8+u16 to rank 0"),
+            "assets": n_assets, "width": W, "height": H,
             "atlas_b": 32, "atlas_r": 8, "psh_resolution": 64, "mlp": args.mlp,
             "parallelism": f"ray-tile x{args.gpus}",
             "l2": "flushed between timed steps (256 MiB write)"}
@@ -236,13 +284,14 @@ def run_ours(args):
     from paper_2303_04086_b200.render import SceneRenderer, frame_tiles
     B.build()
 
-    scene = build_scene(args.assets)
+    scene, views, W, H, desc = workload(args)
+    n_views = len(views(0))
     R = SceneRenderer(scene)
     if args.mlp == "bf16":
         R.mlp_mode(N.MLP_BF16)
-    W, H, T = args.width, args.height, args.tile
+    T = args.tile
     stride = T * T
-    tiles = frame_tiles(W, H, T)
+    tiles = np.concatenate([frame_tiles(W, H, T, cam=v) for v in range(n_views)])
     n_tiles = len(tiles)
     mine, n_max = shard_tiles(tiles, world, rank)         # tile t -> rank t mod N
     my_tiles = torch.from_numpy(mine).to(dev)
@@ -258,11 +307,12 @@ def run_ours(args):
     slot_tiles_dev = torch.from_numpy(slot_tile_table(tiles, world)).to(dev)
     # two frame buffers so the end-to-end loop can download frame k while
     # frame k+1 renders
-    frames = [(torch.empty((H * W, 4), dtype=torch.uint8, device=dev),
-               torch.empty((H * W,), dtype=torch.int16, device=dev)) for _ in range(2)]
+    NPX = n_views * H * W
+    frames = [(torch.empty((NPX, 4), dtype=torch.uint8, device=dev),
+               torch.empty((NPX,), dtype=torch.int16, device=dev)) for _ in range(2)]
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     n_cam = args.warmup + args.steps + 4
-    cam_arrays = [R.camera_array([camera_for_step(k, W, H)]) for k in range(n_cam)]
+    cam_arrays = [R.camera_array(views(k)) for k in range(n_cam)]
     stream = torch.cuda.current_stream().cuda_stream
 
     def step(k, fb=0):
@@ -318,7 +368,7 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     t_max = float(t.item())
     cnt = out["counters"].cpu().numpy().astype(np.float64) / args.steps
-    npix = W * H
+    npix = NPX
     value = args.steps * npix / t_max / 1e6
 
     # ---- end to end: camera in (H2D param block), encoded frame out (D2H) to pinned host
@@ -328,7 +378,7 @@ def run_ours(args):
         # stream; a copy stream downloads it to pinned host memory while
         # step k+1 renders.  Timed from the first render to the last byte on
         # the host (device events on both streams).
-        hosts = [torch.empty((H * W * 6,), dtype=torch.uint8, pin_memory=True) for _ in range(2)]
+        hosts = [torch.empty((NPX * 6,), dtype=torch.uint8, pin_memory=True) for _ in range(2)]
         copy_stream = torch.cuda.Stream(device=dev)
         comp = torch.cuda.current_stream()
         for k in range(2):
@@ -348,8 +398,8 @@ def run_ours(args):
                 rendered.record(comp)
                 copy_stream.wait_event(rendered)
                 with torch.cuda.stream(copy_stream):
-                    hosts[fb][:H * W * 4].view(H * W, 4).copy_(frames[fb][0], non_blocking=True)
-                    hosts[fb][H * W * 4:].view(torch.int16).copy_(frames[fb][1], non_blocking=True)
+                    hosts[fb][:NPX * 4].view(NPX, 4).copy_(frames[fb][0], non_blocking=True)
+                    hosts[fb][NPX * 4:].view(torch.int16).copy_(frames[fb][1], non_blocking=True)
                 ev = torch.cuda.Event()
                 ev.record(copy_stream)
                 done_copy[fb] = ev
@@ -361,7 +411,7 @@ def run_ours(args):
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e2e = {"value": args.steps * npix / float(te.item()) / 1e6, "unit": UNIT,
-               "h2d_bytes_per_step": int(N.lib().nolf_launch_param_bytes(args.assets, 1)),
+               "h2d_bytes_per_step": int(N.lib().nolf_launch_param_bytes(len(scene), n_views)),
                "d2h_bytes_per_step": int(npix * 6)}
 
     # ---- roofline of the dominant kernel (per-launch algorithmic bytes / event time)
@@ -389,11 +439,11 @@ def run_ours(args):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            rays, el, used = cpu_sample(scene, camera_for_step(0, W, H), tiles, args.cpu_seconds)
+            rays, el, used = cpu_sample(scene, views(0), tiles, args.cpu_seconds)
             cpu = {"value": rays / el / 1e6, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
-                   "sample": f"{used} random 32x32 tiles of the 4K frame, 12 assets each, oracle "
-                             f"render + compose on {os.cpu_count()} OpenMP threads, "
-                             f"{el:.1f} s, extrapolated"}
+                   "sample": f"{used} of {len(tiles)} random {T}x{T} tiles ({len(scene)} assets "
+                             f"each), oracle render + compose on {os.cpu_count()} OpenMP threads, "
+                             f"{el:.1f} s, extrapolated to Mrays/s"}
         except Exception as e:  # noqa: BLE001
             cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
                    "sample": f"failed: {e}"}
@@ -401,9 +451,10 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_max / args.steps * 1e3,
-            "fps": args.steps / t_max, "higher_is_better": True, "scaling": "strong",
+            "fps": args.steps * n_views / t_max, "views_per_step": n_views,
+            "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference-pipeline assets, "
-            "random-init networks)", "config": workload_config(args),
+            "random-init networks)", "config": workload_config(args, desc, W, H, len(scene)),
             "e2e": e2e, "gpu_launches": (3 + (1 if world > 1 else 0)) * args.steps, "roofline": roof, "cpu_baseline": cpu,
             "clocks": clk.summary(),
             "per_frame": {"march_samples": S, "hits": Hh, "pixels": npix},

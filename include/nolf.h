@@ -200,7 +200,8 @@ size_t nolf_launch_param_bytes(int32_t n_inst, int32_t n_cams);
 /* Frame assembly after gathering every rank's tile-packed encode_frame
  * output (rank r: n_per_rank slots of rgba8, then their depth16) into one
  * buffer: slot_tiles (DEVICE, world*n_per_rank, rank-major) gives each slot's
- * tile; writes the row-major rgba8 (H,W,4) and depth16 (H,W) frame. */
+ * tile; writes the row-major rgba8 (H,W,4) and depth16 (H,W) frame of every
+ * camera, camera c at offset c*W*H (all cameras W x H). */
 int nolf_unpack_gathered(const uint8_t *gathered, int32_t world, int32_t n_per_rank, int64_t tile_stride,
                          const NolfTile *slot_tiles, int32_t width, int32_t height, uint8_t *rgba8,
                          uint16_t *depth16, void *stream);

@@ -903,7 +903,7 @@ int nolf_unpack_gathered(const uint8_t *gathered, int32_t world, int32_t n_per_r
   const long long rank_bytes = (long long)n_per_rank * tile_stride * 6;
   k_unpack<<<(unsigned)((n + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
       gathered, rank_bytes, n_per_rank, tile_stride, reinterpret_cast<const TileParams *>(slot_tiles), n_slots,
-      width, reinterpret_cast<uchar4 *>(rgba8), depth16);
+      width, height, reinterpret_cast<uchar4 *>(rgba8), depth16);
   CUDA_TRY(cudaGetLastError());
   return 0;
 }

@@ -668,7 +668,8 @@ __global__ void __launch_bounds__(256) k_compose(ComposeArgs a) {
 // lists the tile of every (rank, slot) in rank-major order.
 __global__ void __launch_bounds__(256) k_unpack(const uint8_t *gathered, long long rank_bytes, int n_per_rank,
                                                 long long tile_stride, const TileParams *slot_tiles,
-                                                long long n_slots, int width, uchar4 *rgba8, uint16_t *depth16) {
+                                                long long n_slots, int width, int height, uchar4 *rgba8,
+                                                uint16_t *depth16) {
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const long long s = i / tile_stride, local = i % tile_stride;
   if (s >= n_slots) return;
@@ -678,7 +679,8 @@ __global__ void __launch_bounds__(256) k_unpack(const uint8_t *gathered, long lo
   const long long r = s / n_per_rank, j = s % n_per_rank;
   const uint8_t *base = gathered + r * rank_bytes;
   const long long src = j * tile_stride + local;
-  const long long dst = (long long)(tp.y0 + (int)(local / w)) * width + (tp.x0 + (int)(local % w));
+  const long long dst = (long long)tp.cam * width * height + (long long)(tp.y0 + (int)(local / w)) * width +
+                        (tp.x0 + (int)(local % w));
   rgba8[dst] = reinterpret_cast<const uchar4 *>(base)[src];
   depth16[dst] = reinterpret_cast<const uint16_t *>(base + (long long)n_per_rank * tile_stride * 4)[src];
 }
