@@ -313,6 +313,7 @@ def run_ours(args):
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     n_cam = args.warmup + args.steps + 4
     cam_arrays = [R.camera_array(views(k)) for k in range(n_cam)]
+    R.reserve(cam_arrays, n_max * stride)
     stream = torch.cuda.current_stream().cuda_stream
 
     def step(k, fb=0):
@@ -362,7 +363,8 @@ def run_ours(args):
     N.check(N.lib().nolf_profile(0))
     clk.mark(h0, time.perf_counter())
     clk.__exit__()
-    t_local = sum(a.elapsed_time(b) for a, b in ev) / 1e3
+    step_ms = np.array([a.elapsed_time(b) for a, b in ev])
+    t_local = float(step_ms.sum()) / 1e3
     t = torch.tensor([t_local], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -458,6 +460,8 @@ def run_ours(args):
             "e2e": e2e, "gpu_launches": (3 + (1 if world > 1 else 0)) * args.steps, "roofline": roof, "cpu_baseline": cpu,
             "clocks": clk.summary(),
             "per_frame": {"march_samples": S, "hits": Hh, "pixels": npix},
+            "step_ms": {"p50": float(np.percentile(step_ms, 50)), "p90": float(np.percentile(step_ms, 90)),
+                        "max": float(step_ms.max()), "min": float(step_ms.min())},
         }
         line["config"]["parallelism"] = f"ray-tile x{world}"
         print(json.dumps(line), flush=True)

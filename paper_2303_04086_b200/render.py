@@ -363,17 +363,32 @@ class SceneRenderer:
         out["counters"] = t.zeros(4, dtype=t.int64, device=self.device)
         return out
 
-    def _workspace(self, cams, P: int):
-        """Tight per-launch workspace (hit queues sized by the instances'
-        screen boxes, compose layers by their maximum overlap)."""
-        t = torch()
+    def _need(self, cams, P: int) -> int:
+        cams = cams if isinstance(cams, C.Array) else self.camera_array(cams)
         need = int(N.lib().nolf_scene_workspace_bytes(self._inst_arr, len(self.insts), cams,
                                                       len(cams), int(P)))
         if need == 0:
             raise errors.DomainError("bad scene for workspace sizing")
+        return need
+
+    def reserve(self, camera_sets, P: int) -> int:
+        """Size the workspace once for every camera set a run will render
+        (growing it mid-run would put a cudaMalloc in the frame loop)."""
+        need = max(self._need(c, P) for c in camera_sets)
+        self._grow(need)
+        return need
+
+    def _grow(self, need: int):
+        t = torch()
         if self._ws is None or self._ws.numel() < need:
             self._ws = None
-            self._ws = t.empty(need, dtype=t.uint8, device=self.device)
+            # 25 % headroom: screen boxes (hence queue sizes) move with the camera
+            self._ws = t.empty(int(need * 1.25) + (1 << 20), dtype=t.uint8, device=self.device)
+
+    def _workspace(self, cams, P: int):
+        """Tight per-launch workspace (hit queues sized by the instances'
+        screen boxes, compose layers by their maximum overlap)."""
+        self._grow(self._need(cams, P))
         return self._ws
 
     @staticmethod
