@@ -102,6 +102,13 @@ typedef struct NolfAssetDesc {        /* LightFieldAsset, lightfield.py:217-248 
     double proxy_min[3], proxy_max[3]; /* Aabb proxy */
     /* ModelWiring, lightfield.py:59-67 */
     int32_t use_hit_point, use_opacity, refine_opacity, use_tint, use_diffuse_color;
+    /* Optional triangle-mesh proxy (object space, inside the proxy box):
+     * the march starts at its first hit.  No reference counterpart
+     * (BASELINE config 2).  mesh_n_triangles == 0: slab proxy only. */
+    const double *mesh_vertices;       /* (n_vertices, 3) */
+    int64_t mesh_n_vertices;
+    const int32_t *mesh_triangles;     /* (n_triangles, 3) vertex indices */
+    int64_t mesh_n_triangles;
 } NolfAssetDesc;
 
 typedef struct NolfAsset *nolf_asset_t;

@@ -83,6 +83,9 @@ typedef struct {
     double step, t_stop, alpha_floor;
     double pmin[3], pmax[3];
     int use_hit_point, use_opacity, refine_opacity, use_tint, use_diffuse_color;
+    /* triangle-mesh proxy (no reference counterpart): 9 doubles per triangle */
+    int64_t n_tri;
+    const double *tri;
 } OAsset;
 
 /* optional per-ray debug outputs (NULL to skip) */
@@ -282,6 +285,39 @@ static void hashgrid_encode1(const OAsset *A, const double *x, float *out) {
     }
 }
 
+/* Moller-Trumbore in f64, same operation order as the CUDA kernel
+ * (csrc/nolf_mesh.cuh mt_hit); -1 on miss. */
+static double mt_hit(const double *T, const double *o, const double *d) {
+    double e1x = T[3] - T[0], e1y = T[4] - T[1], e1z = T[5] - T[2];
+    double e2x = T[6] - T[0], e2y = T[7] - T[1], e2z = T[8] - T[2];
+    double px = d[1] * e2z - d[2] * e2y;
+    double py = d[2] * e2x - d[0] * e2z;
+    double pz = d[0] * e2y - d[1] * e2x;
+    double det = (e1x * px + e1y * py) + e1z * pz;
+    if (fabs(det) < 1e-300) return -1.0;
+    double inv = 1.0 / det;
+    double sx = o[0] - T[0], sy = o[1] - T[1], sz = o[2] - T[2];
+    double u = ((sx * px + sy * py) + sz * pz) * inv;
+    if (u < 0.0 || u > 1.0) return -1.0;
+    double qx = sy * e1z - sz * e1y;
+    double qy = sz * e1x - sx * e1z;
+    double qz = sx * e1y - sy * e1x;
+    double v = ((d[0] * qx + d[1] * qy) + d[2] * qz) * inv;
+    if (v < 0.0 || u + v > 1.0) return -1.0;
+    double t = ((e2x * qx + e2y * qy) + e2z * qz) * inv;
+    return t >= 0.0 ? t : -1.0;
+}
+
+/* brute-force first hit over every triangle */
+double oracle_mesh_hit(const double *tri, int64_t n_tri, const double *o, const double *d) {
+    double best = -1.0;
+    for (int64_t i = 0; i < n_tri; ++i) {
+        double t = mt_hit(tri + 9 * i, o, d);
+        if (t >= 0.0 && (best < 0.0 || t < best)) best = t;
+    }
+    return best;
+}
+
 /* lightfield.py:400-456 for one world ray */
 static void render_one(const OAsset *A, const double *w2o, double scale, const double *o_w,
                        const double *d_w, float *rgba, float *depth, int64_t *cnt, ODebug *dbg,
@@ -320,6 +356,11 @@ static void render_one(const OAsset *A, const double *w2o, double scale, const d
     int boxhit = t_near <= t_far;
     if (dbg && dbg->boxhit) dbg->boxhit[ri] = (uint8_t)boxhit;
     if (dbg && dbg->t_near) { dbg->t_near[ri] = t_near; dbg->t_far[ri] = t_far; }
+    if (boxhit && A->n_tri > 0) {   /* mesh proxy: march from its first hit */
+        double tm = oracle_mesh_hit(A->tri, A->n_tri, o, d);
+        if (tm < 0.0) boxhit = 0;
+        else t_near = tm;
+    }
     if (!boxhit) return;
 
     /* lightfield.py:129-186 march, every fixed step evaluated */

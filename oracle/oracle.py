@@ -59,6 +59,7 @@ class OAsset(C.Structure):
         ("pmin", C.c_double * 3), ("pmax", C.c_double * 3),
         ("use_hit_point", C.c_int), ("use_opacity", C.c_int), ("refine_opacity", C.c_int),
         ("use_tint", C.c_int), ("use_diffuse_color", C.c_int),
+        ("n_tri", C.c_int64), ("tri", C.c_void_p),
     ]
 
 
@@ -84,6 +85,8 @@ def lib():
                                          C.c_int, C.c_int, C.c_int, C.c_int, vp, vp, vp, C.c_int]
         L.oracle_compose.argtypes = [C.c_int, i64, vp, vp, dbl, vp, vp, C.c_int]
         L.oracle_camera_dirs.argtypes = [vp, dbl, dbl, dbl, dbl, vp, vp, i64, vp]
+        L.oracle_mesh_hit.argtypes = [vp, i64, vp, vp]
+        L.oracle_mesh_hit.restype = dbl
         _lib = L
     return _lib
 
@@ -153,6 +156,12 @@ class Asset:
         A.use_hit_point, A.use_opacity = int(w.use_hit_point), int(w.use_opacity)
         A.refine_opacity, A.use_tint = int(w.refine_opacity), int(w.use_tint)
         A.use_diffuse_color = int(w.use_diffuse_color)
+        mesh = getattr(asset, "proxy_mesh", None)
+        if mesh is not None:
+            v = np.asarray(mesh[0], np.float64).reshape(-1, 3)
+            t = np.asarray(mesh[1], np.int64).reshape(-1, 3)
+            tri = arr(v[t].reshape(-1, 9), np.float64)
+            A.n_tri, A.tri = len(tri), _p(tri)
         self.A = A
         o2w = np.asarray(asset.object_to_world, np.float64)
         self.w2o = np.ascontiguousarray(np.linalg.inv(o2w))

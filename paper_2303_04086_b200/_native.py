@@ -48,6 +48,8 @@ class AssetDesc(C.Structure):
         ("proxy_min", C.c_double * 3), ("proxy_max", C.c_double * 3),
         ("use_hit_point", C.c_int32), ("use_opacity", C.c_int32), ("refine_opacity", C.c_int32),
         ("use_tint", C.c_int32), ("use_diffuse_color", C.c_int32),
+        ("mesh_vertices", C.c_void_p), ("mesh_n_vertices", C.c_int64),
+        ("mesh_triangles", C.c_void_p), ("mesh_n_triangles", C.c_int64),
     ]
 
 
@@ -206,6 +208,12 @@ def asset_desc(asset):
     for k in range(3):
         d.proxy_min[k] = float(asset.proxy.min[k])
         d.proxy_max[k] = float(asset.proxy.max[k])
+    mesh = getattr(asset, "proxy_mesh", None)
+    if mesh is not None:
+        mv = arr(mesh[0], np.float64).reshape(-1, 3)
+        mt = arr(mesh[1], np.int32).reshape(-1, 3)
+        d.mesh_vertices, d.mesh_n_vertices = _ptr(mv), len(mv)
+        d.mesh_triangles, d.mesh_n_triangles = _ptr(mt), len(mt)
     w = asset.wiring
     d.use_hit_point = int(bool(w.use_hit_point))
     d.use_opacity = int(bool(w.use_opacity))

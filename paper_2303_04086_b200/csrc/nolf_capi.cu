@@ -134,6 +134,114 @@ int upload_atlas(NolfAsset *A, const NolfAtlasDesc &d, int channels, DevAtlas *o
   return 0;
 }
 
+// Median-split BVH over triangle centroids (longest centroid axis, leaves of
+// <= 4 triangles); node boxes rounded outward to fp32 and padded so the fp32
+// traversal test only ever over-approximates.
+struct BvhBuilder {
+  const double *V;
+  const int32_t *T;
+  std::vector<int> order;
+  std::vector<BvhNode> nodes;
+  std::vector<double> cen;
+  void bounds(int first, int count, double lo[3], double hi[3]) const {
+    for (int k = 0; k < 3; ++k) { lo[k] = 1e300; hi[k] = -1e300; }
+    for (int i = first; i < first + count; ++i)
+      for (int c = 0; c < 3; ++c) {
+        const double *v = V + 3ll * T[3ll * order[(size_t)i] + c];
+        for (int k = 0; k < 3; ++k) { lo[k] = std::min(lo[k], v[k]); hi[k] = std::max(hi[k], v[k]); }
+      }
+  }
+  // writes the subtree over order[first, first+count) into nodes[slot]
+  void build(int slot, int first, int count) {
+    double lo[3], hi[3];
+    bounds(first, count, lo, hi);
+    BvhNode n{};
+    for (int k = 0; k < 3; ++k) {
+      const double pad = 1e-6 * (hi[k] - lo[k]) + 1e-6;
+      n.lo[k] = nextafterf((float)(lo[k] - pad), -INFINITY);
+      n.hi[k] = nextafterf((float)(hi[k] + pad), INFINITY);
+    }
+    if (count <= 4) {
+      n.first = first;
+      n.count = count;
+      nodes[(size_t)slot] = n;
+      return;
+    }
+    double clo[3] = {1e300, 1e300, 1e300}, chi[3] = {-1e300, -1e300, -1e300};
+    for (int i = first; i < first + count; ++i)
+      for (int k = 0; k < 3; ++k) {
+        const double c = cen[3ull * order[(size_t)i] + k];
+        clo[k] = std::min(clo[k], c);
+        chi[k] = std::max(chi[k], c);
+      }
+    int ax = 0;
+    for (int k = 1; k < 3; ++k)
+      if (chi[k] - clo[k] > chi[ax] - clo[ax]) ax = k;
+    const int mid = first + count / 2;
+    std::nth_element(order.begin() + first, order.begin() + mid, order.begin() + first + count, [&](int a, int b) {
+      const double ca = cen[3ull * a + ax], cb = cen[3ull * b + ax];
+      return ca < cb || (ca == cb && a < b);
+    });
+    const int left = (int)nodes.size();
+    nodes.push_back(BvhNode{});
+    nodes.push_back(BvhNode{});
+    build(left, first, mid - first);
+    build(left + 1, mid, first + count - mid);
+    n.first = left;
+    n.count = 0;
+    nodes[(size_t)slot] = n;
+  }
+};
+
+int upload_mesh(NolfAsset *A, const NolfAssetDesc &d, DevMesh *out) {
+  out->nodes = nullptr;
+  out->tri = nullptr;
+  out->n_tri = 0;
+  if (d.mesh_n_triangles <= 0) return 0;
+  if (!d.mesh_vertices || !d.mesh_triangles || d.mesh_n_vertices <= 0)
+    return fail(NOLF_EINVAL, "mesh proxy: missing arrays");
+  if (d.mesh_n_triangles >= (1ll << 30)) return fail(NOLF_EINVAL, "mesh proxy: too many triangles");
+  for (int64_t i = 0; i < 3 * d.mesh_n_triangles; ++i)
+    if (d.mesh_triangles[i] < 0 || d.mesh_triangles[i] >= d.mesh_n_vertices)
+      return fail(NOLF_EINVAL, "mesh proxy: triangle index out of range");
+  for (int64_t i = 0; i < d.mesh_n_vertices; ++i)
+    for (int k = 0; k < 3; ++k) {
+      const double v = d.mesh_vertices[3 * i + k];
+      if (!(v >= d.proxy_min[k] && v <= d.proxy_max[k]))
+        return fail(NOLF_EINVAL, "mesh proxy: vertices must lie inside the proxy box");
+    }
+  BvhBuilder B;
+  B.V = d.mesh_vertices;
+  B.T = d.mesh_triangles;
+  const int nt = (int)d.mesh_n_triangles;
+  B.order.resize((size_t)nt);
+  B.cen.resize(3ull * nt);
+  for (int i = 0; i < nt; ++i) {
+    B.order[(size_t)i] = i;
+    for (int k = 0; k < 3; ++k) {
+      double c = 0;
+      for (int v = 0; v < 3; ++v) c += d.mesh_vertices[3ll * d.mesh_triangles[3ll * i + v] + k];
+      B.cen[3ull * i + k] = c / 3.0;
+    }
+  }
+  B.nodes.push_back(BvhNode{});
+  B.build(0, 0, nt);
+  std::vector<double> tri(9ull * nt);
+  for (int i = 0; i < nt; ++i)
+    for (int v = 0; v < 3; ++v)
+      for (int k = 0; k < 3; ++k)
+        tri[9ull * i + 3 * v + k] = d.mesh_vertices[3ll * d.mesh_triangles[3ll * B.order[(size_t)i] + v] + k];
+  BvhNode *nd;
+  double *tp;
+  int rc;
+  if ((rc = A->upload(B.nodes.data(), B.nodes.size(), &nd))) return rc;
+  if ((rc = A->upload(tri.data(), tri.size(), &tp))) return rc;
+  out->nodes = nd;
+  out->tri = tp;
+  out->n_tri = nt;
+  return 0;
+}
+
 int pack_mlp(NolfAsset *A, const NolfMlpDesc &m, DevMlp *out, const char *what) {
   if (m.n_layers != 2 && m.n_layers != 3)
     return fail(NOLF_EINVAL, "%s MLP: %d layers unsupported (need 2 or 3)", what, m.n_layers);
@@ -506,6 +614,7 @@ int nolf_asset_create(const NolfAssetDesc *d, int device, nolf_asset_t *out) {
     H.pmin[k] = d->proxy_min[k];
     H.pmax[k] = d->proxy_max[k];
   }
+  if ((rc = upload_mesh(A, *d, &H.mesh))) return bail(rc);
   H.use_hit_point = d->use_hit_point;
   H.use_opacity = d->use_opacity;
   H.refine_opacity = d->refine_opacity;

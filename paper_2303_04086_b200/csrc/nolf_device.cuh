@@ -7,6 +7,8 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include "nolf_mesh.cuh"
+
 namespace nolf {
 
 constexpr int kHid = 64;       // MLP hidden width (lightfield.py:594 hidden=64)
@@ -70,6 +72,7 @@ struct DevAsset {              // LightFieldAsset (lightfield.py:217-248)
   const uint8_t *tc_w;         // bf16 W0 [64 x 32] then W1 [64 x 64], UMMA K-major layout
   const uint16_t *phi16;       // Phi narrowed to u16 (m <= 65536), else null
   uint32_t phi16_bytes;        // padded to 16 B for the TMA bulk copy
+  DevMesh mesh;                // triangle-mesh proxy (nodes == null: slab only)
 };
 
 // One placed asset for a launch (NolfInstance minus the host handle).

@@ -257,6 +257,11 @@ __global__ void __launch_bounds__(128) k_march(MarchArgs args) {
         to_object(I.w2o, ow, dw, o, d);
       }
       bool boxhit = slab(A.pmin, A.pmax, o, d, t_near, t_far, inv);
+      if (boxhit && A.mesh.nodes) {          // mesh proxy: march from its first hit
+        const double tm = mesh_first_hit(A.mesh, o, d);
+        if (tm < 0.0) boxhit = false;
+        else t_near = tm;
+      }
       if (boxhit) {
         mr = march_ray(A, o, d, inv, t_near, t_far);
         samples_total += (unsigned long long)mr.samples;

@@ -1,0 +1,87 @@
+// nolf_mesh.cuh -- triangle-mesh proxy first hit (BVH traversal).
+//
+// The reference's proxy is an AABB (lightfield.py:229, slab test core.py:206);
+// BASELINE config 2 / the north star add a mesh proxy with no reference
+// counterpart.  Semantics here: the march starts at the mesh's first hit
+// t_mesh >= 0 (instead of the slab's t_near) and ends at the slab's t_far of
+// the proxy box; a ray that misses every triangle is a miss.  Triangle
+// tests are fp64 Moller-Trumbore written with explicit *_rn operations so
+// the brute-force oracle (oracle/nolf_oracle.c, oracle_mesh_hit) reproduces
+// t_mesh bit for bit; the BVH only prunes (fp32 boxes padded outward).
+#pragma once
+#include <cstdint>
+
+namespace nolf {
+
+struct BvhNode {              // 32 B
+  float lo[3], hi[3];
+  int first;                  // leaf: first triangle ; inner: left child (right = first + 1)
+  int count;                  // > 0 leaf
+};
+
+struct DevMesh {
+  const BvhNode *nodes;       // null: no mesh proxy
+  const double *tri;          // 9 doubles per triangle (v0, v1, v2), BVH leaf order
+  int n_tri;
+};
+
+// Moller-Trumbore (fp64, explicit rounding) -> t or -1.
+__device__ __forceinline__ double mt_hit(const double *T, const double o[3], const double d[3]) {
+  const double e1x = __dsub_rn(T[3], T[0]), e1y = __dsub_rn(T[4], T[1]), e1z = __dsub_rn(T[5], T[2]);
+  const double e2x = __dsub_rn(T[6], T[0]), e2y = __dsub_rn(T[7], T[1]), e2z = __dsub_rn(T[8], T[2]);
+  const double px = __dsub_rn(__dmul_rn(d[1], e2z), __dmul_rn(d[2], e2y));
+  const double py = __dsub_rn(__dmul_rn(d[2], e2x), __dmul_rn(d[0], e2z));
+  const double pz = __dsub_rn(__dmul_rn(d[0], e2y), __dmul_rn(d[1], e2x));
+  const double det = __dadd_rn(__dadd_rn(__dmul_rn(e1x, px), __dmul_rn(e1y, py)), __dmul_rn(e1z, pz));
+  if (fabs(det) < 1e-300) return -1.0;
+  const double inv = __ddiv_rn(1.0, det);
+  const double sx = __dsub_rn(o[0], T[0]), sy = __dsub_rn(o[1], T[1]), sz = __dsub_rn(o[2], T[2]);
+  const double u = __dmul_rn(__dadd_rn(__dadd_rn(__dmul_rn(sx, px), __dmul_rn(sy, py)), __dmul_rn(sz, pz)), inv);
+  if (u < 0.0 || u > 1.0) return -1.0;
+  const double qx = __dsub_rn(__dmul_rn(sy, e1z), __dmul_rn(sz, e1y));
+  const double qy = __dsub_rn(__dmul_rn(sz, e1x), __dmul_rn(sx, e1z));
+  const double qz = __dsub_rn(__dmul_rn(sx, e1y), __dmul_rn(sy, e1x));
+  const double v = __dmul_rn(__dadd_rn(__dadd_rn(__dmul_rn(d[0], qx), __dmul_rn(d[1], qy)), __dmul_rn(d[2], qz)), inv);
+  if (v < 0.0 || __dadd_rn(u, v) > 1.0) return -1.0;
+  const double t = __dmul_rn(__dadd_rn(__dadd_rn(__dmul_rn(e2x, qx), __dmul_rn(e2y, qy)), __dmul_rn(e2z, qz)), inv);
+  return t >= 0.0 ? t : -1.0;
+}
+
+// Closest hit over the mesh: t_mesh >= 0, or -1 when the ray misses it.
+__device__ __forceinline__ double mesh_first_hit(const DevMesh &M, const double o[3], const double d[3]) {
+  const float ox = (float)o[0], oy = (float)o[1], oz = (float)o[2];
+  // finite reciprocals: a zero component gets +-1e30 so (lo - o) * inv is never 0*inf
+  auto rcp = [](double x) { const float f = (float)x; return 1.0f / copysignf(fmaxf(fabsf(f), 1e-30f), f); };
+  const float ix = rcp(d[0]), iy = rcp(d[1]), iz = rcp(d[2]);
+  double best = -1.0;
+  float best_f = __int_as_float(0x7f800000);
+  int stack[48];
+  int sp = 0;
+  stack[sp++] = 0;
+  while (sp) {
+    const BvhNode n = M.nodes[stack[--sp]];
+    // conservative fp32 slab (boxes padded at build time; +-2% in t)
+    float t0 = (n.lo[0] - ox) * ix, t1 = (n.hi[0] - ox) * ix;
+    float tmin = fminf(t0, t1), tmax = fmaxf(t0, t1);
+    t0 = (n.lo[1] - oy) * iy; t1 = (n.hi[1] - oy) * iy;
+    tmin = fmaxf(tmin, fminf(t0, t1)); tmax = fminf(tmax, fmaxf(t0, t1));
+    t0 = (n.lo[2] - oz) * iz; t1 = (n.hi[2] - oz) * iz;
+    tmin = fmaxf(tmin, fminf(t0, t1)); tmax = fminf(tmax, fmaxf(t0, t1));
+    if (tmax < 0.0f || tmin > tmax * 1.02f + 1e-6f || tmin > best_f * 1.02f + 1e-6f) continue;
+    if (n.count > 0) {
+      for (int i = 0; i < n.count; ++i) {
+        const double t = mt_hit(M.tri + 9ll * (n.first + i), o, d);
+        if (t >= 0.0 && (best < 0.0 || t < best)) {
+          best = t;
+          best_f = (float)t;
+        }
+      }
+    } else if (sp < 46) {
+      stack[sp++] = n.first + 1;
+      stack[sp++] = n.first;
+    }
+  }
+  return best;
+}
+
+}  // namespace nolf

@@ -207,6 +207,10 @@ class LightFieldAsset:
     analytic_density: object = None
     analytic_color: object = None
     name: str = "asset"
+    # optional triangle-mesh proxy (vertices (n,3) f64, triangles (m,3) int32),
+    # object space inside `proxy`; the march starts at its first hit.  Not in
+    # the reference (BASELINE config 2).
+    proxy_mesh: tuple | None = None
 
 
 @dataclass(frozen=True)

@@ -119,6 +119,11 @@ def read_asset(path_or_bytes) -> LightFieldAsset:
     dfeat = [_arr(s, f"ed_feat_{i}", np.float32, (rows, em["features_per_level"]))
              for i, rows in enumerate(enc.row_counts)]
     mm, wm = meta["march"], meta["wiring"]
+    mesh = None
+    if "proxy_mesh" in meta:      # extension section (not written by the reference)
+        pm2 = meta["proxy_mesh"]
+        mesh = (_arr(s, "mesh_vertices", np.float64, (pm2["vertices"], 3)),
+                _arr(s, "mesh_triangles", np.int32, (pm2["triangles"], 3)))
     return LightFieldAsset(
         density_atlas=den, psh=psh, psh_features=feats, diffuse_encoder=enc,
         diffuse_features=dfeat, specular_mlp=_mlp(meta["specular_mlp"], s, "fs"),
@@ -126,7 +131,8 @@ def read_asset(path_or_bytes) -> LightFieldAsset:
         march=MarchParams(step=mm["step"], t_stop=mm["t_stop"], alpha_floor=mm["alpha_floor"]),
         proxy=Aabb(min=np.array(meta["proxy"]["min"]), max=np.array(meta["proxy"]["max"])),
         object_to_world=np.array(meta["transform"], dtype=np.float64).reshape(4, 4),
-        diffuse_atlas=dif, wiring=ModelWiring(**wm), name=meta.get("name", "asset"))
+        diffuse_atlas=dif, wiring=ModelWiring(**wm), name=meta.get("name", "asset"),
+        proxy_mesh=mesh)
 
 
 def _le(a: np.ndarray) -> bytes:
@@ -174,6 +180,9 @@ def write_asset(asset, path=None) -> bytes:
         "diffuse_mlp": mlp_meta(asset.diffuse_mlp),
         "has_diffuse_atlas": asset.diffuse_atlas is not None,
     }
+    mesh = getattr(asset, "proxy_mesh", None)
+    if mesh is not None:
+        meta["proxy_mesh"] = {"vertices": int(len(mesh[0])), "triangles": int(len(mesh[1]))}
     if asset.diffuse_atlas is not None:
         meta["diffuse_atlas"] = {"b": asset.diffuse_atlas.base_resolution,
                                  "r": asset.diffuse_atlas.cube_resolution,
@@ -195,6 +204,9 @@ def write_asset(asset, path=None) -> bytes:
             sec[f"{tag}_w{i}"] = _le(np.asarray(w, np.float32))
         for i, b in enumerate(m.biases):
             sec[f"{tag}_b{i}"] = _le(np.asarray(b, np.float32))
+    if mesh is not None:
+        sec["mesh_vertices"] = _le(np.asarray(mesh[0], np.float64).reshape(-1, 3))
+        sec["mesh_triangles"] = _le(np.asarray(mesh[1], np.int32).reshape(-1, 3))
     data = pack_sections(sec)
     if path is not None:
         Path(path).write_bytes(data)

@@ -119,6 +119,9 @@ def _fingerprint(asset, device_index):
         arrays += [asset.diffuse_atlas.index, asset.diffuse_atlas.cubes]
     if asset.diffuse_features is not None:
         arrays += list(asset.diffuse_features)
+    mesh = getattr(asset, "proxy_mesh", None)
+    if mesh is not None:
+        arrays += [mesh[0], mesh[1]]
     crc = 0
     for m in (asset.specular_mlp, asset.diffuse_mlp):
         if m is not None:

@@ -391,6 +391,47 @@ def march_only_asset(atlas: CubeAtlas, march: MarchParams) -> LightFieldAsset:
                            diffuse_mlp=None, march=march, wiring=ModelWiring(use_diffuse_color=False))
 
 
+# ------------------------------------------------------------------ mesh proxies
+def box_mesh(lo=(0.0, 0.0, 0.0), hi=(1.0, 1.0, 1.0)):
+    """The 12-triangle tessellation of an AABB (outward winding)."""
+    lo, hi = np.asarray(lo, np.float64), np.asarray(hi, np.float64)
+    v = np.array([[hi[k] if (c >> k) & 1 else lo[k] for k in range(3)] for c in range(8)])
+    quads = [(0, 2, 3, 1), (4, 5, 7, 6), (0, 1, 5, 4), (2, 6, 7, 3), (0, 4, 6, 2), (1, 3, 7, 5)]
+    tris = []
+    for a, b, c, d in quads:
+        tris += [(a, b, c), (a, c, d)]
+    return v, np.asarray(tris, np.int32)
+
+
+def icosphere(center=(0.5, 0.5, 0.5), radius=0.27, level=3):
+    """Subdivided icosahedron (20 * 4**level triangles) -- a tight proxy for
+    the sphere density (radius 0.25)."""
+    t = (1.0 + 5 ** 0.5) / 2.0
+    v = [(-1, t, 0), (1, t, 0), (-1, -t, 0), (1, -t, 0), (0, -1, t), (0, 1, t), (0, -1, -t),
+         (0, 1, -t), (t, 0, -1), (t, 0, 1), (-t, 0, -1), (-t, 0, 1)]
+    v = [np.asarray(p, np.float64) / np.linalg.norm(p) for p in v]
+    f = [(0, 11, 5), (0, 5, 1), (0, 1, 7), (0, 7, 10), (0, 10, 11), (1, 5, 9), (5, 11, 4),
+         (11, 10, 2), (10, 7, 6), (7, 1, 8), (3, 9, 4), (3, 4, 2), (3, 2, 6), (3, 6, 8), (3, 8, 9),
+         (4, 9, 5), (2, 4, 11), (6, 2, 10), (8, 6, 7), (9, 8, 1)]
+    for _ in range(level):
+        cache, nf = {}, []
+
+        def mid(a, b):
+            key = (min(a, b), max(a, b))
+            if key not in cache:
+                m = v[a] + v[b]
+                v.append(m / np.linalg.norm(m))
+                cache[key] = len(v) - 1
+            return cache[key]
+
+        for a, b, c in f:
+            ab, bc, ca = mid(a, b), mid(b, c), mid(c, a)
+            nf += [(a, ab, ca), (b, bc, ab), (c, ca, bc), (ab, bc, ca)]
+        f = nf
+    verts = np.asarray(center, np.float64) + radius * np.asarray(v)
+    return np.clip(verts, 0.0, 1.0), np.asarray(f, np.int32)
+
+
 # ------------------------------------------------------------------ scenes
 def zodiac_transforms(n=12, ring_radius=2.0, scale=0.5):
     """Config 4's "zodiac" ring: uniform scale 0.5, translations on a ring of
