@@ -44,7 +44,7 @@ def parse():
     p.add_argument("--steps", type=int, default=200)
     p.add_argument("--warmup", type=int, default=10)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--config", type=int, default=4, choices=[1, 3, 4, 5])
+    p.add_argument("--config", type=int, default=4, choices=[1, 2, 3, 4, 5])
     p.add_argument("--width", type=int, default=3840)
     p.add_argument("--height", type=int, default=2160)
     p.add_argument("--assets", type=int, default=12)
@@ -85,6 +85,8 @@ def workload(args):
     """(scene, views(k) -> [Camera], W, H, description) of a BASELINE config.
 
     1: single asset, one 256x256 view           (orbit_camera(0.8, 0.3, 2.0))
+    2: single asset with a triangle-mesh proxy (icosphere, 1280 triangles, BVH)
+       at 1920x1080
     3: single asset, 16 viewpoints at 3840x2160  (orbit azimuth 2 pi v/16, radius 1.5)
     4: 12-asset zodiac scene at 3840x2160         (the metric's configuration)
     5: 12-asset scene, 8 users x 2 eyes at 2160x2160 (eyes +-0.032 along camera right)
@@ -94,6 +96,13 @@ def workload(args):
     from paper_2303_04086_b200 import synth
     from paper_2303_04086_b200.model import Camera, orbit_camera
     c = args.config
+    if c == 2:
+        import dataclasses
+        a = dataclasses.replace(build_scene(1)[0][0], proxy_mesh=synth.icosphere(radius=0.3, level=3))
+        W, H = 1920, 1080
+        return [(a, np.eye(4))], (lambda k: [orbit_camera(0.8 + 0.005 * k, 0.3, radius=2.0, width=W,
+                                                          height=H)]), W, H, \
+            "BASELINE config 2: single asset, mesh proxy (1280-triangle icosphere, BVH), 1920x1080"
     if c in (1, 3):
         scene = build_scene(1)[:1]
         scene = [(scene[0][0], np.eye(4))]
