@@ -53,6 +53,9 @@ def parse():
     p.add_argument("--cpu-seconds", type=float, default=12.0)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--exchange", default="p2p", choices=["p2p", "gather"],
+                   help="N>1 frame composer: compose stores into rank 0's frame over NVLink "
+                        "(CUDA IPC peer memory) or NCCL gather + unpack kernel")
     return p.parse_args()
 
 
@@ -325,7 +328,43 @@ def run_ours(args):
     R.reserve(cam_arrays, n_max * stride)
     stream = torch.cuda.current_stream().cuda_stream
 
-    def step(k, fb=0):
+    # ---- p2p frame composer: rank 0 owns the frame buffers, every rank maps
+    # them (CUDA IPC) and its compose kernel stores straight into them
+    p2p = world > 1 and args.exchange == "p2p"
+    peer_frames = []
+    token = torch.zeros(1, dtype=torch.float32, device=dev)
+    if p2p:
+        import ctypes
+        FB = NPX * 6
+        hbuf = torch.zeros(2 * 64, dtype=torch.uint8, device=dev)
+        raw = []
+        if rank == 0:
+            hh = (ctypes.c_uint8 * 128)()
+            for i in range(2):
+                ptr = ctypes.c_void_p()
+                N.check(N.lib().nolf_device_alloc(FB, ctypes.byref(ptr)))
+                N.check(N.lib().nolf_ipc_get_handle(ptr, ctypes.byref(hh, 64 * i)))
+                raw.append(ptr.value)
+            hbuf.copy_(torch.tensor(list(bytes(hh)), dtype=torch.uint8))
+        dist.broadcast(hbuf, src=0)
+        if rank != 0:
+            hh = (ctypes.c_uint8 * 128)(*hbuf.cpu().tolist())
+            for i in range(2):
+                ptr = ctypes.c_void_p()
+                N.check(N.lib().nolf_ipc_open_handle(ctypes.byref(hh, 64 * i), ctypes.byref(ptr)))
+                raw.append(ptr.value)
+        peer_frames = [(p, p + NPX * 4) for p in raw]
+
+    def step(k, fb=0, before_barrier=None):
+        if p2p:
+            o2 = {"rgba8": peer_frames[fb][0], "depth16": peer_frames[fb][1],
+                  "counters": out["counters"]}
+            R.render(cam_arrays[k % n_cam], my_tiles, n_max, stride, o2, frame_layout=True,
+                     peer=(rank != 0))
+            if before_barrier is not None:
+                torch.cuda.current_stream().wait_event(before_barrier)
+            dist.all_reduce(token)         # every rank's peer stores have landed
+            return
         frame, frame_d = frames[fb]
         if world == 1:             # single GPU: compose writes the frame directly
             out["rgba8"], out["depth16"] = frame, frame_d
@@ -403,14 +442,21 @@ def run_ours(args):
             fb = k % 2
             if done_copy[fb] is not None:
                 comp.wait_event(done_copy[fb])       # buffer free again
-            step(k, fb)
+            # p2p: other ranks write buffer fb^1 at step k+1 once this step's
+            # completion collective passes, so rank 0 enters it only after
+            # the download of step k-1 (buffer fb^1) finished
+            step(k, fb, before_barrier=done_copy[fb ^ 1] if (p2p and rank == 0) else None)
             if rank == 0:
                 rendered = torch.cuda.Event()
                 rendered.record(comp)
                 copy_stream.wait_event(rendered)
                 with torch.cuda.stream(copy_stream):
-                    hosts[fb][:NPX * 4].view(NPX, 4).copy_(frames[fb][0], non_blocking=True)
-                    hosts[fb][NPX * 4:].view(torch.int16).copy_(frames[fb][1], non_blocking=True)
+                    if p2p:
+                        N.check(N.lib().nolf_memcpy_async(hosts[fb].data_ptr(), peer_frames[fb][0],
+                                                          NPX * 6, copy_stream.cuda_stream))
+                    else:
+                        hosts[fb][:NPX * 4].view(NPX, 4).copy_(frames[fb][0], non_blocking=True)
+                        hosts[fb][NPX * 4:].view(torch.int16).copy_(frames[fb][1], non_blocking=True)
                 ev = torch.cuda.Event()
                 ev.record(copy_stream)
                 done_copy[fb] = ev
@@ -466,15 +512,24 @@ def run_ours(args):
             "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference-pipeline assets, "
             "random-init networks)", "config": workload_config(args, desc, W, H, len(scene)),
-            "e2e": e2e, "gpu_launches": (3 + (1 if world > 1 else 0)) * args.steps, "roofline": roof, "cpu_baseline": cpu,
+            "e2e": e2e, "gpu_launches": (3 + (1 if (world > 1 and not p2p) else 0)) * args.steps, "roofline": roof, "cpu_baseline": cpu,
             "clocks": clk.summary(),
             "per_frame": {"march_samples": S, "hits": Hh, "pixels": npix},
             "step_ms": {"p50": float(np.percentile(step_ms, 50)), "p90": float(np.percentile(step_ms, 90)),
                         "max": float(step_ms.max()), "min": float(step_ms.min())},
         }
         line["config"]["parallelism"] = f"ray-tile x{world}"
+        if world > 1:
+            line["config"]["exchange"] = ("compose epilogue stores into rank 0's frame over NVLink "
+                                          "(CUDA IPC peer memory) + 1-element NCCL all-reduce"
+                                          if p2p else "NCCL gather of encoded tiles + unpack kernel")
         print(json.dumps(line), flush=True)
     if world > 1:
+        dist.barrier()
+        torch.cuda.synchronize()
+        if p2p:
+            for p in ([f[0] for f in peer_frames]):
+                N.lib().nolf_ipc_close_handle(p) if rank != 0 else N.lib().nolf_device_free(p)
         dist.barrier()
         dist.destroy_process_group()
 

@@ -146,6 +146,9 @@ typedef struct NolfSceneOut {
     double depth_far;                  /* encode_frame far plane */
     int32_t layout;                    /* 0: tile-packed (above); 1: row-major frame per
                                           camera, cameras concatenated in order */
+    int32_t peer;                      /* 1: outputs live in another GPU's memory (CUDA IPC
+                                          mapping); the compose epilogue stores them over
+                                          NVLink and ends with a system-scope fence */
 } NolfSceneOut;
 
 int nolf_abi_version(void);
@@ -217,6 +220,16 @@ int nolf_unpack_gathered(const uint8_t *gathered, int32_t world, int32_t n_per_r
  * device rows -> out (n, 4) f32 post-head, via the tcgen05 bf16 path
  * (NOLF_MLP_BF16) or the fp32 CUDA-core path (NOLF_MLP_FP32). */
 int nolf_mlp_eval(nolf_asset_t asset, int mode, const float *x, int64_t n, float *out, void *stream);
+
+/* Device buffers that can be shared across processes (CUDA IPC): the
+ * multi-GPU frame composer maps rank 0's frame into every rank so compose
+ * kernels store their pixels straight into it over NVLink / NVSwitch. */
+int nolf_device_alloc(size_t bytes, void **ptr);
+int nolf_device_free(void *ptr);
+int nolf_ipc_get_handle(void *ptr, void *handle64);          /* 64-byte handle out */
+int nolf_ipc_open_handle(const void *handle64, void **ptr);  /* peer mapping */
+int nolf_ipc_close_handle(void *ptr);
+int nolf_memcpy_async(void *dst, const void *src, size_t bytes, void *stream);
 
 /* frames: rgba (K, P, 4) f32, depth (K, P) f32, all device pointers. */
 int nolf_compose(int32_t K, int64_t P, const float *rgba, const float *depth, double alpha_vis,

@@ -66,7 +66,7 @@ class Camera(C.Structure):
 class SceneOut(C.Structure):
     _fields_ = [("rgba", C.c_void_p), ("depth", C.c_void_p), ("rgba8", C.c_void_p),
                 ("depth16", C.c_void_p), ("tile_stride", C.c_int64), ("depth_far", C.c_double),
-                ("layout", C.c_int32)]
+                ("layout", C.c_int32), ("peer", C.c_int32)]
 
 
 _lib = None
@@ -102,6 +102,12 @@ def lib():
         "nolf_eval_diffuse": ([vp, vp, i64, vp, vp], C.c_int),
         "nolf_profile": ([C.c_int], C.c_int),
         "nolf_mlp_eval": ([vp, C.c_int, vp, i64, vp, vp], C.c_int),
+        "nolf_device_alloc": ([C.c_size_t, C.POINTER(vp)], C.c_int),
+        "nolf_device_free": ([vp], C.c_int),
+        "nolf_ipc_get_handle": ([vp, vp], C.c_int),
+        "nolf_ipc_open_handle": ([vp, C.POINTER(vp)], C.c_int),
+        "nolf_ipc_close_handle": ([vp], C.c_int),
+        "nolf_memcpy_async": ([vp, vp, C.c_size_t, vp], C.c_int),
         "nolf_profile_read": ([C.POINTER(C.c_float)], C.c_int),
         "nolf_launch_param_bytes": ([i32, i32], C.c_size_t),
         "nolf_unpack_gathered": ([vp, i32, i32, i64, vp, i32, i32, vp, vp, vp], C.c_int),

@@ -829,6 +829,7 @@ int launch_march_shade(int mode, const NolfInstance *ins, int n_inst, const Nolf
     ca.tile_stride = tile_stride;
     ca.cams = dp->cams;
     ca.frame_layout = sout->layout;
+    ca.peer = sout->peer;
     ca.alpha_vis = (float)alpha_vis;
     ca.out_rgba = sout->rgba;
     ca.out_depth = sout->depth;
@@ -1014,6 +1015,47 @@ int nolf_unpack_gathered(const uint8_t *gathered, int32_t world, int32_t n_per_r
       gathered, rank_bytes, n_per_rank, tile_stride, reinterpret_cast<const TileParams *>(slot_tiles), n_slots,
       width, height, reinterpret_cast<uchar4 *>(rgba8), depth16);
   CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+int nolf_device_alloc(size_t bytes, void **ptr) {
+  if (!ptr) return fail(NOLF_EINVAL, "null out pointer");
+  *ptr = nullptr;
+  cudaError_t e = cudaMalloc(ptr, bytes ? bytes : 1);
+  if (e != cudaSuccess) return fail(NOLF_ENOMEM, "cudaMalloc(%zu): %s", bytes, cudaGetErrorString(e));
+  return 0;
+}
+
+int nolf_device_free(void *ptr) {
+  if (ptr) CUDA_TRY(cudaFree(ptr));
+  return 0;
+}
+
+int nolf_ipc_get_handle(void *ptr, void *handle64) {
+  if (!ptr || !handle64) return fail(NOLF_EINVAL, "null argument");
+  cudaIpcMemHandle_t h;
+  CUDA_TRY(cudaIpcGetMemHandle(&h, ptr));
+  memcpy(handle64, &h, sizeof(h));
+  return 0;
+}
+
+int nolf_ipc_open_handle(const void *handle64, void **ptr) {
+  if (!ptr || !handle64) return fail(NOLF_EINVAL, "null argument");
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle64, sizeof(h));
+  CUDA_TRY(cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  return 0;
+}
+
+int nolf_ipc_close_handle(void *ptr) {
+  if (ptr) CUDA_TRY(cudaIpcCloseMemHandle(ptr));
+  return 0;
+}
+
+int nolf_memcpy_async(void *dst, const void *src, size_t bytes, void *stream) {
+  if (bytes == 0) return 0;
+  if (!dst || !src) return fail(NOLF_EINVAL, "null buffer");
+  CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, static_cast<cudaStream_t>(stream)));
   return 0;
 }
 

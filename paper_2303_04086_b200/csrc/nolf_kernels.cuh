@@ -587,6 +587,7 @@ struct ComposeArgs {
   long long tile_stride;
   const CamParams *cams;       // frame layout: camera sizes / output bases
   int frame_layout;            // 0: outputs tile-packed at p ; 1: row-major frame per camera
+  int peer;                    // outputs are a peer GPU's memory: fence system-wide at the end
   float alpha_vis;             // compared in f32 (numpy 2 weak scalar)
   float *out_rgba;
   float *out_depth;
@@ -666,6 +667,7 @@ __global__ void __launch_bounds__(256) k_compose(ComposeArgs a) {
     if (isfinite(od)) qd = (uint16_t)rintf(fminf(od, a.depth_far) / a.depth_far * 65534.0f);
     a.out_depth16[q] = qd;
   }
+  if (a.peer) __threadfence_system();   // peer stores visible before the completion collective
 }
 
 // Frame assembly after an all-rank gather: rank r's buffer holds n_per_rank

@@ -402,16 +402,21 @@ class SceneRenderer:
         return cams
 
     def render(self, cameras, tiles_dev, n_tiles: int, tile_stride: int, out: dict, stream=None,
-               frame_layout: bool = False):
+               frame_layout: bool = False, peer: bool = False):
         cams = cameras if isinstance(cameras, C.Array) else self.camera_array(cameras)
         so = N.SceneOut()
-        so.rgba = out["rgba"].data_ptr() if "rgba" in out else None
-        so.depth = out["depth"].data_ptr() if "depth" in out else None
-        so.rgba8 = out["rgba8"].data_ptr() if "rgba8" in out else None
-        so.depth16 = out["depth16"].data_ptr() if "depth16" in out else None
+        def ptr(key):              # tensors, or raw device addresses (peer mappings)
+            v = out.get(key)
+            return None if v is None else (v if isinstance(v, int) else v.data_ptr())
+
+        so.rgba = ptr("rgba")
+        so.depth = ptr("depth")
+        so.rgba8 = ptr("rgba8")
+        so.depth16 = ptr("depth16")
         so.tile_stride = int(tile_stride)
         so.depth_far = self.depth_far
         so.layout = 1 if frame_layout else 0
+        so.peer = 1 if peer else 0
         st = stream if stream is not None else _stream_ptr()
         ws = self._workspace(cams, int(n_tiles) * int(tile_stride))
         N.check(N.lib().nolf_render_scene(self._inst_arr, len(self.insts), cams, len(cams),
