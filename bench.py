@@ -53,6 +53,9 @@ def parse():
     p.add_argument("--cpu-seconds", type=float, default=12.0)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--verify", action="store_true",
+                   help="rank 0 re-renders the last frame alone and compares bitwise with the "
+                        "multi-GPU assembled frame")
     p.add_argument("--exchange", default="p2p", choices=["p2p", "gather"],
                    help="N>1 frame composer: compose stores into rank 0's frame over NVLink "
                         "(CUDA IPC peer memory) or NCCL gather + unpack kernel")
@@ -471,6 +474,34 @@ def run_ours(args):
                "h2d_bytes_per_step": int(N.lib().nolf_launch_param_bytes(len(scene), n_views)),
                "d2h_bytes_per_step": int(npix * 6)}
 
+    # ---- multi-GPU frame == single-GPU frame (bitwise)
+    verify = None
+    if args.verify:
+        kv = args.warmup + args.steps - 1
+        step(kv, 0)
+        barrier()
+        if rank == 0:
+            import ctypes
+            got = torch.empty(NPX * 6, dtype=torch.uint8, device=dev)
+            if p2p:
+                N.check(N.lib().nolf_memcpy_async(got.data_ptr(), peer_frames[0][0], NPX * 6,
+                                                  torch.cuda.current_stream().cuda_stream))
+            else:
+                got[:NPX * 4].copy_(frames[0][0].view(-1))
+                got[NPX * 4:].copy_(frames[0][1].view(torch.uint8).view(-1))
+            all_tiles = torch.from_numpy(tiles.astype(np.int32)).to(dev)
+            ref = {"rgba8": torch.empty((NPX, 4), dtype=torch.uint8, device=dev),
+                   "depth16": torch.empty(NPX, dtype=torch.int16, device=dev),
+                   "counters": torch.zeros(4, dtype=torch.int64, device=dev)}
+            R.reserve([cam_arrays[kv % n_cam]], n_tiles * stride)
+            R.render(cam_arrays[kv % n_cam], all_tiles, n_tiles, stride, ref, frame_layout=True)
+            exp = torch.cat([ref["rgba8"].view(-1), ref["depth16"].view(torch.uint8).view(-1)])
+            torch.cuda.synchronize()
+            verify = {"bitwise_equal": bool(torch.equal(got, exp)),
+                      "mismatched_bytes": int((got != exp).sum().item()),
+                      "what": "assembled multi-GPU frame vs rank 0 rendering every tile alone"}
+        barrier()
+
     # ---- roofline of the dominant kernel (per-launch algorithmic bytes / event time)
     peaks = {}
     try:
@@ -513,7 +544,7 @@ def run_ours(args):
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference-pipeline assets, "
             "random-init networks)", "config": workload_config(args, desc, W, H, len(scene)),
             "e2e": e2e, "gpu_launches": (3 + (1 if (world > 1 and not p2p) else 0)) * args.steps, "roofline": roof, "cpu_baseline": cpu,
-            "clocks": clk.summary(),
+            "clocks": clk.summary(), "verify": verify,
             "per_frame": {"march_samples": S, "hits": Hh, "pixels": npix},
             "step_ms": {"p50": float(np.percentile(step_ms, 50)), "p90": float(np.percentile(step_ms, 90)),
                         "max": float(step_ms.max()), "min": float(step_ms.min())},
