@@ -128,49 +128,9 @@ int upload_atlas(NolfAsset *A, const NolfAtlasDesc &d, int channels, DevAtlas *o
   } else if ((rc = A->upload(d.cubes, nc, &cubes))) {
     return rc;
   }
-  // per-cube sub-voxel distance field (density atlas only): 0 where a corner
-  // is non-zero, else the Chebyshev distance (in sub-voxels, within the cube)
-  // to the nearest such sub-voxel (255 if none); a zero sub-voxel's trilinear
-  // value is +0.  Separable L-inf transform, as for the cell grid.
-  const int r = d.r, r3 = r * r * r;
-  std::vector<uint8_t> zd(channels == 1 ? (size_t)std::max<int64_t>(d.n_cubes, 1) * r3 : 1, 0);
-  if (channels == 1) {
-    const int BIG = 1 << 20;
-    std::vector<int> f1((size_t)r3), f2((size_t)r3);
-    auto id3 = [r](int x, int y, int z) { return (x * r + y) * r + z; };
-    for (int64_t c = 0; c < d.n_cubes; ++c) {
-      const float *cube = d.cubes + (size_t)c * s * s * s;
-      for (int x = 0; x < r; ++x)
-        for (int y = 0; y < r; ++y)
-          for (int z = 0; z < r; ++z) {
-            bool zero = true;
-            for (int q = 0; q < 8 && zero; ++q)
-              zero = cube[((size_t)((x + (q & 1)) * s + (y + ((q >> 1) & 1))) * s + (z + ((q >> 2) & 1)))] == 0.0f;
-            f1[(size_t)id3(x, y, z)] = zero ? BIG : 0;
-          }
-      for (int axis = 0; axis < 3; ++axis) {
-        for (int u = 0; u < r; ++u)
-          for (int v = 0; v < r; ++v)
-            for (int w = 0; w < r; ++w) {
-              int best = BIG;
-              for (int t = 0; t < r; ++t) {
-                const int src = axis == 0 ? id3(t, u, v) : axis == 1 ? id3(u, t, v) : id3(u, v, t);
-                best = std::min(best, std::max(std::abs(w - t), f1[(size_t)src]));
-              }
-              const int dst = axis == 0 ? id3(w, u, v) : axis == 1 ? id3(u, w, v) : id3(u, v, w);
-              f2[(size_t)dst] = best;
-            }
-        f1.swap(f2);
-      }
-      for (int i = 0; i < r3; ++i) zd[(size_t)c * r3 + i] = (uint8_t)std::min(f1[(size_t)i], 255);
-    }
-  }
-  uint8_t *zdp;
-  if ((rc = A->upload(zd.data(), zd.size(), &zdp))) return rc;
   out->index = idx;
   out->dist = mac;
   out->cubes = cubes;
-  out->zdist = zdp;
   return 0;
 }
 

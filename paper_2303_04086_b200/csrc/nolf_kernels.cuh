@@ -167,55 +167,10 @@ __device__ __forceinline__ MarchOut march_ray(const DevAsset &A, const double o[
       i = next;
       continue;
     }
-    // Sub-voxels whose 8 corner densities are all 0 give sigma = +0 exactly:
-    // absorb = exp(-0) = 1 and w = 0, so such a sample only increments the
-    // active-sample count.  The cube's sub-voxel distance field bounds a box
-    // of zero sub-voxels; jump over it with the same verified, monotone
-    // argument as the empty cells (all skipped samples lie in this same
-    // active cell, so each is counted), adding the jumped samples.
-    int base[3];
-    double frac[3];
-    atlas_subvoxel(at, pos, base, frac);
-    const int sv = (base[0] * at.r + base[1]) * at.r + base[2];
-    const int zd = __ldg(at.zdist + (size_t)cid * (at.r * at.r * at.r) + sv);
-    if (zd > 0) {
-      int blo[3], bhi[3];
-      double lo[3], hi[3];
-      const double inv_br = 1.0 / ((double)b * at.r);
-#pragma unroll
-      for (int k = 0; k < 3; ++k) {
-        blo[k] = max(base[k] - (zd - 1), 0);
-        bhi[k] = min(base[k] + (zd - 1), at.r - 1);
-        const int g0 = cell[k] * at.r + blo[k], g1 = cell[k] * at.r + bhi[k] + 1;
-        lo[k] = g0 > 0 ? g0 * inv_br : -1.0;
-        hi[k] = g1 < b * at.r ? g1 * inv_br : 2.0;
-      }
-      const double te = box_exit(o, d, inv, lo, hi);
-      const double tl = fmin(te, t_far);
-      double jf = floor((tl - t_near) * inv_delta - 0.5);
-      long long j = jf > 9.0e15 ? (long long)9.0e15 : (long long)jf;
-      long long next = i + 1;
-      for (int attempt = 0; attempt < 2 && j > i; ++attempt, --j) {
-        double pj[3];
-        int cj[3], bj[3];
-        double fj[3];
-        const double tj = sample_cell(o, d, t_near, delta, j, b, pj, cj);
-        bool inside = tj < t_far && cj[0] == cell[0] && cj[1] == cell[1] && cj[2] == cell[2];
-        if (inside) {
-          atlas_subvoxel(at, pj, bj, fj);
-#pragma unroll
-          for (int k = 0; k < 3; ++k) inside = inside && bj[k] >= blo[k] && bj[k] <= bhi[k];
-        }
-        if (inside) { next = j + 1; break; }
-      }
-      samples += (int)(next - i);
-      i = next;
-      continue;
-    }
-    ++samples;
     float s;
-    atlas_trilinear_at<1>(at, cid, base, frac, &s);
+    atlas_trilinear<1>(at, cid, pos, &s);
     const double sigma = (double)s;
+    ++samples;
     const double absorb = exp(__dmul_rn(-sigma, delta));
     const double w = __dmul_rn(trans, __dsub_rn(1.0, absorb));
     if (w > best_w) { best_w = w; t_hit = t_mid; }
@@ -661,14 +616,6 @@ __global__ void __launch_bounds__(256) k_compose(ComposeArgs a) {
     }
   }
   const int n = a.nhit ? (int)a.nhit[p] : a.K;
-  if (n == 0) {                // nothing composited: alpha 0 -> miss sentinel (farm.py:169-171)
-    if (a.out_rgba) reinterpret_cast<float4 *>(a.out_rgba)[q] = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (a.out_depth) a.out_depth[q] = __int_as_float(0x7f800000);
-    if (a.out_rgba8) reinterpret_cast<uchar4 *>(a.out_rgba8)[q] = make_uchar4(0, 0, 0, 0);
-    if (a.out_depth16) a.out_depth16[q] = 65535;
-    if (a.peer) __threadfence_system();
-    return;
-  }
   float dk[kMaxLayers];
   unsigned char ord[kMaxLayers];
   // stable insertion sort by depth (np.argsort kind="stable")
