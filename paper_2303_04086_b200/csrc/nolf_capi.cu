@@ -128,9 +128,32 @@ int upload_atlas(NolfAsset *A, const NolfAtlasDesc &d, int channels, DevAtlas *o
   } else if ((rc = A->upload(d.cubes, nc, &cubes))) {
     return rc;
   }
+  // per-cube sub-voxel zero mask (8 corners exactly 0 -> trilinear value +0)
+  const int r = d.r, words = (r * r * r + 31) / 32;
+  std::vector<uint32_t> zm((size_t)std::max<int64_t>(d.n_cubes, 1) * words, 0u);
+  for (int64_t c = 0; c < d.n_cubes; ++c) {
+    const float *cube = d.cubes + (size_t)c * s * s * s * channels;
+    for (int x = 0; x < r; ++x)
+      for (int y = 0; y < r; ++y)
+        for (int z = 0; z < r; ++z) {
+          bool zero = true;
+          for (int q = 0; q < 8 && zero; ++q) {
+            const float *v = cube + ((size_t)((x + (q & 1)) * s + (y + ((q >> 1) & 1))) * s + (z + ((q >> 2) & 1))) * channels;
+            for (int ch = 0; ch < channels; ++ch) zero = zero && v[ch] == 0.0f;
+          }
+          if (zero) {
+            const int bit = (x * r + y) * r + z;
+            zm[(size_t)c * words + (bit >> 5)] |= 1u << (bit & 31);
+          }
+        }
+  }
+  uint32_t *zmp;
+  if ((rc = A->upload(zm.data(), zm.size(), &zmp))) return rc;
   out->index = idx;
   out->dist = mac;
   out->cubes = cubes;
+  out->zmask = zmp;
+  out->zwords = words;
   return 0;
 }
 

@@ -21,6 +21,8 @@ struct DevAtlas {              // CubeAtlas (atlas.py:25-51)
   const float *cubes;          // n * s^3 * C
   const uint8_t *dist;         // b^3: Chebyshev distance (cells) to the nearest
                                // occupied cell, 0 = occupied, capped at 255
+  const uint32_t *zmask;       // per cube, r^3 bits: sub-voxel whose 8 corners are all 0
+  int zwords;                  // 32-bit words per cube
 };
 
 // Fully fused MLP parameter block (neural.py:29-108), fp32, padded:
@@ -179,12 +181,9 @@ __device__ __forceinline__ bool slab(const double pmin[3], const double pmax[3],
   return t_near <= t_far;
 }
 
-// query_atlas (atlas.py:158-185) inside a known non-empty cube; C <= 4.
-template <int C>
-__device__ __forceinline__ void atlas_trilinear(const DevAtlas &at, int cid, const double x[3], float out[C]) {
+// Sub-voxel of x inside its cube and the trilinear fractions (atlas.py:162-172).
+__device__ __forceinline__ void atlas_subvoxel(const DevAtlas &at, const double x[3], int base[3], double frac[3]) {
   const double bd = (double)at.b, rd = (double)at.r;
-  int base[3];
-  double frac[3];
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
     double scaled = __dmul_rn(x[k], bd);
@@ -193,6 +192,24 @@ __device__ __forceinline__ void atlas_trilinear(const DevAtlas &at, int cid, con
     base[k] = clampi((int)floor(local), 0, at.r - 1);
     frac[k] = __dsub_rn(local, (double)base[k]);
   }
+}
+
+template <int C>
+__device__ __forceinline__ void atlas_trilinear_at(const DevAtlas &at, int cid, const int base[3], const double frac[3],
+                                                   float out[C]);
+
+// query_atlas (atlas.py:158-185) inside a known non-empty cube; C <= 4.
+template <int C>
+__device__ __forceinline__ void atlas_trilinear(const DevAtlas &at, int cid, const double x[3], float out[C]) {
+  int base[3];
+  double frac[3];
+  atlas_subvoxel(at, x, base, frac);
+  atlas_trilinear_at<C>(at, cid, base, frac, out);
+}
+
+template <int C>
+__device__ __forceinline__ void atlas_trilinear_at(const DevAtlas &at, int cid, const int base[3], const double frac[3],
+                                                   float out[C]) {
   const int s = at.s;
   const float *cube = at.cubes + (size_t)cid * (size_t)(s * s * s * C);
   double acc[C];

@@ -167,10 +167,20 @@ __device__ __forceinline__ MarchOut march_ray(const DevAsset &A, const double o[
       i = next;
       continue;
     }
-    float s;
-    atlas_trilinear<1>(at, cid, pos, &s);
-    const double sigma = (double)s;
+    // sub-voxel whose 8 corner densities are all 0: sigma = +0 exactly, so
+    // absorb = exp(-0) = 1, w = 0 -- only the active-sample count changes
+    int base[3];
+    double frac[3];
+    atlas_subvoxel(at, pos, base, frac);
+    const int bit = (base[0] * at.r + base[1]) * at.r + base[2];
     ++samples;
+    if ((__ldg(at.zmask + (size_t)cid * at.zwords + (bit >> 5)) >> (bit & 31)) & 1u) {
+      ++i;
+      continue;
+    }
+    float s;
+    atlas_trilinear_at<1>(at, cid, base, frac, &s);
+    const double sigma = (double)s;
     const double absorb = exp(__dmul_rn(-sigma, delta));
     const double w = __dmul_rn(trans, __dsub_rn(1.0, absorb));
     if (w > best_w) { best_w = w; t_hit = t_mid; }
@@ -616,6 +626,14 @@ __global__ void __launch_bounds__(256) k_compose(ComposeArgs a) {
     }
   }
   const int n = a.nhit ? (int)a.nhit[p] : a.K;
+  if (n == 0) {                // nothing composited: alpha 0 -> miss sentinel (farm.py:169-171)
+    if (a.out_rgba) reinterpret_cast<float4 *>(a.out_rgba)[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (a.out_depth) a.out_depth[q] = __int_as_float(0x7f800000);
+    if (a.out_rgba8) reinterpret_cast<uchar4 *>(a.out_rgba8)[q] = make_uchar4(0, 0, 0, 0);
+    if (a.out_depth16) a.out_depth16[q] = 65535;
+    if (a.peer) __threadfence_system();
+    return;
+  }
   float dk[kMaxLayers];
   unsigned char ord[kMaxLayers];
   // stable insertion sort by depth (np.argsort kind="stable")
