@@ -379,7 +379,8 @@ int fill_inst(const NolfInstance *in, DevInst *out) {
 }
 
 int run_shade(const DevInst *inst, const long long *qoff, int n_inst, const Workspace &w, int mode, float *rgba,
-              float *depth, long long layer_stride, unsigned long long *counters, cudaStream_t st, bool use_tc);
+              float *depth, long long layer_stride, unsigned long long *counters, cudaStream_t st, bool use_tc,
+              uint32_t phi_smem_bytes);
 
 }  // namespace
 
@@ -696,7 +697,8 @@ size_t nolf_scene_workspace_bytes(const NolfInstance *inst, int32_t n_inst, cons
 namespace {
 
 int run_shade(const DevInst *inst, const long long *qoff, int n_inst, const Workspace &w, int mode, float *rgba,
-              float *depth, long long layer_stride, unsigned long long *counters, cudaStream_t st, bool use_tc) {
+              float *depth, long long layer_stride, unsigned long long *counters, cudaStream_t st, bool use_tc,
+              uint32_t phi_smem_bytes) {
   ShadeArgs sa{};
   sa.inst = inst;
   sa.n_inst = n_inst;
@@ -709,7 +711,12 @@ int run_shade(const DevInst *inst, const long long *qoff, int n_inst, const Work
   sa.layer_stride = layer_stride;
   sa.counters = counters;
   if (use_tc) {
-    k_shade_tc<<<num_sms() * 2, kTcThreads, kTcSmem, st>>>(sa);
+    // dynamic smem sized to the largest Phi the launch stages (not the 64 KB
+    // worst case) so more CTAs fit per SM
+    const size_t smem = kTcSmem - kTcPhiMax + phi_smem_bytes;
+    int per_sm = 0;
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_shade_tc, kTcThreads, smem));
+    k_shade_tc<<<num_sms() * std::max(per_sm, 1), kTcThreads, smem, st>>>(sa);
   } else {
     k_shade<<<num_sms() * 3, kShadeThreads, kShadeSmem, st>>>(sa);
   }
@@ -798,9 +805,12 @@ int launch_march_shade(int mode, const NolfInstance *ins, int n_inst, const Nolf
   int slot;
   if ((rc = ring_acquire(&hp, &dp, &slot))) return rc;
   bool use_tc = true;
+  uint32_t phi_smem = 0;
   for (int k = 0; k < n_inst; ++k) {
     if ((rc = fill_inst(ins + k, hp->inst + k))) return rc;
-    use_tc = use_tc && ins[k].asset->host.mlp_mode == NOLF_MLP_BF16;
+    const DevAsset &H = ins[k].asset->host;
+    use_tc = use_tc && H.mlp_mode == NOLF_MLP_BF16;
+    if (H.phi16 && H.phi16_bytes <= kTcPhiMax) phi_smem = std::max(phi_smem, H.phi16_bytes);
   }
   for (int c = 0; c < n_cams; ++c) hp->cams[c] = hcams[(size_t)c];
   hp->rect = rect;
@@ -838,7 +848,8 @@ int launch_march_shade(int mode, const NolfInstance *ins, int n_inst, const Nolf
   CUDA_TRY(cudaGetLastError());
   if ((rc = prof_mark(1, st))) return rc;
   if (mode == kModeScene) {
-    if ((rc = run_shade(dp->inst, dp->qoff, n_inst, w, mode, w.lrgba, w.ldepth, w.P, counters, st, use_tc)))
+    if ((rc = run_shade(dp->inst, dp->qoff, n_inst, w, mode, w.lrgba, w.ldepth, w.P, counters, st, use_tc,
+                        phi_smem)))
       return rc;
     if ((rc = prof_mark(2, st))) return rc;
     ComposeArgs ca{};
@@ -863,7 +874,8 @@ int launch_march_shade(int mode, const NolfInstance *ins, int n_inst, const Nolf
     CUDA_TRY(cudaGetLastError());
     if ((rc = prof_mark(3, st))) return rc;
   } else {
-    if ((rc = run_shade(dp->inst, dp->qoff, n_inst, w, mode, rgba, depth, 0, counters, st, use_tc))) return rc;
+    if ((rc = run_shade(dp->inst, dp->qoff, n_inst, w, mode, rgba, depth, 0, counters, st, use_tc, phi_smem)))
+      return rc;
     if ((rc = prof_mark(2, st))) return rc;
     if ((rc = prof_mark(3, st))) return rc;
   }

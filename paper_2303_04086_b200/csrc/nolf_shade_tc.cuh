@@ -174,7 +174,7 @@ __device__ __forceinline__ void tc_stage_asset(const DevAsset &A, const TcSmemPt
   tma_phase ^= 1;
 }
 
-__global__ void __launch_bounds__(kTcThreads) k_shade_tc(ShadeArgs args) {
+__global__ void __launch_bounds__(kTcThreads, 3) k_shade_tc(ShadeArgs args) {
   extern __shared__ uint8_t smem_raw[];
   const TcSmemPtrs S = tc_carve(smem_raw);
   const int tid = threadIdx.x, warp = tid >> 5;
