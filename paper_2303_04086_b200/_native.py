@@ -15,7 +15,8 @@ import numpy as np
 from . import errors
 
 LIB_NAME = "libnolf_b200.so"
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
+LIB_PATH = os.environ.get("NOLF_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)),
+                                                     LIB_NAME)
 
 NOLF_EINVAL, NOLF_ESTATE, NOLF_EDATA, NOLF_ECUDA, NOLF_ENOMEM = -1, -2, -3, -4, -5
 HEAD_ACT = {"identity": 0, "sigmoid": 1, "exponential": 2}

@@ -1,6 +1,7 @@
 // nolf_capi.cu -- C ABI (include/nolf.h): asset upload, workspace layout and
 // the launch sequence of the i-NOLF hot path on sm_100a.
 #include <cstdarg>
+#include <cstdlib>
 #include <cstdio>
 #include <algorithm>
 #include <cmath>
@@ -713,9 +714,19 @@ int run_shade(const DevInst *inst, const long long *qoff, int n_inst, const Work
   if (use_tc) {
     // dynamic smem sized to the largest Phi the launch stages (not the 64 KB
     // worst case) so more CTAs fit per SM
+    sa.tile_order = 1;               // blocked tile ranges per CTA
     const size_t smem = kTcSmem - kTcPhiMax + phi_smem_bytes;
-    int per_sm = 0;
-    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_shade_tc, kTcThreads, smem));
+    // resident CTAs per SM from registers and shared memory (TMEM: 64 columns
+    // each, never the limit below 8)
+    static int regs = 0;
+    if (!regs) {
+      cudaFuncAttributes fa{};
+      CUDA_TRY(cudaFuncGetAttributes(&fa, k_shade_tc));
+      regs = fa.numRegs > 0 ? fa.numRegs : 168;
+    }
+    const int by_regs = 65536 / (((regs + 7) / 8 * 8) * kTcThreads);
+    const int by_smem = (int)((227u * 1024u) / (smem + 1024u));
+    int per_sm = std::max(1, std::min(std::min(by_regs, by_smem), 4));
     k_shade_tc<<<num_sms() * std::max(per_sm, 1), kTcThreads, smem, st>>>(sa);
   } else {
     k_shade<<<num_sms() * 3, kShadeThreads, kShadeSmem, st>>>(sa);
@@ -832,6 +843,7 @@ int launch_march_shade(int mode, const NolfInstance *ins, int n_inst, const Nolf
   ma.tiles = mode == kModeScene ? reinterpret_cast<const TileParams *>(tiles_dev) : &dp->rect;
   ma.tile_stride = tile_stride;
   ma.cull = n_cams > 0 ? dp->cull : nullptr;
+  ma.use_zmask = 1;
   ma.n_cams = n_cams > 0 ? n_cams : 1;
   ma.queue = w.queue;
   ma.qoff = dp->qoff;

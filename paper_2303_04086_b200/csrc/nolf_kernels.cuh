@@ -55,6 +55,7 @@ struct MarchArgs {
   unsigned long long *counters;
   // march_rays mode (lightfield.py:129-186 outputs per ray, no queue)
   int raw_rays;                // 1: rays are already in object space (no w2o, no renormalise)
+  int use_zmask;               // skip zero-corner sub-voxels (always on; 0 for A/B checks)
   uint8_t *out_hit;
   double *out_t_hit, *out_alpha_c, *out_p_h;
   long long *out_samples;
@@ -108,7 +109,7 @@ struct MarchOut {
 };
 
 __device__ __forceinline__ MarchOut march_ray(const DevAsset &A, const double o[3], const double d[3],
-                                              const double inv[3], double t_near, double t_far) {
+                                              const double inv[3], double t_near, double t_far, bool use_zmask) {
   MarchOut r;
   r.alpha_c = 0.0;
   r.t_hit = __longlong_as_double(0x7ff0000000000000ll);
@@ -174,7 +175,7 @@ __device__ __forceinline__ MarchOut march_ray(const DevAsset &A, const double o[
     atlas_subvoxel(at, pos, base, frac);
     const int bit = (base[0] * at.r + base[1]) * at.r + base[2];
     ++samples;
-    if ((__ldg(at.zmask + (size_t)cid * at.zwords + (bit >> 5)) >> (bit & 31)) & 1u) {
+    if (use_zmask && ((__ldg(at.zmask + (size_t)cid * at.zwords + (bit >> 5)) >> (bit & 31)) & 1u)) {
       ++i;
       continue;
     }
@@ -273,7 +274,7 @@ __global__ void __launch_bounds__(128) k_march(MarchArgs args) {
         else t_near = tm;
       }
       if (boxhit) {
-        mr = march_ray(A, o, d, inv, t_near, t_far);
+        mr = march_ray(A, o, d, inv, t_near, t_far, args.use_zmask);
         samples_total += (unsigned long long)mr.samples;
         hit = mr.hit;
       }
@@ -338,6 +339,7 @@ struct ShadeArgs {
   float *rgba;                 // rays/rect: (n,4); scene: layers (L, P, 4)
   float *depth;                // rays/rect: (n,);  scene: layers (L, P)
   long long layer_stride;      // scene: P
+  int tile_order;              // 0 round-robin tiles over CTAs, 1 blocked ranges
   unsigned long long *counters;
 };
 
@@ -416,7 +418,14 @@ __global__ void __launch_bounds__(kShadeThreads) k_shade(ShadeArgs args) {
   const int tid = threadIdx.x;
   int cur = -1;
   unsigned long long n_fs = 0, n_fd = 0;
-  for (long long tile = blockIdx.x;; tile += gridDim.x) {
+  // blocked tile ranges: consecutive tiles (mostly one instance) per CTA, so
+  // each CTA reloads few assets' weights
+  long long total_tiles = 0;
+  for (int q = 0; q < args.n_inst; ++q)
+    total_tiles += (min((long long)args.counts[q], args.qoff[q + 1] - args.qoff[q]) + kShadeThreads - 1) / kShadeThreads;
+  const long long tile_lo = total_tiles * blockIdx.x / gridDim.x;
+  const long long tile_hi = total_tiles * (blockIdx.x + 1) / gridDim.x;
+  for (long long tile = tile_lo; tile < tile_hi; ++tile) {
     // map the global tile id onto (instance, first record)
     int k = 0;
     long long t = tile;

@@ -174,7 +174,7 @@ __device__ __forceinline__ void tc_stage_asset(const DevAsset &A, const TcSmemPt
   tma_phase ^= 1;
 }
 
-__global__ void __launch_bounds__(kTcThreads, 3) k_shade_tc(ShadeArgs args) {
+__global__ void __launch_bounds__(kTcThreads) k_shade_tc(ShadeArgs args) {
   extern __shared__ uint8_t smem_raw[];
   const TcSmemPtrs S = tc_carve(smem_raw);
   const int tid = threadIdx.x, warp = tid >> 5;
@@ -192,7 +192,15 @@ __global__ void __launch_bounds__(kTcThreads, 3) k_shade_tc(ShadeArgs args) {
   int cur = -1;
   bool phi_smem = false, tab_smem = false;
   unsigned long long n_fs = 0;
-  for (long long tile = blockIdx.x;; tile += gridDim.x) {
+  // tile order: blocked ranges per CTA (args.tile_order == 1) or round-robin
+  long long total_tiles = 0;
+  for (int q = 0; q < args.n_inst; ++q)
+    total_tiles += (min((long long)args.counts[q], args.qoff[q + 1] - args.qoff[q]) + kTcThreads - 1) / kTcThreads;
+  const bool blocked = args.tile_order == 1;
+  const long long tile_lo = blocked ? total_tiles * blockIdx.x / gridDim.x : blockIdx.x;
+  const long long tile_hi = blocked ? total_tiles * (blockIdx.x + 1) / gridDim.x : total_tiles;
+  const long long tile_step = blocked ? 1 : gridDim.x;
+  for (long long tile = tile_lo; tile < tile_hi; tile += tile_step) {
     int k = 0;
     long long t = tile;
     unsigned cnt = 0;
