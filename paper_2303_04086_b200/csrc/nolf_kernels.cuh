@@ -198,7 +198,10 @@ __device__ __forceinline__ MarchOut march_ray(const DevAsset &A, const double o[
 }
 
 template <int MODE>
-__global__ void __launch_bounds__(128) k_march(MarchArgs args) {
+#ifndef NOLF_MARCH_MINB
+#define NOLF_MARCH_MINB 8  // latency-bound: 50% occupancy beats the spills it costs (measured 4..8)
+#endif
+__global__ void __launch_bounds__(128, NOLF_MARCH_MINB) k_march(MarchArgs args) {
   const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const unsigned lane = threadIdx.x & 31;
   bool valid = gid < args.n_rays;
