@@ -53,6 +53,10 @@ def parse():
     p.add_argument("--cpu-seconds", type=float, default=12.0)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--e2e-mode", default="hostmap", choices=["hostmap", "copy"],
+                   help="hostmap: compose stores every rank's tiles straight into one shared, "
+                        "page-locked host frame (zero-copy, each GPU over its own PCIe link); "
+                        "copy: rank 0 downloads the assembled frame with cudaMemcpyAsync")
     p.add_argument("--verify", action="store_true",
                    help="rank 0 re-renders the last frame alone and compares bitwise with the "
                         "multi-GPU assembled frame")
@@ -424,9 +428,56 @@ def run_ours(args):
     npix = NPX
     value = args.steps * npix / t_max / 1e6
 
-    # ---- end to end: camera in (H2D param block), encoded frame out (D2H) to pinned host
+    # ---- end to end: camera in (H2D param block), encoded frame out to host memory
     e2e = None
-    if not args.no_e2e:
+    shm = host_map = None
+    if not args.no_e2e and args.e2e_mode == "hostmap":
+        # Every rank maps one shared, page-locked host frame (double buffered)
+        # and its compose kernel stores its tiles straight into it (zero-copy
+        # over its own PCIe link, system-scope fence); a 1-element all-reduce
+        # marks the frame complete.  Timed from the first render to the last
+        # rank's completion (device events, max over ranks).
+        import ctypes
+        from multiprocessing import resource_tracker, shared_memory
+        FB = NPX * 6
+        name = f"nolf_frame_{os.environ.get('MASTER_PORT', 'solo')}_{os.environ.get('TORCHELASTIC_RUN_ID', os.getpid())}"
+        if rank == 0:
+            shm = shared_memory.SharedMemory(name=name, create=True, size=2 * FB)
+        if world > 1:
+            dist.barrier()
+        if rank != 0:
+            shm = shared_memory.SharedMemory(name=name)
+            resource_tracker.unregister(shm._name, "shared_memory")   # rank 0 owns it
+        host_addr = ctypes.addressof(ctypes.c_char.from_buffer(shm.buf))
+        dptr = ctypes.c_void_p()
+        N.check(N.lib().nolf_host_register(host_addr, 2 * FB, ctypes.byref(dptr)))
+        host_map = [(dptr.value + fb * FB, dptr.value + fb * FB + NPX * 4) for fb in range(2)]
+
+        def step_host(k, fb):
+            o2 = {"rgba8": host_map[fb][0], "depth16": host_map[fb][1], "counters": out["counters"]}
+            R.render(cam_arrays[k % n_cam], my_tiles, n_max, stride, o2, frame_layout=True, peer=True)
+            if world > 1:
+                dist.all_reduce(token)
+
+        for k in range(2):
+            step_host(k, k % 2)
+        barrier()
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record()
+        for k in range(args.steps):
+            step_host(k, k % 2)
+        t1.record()
+        t1.synchronize()
+        barrier()
+        te = torch.tensor([t0.elapsed_time(t1) / 1e3], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": args.steps * npix / float(te.item()) / 1e6, "unit": UNIT,
+               "h2d_bytes_per_step": int(N.lib().nolf_launch_param_bytes(len(scene), n_views)),
+               "d2h_bytes_per_step": int(npix * 6),
+               "mode": "compose stores into a shared page-locked host frame (zero-copy, per-GPU PCIe)"}
+    elif not args.no_e2e:
         # Pipelined: step k renders into frame buffer k%2 on the compute
         # stream; a copy stream downloads it to pinned host memory while
         # step k+1 renders.  Timed from the first render to the last byte on
@@ -472,7 +523,8 @@ def run_ours(args):
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e2e = {"value": args.steps * npix / float(te.item()) / 1e6, "unit": UNIT,
                "h2d_bytes_per_step": int(N.lib().nolf_launch_param_bytes(len(scene), n_views)),
-               "d2h_bytes_per_step": int(npix * 6)}
+               "d2h_bytes_per_step": int(npix * 6),
+               "mode": "rank 0 cudaMemcpyAsync of the assembled frame, double-buffered"}
 
     # ---- multi-GPU frame == single-GPU frame (bitwise)
     verify = None
@@ -500,6 +552,14 @@ def run_ours(args):
             verify = {"bitwise_equal": bool(torch.equal(got, exp)),
                       "mismatched_bytes": int((got != exp).sum().item()),
                       "what": "assembled multi-GPU frame vs rank 0 rendering every tile alone"}
+            if host_map is not None:      # last e2e frame (host memory) vs the same camera alone
+                ke = args.steps - 1
+                R.render(cam_arrays[ke % n_cam], all_tiles, n_tiles, stride, ref, frame_layout=True)
+                exp2 = torch.cat([ref["rgba8"].view(-1), ref["depth16"].view(torch.uint8).view(-1)])
+                FBn = NPX * 6
+                hostf = torch.frombuffer(shm.buf, dtype=torch.uint8)[(ke % 2) * FBn:(ke % 2 + 1) * FBn]
+                verify["host_frame_bitwise_equal"] = bool(torch.equal(hostf, exp2.cpu()))
+                del hostf
         barrier()
 
     # ---- roofline of the dominant kernel (per-launch algorithmic bytes / event time)
@@ -555,6 +615,20 @@ def run_ours(args):
                                           "(CUDA IPC peer memory) + 1-element NCCL all-reduce"
                                           if p2p else "NCCL gather of encoded tiles + unpack kernel")
         print(json.dumps(line), flush=True)
+    if host_map is not None:
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        import ctypes
+        N.lib().nolf_host_unregister(ctypes.addressof(ctypes.c_char.from_buffer(shm.buf)))
+        try:
+            shm.close()
+        except BufferError:       # a view is still referenced; the mapping dies with the process
+            pass
+        if world > 1:
+            dist.barrier()
+        if rank == 0:
+            shm.unlink()
     if world > 1:
         dist.barrier()
         torch.cuda.synchronize()

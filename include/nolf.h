@@ -230,6 +230,11 @@ int nolf_ipc_get_handle(void *ptr, void *handle64);          /* 64-byte handle o
 int nolf_ipc_open_handle(const void *handle64, void **ptr);  /* peer mapping */
 int nolf_ipc_close_handle(void *ptr);
 int nolf_memcpy_async(void *dst, const void *src, size_t bytes, void *stream);
+/* Page-lock host memory (e.g. a shared-memory frame buffer mapped by every
+ * rank) and map it into the device address space: compose kernels then
+ * store frames straight into host memory over each GPU's own PCIe link. */
+int nolf_host_register(void *host_ptr, size_t bytes, void **dev_ptr);
+int nolf_host_unregister(void *host_ptr);
 
 /* frames: rgba (K, P, 4) f32, depth (K, P) f32, all device pointers. */
 int nolf_compose(int32_t K, int64_t P, const float *rgba, const float *depth, double alpha_vis,

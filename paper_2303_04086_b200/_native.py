@@ -109,6 +109,8 @@ def lib():
         "nolf_ipc_open_handle": ([vp, C.POINTER(vp)], C.c_int),
         "nolf_ipc_close_handle": ([vp], C.c_int),
         "nolf_memcpy_async": ([vp, vp, C.c_size_t, vp], C.c_int),
+        "nolf_host_register": ([vp, C.c_size_t, C.POINTER(vp)], C.c_int),
+        "nolf_host_unregister": ([vp], C.c_int),
         "nolf_profile_read": ([C.POINTER(C.c_float)], C.c_int),
         "nolf_launch_param_bytes": ([i32, i32], C.c_size_t),
         "nolf_unpack_gathered": ([vp, i32, i32, i64, vp, i32, i32, vp, vp, vp], C.c_int),

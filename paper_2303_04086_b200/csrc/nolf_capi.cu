@@ -1106,6 +1106,18 @@ int nolf_memcpy_async(void *dst, const void *src, size_t bytes, void *stream) {
   return 0;
 }
 
+int nolf_host_register(void *host_ptr, size_t bytes, void **dev_ptr) {
+  if (!host_ptr || !dev_ptr || bytes == 0) return fail(NOLF_EINVAL, "bad host buffer");
+  CUDA_TRY(cudaHostRegister(host_ptr, bytes, cudaHostRegisterMapped | cudaHostRegisterPortable));
+  CUDA_TRY(cudaHostGetDevicePointer(dev_ptr, host_ptr, 0));
+  return 0;
+}
+
+int nolf_host_unregister(void *host_ptr) {
+  if (host_ptr) CUDA_TRY(cudaHostUnregister(host_ptr));
+  return 0;
+}
+
 int nolf_compose(int32_t K, int64_t P, const float *rgba, const float *depth, double alpha_vis, float *out_rgba,
                  float *out_depth, void *stream) {
   if (K < 1) return fail(NOLF_EINVAL, "compose needs at least one frame");
