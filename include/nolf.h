@@ -230,6 +230,8 @@ int nolf_ipc_get_handle(void *ptr, void *handle64);          /* 64-byte handle o
 int nolf_ipc_open_handle(const void *handle64, void **ptr);  /* peer mapping */
 int nolf_ipc_close_handle(void *ptr);
 int nolf_memcpy_async(void *dst, const void *src, size_t bytes, void *stream);
+int nolf_memcpy2d_async(void *dst, size_t dpitch, const void *src, size_t spitch, size_t width_bytes,
+                        size_t height, void *stream);
 /* Page-lock host memory (e.g. a shared-memory frame buffer mapped by every
  * rank) and map it into the device address space: compose kernels then
  * store frames straight into host memory over each GPU's own PCIe link. */

@@ -109,6 +109,7 @@ def lib():
         "nolf_ipc_open_handle": ([vp, C.POINTER(vp)], C.c_int),
         "nolf_ipc_close_handle": ([vp], C.c_int),
         "nolf_memcpy_async": ([vp, vp, C.c_size_t, vp], C.c_int),
+        "nolf_memcpy2d_async": ([vp, C.c_size_t, vp, C.c_size_t, C.c_size_t, C.c_size_t, vp], C.c_int),
         "nolf_host_register": ([vp, C.c_size_t, C.POINTER(vp)], C.c_int),
         "nolf_host_unregister": ([vp], C.c_int),
         "nolf_profile_read": ([C.POINTER(C.c_float)], C.c_int),

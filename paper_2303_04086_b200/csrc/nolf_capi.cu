@@ -1106,6 +1106,15 @@ int nolf_memcpy_async(void *dst, const void *src, size_t bytes, void *stream) {
   return 0;
 }
 
+int nolf_memcpy2d_async(void *dst, size_t dpitch, const void *src, size_t spitch, size_t width_bytes, size_t height,
+                        void *stream) {
+  if (width_bytes == 0 || height == 0) return 0;
+  if (!dst || !src) return fail(NOLF_EINVAL, "null buffer");
+  CUDA_TRY(cudaMemcpy2DAsync(dst, dpitch, src, spitch, width_bytes, height, cudaMemcpyDefault,
+                             static_cast<cudaStream_t>(stream)));
+  return 0;
+}
+
 int nolf_host_register(void *host_ptr, size_t bytes, void **dev_ptr) {
   if (!host_ptr || !dev_ptr || bytes == 0) return fail(NOLF_EINVAL, "bad host buffer");
   CUDA_TRY(cudaHostRegister(host_ptr, bytes, cudaHostRegisterMapped | cudaHostRegisterPortable));

@@ -318,13 +318,35 @@ class FarmAssigner:
 
 
 def tile_partition(n_tiles: int, world: int, rank: int) -> np.ndarray:
-    """Throughput-mode ray-tile -> GPU map: tile t renders on GPU t mod N."""
+    """Tile-interleaved ray-tile -> GPU map: tile t renders on GPU t mod N."""
     return np.arange(rank, n_tiles, world, dtype=np.int64)
 
 
-def gather_slots(n_tiles: int, world: int) -> np.ndarray:
+def row_partition(tiles: np.ndarray, world: int, rank: int, tile: int) -> np.ndarray:
+    """Throughput-mode map: tile ROWS interleaved over GPUs (row index
+    counted across cameras), so a GPU's pixels form evenly strided bands of
+    the frame -- one strided DMA per frame moves them to host memory."""
+    tiles = np.asarray(tiles)
+    heights = np.zeros(int(tiles[:, 0].max()) + 1 if len(tiles) else 1, np.int64)
+    for c in range(len(heights)):
+        sel = tiles[:, 0] == c
+        heights[c] = tiles[sel, 4].max() if sel.any() else 0
+    rows_per_cam = -(-heights // tile)
+    base = np.concatenate([[0], np.cumsum(rows_per_cam)[:-1]])
+    row = base[tiles[:, 0]] + tiles[:, 2] // tile
+    return np.flatnonzero(row % world == rank).astype(np.int64)
+
+
+def gather_slots(n_tiles: int, world: int, parts=None) -> np.ndarray:
     """Rank-major slot of every tile after an equal-size gather of each
-    rank's ceil(n_tiles/N) tile slots."""
-    n_max = -(-n_tiles // world)
-    t = np.arange(n_tiles)
-    return (t % world) * n_max + t // world
+    rank's n_max tile slots (parts: per-rank tile index lists; default the
+    tile-interleaved partition)."""
+    if parts is None:
+        n_max = -(-n_tiles // world)
+        t = np.arange(n_tiles)
+        return (t % world) * n_max + t // world
+    n_max = max(len(p) for p in parts)
+    slots = np.full(n_tiles, -1, np.int64)
+    for r, p in enumerate(parts):
+        slots[p] = r * n_max + np.arange(len(p))
+    return slots

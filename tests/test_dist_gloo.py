@@ -11,8 +11,8 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2303_04086_b200.dist import (gather_to_root, rank_buffer_bytes, shard_tiles,
-                                        slot_tile_table)
+from paper_2303_04086_b200.dist import (gather_to_root, partition, rank_buffer_bytes, row_bands,
+                                        shard_tiles, slot_tile_table)
 from paper_2303_04086_b200.render import frame_tiles
 
 W, H, T = 70, 45, 16
@@ -23,13 +23,14 @@ def pixel_code(x, y):
     return ((x * 7 + y * 13) % 251).astype(np.uint8)
 
 
-def worker(rank, world, port, q):
+def worker(rank, world, port, q, by_rows):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         tiles = frame_tiles(W, H, T)
-        mine, n_max = shard_tiles(tiles, world, rank)
+        parts = partition(tiles, world, T, by_rows=by_rows)
+        mine, n_max = shard_tiles(tiles, world, rank, parts)
         P = n_max * STRIDE
         buf = np.zeros(rank_buffer_bytes(n_max, STRIDE), np.uint8)
         rgba = buf[:P * 4].reshape(P, 4)
@@ -45,7 +46,7 @@ def worker(rank, world, port, q):
         out = gather_to_root(t, gathered, world, rank)
         if rank == 0:
             g = out.numpy()
-            table = slot_tile_table(tiles, world)
+            table = slot_tile_table(tiles, world, parts)
             frame = np.zeros((H * W, 4), np.uint8)
             fdepth = np.zeros(H * W, np.uint16)
             per = rank_buffer_bytes(n_max, STRIDE)
@@ -62,13 +63,14 @@ def worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-def test_two_rank_gather_assembles_the_frame():
+@pytest.mark.parametrize("by_rows", [False, True])
+def test_two_rank_gather_assembles_the_frame(by_rows):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
         port = s.getsockname()[1]
-    procs = [ctx.Process(target=worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=worker, args=(r, 2, port, q, by_rows)) for r in range(2)]
     for p in procs:
         p.start()
     frame, fdepth = q.get(timeout=120)
@@ -80,6 +82,18 @@ def test_two_rank_gather_assembles_the_frame():
     assert np.array_equal(frame[:, 0].reshape(H, W), pixel_code(xs, ys))
     tiles = frame_tiles(W, H, T)
     owner = np.zeros((H, W), np.uint8)
-    for t, (c, x0, y0, x1, y1) in enumerate(tiles):
-        owner[y0:y1, x0:x1] = t % 2 + 1
-    assert np.array_equal(frame[:, 1].reshape(H, W), owner)   # tile t rendered by rank t mod 2
+    for r, p in enumerate(partition(tiles, 2, T, by_rows=by_rows)):
+        for c, x0, y0, x1, y1 in tiles[p]:
+            owner[y0:y1, x0:x1] = r + 1
+    assert np.array_equal(frame[:, 1].reshape(H, W), owner)   # each tile rendered by its owner
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 4, 8])
+def test_row_bands_cover_every_pixel_once(world):
+    for V, w, h, t in ((1, 3840, 2160, 32), (16, 216, 216, 32), (2, 64, 45, 16)):
+        cnt = np.zeros(V * h * w, np.int32)
+        for r in range(world):
+            for first, wpx, ppx, hgt in row_bands(world, r, V, w, h, t):
+                for k in range(hgt):
+                    cnt[first + k * ppx:first + k * ppx + wpx] += 1
+        assert cnt.min() == 1 and cnt.max() == 1
