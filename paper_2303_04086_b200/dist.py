@@ -60,3 +60,17 @@ def row_bands(world: int, rank: int, n_views: int, width: int, height: int, tile
             out.append(((c * height + ty * tile) * width, (height - ty * tile) * width,
                         (height - ty * tile) * width, 1))
     return out
+
+
+def rank_buffer_bytes(n_max: int, tile_stride: int) -> int:
+    """Per-rank gather payload: n_max slots of rgba8 then their depth16."""
+    return n_max * tile_stride * 6
+
+
+def gather_to_root(buf, gathered, world: int, rank: int):
+    """One collective per frame: every rank's encoded tiles to rank 0."""
+    import torch.distributed as dist
+    if world == 1:
+        return buf
+    dist.gather(buf, list(gathered.chunk(world)) if rank == 0 else None, dst=0)
+    return gathered
