@@ -57,6 +57,9 @@ def parse():
                    help="hostmap: compose stores every rank's tiles straight into one shared, "
                         "page-locked host frame (zero-copy, each GPU over its own PCIe link); "
                         "copy: rank 0 downloads the assembled frame with cudaMemcpyAsync")
+    p.add_argument("--partition", default="rows", choices=["rows", "tiles"],
+                   help="ray tiles over GPUs: interleaved tile rows (default; each rank's pixels "
+                        "are strided bands of the frame) or interleaved tiles")
     p.add_argument("--verify", action="store_true",
                    help="rank 0 re-renders the last frame alone and compares bitwise with the "
                         "multi-GPU assembled frame")
@@ -279,7 +282,7 @@ def workload_config(args, desc, W, H, n_assets):
                          f"NCCL gather of rgba8+u16 to rank 0"),
             "assets": n_assets, "width": W, "height": H,
             "atlas_b": 32, "atlas_r": 8, "psh_resolution": 64, "mlp": args.mlp,
-            "parallelism": f"ray-tile x{args.gpus}",
+            "parallelism": f"ray-tile x{args.gpus}", "partition": args.partition,
             "l2": "flushed between timed steps (256 MiB write)"}
 
 
@@ -312,7 +315,7 @@ def run_ours(args):
     stride = T * T
     tiles = np.concatenate([frame_tiles(W, H, T, cam=v) for v in range(n_views)])
     n_tiles = len(tiles)
-    parts = partition(tiles, world, T, by_rows=True)       # tile rows interleaved over ranks
+    parts = partition(tiles, world, T, by_rows=args.partition == "rows")
     mine, n_max = shard_tiles(tiles, world, rank, parts)
     my_tiles = torch.from_numpy(mine).to(dev)
     P = n_max * stride
@@ -422,7 +425,13 @@ def run_ours(args):
     step_ms = np.array([a.elapsed_time(b) for a, b in ev])
     t_local = float(step_ms.sum()) / 1e3
     t = torch.tensor([t_local], dtype=torch.float64, device=dev)
+    # per-rank kernel time (march + shade + compose per step), for imbalance
+    kr = torch.tensor([float(kern.sum()) / args.steps], dtype=torch.float64, device=dev)
+    rank_kernel_ms = [float(kr.item())]
     if world > 1:
+        allk = [torch.zeros_like(kr) for _ in range(world)]
+        dist.all_gather(allk, kr)
+        rank_kernel_ms = [round(float(x.item()), 4) for x in allk]
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     t_max = float(t.item())
     cnt = out["counters"].cpu().numpy().astype(np.float64) / args.steps
@@ -432,6 +441,8 @@ def run_ours(args):
     # ---- end to end: camera in (H2D param block), encoded frame out to host memory
     e2e = None
     shm = host_map = None
+    if args.partition == "tiles" and args.e2e_mode == "hostmap":
+        args.e2e_mode = "copy"          # strided row DMA needs the row partition
     if not args.no_e2e and args.e2e_mode == "hostmap":
         # One shared page-locked host frame stack (double buffered) mapped by
         # every rank.  Each rank composes its tile rows into its own device
@@ -629,7 +640,7 @@ def run_ours(args):
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference-pipeline assets, "
             "random-init networks)", "config": workload_config(args, desc, W, H, len(scene)),
             "e2e": e2e, "gpu_launches": (3 + (1 if (world > 1 and not p2p) else 0)) * args.steps, "roofline": roof, "cpu_baseline": cpu,
-            "clocks": clk.summary(), "verify": verify,
+            "clocks": clk.summary(), "verify": verify, "rank_kernel_ms": rank_kernel_ms,
             "per_frame": {"march_samples": S, "hits": Hh, "pixels": npix},
             "step_ms": {"p50": float(np.percentile(step_ms, 50)), "p90": float(np.percentile(step_ms, 90)),
                         "max": float(step_ms.max()), "min": float(step_ms.min())},
