@@ -426,12 +426,13 @@ def run_ours(args):
     t_local = float(step_ms.sum()) / 1e3
     t = torch.tensor([t_local], dtype=torch.float64, device=dev)
     # per-rank kernel time (march + shade + compose per step), for imbalance
-    kr = torch.tensor([float(kern.sum()) / args.steps], dtype=torch.float64, device=dev)
-    rank_kernel_ms = [float(kr.item())]
+    csum = clk.summary()
+    kr = torch.tensor(list(kern / args.steps) + [csum["sm_mhz"] or 0.0], dtype=torch.float64, device=dev)
+    rank_kernel_ms = [[round(float(v), 4) for v in kr.tolist()]]
     if world > 1:
         allk = [torch.zeros_like(kr) for _ in range(world)]
         dist.all_gather(allk, kr)
-        rank_kernel_ms = [round(float(x.item()), 4) for x in allk]
+        rank_kernel_ms = [[round(float(v), 4) for v in x.tolist()] for x in allk]
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     t_max = float(t.item())
     cnt = out["counters"].cpu().numpy().astype(np.float64) / args.steps
@@ -640,7 +641,9 @@ def run_ours(args):
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference-pipeline assets, "
             "random-init networks)", "config": workload_config(args, desc, W, H, len(scene)),
             "e2e": e2e, "gpu_launches": (3 + (1 if (world > 1 and not p2p) else 0)) * args.steps, "roofline": roof, "cpu_baseline": cpu,
-            "clocks": clk.summary(), "verify": verify, "rank_kernel_ms": rank_kernel_ms,
+            "clocks": csum, "verify": verify,
+            "rank_kernel_ms": {"fields": ["k_march", "k_shade", "k_compose", "sm_mhz"],
+                               "ranks": rank_kernel_ms},
             "per_frame": {"march_samples": S, "hits": Hh, "pixels": npix},
             "step_ms": {"p50": float(np.percentile(step_ms, 50)), "p90": float(np.percentile(step_ms, 90)),
                         "max": float(step_ms.max()), "min": float(step_ms.min())},

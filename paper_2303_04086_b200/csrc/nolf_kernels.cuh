@@ -623,9 +623,7 @@ constexpr int kMaxLayers = 64;
 // farm.compose (farm.py:129-172) for one pixel; frames whose pixel is a miss
 // (rgba 0, depth inf) sort last and leave out_c and T unchanged, so
 // compositing only the hit layers is bitwise equal to compositing all K.
-__global__ void __launch_bounds__(256) k_compose(ComposeArgs a) {
-  const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= a.n_pix) return;
+__device__ __forceinline__ void compose_one(const ComposeArgs &a, const long long p) {
   long long q = p;             // output index
   if (a.tiles) {
     const TileParams tp = a.tiles[p / a.tile_stride];
@@ -643,7 +641,6 @@ __global__ void __launch_bounds__(256) k_compose(ComposeArgs a) {
     if (a.out_depth) a.out_depth[q] = __int_as_float(0x7f800000);
     if (a.out_rgba8) reinterpret_cast<uchar4 *>(a.out_rgba8)[q] = make_uchar4(0, 0, 0, 0);
     if (a.out_depth16) a.out_depth16[q] = 65535;
-    if (a.peer) __threadfence_system();
     return;
   }
   float dk[kMaxLayers];
@@ -697,7 +694,15 @@ __global__ void __launch_bounds__(256) k_compose(ComposeArgs a) {
     if (isfinite(od)) qd = (uint16_t)rintf(fminf(od, a.depth_far) / a.depth_far * 65534.0f);
     a.out_depth16[q] = qd;
   }
-  if (a.peer) __threadfence_system();   // peer stores visible before the completion collective
+}
+
+__global__ void __launch_bounds__(256) k_compose(ComposeArgs a) {
+  const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p < a.n_pix) compose_one(a, p);
+  if (a.peer) {                // outputs in another GPU's memory: the barrier
+    __syncthreads();           // orders the CTA's stores before one system-scope
+    if (threadIdx.x == 0) __threadfence_system();   // fence (cumulative), ahead of
+  }                            // the completion collective that follows
 }
 
 // Frame assembly after an all-rank gather: rank r's buffer holds n_per_rank
