@@ -278,8 +278,8 @@ def run_reference(args):
 
 
 def workload_config(args, desc, W, H, n_assets):
-    return {"workload": (f"{desc}, {args.tile}x{args.tile} ray tiles interleaved over ranks, "
-                         f"NCCL gather of rgba8+u16 to rank 0"),
+    return {"workload": (f"{desc}, {args.tile}x{args.tile} ray tiles (tile rows interleaved over "
+                         f"ranks), encode_frame rgba8+u16 assembled into one frame on rank 0"),
             "assets": n_assets, "width": W, "height": H,
             "atlas_b": 32, "atlas_r": 8, "psh_resolution": 64, "mlp": args.mlp,
             "parallelism": f"ray-tile x{args.gpus}", "partition": args.partition,
