@@ -399,7 +399,8 @@ size_t param_bytes(int n_inst, int n_cams) {   // cull tail is n_inst x n_cams
   return offsetof(ParamBlock, cull) + sizeof(ScreenBox) * (size_t)n_inst * (size_t)(n_cams > 0 ? n_cams : 1);
 }
 
-// Conservative image rectangle of an instance's proxy box for one camera.
+// Conservative image rectangle of an instance's culling box (occupied cells,
+// see nolf_asset_create) for one camera.
 // All 8 world corners strictly in front of the camera: the projection of the
 // (convex) box is the hull of the projected corners, so pixels outside their
 // bounding rectangle (plus a 2-pixel margin for rounding) cannot hit it.
@@ -416,11 +417,12 @@ ScreenBox screen_box(const NolfInstance &in, const DevAsset &H, const CamParams 
   const double Ai[9] = {(a11 * a22 - a12 * a21) * id, (a02 * a21 - a01 * a22) * id, (a01 * a12 - a02 * a11) * id,
                         (a12 * a20 - a10 * a22) * id, (a00 * a22 - a02 * a20) * id, (a02 * a10 - a00 * a12) * id,
                         (a10 * a21 - a11 * a20) * id, (a01 * a20 - a00 * a21) * id, (a00 * a11 - a01 * a10) * id};
+  if (H.cull_empty) return ScreenBox{1, 1, 0, 0};
   double xmin = 1e300, xmax = -1e300, ymin = 1e300, ymax = -1e300;
   int behind = 0, near = 0;
   for (int cnr = 0; cnr < 8; ++cnr) {
-    const double po[3] = {(cnr & 1) ? H.pmax[0] : H.pmin[0], (cnr & 2) ? H.pmax[1] : H.pmin[1],
-                          (cnr & 4) ? H.pmax[2] : H.pmin[2]};
+    const double po[3] = {(cnr & 1) ? H.cull_hi[0] : H.cull_lo[0], (cnr & 2) ? H.cull_hi[1] : H.cull_lo[1],
+                          (cnr & 4) ? H.cull_hi[2] : H.cull_lo[2]};
     const double q[3] = {po[0] - w[3], po[1] - w[7], po[2] - w[11]};
     double pw[3];
     for (int r = 0; r < 3; ++r) pw[r] = Ai[3 * r] * q[0] + Ai[3 * r + 1] * q[1] + Ai[3 * r + 2] * q[2];
@@ -640,6 +642,32 @@ int nolf_asset_create(const NolfAssetDesc *d, int device, nolf_asset_t *out) {
     H.pmax[k] = d->proxy_max[k];
   }
   if ((rc = upload_mesh(A, *d, &H.mesh))) return bail(rc);
+  {
+    // Rays that never enter an occupied cell sample only empty cells: sigma = 0
+    // everywhere, so the march returns "miss, 0 samples" exactly.  A pixel whose
+    // ray misses the occupied-cell AABB (grown by a full cell, far beyond any
+    // rounding of sample positions) can therefore skip the asset entirely.
+    const int b = d->density.b;
+    int lo[3] = {b, b, b}, hi[3] = {-1, -1, -1};
+    for (int x = 0; x < b; ++x)
+      for (int y = 0; y < b; ++y)
+        for (int z = 0; z < b; ++z)
+          if (d->density.index[((int64_t)x * b + y) * b + z] != -1) {
+            const int c[3] = {x, y, z};
+            for (int k = 0; k < 3; ++k) {
+              lo[k] = std::min(lo[k], c[k]);
+              hi[k] = std::max(hi[k], c[k]);
+            }
+          }
+    H.cull_empty = hi[0] < 0 ? 1 : 0;
+    for (int k = 0; k < 3; ++k) {
+      double l = (lo[k] - 1) / (double)b, h = (hi[k] + 2) / (double)b;
+      if (l <= 0.0) l = std::min(0.0, d->proxy_min[k]);   // clipped positions reach face cells
+      if (h >= 1.0) h = std::max(1.0, d->proxy_max[k]);
+      H.cull_lo[k] = std::max(l, d->proxy_min[k]);
+      H.cull_hi[k] = std::min(h, d->proxy_max[k]);
+    }
+  }
   H.use_hit_point = d->use_hit_point;
   H.use_opacity = d->use_opacity;
   H.refine_opacity = d->refine_opacity;

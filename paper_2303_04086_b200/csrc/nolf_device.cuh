@@ -75,6 +75,11 @@ struct DevAsset {              // LightFieldAsset (lightfield.py:217-248)
   const uint16_t *phi16;       // Phi narrowed to u16 (m <= 65536), else null
   uint32_t phi16_bytes;        // padded to 16 B for the TMA bulk copy
   DevMesh mesh;                // triangle-mesh proxy (nodes == null: slab only)
+  // host-side culling box: AABB of the occupied density cells grown by one
+  // cell (faces reaching the unit-cube boundary extended to the proxy, where
+  // clipped sample positions land), clipped to the proxy box
+  double cull_lo[3], cull_hi[3];
+  int cull_empty;              // no occupied cell: no ray can ever sample density
 };
 
 // One placed asset for a launch (NolfInstance minus the host handle).
