@@ -109,7 +109,8 @@ struct MarchOut {
 };
 
 __device__ __forceinline__ MarchOut march_ray(const DevAsset &A, const double o[3], const double d[3],
-                                              const double inv[3], double t_near, double t_far, bool use_zmask) {
+                                              const double inv[3], double t_near, double t_far, bool use_zmask,
+                                              long long i_start, double t_end) {
   MarchOut r;
   r.alpha_c = 0.0;
   r.t_hit = __longlong_as_double(0x7ff0000000000000ll);
@@ -123,12 +124,12 @@ __device__ __forceinline__ MarchOut march_ray(const DevAsset &A, const double o[
   const double inv_delta = 1.0 / delta;
   double best_w = 0.0, trans = 1.0, alpha_c = 0.0, t_hit = r.t_hit;
   int samples = 0;
-  long long i = 0;
+  long long i = i_start;       // samples before i_start and from t_end on are empty
   for (;;) {
     double pos[3];
     int cell[3];
     const double t_mid = sample_cell(o, d, t_near, delta, i, b, pos, cell);
-    if (!(t_mid < t_far)) break;
+    if (!(t_mid < t_far) || !(t_mid < t_end)) break;
     int lo_c[3], hi_c[3];
     bool empty = false;
     int cid = -1;
@@ -260,7 +261,7 @@ __global__ void __launch_bounds__(128, NOLF_MARCH_MINB) k_march(MarchArgs args) 
     const DevInst &I = args.inst[k];
     const DevAsset &A = *I.a;
     bool hit = false;
-    double o[3], d[3], inv[3], t_near = 0, t_far = 0;
+    double o[3], d[3], inv[3], inv_unused[3], t_near = 0, t_far = 0;
     MarchOut mr{0.0, __longlong_as_double(0x7ff0000000000000ll), 0, false};
     const bool live = (lane_mask >> k) & 1ull;
     if (live) {
@@ -276,8 +277,24 @@ __global__ void __launch_bounds__(128, NOLF_MARCH_MINB) k_march(MarchArgs args) 
         if (tm < 0.0) boxhit = false;
         else t_near = tm;
       }
+      // Clip the march to the ray's span in the culling box (occupied cells
+      // grown by one cell): every sample outside it lies in an empty cell, so
+      // starting 2 samples before the entry and stopping 2 after the exit
+      // leaves the result bit-identical (empty samples change nothing).
+      long long i_start = 0;
+      double t_end = t_far;
+      if (boxhit && t_near < t_far) {
+        double ca, cb;
+        if (!slab(A.cull_lo, A.cull_hi, o, d, ca, cb, inv_unused) || A.cull_empty) {
+          boxhit = false;                     // never meets an occupied cell: exact miss
+        } else {
+          const double f = floor((ca - t_near) / A.step - 2.5);
+          i_start = f > 0.0 ? (long long)f : 0;
+          t_end = cb + 2.0 * A.step;
+        }
+      }
       if (boxhit) {
-        mr = march_ray(A, o, d, inv, t_near, t_far, args.use_zmask);
+        mr = march_ray(A, o, d, inv, t_near, t_far, args.use_zmask, i_start, t_end);
         samples_total += (unsigned long long)mr.samples;
         hit = mr.hit;
       }
