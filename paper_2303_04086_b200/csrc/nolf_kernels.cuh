@@ -91,6 +91,21 @@ __device__ __forceinline__ double sample_cell(const double o[3], const double d[
   return t_mid;
 }
 
+// Pixel of packed slot `local` inside a w x h tile.  Tiles whose sides are
+// multiples of 8 x 4 are stored in 8x4 blocks of 32 slots (one warp marches a
+// compact 8x4 pixel patch -> coherent rays, less divergence); other tiles are
+// row-major.  render.py:unpack_index mirrors this.
+__device__ __forceinline__ void slot_xy(long long local, int w, int h, int &x, int &y) {
+  if ((w & 7) == 0 && (h & 3) == 0) {
+    const int blk = (int)(local >> 5), l = (int)(local & 31), bx = w >> 3;
+    x = (blk % bx) * 8 + (l & 7);
+    y = (blk / bx) * 4 + (l >> 3);
+  } else {
+    x = (int)(local % w);
+    y = (int)(local / w);
+  }
+}
+
 // march_rays (lightfield.py:129-186) for one ray.
 //
 // Exact empty-space skipping: an empty sample has sigma = 0, so absorb = 1,
@@ -222,8 +237,14 @@ __global__ void __launch_bounds__(128, NOLF_MARCH_MINB) k_march(MarchArgs args) 
         valid = false;
       } else {
         cam = tp.cam;
-        pix_x = tp.x0 + (int)(local % w);
-        pix_y = tp.y0 + (int)(local / w);
+        if (MODE == kModeScene) {
+          slot_xy(local, w, h, pix_x, pix_y);
+          pix_x += tp.x0;
+          pix_y += tp.y0;
+        } else {
+          pix_x = tp.x0 + (int)(local % w);
+          pix_y = tp.y0 + (int)(local / w);
+        }
       }
     }
     if (MODE != kModeScene && valid && args.rgba) {   // miss defaults (lightfield.py:415-416)
@@ -645,11 +666,13 @@ __device__ __forceinline__ void compose_one(const ComposeArgs &a, const long lon
   if (a.tiles) {
     const TileParams tp = a.tiles[p / a.tile_stride];
     const long long local = p % a.tile_stride;
-    const int w = tp.x1 - tp.x0;
-    if (local >= (long long)w * (tp.y1 - tp.y0)) return;
+    const int w = tp.x1 - tp.x0, h = tp.y1 - tp.y0;
+    if (local >= (long long)w * h) return;
     if (a.frame_layout) {
       const CamParams &cp = a.cams[tp.cam];
-      q = cp.pix_base + (long long)(tp.y0 + (int)(local / w)) * cp.width + (tp.x0 + (int)(local % w));
+      int x, y;
+      slot_xy(local, w, h, x, y);
+      q = cp.pix_base + (long long)(tp.y0 + y) * cp.width + (tp.x0 + x);
     }
   }
   const int n = a.nhit ? (int)a.nhit[p] : a.K;
@@ -733,13 +756,14 @@ __global__ void __launch_bounds__(256) k_unpack(const uint8_t *gathered, long lo
   const long long s = i / tile_stride, local = i % tile_stride;
   if (s >= n_slots) return;
   const TileParams tp = slot_tiles[s];
-  const int w = tp.x1 - tp.x0;
-  if (local >= (long long)w * (tp.y1 - tp.y0)) return;
+  const int w = tp.x1 - tp.x0, h = tp.y1 - tp.y0;
+  if (local >= (long long)w * h) return;
   const long long r = s / n_per_rank, j = s % n_per_rank;
   const uint8_t *base = gathered + r * rank_bytes;
   const long long src = j * tile_stride + local;
-  const long long dst = (long long)tp.cam * width * height + (long long)(tp.y0 + (int)(local / w)) * width +
-                        (tp.x0 + (int)(local % w));
+  int x, y;
+  slot_xy(local, w, h, x, y);
+  const long long dst = (long long)tp.cam * width * height + (long long)(tp.y0 + y) * width + (tp.x0 + x);
   rgba8[dst] = reinterpret_cast<const uchar4 *>(base)[src];
   depth16[dst] = reinterpret_cast<const uint16_t *>(base + (long long)n_per_rank * tile_stride * 4)[src];
 }

@@ -425,16 +425,32 @@ class SceneRenderer:
                                           ws.data_ptr(), ws.numel(), st))
 
 
+def slot_xy(local, w: int, h: int):
+    """(x, y) inside a w x h tile of packed slot ``local`` (nolf_kernels.cuh:slot_xy)."""
+    local = np.asarray(local, np.int64)
+    if w % 8 == 0 and h % 4 == 0:
+        blk, lane = local // 32, local % 32
+        return (blk % (w // 8)) * 8 + lane % 8, (blk // (w // 8)) * 4 + lane // 8
+    return local % w, local // w
+
+
 def unpack_index(tiles: np.ndarray, tile_stride: int, width: int, height: int, cam: int = 0):
-    """Packed-slot index of every pixel of camera ``cam`` (row-major H*W), -1 if absent."""
+    """Packed-slot index of every pixel of camera ``cam`` (row-major H*W), -1 if absent.
+
+    Inside a tile whose sides are multiples of 8 x 4 the slots run over 8x4
+    pixel blocks (block-row-major, row-major inside a block: one warp per
+    block); other tiles are row-major (nolf_kernels.cuh:slot_xy)."""
     idx = np.full(height * width, -1, dtype=np.int64)
     for t, (c, x0, y0, x1, y1) in enumerate(tiles):
         if c != cam:
             continue
-        w = x1 - x0
-        ys, xs = np.mgrid[y0:y1, x0:x1]
-        idx[(ys * width + xs).reshape(-1)] = t * tile_stride + (
-            (ys - y0) * w + (xs - x0)).reshape(-1)
+        w, h = x1 - x0, y1 - y0
+        ys, xs = np.mgrid[0:h, 0:w]
+        if w % 8 == 0 and h % 4 == 0:
+            local = ((ys // 4) * (w // 8) + xs // 8) * 32 + (ys % 4) * 8 + xs % 8
+        else:
+            local = ys * w + xs
+        idx[((ys + y0) * width + xs + x0).reshape(-1)] = t * tile_stride + local.reshape(-1)
     return idx
 
 

@@ -13,7 +13,7 @@ import torch.multiprocessing as mp
 
 from paper_2303_04086_b200.dist import (gather_to_root, partition, rank_buffer_bytes, row_bands,
                                         shard_tiles, slot_tile_table)
-from paper_2303_04086_b200.render import frame_tiles
+from paper_2303_04086_b200.render import frame_tiles, slot_xy
 
 W, H, T = 70, 45, 16
 STRIDE = T * T
@@ -36,9 +36,10 @@ def worker(rank, world, port, q, by_rows):
         rgba = buf[:P * 4].reshape(P, 4)
         depth = buf[P * 4:].view(np.uint16)
         for j, (c, x0, y0, x1, y1) in enumerate(mine):   # "render": encode pixel coordinates
-            w = x1 - x0
-            for l in range((x1 - x0) * (y1 - y0)):
-                x, y = x0 + l % w, y0 + l // w
+            w, h = x1 - x0, y1 - y0
+            for l in range(w * h):
+                lx, ly = slot_xy(l, w, h)
+                x, y = x0 + lx, y0 + ly
                 rgba[j * STRIDE + l] = [pixel_code(np.int64(x), np.int64(y)), rank + 1, 0, 255]
                 depth[j * STRIDE + l] = y * W + x
         t = torch.from_numpy(buf)
@@ -53,9 +54,10 @@ def worker(rank, world, port, q, by_rows):
             for s, (c, x0, y0, x1, y1) in enumerate(table):   # what k_unpack does
                 r, j = divmod(s, n_max)
                 base = g[r * per:(r + 1) * per]
-                w = x1 - x0
-                for l in range(w * (y1 - y0)):
-                    dst = (y0 + l // w) * W + x0 + l % w
+                w, h = x1 - x0, y1 - y0
+                for l in range(w * h):
+                    lx, ly = slot_xy(l, w, h)
+                    dst = (y0 + ly) * W + x0 + lx
                     frame[dst] = base[(j * STRIDE + l) * 4:(j * STRIDE + l) * 4 + 4]
                     fdepth[dst] = base[P * 4:].view(np.uint16)[j * STRIDE + l]
             q.put((frame, fdepth))
