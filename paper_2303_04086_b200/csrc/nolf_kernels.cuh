@@ -12,6 +12,8 @@
 //              over in f64 + encode_frame RAW quantisation (farm.py:129-172,
 //              protocol.py:256-266).
 #pragma once
+#include <climits>
+
 #include "nolf_device.cuh"
 
 namespace nolf {
@@ -229,8 +231,17 @@ __global__ void __launch_bounds__(128, NOLF_MARCH_MINB) k_march(MarchArgs args) 
       ow[0] = op[0]; ow[1] = op[1]; ow[2] = op[2];
       dw[0] = args.dirs[3 * gid]; dw[1] = args.dirs[3 * gid + 1]; dw[2] = args.dirs[3 * gid + 2];
     } else {
-      long long t = MODE == kModeRect ? 0 : gid / args.tile_stride;
-      long long local = MODE == kModeRect ? gid : gid % args.tile_stride;
+      long long t = 0, local = gid;
+      if (MODE != kModeRect) {
+        if (gid < 0xffffffffll && args.tile_stride < 0xffffffffll) {   // 32-bit divide
+          const unsigned g32 = (unsigned)gid, s32 = (unsigned)args.tile_stride;
+          t = g32 / s32;
+          local = g32 - (unsigned)t * s32;
+        } else {
+          t = gid / args.tile_stride;
+          local = gid % args.tile_stride;
+        }
+      }
       const TileParams tp = args.tiles[t];
       const int w = tp.x1 - tp.x0, h = tp.y1 - tp.y0;
       if (local >= (long long)w * h) {
@@ -252,16 +263,39 @@ __global__ void __launch_bounds__(128, NOLF_MARCH_MINB) k_march(MarchArgs args) 
       args.depth[gid] = __int_as_float(0x7f800000);
     }
   }
-  unsigned long long samples_total = 0;
+  unsigned samples_total = 0;  // per lane (< 2^32: at most n_inst * samples per ray)
   unsigned ordinal = 0;
   // Instances whose conservative screen box covers this lane's pixel, then
   // OR-ed over the warp so the instance loop below is warp-uniform and only
   // visits candidates (ascending = scene order, so layer ordinals match).
   unsigned long long lane_mask = 0;
-  if (valid) {
-    if (MODE == kModeRays || !args.cull) {
-      lane_mask = args.n_inst >= 64 ? ~0ull : ((1ull << args.n_inst) - 1ull);
-    } else {
+  if (MODE == kModeRays || !args.cull) {
+    if (valid) lane_mask = args.n_inst >= 64 ? ~0ull : ((1ull << args.n_inst) - 1ull);
+  } else {
+    const int cmin = __reduce_min_sync(0xffffffffu, valid ? cam : INT_MAX);
+    const int cmax = __reduce_max_sync(0xffffffffu, valid ? cam : -1);
+    if (cmin == cmax) {
+      // one camera for the whole warp: lane k tests instance k's box against
+      // the warp's pixel rectangle, then only the candidates are tested per pixel
+      const int xmin = __reduce_min_sync(0xffffffffu, valid ? pix_x : INT_MAX);
+      const int xmax = __reduce_max_sync(0xffffffffu, valid ? pix_x : INT_MIN);
+      const int ymin = __reduce_min_sync(0xffffffffu, valid ? pix_y : INT_MAX);
+      const int ymax = __reduce_max_sync(0xffffffffu, valid ? pix_y : INT_MIN);
+      for (int base = 0; base < args.n_inst; base += 32) {
+        const int k = base + (int)lane;
+        ScreenBox bb{1, 1, 0, 0};
+        if (k < args.n_inst) bb = args.cull[k * args.n_cams + cmin];
+        unsigned cand = __ballot_sync(0xffffffffu, bb.x0 <= xmax && bb.x1 >= xmin && bb.y0 <= ymax && bb.y1 >= ymin &&
+                                                       bb.x0 <= bb.x1);
+        while (cand) {
+          const int j = __ffs(cand) - 1;
+          cand &= cand - 1;
+          const int x0 = __shfl_sync(0xffffffffu, bb.x0, j), x1 = __shfl_sync(0xffffffffu, bb.x1, j);
+          const int y0 = __shfl_sync(0xffffffffu, bb.y0, j), y1 = __shfl_sync(0xffffffffu, bb.y1, j);
+          if (valid && pix_x >= x0 && pix_x <= x1 && pix_y >= y0 && pix_y <= y1) lane_mask |= 1ull << (base + j);
+        }
+      }
+    } else if (valid) {
       for (int k = 0; k < args.n_inst; ++k) {
         const ScreenBox bb = args.cull[k * args.n_cams + cam];
         if (pix_x >= bb.x0 && pix_x <= bb.x1 && pix_y >= bb.y0 && pix_y <= bb.y1) lane_mask |= 1ull << k;
@@ -316,7 +350,7 @@ __global__ void __launch_bounds__(128, NOLF_MARCH_MINB) k_march(MarchArgs args) 
       }
       if (boxhit) {
         mr = march_ray(A, o, d, inv, t_near, t_far, args.use_zmask, i_start, t_end);
-        samples_total += (unsigned long long)mr.samples;
+        samples_total += (unsigned)mr.samples;
         hit = mr.hit;
       }
     }
@@ -364,9 +398,8 @@ __global__ void __launch_bounds__(128, NOLF_MARCH_MINB) k_march(MarchArgs args) 
   }
   if (MODE == kModeScene && valid) args.nhit[gid] = (uint8_t)ordinal;
   // march_samples counter (lightfield.py:430-431)
-#pragma unroll
-  for (int off = 16; off; off >>= 1) samples_total += __shfl_xor_sync(0xffffffffu, samples_total, off);
-  if (lane == 0 && samples_total && args.counters) atomicAdd(args.counters + 3, samples_total);
+  const unsigned warp_samples = __reduce_add_sync(0xffffffffu, samples_total);
+  if (lane == 0 && warp_samples && args.counters) atomicAdd(args.counters + 3, (unsigned long long)warp_samples);
 }
 
 // ---------------------------------------------------------------- shading
