@@ -436,6 +436,11 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     t_max = float(t.item())
     cnt = out["counters"].cpu().numpy().astype(np.float64) / args.steps
+    if os.environ.get("NOLF_STATS_DUMP") and hasattr(N.lib(), "nolf_stats_read"):
+        import ctypes                # diagnostic build (-DNOLF_STATS): march work counters
+        st = (ctypes.c_ulonglong * 16)()
+        N.lib().nolf_stats_read(st, 0)
+        print("STATS per frame", [round(v / (args.steps + args.warmup), 1) for v in st], file=sys.stderr)
     npix = NPX
     value = args.steps * npix / t_max / 1e6
 

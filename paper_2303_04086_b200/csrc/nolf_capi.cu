@@ -1178,3 +1178,14 @@ int nolf_compose(int32_t K, int64_t P, const float *rgba, const float *depth, do
 }
 
 }  // extern "C"
+
+#ifdef NOLF_STATS
+extern "C" int nolf_stats_read(unsigned long long *out, int reset) {
+  cudaMemcpyFromSymbol(out, nolf::g_stats, sizeof(unsigned long long) * 16);
+  if (reset) {
+    static const unsigned long long z[16] = {};
+    cudaMemcpyToSymbol(nolf::g_stats, z, sizeof(z));
+  }
+  return (int)cudaGetLastError();
+}
+#endif

@@ -93,6 +93,13 @@ __device__ __forceinline__ double sample_cell(const double o[3], const double d[
   return t_mid;
 }
 
+#ifdef NOLF_STATS   // diagnostic build only: march work counters
+__device__ unsigned long long g_stats[16];
+#define NOLF_STAT(k, v) atomicAdd(&g_stats[k], (unsigned long long)(v))
+#else
+#define NOLF_STAT(k, v) ((void)0)
+#endif
+
 // Pixel of packed slot `local` inside a w x h tile.  Tiles whose sides are
 // multiples of 8 x 4 are stored in 8x4 blocks of 32 slots (one warp marches a
 // compact 8x4 pixel patch -> coherent rays, less divergence); other tiles are
@@ -147,6 +154,7 @@ __device__ __forceinline__ MarchOut march_ray(const DevAsset &A, const double o[
     int cell[3];
     const double t_mid = sample_cell(o, d, t_near, delta, i, b, pos, cell);
     if (!(t_mid < t_far) || !(t_mid < t_end)) break;
+    NOLF_STAT(7, 1);
     int lo_c[3], hi_c[3];
     bool empty = false;
     int cid = -1;
@@ -163,6 +171,7 @@ __device__ __forceinline__ MarchOut march_ray(const DevAsset &A, const double o[
       cid = __ldg(at.index + ci);
     }
     if (empty) {
+      NOLF_STAT(3, 1);
       double lo[3], hi[3];
 #pragma unroll
       for (int k = 0; k < 3; ++k) {
@@ -194,10 +203,12 @@ __device__ __forceinline__ MarchOut march_ray(const DevAsset &A, const double o[
     const int bit = (base[0] * at.r + base[1]) * at.r + base[2];
     ++samples;
     if (use_zmask && ((__ldg(at.zmask + (size_t)cid * at.zwords + (bit >> 5)) >> (bit & 31)) & 1u)) {
+      NOLF_STAT(5, 1);
       ++i;
       continue;
     }
     float s;
+    NOLF_STAT(6, 1);
     atlas_trilinear_at<1>(at, cid, base, frac, &s);
     const double sigma = (double)s;
     const double absorb = exp(__dmul_rn(-sigma, delta));
@@ -319,7 +330,9 @@ __global__ void __launch_bounds__(128, NOLF_MARCH_MINB) k_march(MarchArgs args) 
     double o[3], d[3], inv[3], inv_unused[3], t_near = 0, t_far = 0;
     MarchOut mr{0.0, __longlong_as_double(0x7ff0000000000000ll), 0, false};
     const bool live = (lane_mask >> k) & 1ull;
+    if (lane == 0) NOLF_STAT(8, 1);
     if (live) {
+      NOLF_STAT(0, 1);
       if (args.raw_rays) {
 #pragma unroll
         for (int q = 0; q < 3; ++q) { o[q] = ow[q]; d[q] = dw[q]; }
@@ -338,6 +351,7 @@ __global__ void __launch_bounds__(128, NOLF_MARCH_MINB) k_march(MarchArgs args) 
       // leaves the result bit-identical (empty samples change nothing).
       long long i_start = 0;
       double t_end = t_far;
+      if (boxhit) NOLF_STAT(1, 1);
       if (boxhit && t_near < t_far) {
         double ca, cb;
         if (!slab(A.cull_lo, A.cull_hi, o, d, ca, cb, inv_unused) || A.cull_empty) {
@@ -349,6 +363,7 @@ __global__ void __launch_bounds__(128, NOLF_MARCH_MINB) k_march(MarchArgs args) 
         }
       }
       if (boxhit) {
+        NOLF_STAT(2, 1);
         mr = march_ray(A, o, d, inv, t_near, t_far, args.use_zmask, i_start, t_end);
         samples_total += (unsigned)mr.samples;
         hit = mr.hit;
