@@ -250,3 +250,17 @@ def camera_dirs(cam, px, py):
     lib().oracle_camera_dirs(_p(pose), cam.fx, cam.fy, cam.cx, cam.cy, _p(px), _p(py), len(px),
                              _p(out))
     return out
+
+
+def encode_frame(rgba, depth, depth_far=10.0):
+    """protocol.encode_frame RAW (protocol.py:256-266) restated in numpy:
+    rgba8 = clip(round(rgba*255)) in float32 (half-to-even), depth16 =
+    round(min(d, far)/far*65534) for finite d, else 65535."""
+    rgba = np.asarray(rgba, np.float32)
+    depth = np.asarray(depth, np.float32)
+    r8 = np.clip(np.round(rgba * np.float32(255.0)), 0, 255).astype(np.uint8)
+    q = np.full(depth.shape, 65535, np.uint16)
+    fin = np.isfinite(depth)
+    far = np.float32(depth_far)
+    q[fin] = np.round(np.minimum(depth[fin], far) / far * np.float32(65534.0)).astype(np.uint16)
+    return r8, q

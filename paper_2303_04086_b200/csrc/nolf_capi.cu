@@ -910,7 +910,10 @@ int launch_march_shade(int mode, const NolfInstance *ins, int n_inst, const Nolf
     ca.out_rgba8 = sout->rgba8;
     ca.out_depth16 = sout->depth16;
     ca.depth_far = (float)sout->depth_far;
-    k_compose<<<(unsigned)((n_rays + 255) / 256), 256, 0, st>>>(ca);
+    ca.four = (tile_stride % 4 == 0 && n_rays % 4 == 0 && ((uintptr_t)w.nhit & 3) == 0 &&
+               ((uintptr_t)sout->rgba8 & 15) == 0 && ((uintptr_t)sout->depth16 & 7) == 0) ? 1 : 0;
+    const long long n_thr = ca.four ? n_rays / 4 : n_rays;
+    k_compose<<<(unsigned)((n_thr + 255) / 256), 256, 0, st>>>(ca);
     CUDA_TRY(cudaGetLastError());
     if ((rc = prof_mark(3, st))) return rc;
   } else {

@@ -105,13 +105,36 @@ __device__ unsigned long long g_stats[16];
 // compact 8x4 pixel patch -> coherent rays, less divergence); other tiles are
 // row-major.  render.py:unpack_index mirrors this.
 __device__ __forceinline__ void slot_xy(long long local, int w, int h, int &x, int &y) {
+  const unsigned lo = (unsigned)local;         // local < w*h < 2^31
   if ((w & 7) == 0 && (h & 3) == 0) {
-    const int blk = (int)(local >> 5), l = (int)(local & 31), bx = w >> 3;
-    x = (blk % bx) * 8 + (l & 7);
-    y = (blk / bx) * 4 + (l >> 3);
+    const unsigned blk = lo >> 5, l = lo & 31u, bx = (unsigned)w >> 3;
+    unsigned by, bxi;
+    if ((bx & (bx - 1u)) == 0u) {               // power-of-two blocks per row (32-wide tiles)
+      const int sh = __ffs(bx) - 1;
+      by = blk >> sh;
+      bxi = blk & (bx - 1u);
+    } else {
+      by = blk / bx;
+      bxi = blk - by * bx;
+    }
+    x = (int)(bxi * 8u + (l & 7u));
+    y = (int)(by * 4u + (l >> 3));
   } else {
-    x = (int)(local % w);
-    y = (int)(local / w);
+    const unsigned uy = lo / (unsigned)w;
+    x = (int)(lo - uy * (unsigned)w);
+    y = (int)uy;
+  }
+}
+
+// (tile, local slot) of packed index p; 32-bit divide when it fits.
+__device__ __forceinline__ void split_slot(long long p, long long stride, long long &t, long long &local) {
+  if (p < 0xffffffffll && stride < 0xffffffffll) {
+    const unsigned p32 = (unsigned)p, s32 = (unsigned)stride, t32 = p32 / s32;
+    t = t32;
+    local = p32 - t32 * s32;
+  } else {
+    t = p / stride;
+    local = p % stride;
   }
 }
 
@@ -243,16 +266,7 @@ __global__ void __launch_bounds__(128, NOLF_MARCH_MINB) k_march(MarchArgs args) 
       dw[0] = args.dirs[3 * gid]; dw[1] = args.dirs[3 * gid + 1]; dw[2] = args.dirs[3 * gid + 2];
     } else {
       long long t = 0, local = gid;
-      if (MODE != kModeRect) {
-        if (gid < 0xffffffffll && args.tile_stride < 0xffffffffll) {   // 32-bit divide
-          const unsigned g32 = (unsigned)gid, s32 = (unsigned)args.tile_stride;
-          t = g32 / s32;
-          local = g32 - (unsigned)t * s32;
-        } else {
-          t = gid / args.tile_stride;
-          local = gid % args.tile_stride;
-        }
-      }
+      if (MODE != kModeRect) split_slot(gid, args.tile_stride, t, local);
       const TileParams tp = args.tiles[t];
       const int w = tp.x1 - tp.x0, h = tp.y1 - tp.y0;
       if (local >= (long long)w * h) {
@@ -702,35 +716,20 @@ struct ComposeArgs {
   uint8_t *out_rgba8;
   uint16_t *out_depth16;
   float depth_far;
+  int four;                    // 4 slots per thread (tiles && nhit && tile_stride % 4 == 0)
 };
 
 constexpr int kMaxLayers = 64;
 
-// farm.compose (farm.py:129-172) for one pixel; frames whose pixel is a miss
-// (rgba 0, depth inf) sort last and leave out_c and T unchanged, so
-// compositing only the hit layers is bitwise equal to compositing all K.
-__device__ __forceinline__ void compose_one(const ComposeArgs &a, const long long p) {
-  long long q = p;             // output index
-  if (a.tiles) {
-    const TileParams tp = a.tiles[p / a.tile_stride];
-    const long long local = p % a.tile_stride;
-    const int w = tp.x1 - tp.x0, h = tp.y1 - tp.y0;
-    if (local >= (long long)w * h) return;
-    if (a.frame_layout) {
-      const CamParams &cp = a.cams[tp.cam];
-      int x, y;
-      slot_xy(local, w, h, x, y);
-      q = cp.pix_base + (long long)(tp.y0 + y) * cp.width + (tp.x0 + x);
-    }
-  }
-  const int n = a.nhit ? (int)a.nhit[p] : a.K;
-  if (n == 0) {                // nothing composited: alpha 0 -> miss sentinel (farm.py:169-171)
-    if (a.out_rgba) reinterpret_cast<float4 *>(a.out_rgba)[q] = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (a.out_depth) a.out_depth[q] = __int_as_float(0x7f800000);
-    if (a.out_rgba8) reinterpret_cast<uchar4 *>(a.out_rgba8)[q] = make_uchar4(0, 0, 0, 0);
-    if (a.out_depth16) a.out_depth16[q] = 65535;
-    return;
-  }
+// farm.compose (farm.py:129-172) of slot p's n hit layers; frames whose
+// pixel is a miss (rgba 0, depth inf) sort last and leave out_c and T
+// unchanged, so compositing only the hit layers is bitwise equal to
+// compositing all K.  n == 0 -> the miss sentinel (farm.py:169-171).
+__device__ __forceinline__ void compose_px(const ComposeArgs &a, const long long p, const int n, float4 &o,
+                                           float &od) {
+  o = make_float4(0.f, 0.f, 0.f, 0.f);
+  od = __int_as_float(0x7f800000);
+  if (n == 0) return;
   float dk[kMaxLayers];
   unsigned char ord[kMaxLayers];
   // stable insertion sort by depth (np.argsort kind="stable")
@@ -742,7 +741,6 @@ __device__ __forceinline__ void compose_one(const ComposeArgs &a, const long lon
     ord[j] = (unsigned char)k;
   }
   double oc0 = 0.0, oc1 = 0.0, oc2 = 0.0, trans = 1.0;
-  float od = __int_as_float(0x7f800000);
   bool set = false;
   for (int r = 0; r < n; ++r) {
     const int k = ord[r];
@@ -753,7 +751,6 @@ __device__ __forceinline__ void compose_one(const ComposeArgs &a, const long lon
     if (!set && c.w > a.alpha_vis) { od = dk[r]; set = true; }
     trans = __dmul_rn(trans, (double)(1.0f - c.w));
   }
-  float4 o;
   o.x = (float)clampd(oc0, 0.0, 1.0);
   o.y = (float)clampd(oc1, 0.0, 1.0);
   o.z = (float)clampd(oc2, 0.0, 1.0);
@@ -762,31 +759,110 @@ __device__ __forceinline__ void compose_one(const ComposeArgs &a, const long lon
     o = make_float4(0.f, 0.f, 0.f, 0.f);
     od = __int_as_float(0x7f800000);
   }
+}
+
+// encode_frame (protocol.py:256-266): clip(round(x*255)) and the u16 depth
+__device__ __forceinline__ uchar4 encode_rgba8(const float4 o) {
+  const float qv[4] = {o.x, o.y, o.z, o.w};
+  unsigned char uu[4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    float v = rintf(qv[c] * 255.0f);
+    v = v < 0.f ? 0.f : (v > 255.f ? 255.f : v);
+    uu[c] = (unsigned char)v;
+  }
+  return make_uchar4(uu[0], uu[1], uu[2], uu[3]);
+}
+__device__ __forceinline__ uint16_t encode_depth16(const float od, const float far) {
+  return isfinite(od) ? (uint16_t)rintf(fminf(od, far) / far * 65534.0f) : (uint16_t)65535;
+}
+
+// Output index of slot p (-1 for tile padding).
+__device__ __forceinline__ long long compose_dst(const ComposeArgs &a, const TileParams &tp, long long local,
+                                                 long long p) {
+  const int w = tp.x1 - tp.x0, h = tp.y1 - tp.y0;
+  if (local >= (long long)w * h) return -1;
+  if (!a.frame_layout) return p;
+  const CamParams &cp = a.cams[tp.cam];
+  int x, y;
+  slot_xy(local, w, h, x, y);
+  return cp.pix_base + (long long)(tp.y0 + y) * cp.width + (tp.x0 + x);
+}
+
+__device__ __forceinline__ void compose_store(const ComposeArgs &a, long long q, const float4 o, const float od) {
   if (a.out_rgba) reinterpret_cast<float4 *>(a.out_rgba)[q] = o;
   if (a.out_depth) a.out_depth[q] = od;
-  if (a.out_rgba8) {           // encode_frame (protocol.py:256-266): clip(round(x*255))
-    const float qv[4] = {o.x, o.y, o.z, o.w};
-    uchar4 u;
-    unsigned char uu[4];
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      float v = rintf(qv[c] * 255.0f);
-      v = v < 0.f ? 0.f : (v > 255.f ? 255.f : v);
-      uu[c] = (unsigned char)v;
-    }
-    u.x = uu[0]; u.y = uu[1]; u.z = uu[2]; u.w = uu[3];
-    reinterpret_cast<uchar4 *>(a.out_rgba8)[q] = u;
+  if (a.out_rgba8) reinterpret_cast<uchar4 *>(a.out_rgba8)[q] = encode_rgba8(o);
+  if (a.out_depth16) a.out_depth16[q] = encode_depth16(od, a.depth_far);
+}
+
+__device__ __forceinline__ void compose_one(const ComposeArgs &a, const long long p) {
+  long long q = p;             // output index
+  if (a.tiles) {
+    long long t, local;
+    split_slot(p, a.tile_stride, t, local);
+    q = compose_dst(a, a.tiles[t], local, p);
+    if (q < 0) return;
   }
-  if (a.out_depth16) {
-    uint16_t qd = 65535;
-    if (isfinite(od)) qd = (uint16_t)rintf(fminf(od, a.depth_far) / a.depth_far * 65534.0f);
-    a.out_depth16[q] = qd;
+  float4 o;
+  float od;
+  compose_px(a, p, a.nhit ? (int)a.nhit[p] : a.K, o, od);
+  compose_store(a, q, o, od);
+}
+
+// Four consecutive slots of one tile per thread (scene mode, tile_stride % 4
+// == 0): one tile/camera lookup and one 4-byte layer-count load per thread,
+// and 16 B rgba8 / 8 B depth16 stores when the 4 pixels are one aligned run
+// (8x4-block layout: slots 4k..4k+3 are 4 adjacent pixels of one row).
+__device__ __forceinline__ void compose_four(const ComposeArgs &a, const long long p0) {
+  long long t, local0;
+  split_slot(p0, a.tile_stride, t, local0);
+  const TileParams tp = a.tiles[t];
+  const uchar4 nh = *reinterpret_cast<const uchar4 *>(a.nhit + p0);
+  const int ns[4] = {nh.x, nh.y, nh.z, nh.w};
+  long long q[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) q[j] = compose_dst(a, tp, local0 + j, p0 + j);
+  const bool run = q[0] >= 0 && (q[0] & 3) == 0 && q[1] == q[0] + 1 && q[2] == q[0] + 2 && q[3] == q[0] + 3 &&
+                   !a.out_rgba && !a.out_depth;
+  if (run && (ns[0] | ns[1] | ns[2] | ns[3]) == 0) {     // common case: four misses
+    if (a.out_rgba8) reinterpret_cast<uint4 *>(a.out_rgba8)[q[0] >> 2] = make_uint4(0u, 0u, 0u, 0u);
+    if (a.out_depth16) reinterpret_cast<uint2 *>(a.out_depth16)[q[0] >> 2] = make_uint2(0xffffffffu, 0xffffffffu);
+    return;
+  }
+  if (run) {
+    unsigned c8[4], d16[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      float4 o;
+      float od;
+      compose_px(a, p0 + j, ns[j], o, od);
+      const uchar4 u = encode_rgba8(o);
+      c8[j] = (unsigned)u.x | ((unsigned)u.y << 8) | ((unsigned)u.z << 16) | ((unsigned)u.w << 24);
+      d16[j] = encode_depth16(od, a.depth_far);
+    }
+    if (a.out_rgba8) reinterpret_cast<uint4 *>(a.out_rgba8)[q[0] >> 2] = make_uint4(c8[0], c8[1], c8[2], c8[3]);
+    if (a.out_depth16)
+      reinterpret_cast<uint2 *>(a.out_depth16)[q[0] >> 2] = make_uint2(d16[0] | (d16[1] << 16), d16[2] | (d16[3] << 16));
+    return;
+  }
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    if (q[j] < 0) continue;
+    float4 o;
+    float od;
+    compose_px(a, p0 + j, ns[j], o, od);
+    compose_store(a, q[j], o, od);
   }
 }
 
 __global__ void __launch_bounds__(256) k_compose(ComposeArgs a) {
-  const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (p < a.n_pix) compose_one(a, p);
+  const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (a.four) {
+    if (4 * gid < a.n_pix) compose_four(a, 4 * gid);
+  } else if (gid < a.n_pix) {
+    compose_one(a, gid);
+  }
   if (a.peer) {                // outputs in another GPU's memory: the barrier
     __syncthreads();           // orders the CTA's stores before one system-scope
     if (threadIdx.x == 0) __threadfence_system();   // fence (cumulative), ahead of
@@ -801,7 +877,8 @@ __global__ void __launch_bounds__(256) k_unpack(const uint8_t *gathered, long lo
                                                 long long n_slots, int width, int height, uchar4 *rgba8,
                                                 uint16_t *depth16) {
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  const long long s = i / tile_stride, local = i % tile_stride;
+  long long s, local;
+  split_slot(i, tile_stride, s, local);
   if (s >= n_slots) return;
   const TileParams tp = slot_tiles[s];
   const int w = tp.x1 - tp.x0, h = tp.y1 - tp.y0;

@@ -156,3 +156,29 @@ def test_live_diffuse_eval_vs_reference():
     N.check(N.lib().nolf_eval_diffuse(dev.handle, p.data_ptr(), len(p), out.data_ptr(),
                                       R._stream_ptr()))
     np.testing.assert_allclose(out.cpu().numpy(), g["diffuse"], rtol=0, atol=2e-6)
+
+
+@pytest.mark.parametrize("tile", [32, 17, 8])
+def test_fused_scene_encoded_frame(tile):
+    """rgba8 + u16 depth written by the compose epilogue (encode_frame RAW,
+    protocol.py:256-266): bit-equal to the oracle's encoder applied to the
+    fused f32 frame, and within one rgba8 step / bit-equal depth vs the
+    reference-encoded golden (tile 32 and 8 take the 4-slot vector path,
+    tile 17 the per-slot path)."""
+    import torch
+    g, scene = _scene()
+    enc = load("encode.npz")
+    cam = camera(g)
+    f32 = R.render_scene(scene, cam, tile=tile)
+    r = R.SceneRenderer(scene)
+    tiles = R.frame_tiles(cam.width, cam.height, tile)
+    out = r.alloc(len(tiles), tile * tile, want_f32=False, want_u8=True)
+    r.render([cam], torch.from_numpy(tiles).to(r.device), len(tiles), tile * tile, out, frame_layout=True)
+    npx = cam.width * cam.height
+    rgba8 = out["rgba8"][:npx].cpu().numpy().reshape(cam.height, cam.width, 4)
+    depth16 = out["depth16"][:npx].cpu().numpy().view(np.uint16).reshape(cam.height, cam.width)
+    e8, e16 = O.encode_frame(f32.rgba, f32.depth)
+    np.testing.assert_array_equal(rgba8, e8)
+    np.testing.assert_array_equal(depth16, e16)
+    np.testing.assert_array_equal(depth16, enc["scene_depth16"])
+    assert np.abs(rgba8.astype(int) - enc["scene_rgba8"].astype(int)).max() <= 1

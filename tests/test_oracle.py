@@ -102,3 +102,16 @@ def test_scene_frames_match_reference():
         fin = np.isfinite(g["frame_depth"][k])
         assert np.array_equal(np.isfinite(depth), fin)
         np.testing.assert_array_equal(depth[fin], g["frame_depth"][k][fin])
+
+
+def test_encode_frame_restatement_matches_reference():
+    """protocol.encode_frame RAW (protocol.py:256-266) goldens, incl. .5 ties,
+    clipping, the depth_far clamp and inf depths."""
+    g = load("encode.npz")
+    r8, d16 = O.encode_frame(g["syn_rgba"], g["syn_depth"])
+    np.testing.assert_array_equal(r8, g["syn_rgba8"])
+    np.testing.assert_array_equal(d16, g["syn_depth16"])
+    s = load("scene.npz")
+    r8, d16 = O.encode_frame(s["rgba"], s["depth"])
+    np.testing.assert_array_equal(r8, g["scene_rgba8"])
+    np.testing.assert_array_equal(d16, g["scene_depth16"])
