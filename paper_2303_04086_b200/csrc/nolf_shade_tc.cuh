@@ -29,7 +29,10 @@ constexpr uint32_t kTcW0 = 64 * kTcK0 * 2;   // 4 KB
 constexpr uint32_t kTcW1 = 64 * 64 * 2;      // 8 KB
 constexpr uint32_t kTcWBytes = kTcW0 + kTcW1;
 constexpr int kTcF32 = 64 + 64 + 4 * 64 + 4; // b0, b1, W2, b2
-constexpr uint32_t kTcPhiMax = 64 * 1024;    // Phi bytes staged in smem
+#ifndef NOLF_TC_PHIMAX
+#define NOLF_TC_PHIMAX (64 * 1024)
+#endif
+constexpr uint32_t kTcPhiMax = NOLF_TC_PHIMAX;   // Phi bytes staged in smem
 constexpr uint32_t kTcTabMax = 776;          // residue tables 6*(N+1) for N <= 128 (16-B multiple)
 constexpr uint32_t kTcSmem = 1024 + kTcA + kTcWBytes + kTcF32 * 4 + kTcTabMax * 4 + 64 + kTcPhiMax;
 
@@ -63,9 +66,11 @@ __device__ __forceinline__ void tc_mlp_rows(uint8_t *A, const uint8_t *W, const 
 #pragma unroll
   for (int c = 0; c < 8; ++c) {
     float v[8];
+    const float4 bA = reinterpret_cast<const float4 *>(fp)[2 * c], bB = reinterpret_cast<const float4 *>(fp)[2 * c + 1];
+    const float bb[8] = {bA.x, bA.y, bA.z, bA.w, bB.x, bB.y, bB.z, bB.w};
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
-      const float z = h[8 * c + e] + fp[8 * c + e];
+      const float z = h[8 * c + e] + bb[e];
       v[e] = z > 0.f ? z : 0.f;
     }
     uint4 q;
@@ -93,15 +98,26 @@ __device__ __forceinline__ void tc_mlp_rows(uint8_t *A, const uint8_t *W, const 
   tc::tmem_ld32(trow + 0, h);
   tc::tmem_ld32(trow + 32, h + 32);
   tc::tc_fence_before();
-  // ---- layer 2 (fp32, CUDA cores): 64 -> 4, sequential in the hidden index
-  const float *b1 = fp + 64, *w2 = fp + 128, *b2 = fp + 128 + 256;
+  // ---- layer 2 (fp32, CUDA cores): 64 -> 4, sequential in the hidden index;
+  // W2 is staged hidden-major ([o][4]) so one 16 B load feeds the 4 outputs
+  const float4 *b1 = reinterpret_cast<const float4 *>(fp + 64), *w2 = reinterpret_cast<const float4 *>(fp + 128);
+  const float *b2 = fp + 128 + 256;
   float acc[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-  for (int o = 0; o < 64; ++o) {
-    float z = h[o] + b1[o];
-    z = z > 0.f ? z : 0.f;
+  for (int o4 = 0; o4 < 16; ++o4) {
+    const float4 bv = b1[o4];
+    const float bb[4] = {bv.x, bv.y, bv.z, bv.w};
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[j] = fmaf(z, w2[j * 64 + o], acc[j]);
+    for (int e = 0; e < 4; ++e) {
+      const int o = 4 * o4 + e;
+      float z = h[o] + bb[e];
+      z = z > 0.f ? z : 0.f;
+      const float4 wv = w2[o];
+      acc[0] = fmaf(z, wv.x, acc[0]);
+      acc[1] = fmaf(z, wv.y, acc[1]);
+      acc[2] = fmaf(z, wv.z, acc[2]);
+      acc[3] = fmaf(z, wv.w, acc[3]);
+    }
   }
 #pragma unroll
   for (int j = 0; j < 4; ++j) out4[j] = acc[j] + b2[j];
@@ -163,7 +179,7 @@ __device__ __forceinline__ void tc_stage_asset(const DevAsset &A, const TcSmemPt
     float v;
     if (q < 64) v = P[MlpOff::b0 + q];
     else if (q < 128) v = P[MlpOff::b1 + q - 64];
-    else if (q < 128 + 256) v = P[MlpOff::wl + q - 128];
+    else if (q < 128 + 256) v = P[MlpOff::wl + ((q - 128) & 3) * 64 + ((q - 128) >> 2)];   // [o][4]
     else v = P[MlpOff::bl + q - 384];
     S.fp[q] = v;
   }
@@ -174,7 +190,62 @@ __device__ __forceinline__ void tc_stage_asset(const DevAsset &A, const TcSmemPt
   tma_phase ^= 1;
 }
 
+// Layer-0 input row of one hit (lightfield.py:300-331): PSH features
+// (trilinear over 8 corner slots, f64 accumulation), SH degree-3 of the view
+// direction, and the clamped opacity when refining.  FIXED_F = 2 makes every
+// index static (the row stays in registers); 0 = any F (local array).
+template <int FIXED_F>
+__device__ __forceinline__ void tc_gather_inputs(const DevAsset &A, const TcSmemPtrs &S, const uint32_t *tab,
+                                                 bool phi_smem, const HitRec &rec, float x[kTcK0]) {
+  const int F = FIXED_F ? FIXED_F : A.F;
+  int base[3];
+  double w8[8];
+  base_weights(rec.p, A.N, base, w8);
+  double es[FIXED_F ? FIXED_F : kTcK0] = {};
+  uint32_t slots[8];
+  const int s1 = A.N + 1;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const int xx = base[0] + (c & 1), yy = base[1] + ((c >> 1) & 1), zz = base[2] + ((c >> 2) & 1);
+    uint32_t h0 = tab[xx] + tab[s1 + yy];
+    h0 = h0 >= A.m ? h0 - A.m : h0;
+    h0 += tab[2 * s1 + zz];
+    h0 = h0 >= A.m ? h0 - A.m : h0;
+    uint32_t h1 = tab[3 * s1 + xx] + tab[4 * s1 + yy];
+    h1 = h1 >= A.mphi ? h1 - A.mphi : h1;
+    h1 += tab[5 * s1 + zz];
+    h1 = h1 >= A.mphi ? h1 - A.mphi : h1;
+    const uint32_t off = phi_smem ? (uint32_t)reinterpret_cast<const uint16_t *>(S.phi)[h1] : __ldg(A.phi + h1);
+    uint32_t slot = h0 + off;
+    slots[c] = slot >= A.m ? slot - A.m : slot;
+  }
+  if (FIXED_F == 2) {
+    float2 f[8];               // all 8 gathers in flight before the ordered sum
+#pragma unroll
+    for (int c = 0; c < 8; ++c) f[c] = __ldg(reinterpret_cast<const float2 *>(A.feat) + slots[c]);
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      es[0] = __dadd_rn(es[0], __dmul_rn((double)f[c].x, w8[c]));
+      es[1] = __dadd_rn(es[1], __dmul_rn((double)f[c].y, w8[c]));
+    }
+  } else {
+    for (int c = 0; c < 8; ++c)
+      for (int q = 0; q < F; ++q)
+        es[q] = __dadd_rn(es[q], __dmul_rn((double)__ldg(A.feat + (size_t)slots[c] * F + q), w8[c]));
+  }
+  for (int q = 0; q < F; ++q) x[q] = (float)es[q];
+  double sh[16];
+  sh_encode(rec.d, sh);
+#pragma unroll
+  for (int q = 0; q < 16; ++q) x[F + q] = (float)sh[q];
+  if (A.refine_opacity) x[F + 16] = (float)clampd(rec.alpha_c, 1e-4, 1.0 - 1e-4);
+}
+
+#ifdef NOLF_SHADE_MINB
+__global__ void __launch_bounds__(kTcThreads, NOLF_SHADE_MINB) k_shade_tc(ShadeArgs args) {
+#else
 __global__ void __launch_bounds__(kTcThreads) k_shade_tc(ShadeArgs args) {
+#endif
   extern __shared__ uint8_t smem_raw[];
   const TcSmemPtrs S = tc_carve(smem_raw);
   const int tid = threadIdx.x, warp = tid >> 5;
@@ -223,7 +294,8 @@ __global__ void __launch_bounds__(kTcThreads) k_shade_tc(ShadeArgs args) {
     const long long r = t * kTcThreads + tid;
     const bool valid = r < cnt;
     float x[kTcK0];
-    int nin = 0;
+#pragma unroll
+    for (int q = 0; q < kTcK0; ++q) x[q] = 0.f;
     double cd[3] = {0.0, 0.0, 0.0}, tint = 1.0, alpha_c = 0.0, t_obj = 0.0;
     uint32_t out_idx = 0, ordinal = 0;
     if (valid) {
@@ -232,42 +304,15 @@ __global__ void __launch_bounds__(kTcThreads) k_shade_tc(ShadeArgs args) {
       t_obj = rec.t_obj;
       out_idx = rec.out_idx;
       ordinal = rec.ordinal;
-      int base[3];
-      double w8[8];
-      base_weights(rec.p, A.N, base, w8);
-      double es[4] = {0.0, 0.0, 0.0, 0.0};
       const uint32_t *tab = tab_smem ? S.tab : A.tab;
+      if (A.F == 2) {            // the common layout: every input index is static -> registers
+        tc_gather_inputs<2>(A, S, tab, phi_smem, rec, x);
+      } else {
+        float xl[kTcK0] = {};
+        tc_gather_inputs<0>(A, S, tab, phi_smem, rec, xl);
 #pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        const int xx = base[0] + (c & 1), yy = base[1] + ((c >> 1) & 1), zz = base[2] + ((c >> 2) & 1);
-        const int s1 = A.N + 1;
-        uint32_t h0 = tab[xx] + tab[s1 + yy];
-        h0 = h0 >= A.m ? h0 - A.m : h0;
-        h0 += tab[2 * s1 + zz];
-        h0 = h0 >= A.m ? h0 - A.m : h0;
-        uint32_t h1 = tab[3 * s1 + xx] + tab[4 * s1 + yy];
-        h1 = h1 >= A.mphi ? h1 - A.mphi : h1;
-        h1 += tab[5 * s1 + zz];
-        h1 = h1 >= A.mphi ? h1 - A.mphi : h1;
-        const uint32_t off = phi_smem ? (uint32_t)reinterpret_cast<const uint16_t *>(S.phi)[h1] : __ldg(A.phi + h1);
-        uint32_t slot = h0 + off;
-        slot = slot >= A.m ? slot - A.m : slot;
-        if (A.F == 2) {
-          const float2 f = __ldg(reinterpret_cast<const float2 *>(A.feat) + slot);
-          es[0] = __dadd_rn(es[0], __dmul_rn((double)f.x, w8[c]));
-          es[1] = __dadd_rn(es[1], __dmul_rn((double)f.y, w8[c]));
-        } else {
-          for (int f = 0; f < A.F; ++f)
-            es[f] = __dadd_rn(es[f], __dmul_rn((double)__ldg(A.feat + (size_t)slot * A.F + f), w8[c]));
-        }
+        for (int q = 0; q < kTcK0; ++q) x[q] = xl[q];
       }
-      for (int f = 0; f < A.F; ++f) x[nin++] = (float)es[f];
-      double sh[16];
-      sh_encode(rec.d, sh);
-#pragma unroll
-      for (int q = 0; q < 16; ++q) x[nin + q] = (float)sh[q];
-      nin += 16;
-      if (A.refine_opacity) x[nin++] = (float)clampd(alpha_c, 1e-4, 1.0 - 1e-4);
       if (A.use_diffuse_color && A.has_dif) {
         float dv[4];
         atlas_query<4>(A.dif, rec.p, dv);
@@ -277,7 +322,7 @@ __global__ void __launch_bounds__(kTcThreads) k_shade_tc(ShadeArgs args) {
       if (!A.use_tint) tint = 0.5;
       ++n_fs;
     }
-    tc_write_x(S.A, tid, x, valid ? nin : 0);
+    tc_write_x(S.A, tid, x, kTcK0);   // unused inputs are 0 (W0 is zero-padded too)
     float z4[4];
     tc_mlp_rows(S.A, S.W, S.fp, tmem, S.bar_mma, mma_phase, tid, z4);
     if (valid) {
