@@ -223,17 +223,30 @@ __device__ __forceinline__ void atlas_trilinear_at(const DevAtlas &at, int cid, 
   double g[3];
 #pragma unroll
   for (int k = 0; k < 3; ++k) g[k] = __dsub_rn(1.0, frac[k]);
+  if (C == 4) {                // 8 corner loads in flight, then the ordered f64 sum
+    float4 q[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c)
+      q[c] = __ldg(reinterpret_cast<const float4 *>(
+          cube + (((base[0] + (c & 1)) * s + (base[1] + ((c >> 1) & 1))) * s + (base[2] + ((c >> 2) & 1))) * C));
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const int dx = c & 1, dy = (c >> 1) & 1, dz = (c >> 2) & 1;
+      const double w = __dmul_rn(__dmul_rn(dx ? frac[0] : g[0], dy ? frac[1] : g[1]), dz ? frac[2] : g[2]);
+      const float qq[4] = {q[c].x, q[c].y, q[c].z, q[c].w};
+#pragma unroll
+      for (int ch = 0; ch < C; ++ch) acc[ch] = __dadd_rn(acc[ch], __dmul_rn(w, (double)qq[ch]));
+    }
+#pragma unroll
+    for (int ch = 0; ch < C; ++ch) out[ch] = (float)acc[ch];
+    return;
+  }
 #pragma unroll
   for (int c = 0; c < 8; ++c) {
     const int dx = c & 1, dy = (c >> 1) & 1, dz = (c >> 2) & 1;
     double w = __dmul_rn(__dmul_rn(dx ? frac[0] : g[0], dy ? frac[1] : g[1]), dz ? frac[2] : g[2]);
     const float *v = cube + (((base[0] + dx) * s + (base[1] + dy)) * s + (base[2] + dz)) * C;
-    if (C == 4) {
-      float4 q = __ldg(reinterpret_cast<const float4 *>(v));
-      float qq[4] = {q.x, q.y, q.z, q.w};
-#pragma unroll
-      for (int ch = 0; ch < C; ++ch) acc[ch] = __dadd_rn(acc[ch], __dmul_rn(w, (double)qq[ch]));
-    } else {
+    {
 #pragma unroll
       for (int ch = 0; ch < C; ++ch) acc[ch] = __dadd_rn(acc[ch], __dmul_rn(w, (double)__ldg(v + ch)));
     }
@@ -243,13 +256,28 @@ __device__ __forceinline__ void atlas_trilinear_at(const DevAtlas &at, int cid, 
 }
 
 // query_atlas at an arbitrary point (empty cell -> zeros).
-template <int C>
-__device__ __forceinline__ void atlas_query(const DevAtlas &at, const double x[3], float out[C]) {
+// Cube id of x's index cell (-1 empty): issued early, the load overlaps other work.
+__device__ __forceinline__ int atlas_cell_id(const DevAtlas &at, const double x[3]) {
   const double bd = (double)at.b;
   int cell[3];
 #pragma unroll
   for (int k = 0; k < 3; ++k) cell[k] = clampi((int)floor(__dmul_rn(x[k], bd)), 0, at.b - 1);
-  int cid = __ldg(at.index + (cell[0] * at.b + cell[1]) * at.b + cell[2]);
+  return __ldg(at.index + (cell[0] * at.b + cell[1]) * at.b + cell[2]);
+}
+
+template <int C>
+__device__ __forceinline__ void atlas_query_cid(const DevAtlas &at, int cid, const double x[3], float out[C]) {
+  if (cid < 0) {
+#pragma unroll
+    for (int ch = 0; ch < C; ++ch) out[ch] = 0.f;
+    return;
+  }
+  atlas_trilinear<C>(at, cid, x, out);
+}
+
+template <int C>
+__device__ __forceinline__ void atlas_query(const DevAtlas &at, const double x[3], float out[C]) {
+  const int cid = atlas_cell_id(at, x);
   if (cid < 0) {
 #pragma unroll
     for (int ch = 0; ch < C; ++ch) out[ch] = 0.f;

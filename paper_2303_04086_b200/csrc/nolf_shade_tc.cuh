@@ -271,15 +271,40 @@ __global__ void __launch_bounds__(kTcThreads) k_shade_tc(ShadeArgs args) {
   const long long tile_lo = blocked ? total_tiles * blockIdx.x / gridDim.x : blockIdx.x;
   const long long tile_hi = blocked ? total_tiles * (blockIdx.x + 1) / gridDim.x : total_tiles;
   const long long tile_step = blocked ? 1 : gridDim.x;
+  // (instance, tile-in-instance) of tile_lo, found once; blocked ranges then
+  // advance incrementally instead of rescanning the per-instance counts
+  int k_run = 0;
+  long long t_run = tile_lo;
+  unsigned cnt_run = 0;
+  long long nt_run = 0;
+  for (; k_run < args.n_inst; ++k_run) {
+    cnt_run = min((long long)args.counts[k_run], args.qoff[k_run + 1] - args.qoff[k_run]);
+    nt_run = (cnt_run + kTcThreads - 1) / kTcThreads;
+    if (t_run < nt_run) break;
+    t_run -= nt_run;
+  }
   for (long long tile = tile_lo; tile < tile_hi; tile += tile_step) {
     int k = 0;
     long long t = tile;
     unsigned cnt = 0;
-    for (; k < args.n_inst; ++k) {
-      cnt = min((long long)args.counts[k], args.qoff[k + 1] - args.qoff[k]);
-      const long long nt = (cnt + kTcThreads - 1) / kTcThreads;
-      if (t < nt) break;
-      t -= nt;
+    if (blocked) {
+      while (k_run < args.n_inst && t_run >= nt_run) {     // next non-empty instance
+        t_run -= nt_run;
+        if (++k_run < args.n_inst) {
+          cnt_run = min((long long)args.counts[k_run], args.qoff[k_run + 1] - args.qoff[k_run]);
+          nt_run = (cnt_run + kTcThreads - 1) / kTcThreads;
+        }
+      }
+      k = k_run;
+      t = t_run++;
+      cnt = cnt_run;
+    } else {
+      for (; k < args.n_inst; ++k) {
+        cnt = min((long long)args.counts[k], args.qoff[k + 1] - args.qoff[k]);
+        const long long nt = (cnt + kTcThreads - 1) / kTcThreads;
+        if (t < nt) break;
+        t -= nt;
+      }
     }
     if (k >= args.n_inst) break;
     const DevInst &I = args.inst[k];
@@ -305,6 +330,8 @@ __global__ void __launch_bounds__(kTcThreads) k_shade_tc(ShadeArgs args) {
       out_idx = rec.out_idx;
       ordinal = rec.ordinal;
       const uint32_t *tab = tab_smem ? S.tab : A.tab;
+      const bool want_dif = A.use_diffuse_color && A.has_dif;
+      const int dif_cid = want_dif ? atlas_cell_id(A.dif, rec.p) : -1;   // overlaps the PSH gather
       if (A.F == 2) {            // the common layout: every input index is static -> registers
         tc_gather_inputs<2>(A, S, tab, phi_smem, rec, x);
       } else {
@@ -313,9 +340,9 @@ __global__ void __launch_bounds__(kTcThreads) k_shade_tc(ShadeArgs args) {
 #pragma unroll
         for (int q = 0; q < kTcK0; ++q) x[q] = xl[q];
       }
-      if (A.use_diffuse_color && A.has_dif) {
+      if (want_dif) {
         float dv[4];
-        atlas_query<4>(A.dif, rec.p, dv);
+        atlas_query_cid<4>(A.dif, dif_cid, rec.p, dv);
         cd[0] = dv[0]; cd[1] = dv[1]; cd[2] = dv[2];
         tint = dv[3];
       }
