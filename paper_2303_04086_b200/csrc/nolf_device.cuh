@@ -199,6 +199,19 @@ __device__ __forceinline__ void atlas_subvoxel(const DevAtlas &at, const double 
   }
 }
 
+// atlas_subvoxel with the index cell already known (sample_cell computed it
+// from the same pos with the same ops).
+__device__ __forceinline__ void atlas_subvoxel_in(const DevAtlas &at, const double x[3], const int cell[3], int base[3],
+                                                  double frac[3]) {
+  const double bd = (double)at.b, rd = (double)at.r;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const double local = __dmul_rn(__dsub_rn(__dmul_rn(x[k], bd), (double)cell[k]), rd);
+    base[k] = clampi(__double2int_rd(local), 0, at.r - 1);
+    frac[k] = __dsub_rn(local, (double)base[k]);
+  }
+}
+
 template <int C>
 __device__ __forceinline__ void atlas_trilinear_at(const DevAtlas &at, int cid, const int base[3], const double frac[3],
                                                    float out[C]);

@@ -66,29 +66,28 @@ struct MarchArgs {
 // Exit parameter of an axis-aligned box [lo, hi] (object coords) along the
 // ray, with faces on the unit-cube boundary pushed to infinity because march
 // positions are clipped to [0,1] (lightfield.py:166).
-// (An estimate only: the skip target is verified exactly, so 1/d is fine.)
-__device__ __forceinline__ double box_exit(const double o[3], const double d[3], const double inv[3],
+// (An estimate only: the skip target is verified exactly, so fp32 is fine.)
+__device__ __forceinline__ double box_exit(const double o[3], const double d[3], const float invf[3],
                                            const double lo[3], const double hi[3]) {
-  const double INF = __longlong_as_double(0x7ff0000000000000ll);
-  double t = INF;
+  float t = __int_as_float(0x7f800000);
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
-    if (d[k] > 0.0 && hi[k] < 1.0) t = fmin(t, (hi[k] - o[k]) * inv[k]);
-    else if (d[k] < 0.0 && lo[k] > 0.0) t = fmin(t, (lo[k] - o[k]) * inv[k]);
+    if (d[k] > 0.0 && hi[k] < 1.0) t = fminf(t, (float)(hi[k] - o[k]) * invf[k]);
+    else if (d[k] < 0.0 && lo[k] > 0.0) t = fminf(t, (float)(lo[k] - o[k]) * invf[k]);
   }
-  return t;
+  return (double)t;
 }
 
 // Sample i's clipped position and index cell, exactly as march_rays computes
 // them (t_mid = t_near + (i+0.5)*step ; pos = clip(o + t_mid*d, 0, 1)).
 __device__ __forceinline__ double sample_cell(const double o[3], const double d[3], double t_near, double delta,
-                                              long long i, int b, double pos[3], int cell[3]) {
+                                              int i, int b, double pos[3], int cell[3]) {
   double t_mid = __dadd_rn(t_near, __dmul_rn((double)i + 0.5, delta));
   const double bd = (double)b;
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
     pos[k] = clamp01(__dadd_rn(o[k], __dmul_rn(t_mid, d[k])));
-    cell[k] = clampi((int)floor(__dmul_rn(pos[k], bd)), 0, b - 1);
+    cell[k] = min(__double2int_rd(__dmul_rn(pos[k], bd)), b - 1);   // pos in [0,1]: floor >= 0
   }
   return t_mid;
 }
@@ -156,8 +155,8 @@ struct MarchOut {
 };
 
 __device__ __forceinline__ MarchOut march_ray(const DevAsset &A, const double o[3], const double d[3],
-                                              const double inv[3], double t_near, double t_far, bool use_zmask,
-                                              long long i_start, double t_end) {
+                                              const float invf[3], double t_near, double t_far, bool use_zmask,
+                                              int i_start, double t_end) {
   MarchOut r;
   r.alpha_c = 0.0;
   r.t_hit = __longlong_as_double(0x7ff0000000000000ll);
@@ -171,12 +170,15 @@ __device__ __forceinline__ MarchOut march_ray(const DevAsset &A, const double o[
   const double inv_delta = 1.0 / delta;
   double best_w = 0.0, trans = 1.0, alpha_c = 0.0, t_hit = r.t_hit;
   int samples = 0;
-  long long i = i_start;       // samples before i_start and from t_end on are empty
+  // samples before i_start and from t_end on are empty: march [i_start, t_lim)
+  const double t_lim = fmin(t_far, t_end);
+  const double t_stop = A.t_stop;
+  int i = i_start;
   for (;;) {
     double pos[3];
     int cell[3];
     const double t_mid = sample_cell(o, d, t_near, delta, i, b, pos, cell);
-    if (!(t_mid < t_far) || !(t_mid < t_end)) break;
+    if (!(t_mid < t_lim)) break;
     NOLF_STAT(7, 1);
     int lo_c[3], hi_c[3];
     bool empty = false;
@@ -201,16 +203,16 @@ __device__ __forceinline__ MarchOut march_ray(const DevAsset &A, const double o[
         lo[k] = lo_c[k] > 0 ? lo_c[k] * inv_b : -1.0;       // grid faces: clipped
         hi[k] = hi_c[k] < b - 1 ? (hi_c[k] + 1) * inv_b : 2.0;  // positions never leave
       }
-      double te = box_exit(o, d, inv, lo, hi);
-      double tl = fmin(te, t_far);
+      double te = box_exit(o, d, invf, lo, hi);
+      double tl = fmin(te, t_lim);
       double jf = floor((tl - t_near) * inv_delta - 0.5);
-      long long j = jf > 9.0e15 ? (long long)9.0e15 : (long long)jf;
-      long long next = i + 1;
+      int j = jf > 2.0e9 ? 2000000000 : (int)jf;
+      int next = i + 1;
       for (int attempt = 0; attempt < 2 && j > i; ++attempt, --j) {
         double pj[3];
         int cj[3];
         double tj = sample_cell(o, d, t_near, delta, j, b, pj, cj);
-        bool inside = tj < t_far;
+        bool inside = tj < t_lim;
 #pragma unroll
         for (int k = 0; k < 3; ++k) inside = inside && cj[k] >= lo_c[k] && cj[k] <= hi_c[k];
         if (inside) { next = j + 1; break; }
@@ -222,10 +224,10 @@ __device__ __forceinline__ MarchOut march_ray(const DevAsset &A, const double o[
     // absorb = exp(-0) = 1, w = 0 -- only the active-sample count changes
     int base[3];
     double frac[3];
-    atlas_subvoxel(at, pos, base, frac);
+    atlas_subvoxel_in(at, pos, cell, base, frac);
     const int bit = (base[0] * at.r + base[1]) * at.r + base[2];
     ++samples;
-    if (use_zmask && ((__ldg(at.zmask + (size_t)cid * at.zwords + (bit >> 5)) >> (bit & 31)) & 1u)) {
+    if (use_zmask && ((__ldg(at.zmask + (unsigned)(cid * at.zwords + (bit >> 5))) >> (bit & 31)) & 1u)) {
       NOLF_STAT(5, 1);
       ++i;
       continue;
@@ -239,7 +241,7 @@ __device__ __forceinline__ MarchOut march_ray(const DevAsset &A, const double o[
     if (w > best_w) { best_w = w; t_hit = t_mid; }
     alpha_c = __dadd_rn(alpha_c, w);
     trans = __dmul_rn(trans, absorb);
-    if (!(trans > A.t_stop)) break;
+    if (!(trans > t_stop)) break;
     ++i;
   }
   r.alpha_c = alpha_c;
@@ -363,7 +365,7 @@ __global__ void __launch_bounds__(128, NOLF_MARCH_MINB) k_march(MarchArgs args) 
       // grown by one cell): every sample outside it lies in an empty cell, so
       // starting 2 samples before the entry and stopping 2 after the exit
       // leaves the result bit-identical (empty samples change nothing).
-      long long i_start = 0;
+      int i_start = 0;
       double t_end = t_far;
       if (boxhit) NOLF_STAT(1, 1);
       if (boxhit && t_near < t_far) {
@@ -372,13 +374,14 @@ __global__ void __launch_bounds__(128, NOLF_MARCH_MINB) k_march(MarchArgs args) 
           boxhit = false;                     // never meets an occupied cell: exact miss
         } else {
           const double f = floor((ca - t_near) / A.step - 2.5);
-          i_start = f > 0.0 ? (long long)f : 0;
+          i_start = f > 0.0 ? (f < 2.0e9 ? (int)f : 2000000000) : 0;
           t_end = cb + 2.0 * A.step;
         }
       }
       if (boxhit) {
         NOLF_STAT(2, 1);
-        mr = march_ray(A, o, d, inv, t_near, t_far, args.use_zmask, i_start, t_end);
+        const float invf[3] = {(float)inv[0], (float)inv[1], (float)inv[2]};
+        mr = march_ray(A, o, d, invf, t_near, t_far, args.use_zmask, i_start, t_end);
         samples_total += (unsigned)mr.samples;
         hit = mr.hit;
       }
