@@ -258,6 +258,23 @@ template <int MODE>
 __global__ void __launch_bounds__(128, NOLF_MARCH_MINB) k_march(MarchArgs args) {
   const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const unsigned lane = threadIdx.x & 31;
+  if (MODE == kModeScene && args.cull && args.tile_stride % blockDim.x == 0) {
+    // CTA-level pre-cull: all 128 slots lie in one tile; when no instance's
+    // screen box meets the tile, every pixel is a miss (nhit = 0) -- the
+    // common case in a sparse scene, decided with one barrier
+    long long t, local0;
+    split_slot((long long)blockIdx.x * blockDim.x, args.tile_stride, t, local0);
+    const TileParams tp = args.tiles[t];
+    bool meets = false;
+    for (int k = threadIdx.x; k < args.n_inst; k += blockDim.x) {
+      const ScreenBox bb = args.cull[k * args.n_cams + tp.cam];
+      meets = meets || (bb.x0 <= bb.x1 && bb.x0 < tp.x1 && bb.x1 >= tp.x0 && bb.y0 < tp.y1 && bb.y1 >= tp.y0);
+    }
+    if (!__syncthreads_or(meets)) {
+      if (gid < args.n_rays) args.nhit[gid] = 0;
+      return;
+    }
+  }
   bool valid = gid < args.n_rays;
   double ow[3] = {0, 0, 0}, dw[3] = {0, 0, 1};
   int pix_x = 0, pix_y = 0, cam = 0;
