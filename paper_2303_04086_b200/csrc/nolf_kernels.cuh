@@ -80,16 +80,36 @@ __device__ __forceinline__ double box_exit(const double o[3], const double d[3],
 
 // Sample i's clipped position and index cell, exactly as march_rays computes
 // them (t_mid = t_near + (i+0.5)*step ; pos = clip(o + t_mid*d, 0, 1)).
+// CLIP = false when the caller proved every position it will ask for lies in
+// [0,1] already (then clip() is the identity and is skipped).
+template <bool CLIP = true>
 __device__ __forceinline__ double sample_cell(const double o[3], const double d[3], double t_near, double delta,
                                               int i, int b, double pos[3], int cell[3]) {
   double t_mid = __dadd_rn(t_near, __dmul_rn((double)i + 0.5, delta));
   const double bd = (double)b;
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
-    pos[k] = clamp01(__dadd_rn(o[k], __dmul_rn(t_mid, d[k])));
+    const double v = __dadd_rn(o[k], __dmul_rn(t_mid, d[k]));
+    pos[k] = CLIP ? clamp01(v) : v;
     cell[k] = min(__double2int_rd(__dmul_rn(pos[k], bd)), b - 1);   // pos in [0,1]: floor >= 0
   }
   return t_mid;
+}
+
+// True when the unclipped positions of samples lo and hi are inside [0,1]^3:
+// each coordinate fl(o + fl(t_mid*d)) is monotone in the sample index, so all
+// samples between them are inside too and clip() is exactly the identity.
+__device__ __forceinline__ bool samples_inside_unit(const double o[3], const double d[3], double t_near,
+                                                    double delta, int lo, int hi) {
+  const double ta = __dadd_rn(t_near, __dmul_rn((double)lo + 0.5, delta));
+  const double tb = __dadd_rn(t_near, __dmul_rn((double)hi + 0.5, delta));
+  bool in = true;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const double a = __dadd_rn(o[k], __dmul_rn(ta, d[k])), c = __dadd_rn(o[k], __dmul_rn(tb, d[k]));
+    in = in && a >= 0.0 && a <= 1.0 && c >= 0.0 && c <= 1.0;
+  }
+  return in;
 }
 
 #ifdef NOLF_STATS   // diagnostic build only: march work counters
@@ -154,6 +174,7 @@ struct MarchOut {
   bool hit;
 };
 
+template <bool CLIP>
 __device__ __forceinline__ MarchOut march_ray(const DevAsset &A, const double o[3], const double d[3],
                                               const float invf[3], double t_near, double t_far, bool use_zmask,
                                               int i_start, double t_end) {
@@ -177,7 +198,7 @@ __device__ __forceinline__ MarchOut march_ray(const DevAsset &A, const double o[
   for (;;) {
     double pos[3];
     int cell[3];
-    const double t_mid = sample_cell(o, d, t_near, delta, i, b, pos, cell);
+    const double t_mid = sample_cell<CLIP>(o, d, t_near, delta, i, b, pos, cell);
     if (!(t_mid < t_lim)) break;
     NOLF_STAT(7, 1);
     int lo_c[3], hi_c[3];
@@ -211,7 +232,7 @@ __device__ __forceinline__ MarchOut march_ray(const DevAsset &A, const double o[
       for (int attempt = 0; attempt < 2 && j > i; ++attempt, --j) {
         double pj[3];
         int cj[3];
-        double tj = sample_cell(o, d, t_near, delta, j, b, pj, cj);
+        double tj = sample_cell<CLIP>(o, d, t_near, delta, j, b, pj, cj);
         bool inside = tj < t_lim;
 #pragma unroll
         for (int k = 0; k < 3; ++k) inside = inside && cj[k] >= lo_c[k] && cj[k] <= hi_c[k];
@@ -398,7 +419,13 @@ __global__ void __launch_bounds__(128, NOLF_MARCH_MINB) k_march(MarchArgs args) 
       if (boxhit) {
         NOLF_STAT(2, 1);
         const float invf[3] = {(float)inv[0], (float)inv[1], (float)inv[2]};
-        mr = march_ray(A, o, d, invf, t_near, t_far, args.use_zmask, i_start, t_end);
+        // every sample the march can visit has index in [i_start, i_hi]
+        const double lim = fmin(t_far, t_end);
+        const double hf = floor((lim - t_near) / A.step) + 2.0;
+        const bool noclip = t_near < lim && hf < 2.0e9 &&
+                            samples_inside_unit(o, d, t_near, A.step, i_start, (int)hf);
+        if (noclip) mr = march_ray<false>(A, o, d, invf, t_near, t_far, args.use_zmask, i_start, t_end);
+        else mr = march_ray<true>(A, o, d, invf, t_near, t_far, args.use_zmask, i_start, t_end);
         samples_total += (unsigned)mr.samples;
         hit = mr.hit;
       }
