@@ -201,6 +201,12 @@ __device__ __forceinline__ MarchOut march_ray(const DevAsset &A, const double o[
     const double t_mid = sample_cell<CLIP>(o, d, t_near, delta, i, b, pos, cell);
     if (!(t_mid < t_lim)) break;
     NOLF_STAT(7, 1);
+#ifdef NOLF_STATS
+    {
+      const unsigned am = __activemask();
+      if ((threadIdx.x & 31) == (unsigned)(__ffs(am) - 1)) { NOLF_STAT(9, 1); NOLF_STAT(10, __popc(am)); }
+    }
+#endif
     int lo_c[3], hi_c[3];
     bool empty = false;
     int cid = -1;
@@ -297,14 +303,9 @@ __global__ void __launch_bounds__(128, NOLF_MARCH_MINB) k_march(MarchArgs args) 
     }
   }
   bool valid = gid < args.n_rays;
-  double ow[3] = {0, 0, 0}, dw[3] = {0, 0, 1};
   int pix_x = 0, pix_y = 0, cam = 0;
   if (valid) {
-    if (MODE == kModeRays) {
-      const double *op = args.origins + (args.origin_stride ? 3 * gid : 0);
-      ow[0] = op[0]; ow[1] = op[1]; ow[2] = op[2];
-      dw[0] = args.dirs[3 * gid]; dw[1] = args.dirs[3 * gid + 1]; dw[2] = args.dirs[3 * gid + 2];
-    } else {
+    if (MODE != kModeRays) {
       long long t = 0, local = gid;
       if (MODE != kModeRect) split_slot(gid, args.tile_stride, t, local);
       const TileParams tp = args.tiles[t];
@@ -369,12 +370,6 @@ __global__ void __launch_bounds__(128, NOLF_MARCH_MINB) k_march(MarchArgs args) 
   }
   unsigned long long wmask = ((unsigned long long)__reduce_or_sync(0xffffffffu, (unsigned)(lane_mask >> 32)) << 32) |
                              __reduce_or_sync(0xffffffffu, (unsigned)lane_mask);
-  // camera ray (core.py:162-170) only for pixels some instance may cover
-  if (MODE != kModeRays && lane_mask) {
-    const CamParams &cp = args.cams[cam];
-    camera_dir(cp.pose, cp.fx, cp.fy, cp.cx, cp.cy, (double)pix_x, (double)pix_y, dw);
-    ow[0] = cp.pose[3]; ow[1] = cp.pose[7]; ow[2] = cp.pose[11];
-  }
   while (wmask) {
     const int k = __ffsll((long long)wmask) - 1;
     wmask &= wmask - 1;
@@ -387,6 +382,18 @@ __global__ void __launch_bounds__(128, NOLF_MARCH_MINB) k_march(MarchArgs args) 
     if (lane == 0) NOLF_STAT(8, 1);
     if (live) {
       NOLF_STAT(0, 1);
+      // world ray, rebuilt per candidate instead of held across the march
+      // (registers): camera ray (core.py:162-170) or the caller's ray
+      double ow[3], dw[3];
+      if (MODE == kModeRays) {
+        const double *op = args.origins + (args.origin_stride ? 3 * gid : 0);
+        ow[0] = op[0]; ow[1] = op[1]; ow[2] = op[2];
+        dw[0] = args.dirs[3 * gid]; dw[1] = args.dirs[3 * gid + 1]; dw[2] = args.dirs[3 * gid + 2];
+      } else {
+        const CamParams &cp = args.cams[cam];
+        camera_dir(cp.pose, cp.fx, cp.fy, cp.cx, cp.cy, (double)pix_x, (double)pix_y, dw);
+        ow[0] = cp.pose[3]; ow[1] = cp.pose[7]; ow[2] = cp.pose[11];
+      }
       if (args.raw_rays) {
 #pragma unroll
         for (int q = 0; q < 3; ++q) { o[q] = ow[q]; d[q] = dw[q]; }
