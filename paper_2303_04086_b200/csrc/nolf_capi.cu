@@ -1183,6 +1183,13 @@ int nolf_compose(int32_t K, int64_t P, const float *rgba, const float *depth, do
 }  // extern "C"
 
 #ifdef NOLF_STATS
+extern "C" int nolf_stats_cta(unsigned long long *start, unsigned long long *end, int n) {
+  cudaMemcpyFromSymbol(start, nolf::g_cta_start, sizeof(unsigned long long) * n);
+  cudaMemcpyFromSymbol(end, nolf::g_cta_end, sizeof(unsigned long long) * n);
+  static unsigned long long z[1 << 20];
+  cudaMemcpyToSymbol(nolf::g_cta_end, z, sizeof(z));
+  return (int)cudaGetLastError();
+}
 extern "C" int nolf_stats_read(unsigned long long *out, int reset) {
   cudaMemcpyFromSymbol(out, nolf::g_stats, sizeof(unsigned long long) * 16);
   if (reset) {

@@ -112,8 +112,11 @@ __device__ __forceinline__ bool samples_inside_unit(const double o[3], const dou
   return in;
 }
 
-#ifdef NOLF_STATS   // diagnostic build only: march work counters
+#ifdef NOLF_STATS   // diagnostic build only: march work counters (-DNOLF_STATS_CTR) / CTA spans
 __device__ unsigned long long g_stats[16];
+__device__ unsigned long long g_cta_start[1 << 20], g_cta_end[1 << 20];
+#endif
+#if defined(NOLF_STATS) && defined(NOLF_STATS_CTR)
 #define NOLF_STAT(k, v) atomicAdd(&g_stats[k], (unsigned long long)(v))
 #else
 #define NOLF_STAT(k, v) ((void)0)
@@ -195,13 +198,19 @@ __device__ __forceinline__ MarchOut march_ray(const DevAsset &A, const double o[
   const double t_lim = fmin(t_far, t_end);
   const double t_stop = A.t_stop;
   int i = i_start;
+#if defined(NOLF_STATS) && defined(NOLF_STATS_CTR)
+  unsigned iters_dbg = 0;
+#endif
   for (;;) {
     double pos[3];
     int cell[3];
     const double t_mid = sample_cell<CLIP>(o, d, t_near, delta, i, b, pos, cell);
     if (!(t_mid < t_lim)) break;
     NOLF_STAT(7, 1);
-#ifdef NOLF_STATS
+#if defined(NOLF_STATS) && defined(NOLF_STATS_CTR)
+    ++iters_dbg;
+#endif
+#if defined(NOLF_STATS) && defined(NOLF_STATS_CTR)
     {
       const unsigned am = __activemask();
       if ((threadIdx.x & 31) == (unsigned)(__ffs(am) - 1)) { NOLF_STAT(9, 1); NOLF_STAT(10, __popc(am)); }
@@ -271,6 +280,11 @@ __device__ __forceinline__ MarchOut march_ray(const DevAsset &A, const double o[
     if (!(trans > t_stop)) break;
     ++i;
   }
+#if defined(NOLF_STATS) && defined(NOLF_STATS_CTR)
+  atomicMax(&g_stats[11], (unsigned long long)iters_dbg);
+  atomicMax(&g_stats[12], (unsigned long long)samples);
+  atomicMax(&g_stats[13], (unsigned long long)((t_lim - t_near) / delta));
+#endif
   r.alpha_c = alpha_c;
   r.samples = samples;
   r.hit = alpha_c > A.alpha_floor;
@@ -278,52 +292,212 @@ __device__ __forceinline__ MarchOut march_ray(const DevAsset &A, const double o[
   return r;
 }
 
-template <int MODE>
 #ifndef NOLF_MARCH_MINB
 #define NOLF_MARCH_MINB 8  // latency-bound: 50% occupancy beats the spills it costs (measured 4..8)
 #endif
+
+#ifdef NOLF_STATS
+__device__ __forceinline__ void stat_cta_start() {
+  if (threadIdx.x == 0 && blockIdx.x < (1u << 20)) {
+    unsigned long long now;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+    g_cta_start[blockIdx.x] = now;
+  }
+}
+__device__ __forceinline__ void stat_cta_end() {   // global ns timer at the last warp's end
+  unsigned long long now;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+  if ((threadIdx.x & 31) == 0 && blockIdx.x < (1u << 20)) atomicMax(&g_cta_end[blockIdx.x], now);
+}
+#else
+__device__ __forceinline__ void stat_cta_start() {}
+__device__ __forceinline__ void stat_cta_end() {}
+#endif
+
+// CTA-level pre-cull (scene mode): all of the CTA's slots lie in one tile;
+// when no instance's screen box meets the tile every pixel is a miss.  Returns
+// true when the CTA is done (nhit = 0 written).
+__device__ __forceinline__ bool cta_precull(const MarchArgs &args, long long gid) {
+  if (!args.cull || args.tile_stride % blockDim.x != 0) return false;
+  long long t, local0;
+  split_slot((long long)blockIdx.x * blockDim.x, args.tile_stride, t, local0);
+  const TileParams tp = args.tiles[t];
+  bool meets = false;
+  for (int k = threadIdx.x; k < args.n_inst; k += blockDim.x) {
+    const ScreenBox bb = args.cull[k * args.n_cams + tp.cam];
+    meets = meets || (bb.x0 <= bb.x1 && bb.x0 < tp.x1 && bb.x1 >= tp.x0 && bb.y0 < tp.y1 && bb.y1 >= tp.y0);
+  }
+  if (__syncthreads_or(meets)) return false;
+  if (gid < args.n_rays) args.nhit[gid] = 0;
+  return true;
+}
+
+// Pixel (and camera) of ray slot gid; false for tile padding.
+template <int MODE>
+__device__ __forceinline__ bool slot_pixel(const MarchArgs &args, long long gid, int &pix_x, int &pix_y, int &cam) {
+  long long t = 0, local = gid;
+  if (MODE != kModeRect) split_slot(gid, args.tile_stride, t, local);
+  const TileParams tp = args.tiles[t];
+  const int w = tp.x1 - tp.x0, h = tp.y1 - tp.y0;
+  if (local >= (long long)w * h) return false;
+  cam = tp.cam;
+  if (MODE == kModeScene) {
+    slot_xy(local, w, h, pix_x, pix_y);
+    pix_x += tp.x0;
+    pix_y += tp.y0;
+  } else {
+    pix_x = tp.x0 + (int)(local % w);
+    pix_y = tp.y0 + (int)(local / w);
+  }
+  return true;
+}
+
+// Instances whose conservative screen box covers this lane's pixel (all
+// instances without culling).  Warp-collective.
+template <int MODE>
+__device__ __forceinline__ unsigned long long candidate_mask(const MarchArgs &args, bool valid, int pix_x, int pix_y,
+                                                             int cam, unsigned lane) {
+  unsigned long long lane_mask = 0;
+  if (MODE == kModeRays || !args.cull) {
+    if (valid) lane_mask = args.n_inst >= 64 ? ~0ull : ((1ull << args.n_inst) - 1ull);
+    return lane_mask;
+  }
+  const int cmin = __reduce_min_sync(0xffffffffu, valid ? cam : INT_MAX);
+  const int cmax = __reduce_max_sync(0xffffffffu, valid ? cam : -1);
+  if (cmin == cmax) {
+    // one camera for the whole warp: lane k tests instance k's box against
+    // the warp's pixel rectangle, then only the candidates are tested per pixel
+    const int xmin = __reduce_min_sync(0xffffffffu, valid ? pix_x : INT_MAX);
+    const int xmax = __reduce_max_sync(0xffffffffu, valid ? pix_x : INT_MIN);
+    const int ymin = __reduce_min_sync(0xffffffffu, valid ? pix_y : INT_MAX);
+    const int ymax = __reduce_max_sync(0xffffffffu, valid ? pix_y : INT_MIN);
+    for (int base = 0; base < args.n_inst; base += 32) {
+      const int k = base + (int)lane;
+      ScreenBox bb{1, 1, 0, 0};
+      if (k < args.n_inst) bb = args.cull[k * args.n_cams + cmin];
+      unsigned cand = __ballot_sync(0xffffffffu, bb.x0 <= xmax && bb.x1 >= xmin && bb.y0 <= ymax && bb.y1 >= ymin &&
+                                                     bb.x0 <= bb.x1);
+      while (cand) {
+        const int j = __ffs(cand) - 1;
+        cand &= cand - 1;
+        const int x0 = __shfl_sync(0xffffffffu, bb.x0, j), x1 = __shfl_sync(0xffffffffu, bb.x1, j);
+        const int y0 = __shfl_sync(0xffffffffu, bb.y0, j), y1 = __shfl_sync(0xffffffffu, bb.y1, j);
+        if (valid && pix_x >= x0 && pix_x <= x1 && pix_y >= y0 && pix_y <= y1) lane_mask |= 1ull << (base + j);
+      }
+    }
+  } else if (valid) {
+    for (int k = 0; k < args.n_inst; ++k) {
+      const ScreenBox bb = args.cull[k * args.n_cams + cam];
+      if (pix_x >= bb.x0 && pix_x <= bb.x1 && pix_y >= bb.y0 && pix_y <= bb.y1) lane_mask |= 1ull << k;
+    }
+  }
+  return lane_mask;
+}
+
+// World ray of a slot: camera ray (core.py:162-170) or the caller's ray.
+template <int MODE>
+__device__ __forceinline__ void world_ray(const MarchArgs &args, long long gid, int cam, int pix_x, int pix_y,
+                                          double ow[3], double dw[3]) {
+  if (MODE == kModeRays) {
+    const double *op = args.origins + (args.origin_stride ? 3 * gid : 0);
+    ow[0] = op[0]; ow[1] = op[1]; ow[2] = op[2];
+    dw[0] = args.dirs[3 * gid]; dw[1] = args.dirs[3 * gid + 1]; dw[2] = args.dirs[3 * gid + 2];
+  } else {
+    const CamParams &cp = args.cams[cam];
+    camera_dir(cp.pose, cp.fx, cp.fy, cp.cx, cp.cy, (double)pix_x, (double)pix_y, dw);
+    ow[0] = cp.pose[3]; ow[1] = cp.pose[7]; ow[2] = cp.pose[11];
+  }
+}
+
+// Everything march_rays does before its first sample (lightfield.py:129-150):
+// object-space ray, proxy entry/exit (box slab or mesh first hit), then the
+// exact clip of the sample range to the grown occupied-cell box.  False:
+// the ray never samples an occupied cell (exact miss, no samples).
+struct MarchSpan {
+  double t_near, t_far, t_end;
+  int i_start;
+  bool noclip;
+};
+
+__device__ __forceinline__ bool prepare_march(const DevInst &I, const DevAsset &A, bool raw_rays, const double ow[3],
+                                              const double dw[3], double o[3], double d[3], double inv[3],
+                                              MarchSpan &sp) {
+  if (raw_rays) {
+#pragma unroll
+    for (int q = 0; q < 3; ++q) { o[q] = ow[q]; d[q] = dw[q]; }
+  } else {
+    to_object(I.w2o, ow, dw, o, d);
+  }
+  double inv_unused[3];
+  sp.t_near = 0.0;
+  sp.t_far = 0.0;
+  sp.i_start = 0;
+  sp.noclip = false;
+  bool boxhit = slab(A.pmin, A.pmax, o, d, sp.t_near, sp.t_far, inv);
+  if (boxhit && A.mesh.nodes) {          // mesh proxy: march from its first hit
+    const double tm = mesh_first_hit(A.mesh, o, d);
+    if (tm < 0.0) boxhit = false;
+    else sp.t_near = tm;
+  }
+  sp.t_end = sp.t_far;
+  if (boxhit) NOLF_STAT(1, 1);
+  // Clip the march to the ray's span in the culling box (occupied cells
+  // grown by one cell): every sample outside it lies in an empty cell, so
+  // starting 2 samples before the entry and stopping 2 after the exit
+  // leaves the result bit-identical (empty samples change nothing).
+  if (boxhit && sp.t_near < sp.t_far) {
+    double ca, cb;
+    if (!slab(A.cull_lo, A.cull_hi, o, d, ca, cb, inv_unused) || A.cull_empty) {
+      boxhit = false;                     // never meets an occupied cell: exact miss
+    } else {
+      const double f = floor((ca - sp.t_near) / A.step - 2.5);
+      sp.i_start = f > 0.0 ? (f < 2.0e9 ? (int)f : 2000000000) : 0;
+      sp.t_end = cb + 2.0 * A.step;
+    }
+  }
+  if (boxhit) {
+    // every sample the march can visit has index in [i_start, i_hi]
+    const double lim = fmin(sp.t_far, sp.t_end);
+    const double hf = floor((lim - sp.t_near) / A.step) + 2.0;
+    sp.noclip = sp.t_near < lim && hf < 2.0e9 && samples_inside_unit(o, d, sp.t_near, A.step, sp.i_start, (int)hf);
+  }
+  return boxhit;
+}
+
+__device__ __forceinline__ MarchOut run_march(const DevAsset &A, const double o[3], const double d[3],
+                                              const float invf[3], const MarchSpan &sp, bool use_zmask) {
+  if (sp.noclip) return march_ray<false>(A, o, d, invf, sp.t_near, sp.t_far, use_zmask, sp.i_start, sp.t_end);
+  return march_ray<true>(A, o, d, invf, sp.t_near, sp.t_far, use_zmask, sp.i_start, sp.t_end);
+}
+
+// Hit record for the shading pass (lightfield.py:433-445).
+__device__ __forceinline__ HitRec hit_record(const DevAsset &A, const double o[3], const double d[3], double t_near,
+                                             const MarchOut &mr, uint32_t out_idx, uint32_t ordinal) {
+  HitRec rec;
+  double t_obj = mr.t_hit;
+  if (!A.use_hit_point) t_obj = t_near;   // ablation: shade at the proxy entry (lightfield.py:438-445)
+#pragma unroll
+  for (int q = 0; q < 3; ++q) rec.p[q] = clamp01(__dadd_rn(o[q], __dmul_rn(t_obj, d[q])));
+  rec.alpha_c = mr.alpha_c;
+  rec.t_obj = t_obj;
+  rec.d[0] = d[0]; rec.d[1] = d[1]; rec.d[2] = d[2];
+  rec.out_idx = out_idx;
+  rec.ordinal = ordinal;
+  return rec;
+}
+
+// One thread per ray, every candidate instance marched in scene order by
+// that thread (kModeRays / kModeRect, and the march_rays entry point).
+template <int MODE>
 __global__ void __launch_bounds__(128, NOLF_MARCH_MINB) k_march(MarchArgs args) {
   const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const unsigned lane = threadIdx.x & 31;
-  if (MODE == kModeScene && args.cull && args.tile_stride % blockDim.x == 0) {
-    // CTA-level pre-cull: all 128 slots lie in one tile; when no instance's
-    // screen box meets the tile, every pixel is a miss (nhit = 0) -- the
-    // common case in a sparse scene, decided with one barrier
-    long long t, local0;
-    split_slot((long long)blockIdx.x * blockDim.x, args.tile_stride, t, local0);
-    const TileParams tp = args.tiles[t];
-    bool meets = false;
-    for (int k = threadIdx.x; k < args.n_inst; k += blockDim.x) {
-      const ScreenBox bb = args.cull[k * args.n_cams + tp.cam];
-      meets = meets || (bb.x0 <= bb.x1 && bb.x0 < tp.x1 && bb.x1 >= tp.x0 && bb.y0 < tp.y1 && bb.y1 >= tp.y0);
-    }
-    if (!__syncthreads_or(meets)) {
-      if (gid < args.n_rays) args.nhit[gid] = 0;
-      return;
-    }
-  }
+  stat_cta_start();
+  if (MODE == kModeScene && cta_precull(args, gid)) return;
   bool valid = gid < args.n_rays;
   int pix_x = 0, pix_y = 0, cam = 0;
   if (valid) {
-    if (MODE != kModeRays) {
-      long long t = 0, local = gid;
-      if (MODE != kModeRect) split_slot(gid, args.tile_stride, t, local);
-      const TileParams tp = args.tiles[t];
-      const int w = tp.x1 - tp.x0, h = tp.y1 - tp.y0;
-      if (local >= (long long)w * h) {
-        valid = false;
-      } else {
-        cam = tp.cam;
-        if (MODE == kModeScene) {
-          slot_xy(local, w, h, pix_x, pix_y);
-          pix_x += tp.x0;
-          pix_y += tp.y0;
-        } else {
-          pix_x = tp.x0 + (int)(local % w);
-          pix_y = tp.y0 + (int)(local / w);
-        }
-      }
-    }
+    if (MODE != kModeRays) valid = slot_pixel<MODE>(args, gid, pix_x, pix_y, cam);
     if (MODE != kModeScene && valid && args.rgba) {   // miss defaults (lightfield.py:415-416)
       reinterpret_cast<float4 *>(args.rgba)[gid] = make_float4(0.f, 0.f, 0.f, 0.f);
       args.depth[gid] = __int_as_float(0x7f800000);
@@ -331,43 +505,9 @@ __global__ void __launch_bounds__(128, NOLF_MARCH_MINB) k_march(MarchArgs args) 
   }
   unsigned samples_total = 0;  // per lane (< 2^32: at most n_inst * samples per ray)
   unsigned ordinal = 0;
-  // Instances whose conservative screen box covers this lane's pixel, then
-  // OR-ed over the warp so the instance loop below is warp-uniform and only
-  // visits candidates (ascending = scene order, so layer ordinals match).
-  unsigned long long lane_mask = 0;
-  if (MODE == kModeRays || !args.cull) {
-    if (valid) lane_mask = args.n_inst >= 64 ? ~0ull : ((1ull << args.n_inst) - 1ull);
-  } else {
-    const int cmin = __reduce_min_sync(0xffffffffu, valid ? cam : INT_MAX);
-    const int cmax = __reduce_max_sync(0xffffffffu, valid ? cam : -1);
-    if (cmin == cmax) {
-      // one camera for the whole warp: lane k tests instance k's box against
-      // the warp's pixel rectangle, then only the candidates are tested per pixel
-      const int xmin = __reduce_min_sync(0xffffffffu, valid ? pix_x : INT_MAX);
-      const int xmax = __reduce_max_sync(0xffffffffu, valid ? pix_x : INT_MIN);
-      const int ymin = __reduce_min_sync(0xffffffffu, valid ? pix_y : INT_MAX);
-      const int ymax = __reduce_max_sync(0xffffffffu, valid ? pix_y : INT_MIN);
-      for (int base = 0; base < args.n_inst; base += 32) {
-        const int k = base + (int)lane;
-        ScreenBox bb{1, 1, 0, 0};
-        if (k < args.n_inst) bb = args.cull[k * args.n_cams + cmin];
-        unsigned cand = __ballot_sync(0xffffffffu, bb.x0 <= xmax && bb.x1 >= xmin && bb.y0 <= ymax && bb.y1 >= ymin &&
-                                                       bb.x0 <= bb.x1);
-        while (cand) {
-          const int j = __ffs(cand) - 1;
-          cand &= cand - 1;
-          const int x0 = __shfl_sync(0xffffffffu, bb.x0, j), x1 = __shfl_sync(0xffffffffu, bb.x1, j);
-          const int y0 = __shfl_sync(0xffffffffu, bb.y0, j), y1 = __shfl_sync(0xffffffffu, bb.y1, j);
-          if (valid && pix_x >= x0 && pix_x <= x1 && pix_y >= y0 && pix_y <= y1) lane_mask |= 1ull << (base + j);
-        }
-      }
-    } else if (valid) {
-      for (int k = 0; k < args.n_inst; ++k) {
-        const ScreenBox bb = args.cull[k * args.n_cams + cam];
-        if (pix_x >= bb.x0 && pix_x <= bb.x1 && pix_y >= bb.y0 && pix_y <= bb.y1) lane_mask |= 1ull << k;
-      }
-    }
-  }
+  // candidates OR-ed over the warp so the instance loop below is
+  // warp-uniform (ascending = scene order, so layer ordinals match)
+  const unsigned long long lane_mask = candidate_mask<MODE>(args, valid, pix_x, pix_y, cam, lane);
   unsigned long long wmask = ((unsigned long long)__reduce_or_sync(0xffffffffu, (unsigned)(lane_mask >> 32)) << 32) |
                              __reduce_or_sync(0xffffffffu, (unsigned)lane_mask);
   while (wmask) {
@@ -376,63 +516,19 @@ __global__ void __launch_bounds__(128, NOLF_MARCH_MINB) k_march(MarchArgs args) 
     const DevInst &I = args.inst[k];
     const DevAsset &A = *I.a;
     bool hit = false;
-    double o[3], d[3], inv[3], inv_unused[3], t_near = 0, t_far = 0;
+    double o[3], d[3], inv[3];
+    MarchSpan sp{0.0, 0.0, 0.0, 0, false};
     MarchOut mr{0.0, __longlong_as_double(0x7ff0000000000000ll), 0, false};
     const bool live = (lane_mask >> k) & 1ull;
     if (lane == 0) NOLF_STAT(8, 1);
     if (live) {
       NOLF_STAT(0, 1);
-      // world ray, rebuilt per candidate instead of held across the march
-      // (registers): camera ray (core.py:162-170) or the caller's ray
-      double ow[3], dw[3];
-      if (MODE == kModeRays) {
-        const double *op = args.origins + (args.origin_stride ? 3 * gid : 0);
-        ow[0] = op[0]; ow[1] = op[1]; ow[2] = op[2];
-        dw[0] = args.dirs[3 * gid]; dw[1] = args.dirs[3 * gid + 1]; dw[2] = args.dirs[3 * gid + 2];
-      } else {
-        const CamParams &cp = args.cams[cam];
-        camera_dir(cp.pose, cp.fx, cp.fy, cp.cx, cp.cy, (double)pix_x, (double)pix_y, dw);
-        ow[0] = cp.pose[3]; ow[1] = cp.pose[7]; ow[2] = cp.pose[11];
-      }
-      if (args.raw_rays) {
-#pragma unroll
-        for (int q = 0; q < 3; ++q) { o[q] = ow[q]; d[q] = dw[q]; }
-      } else {
-        to_object(I.w2o, ow, dw, o, d);
-      }
-      bool boxhit = slab(A.pmin, A.pmax, o, d, t_near, t_far, inv);
-      if (boxhit && A.mesh.nodes) {          // mesh proxy: march from its first hit
-        const double tm = mesh_first_hit(A.mesh, o, d);
-        if (tm < 0.0) boxhit = false;
-        else t_near = tm;
-      }
-      // Clip the march to the ray's span in the culling box (occupied cells
-      // grown by one cell): every sample outside it lies in an empty cell, so
-      // starting 2 samples before the entry and stopping 2 after the exit
-      // leaves the result bit-identical (empty samples change nothing).
-      int i_start = 0;
-      double t_end = t_far;
-      if (boxhit) NOLF_STAT(1, 1);
-      if (boxhit && t_near < t_far) {
-        double ca, cb;
-        if (!slab(A.cull_lo, A.cull_hi, o, d, ca, cb, inv_unused) || A.cull_empty) {
-          boxhit = false;                     // never meets an occupied cell: exact miss
-        } else {
-          const double f = floor((ca - t_near) / A.step - 2.5);
-          i_start = f > 0.0 ? (f < 2.0e9 ? (int)f : 2000000000) : 0;
-          t_end = cb + 2.0 * A.step;
-        }
-      }
-      if (boxhit) {
+      double ow[3], dw[3];     // rebuilt per candidate instead of held across the march
+      world_ray<MODE>(args, gid, cam, pix_x, pix_y, ow, dw);
+      if (prepare_march(I, A, args.raw_rays, ow, dw, o, d, inv, sp)) {
         NOLF_STAT(2, 1);
         const float invf[3] = {(float)inv[0], (float)inv[1], (float)inv[2]};
-        // every sample the march can visit has index in [i_start, i_hi]
-        const double lim = fmin(t_far, t_end);
-        const double hf = floor((lim - t_near) / A.step) + 2.0;
-        const bool noclip = t_near < lim && hf < 2.0e9 &&
-                            samples_inside_unit(o, d, t_near, A.step, i_start, (int)hf);
-        if (noclip) mr = march_ray<false>(A, o, d, invf, t_near, t_far, args.use_zmask, i_start, t_end);
-        else mr = march_ray<true>(A, o, d, invf, t_near, t_far, args.use_zmask, i_start, t_end);
+        mr = run_march(A, o, d, invf, sp, args.use_zmask);
         samples_total += (unsigned)mr.samples;
         hit = mr.hit;
       }
@@ -457,29 +553,14 @@ __global__ void __launch_bounds__(128, NOLF_MARCH_MINB) k_march(MarchArgs args) 
       base = __shfl_sync(0xffffffffu, base, __ffs(ballot) - 1);
       if (hit) {
         const unsigned pos = base + __popc(ballot & ((1u << lane) - 1u));
-        HitRec rec;
-        double t_obj = mr.t_hit;
-        double p[3];
-        if (A.use_hit_point) {
-#pragma unroll
-          for (int q = 0; q < 3; ++q) p[q] = clamp01(__dadd_rn(o[q], __dmul_rn(t_obj, d[q])));
-        } else {           // ablation: shade at the proxy entry (lightfield.py:438-445)
-          t_obj = t_near;
-#pragma unroll
-          for (int q = 0; q < 3; ++q) p[q] = clamp01(__dadd_rn(o[q], __dmul_rn(t_near, d[q])));
-        }
-        rec.p[0] = p[0]; rec.p[1] = p[1]; rec.p[2] = p[2];
-        rec.alpha_c = mr.alpha_c;
-        rec.t_obj = t_obj;
-        rec.d[0] = d[0]; rec.d[1] = d[1]; rec.d[2] = d[2];
-        rec.out_idx = (uint32_t)gid;
-        rec.ordinal = ordinal;
-        if ((long long)pos < args.qoff[k + 1] - args.qoff[k]) args.queue[args.qoff[k] + pos] = rec;
+        if ((long long)pos < args.qoff[k + 1] - args.qoff[k])
+          args.queue[args.qoff[k] + pos] = hit_record(A, o, d, sp.t_near, mr, (uint32_t)gid, ordinal);
         ++ordinal;
       }
     }
   }
   if (MODE == kModeScene && valid) args.nhit[gid] = (uint8_t)ordinal;
+  stat_cta_end();
   // march_samples counter (lightfield.py:430-431)
   const unsigned warp_samples = __reduce_add_sync(0xffffffffu, samples_total);
   if (lane == 0 && warp_samples && args.counters) atomicAdd(args.counters + 3, (unsigned long long)warp_samples);
@@ -797,6 +878,9 @@ __device__ __forceinline__ void compose_px(const ComposeArgs &a, const long long
   double oc0 = 0.0, oc1 = 0.0, oc2 = 0.0, trans = 1.0;
   bool set = false;
   for (int r = 0; r < n; ++r) {
+    // scene layers: depth inf = a candidate that missed (rgba never written)
+    // or a hit with alpha <= 0 (rgba 0); both sort last and change nothing
+    if (a.nhit && !(dk[r] < __int_as_float(0x7f800000))) break;
     const int k = ord[r];
     const float4 c = reinterpret_cast<const float4 *>(a.rgba)[(long long)k * a.layer_stride + p];
     oc0 = __dadd_rn(oc0, __dmul_rn(trans, (double)c.x));

@@ -96,8 +96,9 @@ class DeviceAsset:
 
     def __del__(self):
         h = getattr(self, "handle", None)
-        if h and N._lib is not None:
-            N._lib.nolf_asset_destroy(h)
+        lib = getattr(N, "_lib", None) if N is not None else None   # None at interpreter exit
+        if h and lib is not None:
+            lib.nolf_asset_destroy(h)
             self.handle = None
 
 
