@@ -53,6 +53,8 @@ def parse():
     p.add_argument("--cpu-seconds", type=float, default=12.0)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-flush", action="store_true",
+                   help="diagnostic only: keep L2 warm between timed steps (not a valid bench line)")
     p.add_argument("--e2e-mode", default="hostmap", choices=["hostmap", "copy"],
                    help="hostmap: compose stores every rank's tiles straight into one shared, "
                         "page-locked host frame (zero-copy, each GPU over its own PCIe link); "
@@ -63,7 +65,7 @@ def parse():
     p.add_argument("--verify", action="store_true",
                    help="rank 0 re-renders the last frame alone and compares bitwise with the "
                         "multi-GPU assembled frame")
-    p.add_argument("--exchange", default="p2p", choices=["p2p", "gather"],
+    p.add_argument("--exchange", default="p2p", choices=["p2p", "dma", "gather"],
                    help="N>1 frame composer: compose stores into rank 0's frame over NVLink "
                         "(CUDA IPC peer memory) or NCCL gather + unpack kernel")
     return p.parse_args()
@@ -283,7 +285,8 @@ def workload_config(args, desc, W, H, n_assets):
             "assets": n_assets, "width": W, "height": H,
             "atlas_b": 32, "atlas_r": 8, "psh_resolution": 64, "mlp": args.mlp,
             "parallelism": f"ray-tile x{args.gpus}", "partition": args.partition,
-            "l2": "flushed between timed steps (256 MiB write)"}
+            "l2": ("NOT flushed (diagnostic run)" if args.no_flush else
+                   "flushed between timed steps (256 MiB write)")}
 
 
 # ------------------------------------------------------------------ our arm
@@ -341,7 +344,11 @@ def run_ours(args):
 
     # ---- p2p frame composer: rank 0 owns the frame buffers, every rank maps
     # them (CUDA IPC) and its compose kernel stores straight into them
-    p2p = world > 1 and args.exchange == "p2p"
+    if args.exchange == "dma" and args.partition != "rows":
+        args.exchange = "p2p"            # strided band copies need the row partition
+    p2p = world > 1 and args.exchange in ("p2p", "dma")
+    dma = p2p and args.exchange == "dma" and rank != 0
+    bands_dev = row_bands(world, rank, n_views, W, H, T) if dma else []
     peer_frames = []
     token = torch.zeros(1, dtype=torch.float32, device=dev)
     if p2p:
@@ -368,10 +375,23 @@ def run_ours(args):
 
     def step(k, fb=0, before_barrier=None):
         if p2p:
-            o2 = {"rgba8": peer_frames[fb][0], "depth16": peer_frames[fb][1],
-                  "counters": out["counters"]}
-            R.render(cam_arrays[k % n_cam], my_tiles, n_max, stride, o2, frame_layout=True,
-                     peer=(rank != 0))
+            if dma:
+                # compose into this GPU's own frame (local HBM stores), then
+                # the copy engine moves its tile-row bands into rank 0's frame
+                # over NVLink (one strided 2-D copy per plane)
+                frame, frame_d = frames[fb]
+                o2 = {"rgba8": frame, "depth16": frame_d, "counters": out["counters"]}
+                R.render(cam_arrays[k % n_cam], my_tiles, n_max, stride, o2, frame_layout=True)
+                for first, wpx, ppx, hgt in bands_dev:
+                    for bpp, dst0, src0 in ((4, peer_frames[fb][0], frame.data_ptr()),
+                                            (2, peer_frames[fb][1], frame_d.data_ptr())):
+                        N.check(N.lib().nolf_memcpy2d_async(dst0 + first * bpp, ppx * bpp, src0 + first * bpp,
+                                                            ppx * bpp, wpx * bpp, hgt, stream))
+            else:
+                o2 = {"rgba8": peer_frames[fb][0], "depth16": peer_frames[fb][1],
+                      "counters": out["counters"]}
+                R.render(cam_arrays[k % n_cam], my_tiles, n_max, stride, o2, frame_layout=True,
+                         peer=(rank != 0))
             if before_barrier is not None:
                 torch.cuda.current_stream().wait_event(before_barrier)
             dist.all_reduce(token)         # every rank's peer stores have landed
@@ -410,7 +430,8 @@ def run_ours(args):
     # the host enqueues every step without waiting (as a serving loop would);
     # each step is bracketed by device events, the L2 flush sits between them
     for k in range(args.steps):
-        flush.fill_(k & 0xFF)                              # evict L2 (untimed)
+        if not args.no_flush:
+            flush.fill_(k & 0xFF)                          # evict L2 (untimed)
         ev[k][0].record()
         step(args.warmup + k)
         ev[k][1].record()
@@ -664,9 +685,12 @@ def run_ours(args):
         }
         line["config"]["parallelism"] = f"ray-tile x{world}"
         if world > 1:
-            line["config"]["exchange"] = ("compose epilogue stores into rank 0's frame over NVLink "
-                                          "(CUDA IPC peer memory) + 1-element NCCL all-reduce"
-                                          if p2p else "NCCL gather of encoded tiles + unpack kernel")
+            line["config"]["exchange"] = (
+                "every rank composes its tile rows locally, the copy engine DMAs them into rank 0's "
+                "frame over NVLink (CUDA IPC, strided 2-D copies) + 1-element NCCL all-reduce"
+                if args.exchange == "dma" else
+                "compose epilogue stores into rank 0's frame over NVLink (CUDA IPC peer memory) "
+                "+ 1-element NCCL all-reduce" if p2p else "NCCL gather of encoded tiles + unpack kernel")
         print(json.dumps(line), flush=True)
     if host_map is not None:
         torch.cuda.synchronize()

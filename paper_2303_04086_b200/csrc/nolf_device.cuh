@@ -236,7 +236,7 @@ __device__ __forceinline__ void atlas_trilinear_at(const DevAtlas &at, int cid, 
   double g[3];
 #pragma unroll
   for (int k = 0; k < 3; ++k) g[k] = __dsub_rn(1.0, frac[k]);
-  if (C == 4) {                // 8 corner loads in flight, then the ordered f64 sum
+  if constexpr (C == 4) {      // 8 corner loads in flight, then the ordered f64 sum
     float4 q[8];
 #pragma unroll
     for (int c = 0; c < 8; ++c)
@@ -252,20 +252,18 @@ __device__ __forceinline__ void atlas_trilinear_at(const DevAtlas &at, int cid, 
     }
 #pragma unroll
     for (int ch = 0; ch < C; ++ch) out[ch] = (float)acc[ch];
-    return;
-  }
+  } else {
 #pragma unroll
-  for (int c = 0; c < 8; ++c) {
-    const int dx = c & 1, dy = (c >> 1) & 1, dz = (c >> 2) & 1;
-    double w = __dmul_rn(__dmul_rn(dx ? frac[0] : g[0], dy ? frac[1] : g[1]), dz ? frac[2] : g[2]);
-    const float *v = cube + (((base[0] + dx) * s + (base[1] + dy)) * s + (base[2] + dz)) * C;
-    {
+    for (int c = 0; c < 8; ++c) {
+      const int dx = c & 1, dy = (c >> 1) & 1, dz = (c >> 2) & 1;
+      const double w = __dmul_rn(__dmul_rn(dx ? frac[0] : g[0], dy ? frac[1] : g[1]), dz ? frac[2] : g[2]);
+      const float *v = cube + (((base[0] + dx) * s + (base[1] + dy)) * s + (base[2] + dz)) * C;
 #pragma unroll
       for (int ch = 0; ch < C; ++ch) acc[ch] = __dadd_rn(acc[ch], __dmul_rn(w, (double)__ldg(v + ch)));
     }
-  }
 #pragma unroll
-  for (int ch = 0; ch < C; ++ch) out[ch] = (float)acc[ch];
+    for (int ch = 0; ch < C; ++ch) out[ch] = (float)acc[ch];
+  }
 }
 
 // query_atlas at an arbitrary point (empty cell -> zeros).
