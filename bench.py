@@ -656,6 +656,22 @@ def run_ours(args):
                        "frac": mlp_tflops / tflops_peak, "flop_per_hit": 11136,
                        "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained"}}
 
+    # DRAM traffic of the dominant kernel from the newest committed ncu
+    # capture of this config (profiles/, `ncu --set full`, per launch)
+    try:
+        import glob
+        caps = sorted(glob.glob(os.path.join(ROOT, "profiles", f"r*_config{args.config}_1gpu*.json")))
+        for path in reversed(caps):
+            kern_caps = json.load(open(path)).get("kernels", {})
+            hit = [v for k, v in kern_caps.items() if k.split("<")[0] == top]
+            if hit:
+                roof["traffic"] = float(hit[0]["dram_bytes_per_launch"])
+                roof["traffic_unit"] = "B/launch (dram__bytes_read.sum + dram__bytes_write.sum)"
+                roof["traffic_source"] = os.path.relpath(path, ROOT)
+                break
+    except (OSError, ValueError, KeyError):
+        pass
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
