@@ -155,6 +155,12 @@ int upload_atlas(NolfAsset *A, const NolfAtlasDesc &d, int channels, DevAtlas *o
   out->cubes = cubes;
   out->zmask = zmp;
   out->zwords = words;
+  auto pow2 = [](int v) { return v > 0 && (v & (v - 1)) == 0; };
+  out->lr = -1;
+  if (pow2(b) && pow2(r) && (int64_t)b * r < (1 << 30)) {
+    out->lr = 0;
+    while ((1 << out->lr) < r) ++out->lr;
+  }
   return 0;
 }
 

@@ -23,6 +23,7 @@ struct DevAtlas {              // CubeAtlas (atlas.py:25-51)
                                // occupied cell, 0 = occupied, capped at 255
   const uint32_t *zmask;       // per cube, r^3 bits: sub-voxel whose 8 corners are all 0
   int zwords;                  // 32-bit words per cube
+  int lr;                      // log2(r) when b and r are both powers of two, else -1
 };
 
 // Fully fused MLP parameter block (neural.py:29-108), fp32, padded:

@@ -96,6 +96,37 @@ __device__ __forceinline__ double sample_cell(const double o[3], const double d[
   return t_mid;
 }
 
+// Power-of-two grids (b = 2^lb, r = 2^lr, the reference defaults 32 / 8):
+// multiplying by b, r or G = b*r is exact, and so is (x*b - cell) (Sterbenz:
+// cell <= x*b < cell+1 <= 2*cell, or cell = 0), hence local = x*G - cell*r
+// EXACTLY.  So with gi = floor(x*G): cell = min(gi >> lr, b-1),
+// base = min(gi - cell*r, r-1), frac = x*G - (cell*r + base), bit-identical
+// to atlas.py:162-172's floor/clip/subtract sequence, in integer ops.
+template <bool CLIP = true>
+__device__ __forceinline__ double sample_grid(const double o[3], const double d[3], double t_near, double delta,
+                                              int i, double G, int lr, int b, double pos[3], int gi[3],
+                                              int cell[3]) {
+  double t_mid = __dadd_rn(t_near, __dmul_rn((double)i + 0.5, delta));
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const double v = __dadd_rn(o[k], __dmul_rn(t_mid, d[k]));
+    pos[k] = CLIP ? clamp01(v) : v;
+    gi[k] = __double2int_rd(__dmul_rn(pos[k], G));
+    cell[k] = min(gi[k] >> lr, b - 1);
+  }
+  return t_mid;
+}
+
+__device__ __forceinline__ void subvoxel_grid(const double pos[3], const int gi[3], const int cell[3], double G,
+                                              int lr, int r, int base[3], double frac[3]) {
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const int c0 = cell[k] << lr;
+    base[k] = min(gi[k] - c0, r - 1);
+    frac[k] = __dsub_rn(__dmul_rn(pos[k], G), (double)(c0 + base[k]));
+  }
+}
+
 // True when the unclipped positions of samples lo and hi are inside [0,1]^3:
 // each coordinate fl(o + fl(t_mid*d)) is monotone in the sample index, so all
 // samples between them are inside too and clip() is exactly the identity.
@@ -177,7 +208,7 @@ struct MarchOut {
   bool hit;
 };
 
-template <bool CLIP>
+template <bool CLIP, bool POW2>
 __device__ __forceinline__ MarchOut march_ray(const DevAsset &A, const double o[3], const double d[3],
                                               const float invf[3], double t_near, double t_far, bool use_zmask,
                                               int i_start, double t_end) {
@@ -198,13 +229,16 @@ __device__ __forceinline__ MarchOut march_ray(const DevAsset &A, const double o[
   const double t_lim = fmin(t_far, t_end);
   const double t_stop = A.t_stop;
   int i = i_start;
+  const int lr = at.lr;
+  const double G = (double)(b * at.r);
 #if defined(NOLF_STATS) && defined(NOLF_STATS_CTR)
   unsigned iters_dbg = 0;
 #endif
   for (;;) {
     double pos[3];
-    int cell[3];
-    const double t_mid = sample_cell<CLIP>(o, d, t_near, delta, i, b, pos, cell);
+    int cell[3], gi[3];
+    const double t_mid = POW2 ? sample_grid<CLIP>(o, d, t_near, delta, i, G, lr, b, pos, gi, cell)
+                              : sample_cell<CLIP>(o, d, t_near, delta, i, b, pos, cell);
     if (!(t_mid < t_lim)) break;
     NOLF_STAT(7, 1);
 #if defined(NOLF_STATS) && defined(NOLF_STATS_CTR)
@@ -247,7 +281,9 @@ __device__ __forceinline__ MarchOut march_ray(const DevAsset &A, const double o[
       for (int attempt = 0; attempt < 2 && j > i; ++attempt, --j) {
         double pj[3];
         int cj[3];
-        double tj = sample_cell<CLIP>(o, d, t_near, delta, j, b, pj, cj);
+        int gj[3];
+        double tj = POW2 ? sample_grid<CLIP>(o, d, t_near, delta, j, G, lr, b, pj, gj, cj)
+                         : sample_cell<CLIP>(o, d, t_near, delta, j, b, pj, cj);
         bool inside = tj < t_lim;
 #pragma unroll
         for (int k = 0; k < 3; ++k) inside = inside && cj[k] >= lo_c[k] && cj[k] <= hi_c[k];
@@ -260,8 +296,9 @@ __device__ __forceinline__ MarchOut march_ray(const DevAsset &A, const double o[
     // absorb = exp(-0) = 1, w = 0 -- only the active-sample count changes
     int base[3];
     double frac[3];
-    atlas_subvoxel_in(at, pos, cell, base, frac);
-    const int bit = (base[0] * at.r + base[1]) * at.r + base[2];
+    if (POW2) subvoxel_grid(pos, gi, cell, G, lr, at.r, base, frac);
+    else atlas_subvoxel_in(at, pos, cell, base, frac);
+    const int bit = POW2 ? (((base[0] << lr) + base[1]) << lr) + base[2] : (base[0] * at.r + base[1]) * at.r + base[2];
     ++samples;
     if (use_zmask && ((__ldg(at.zmask + (unsigned)(cid * at.zwords + (bit >> 5))) >> (bit & 31)) & 1u)) {
       NOLF_STAT(5, 1);
@@ -466,8 +503,12 @@ __device__ __forceinline__ bool prepare_march(const DevInst &I, const DevAsset &
 
 __device__ __forceinline__ MarchOut run_march(const DevAsset &A, const double o[3], const double d[3],
                                               const float invf[3], const MarchSpan &sp, bool use_zmask) {
-  if (sp.noclip) return march_ray<false>(A, o, d, invf, sp.t_near, sp.t_far, use_zmask, sp.i_start, sp.t_end);
-  return march_ray<true>(A, o, d, invf, sp.t_near, sp.t_far, use_zmask, sp.i_start, sp.t_end);
+  if (A.den.lr >= 0) {         // power-of-two grid: integer sub-voxel addressing
+    if (sp.noclip) return march_ray<false, true>(A, o, d, invf, sp.t_near, sp.t_far, use_zmask, sp.i_start, sp.t_end);
+    return march_ray<true, true>(A, o, d, invf, sp.t_near, sp.t_far, use_zmask, sp.i_start, sp.t_end);
+  }
+  if (sp.noclip) return march_ray<false, false>(A, o, d, invf, sp.t_near, sp.t_far, use_zmask, sp.i_start, sp.t_end);
+  return march_ray<true, false>(A, o, d, invf, sp.t_near, sp.t_far, use_zmask, sp.i_start, sp.t_end);
 }
 
 // Hit record for the shading pass (lightfield.py:433-445).
