@@ -886,11 +886,11 @@ int launch_march_shade(int mode, const NolfInstance *ins, int n_inst, const Nolf
   ma.depth = depth;
   ma.nhit = w.nhit;
   ma.counters = counters;
-  const unsigned grid = (unsigned)((n_rays + 127) / 128);
+  const unsigned grid = (unsigned)((n_rays + kMarchThreads - 1) / kMarchThreads);
   if ((rc = prof_mark(0, st))) return rc;
-  if (mode == kModeRays) k_march<kModeRays><<<grid, 128, 0, st>>>(ma);
-  else if (mode == kModeRect) k_march<kModeRect><<<grid, 128, 0, st>>>(ma);
-  else k_march<kModeScene><<<grid, 128, 0, st>>>(ma);
+  if (mode == kModeRays) k_march<kModeRays><<<grid, kMarchThreads, 0, st>>>(ma);
+  else if (mode == kModeRect) k_march<kModeRect><<<grid, kMarchThreads, 0, st>>>(ma);
+  else k_march<kModeScene><<<grid, kMarchThreads, 0, st>>>(ma);
   CUDA_TRY(cudaGetLastError());
   if ((rc = prof_mark(1, st))) return rc;
   if (mode == kModeScene) {

@@ -181,7 +181,11 @@ __device__ __forceinline__ void slot_xy(long long local, int w, int h, int &x, i
 
 // (tile, local slot) of packed index p; 32-bit divide when it fits.
 __device__ __forceinline__ void split_slot(long long p, long long stride, long long &t, long long &local) {
-  if (p < 0xffffffffll && stride < 0xffffffffll) {
+  if ((stride & (stride - 1)) == 0) {          // power-of-two tiles (32x32 = 1024 slots): shift
+    const int sh = __ffsll(stride) - 1;
+    t = p >> sh;
+    local = p & (stride - 1);
+  } else if (p < 0xffffffffll && stride < 0xffffffffll) {
     const unsigned p32 = (unsigned)p, s32 = (unsigned)stride, t32 = p32 / s32;
     t = t32;
     local = p32 - t32 * s32;
@@ -351,16 +355,18 @@ __device__ __forceinline__ void stat_cta_start() {}
 __device__ __forceinline__ void stat_cta_end() {}
 #endif
 
+constexpr int kMarchThreads = 128;   // k_march CTA size (launch uses the same)
+
 // CTA-level pre-cull (scene mode): all of the CTA's slots lie in one tile;
 // when no instance's screen box meets the tile every pixel is a miss.  Returns
 // true when the CTA is done (nhit = 0 written).
 __device__ __forceinline__ bool cta_precull(const MarchArgs &args, long long gid) {
-  if (!args.cull || args.tile_stride % blockDim.x != 0) return false;
+  if (!args.cull || args.tile_stride % kMarchThreads != 0) return false;
   long long t, local0;
-  split_slot((long long)blockIdx.x * blockDim.x, args.tile_stride, t, local0);
+  split_slot((long long)blockIdx.x * kMarchThreads, args.tile_stride, t, local0);
   const TileParams tp = args.tiles[t];
   bool meets = false;
-  for (int k = threadIdx.x; k < args.n_inst; k += blockDim.x) {
+  for (int k = threadIdx.x; k < args.n_inst; k += kMarchThreads) {
     const ScreenBox bb = args.cull[k * args.n_cams + tp.cam];
     meets = meets || (bb.x0 <= bb.x1 && bb.x0 < tp.x1 && bb.x1 >= tp.x0 && bb.y0 < tp.y1 && bb.y1 >= tp.y0);
   }
@@ -530,8 +536,8 @@ __device__ __forceinline__ HitRec hit_record(const DevAsset &A, const double o[3
 // One thread per ray, every candidate instance marched in scene order by
 // that thread (kModeRays / kModeRect, and the march_rays entry point).
 template <int MODE>
-__global__ void __launch_bounds__(128, NOLF_MARCH_MINB) k_march(MarchArgs args) {
-  const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+__global__ void __launch_bounds__(kMarchThreads, NOLF_MARCH_MINB) k_march(MarchArgs args) {
+  const long long gid = (long long)blockIdx.x * kMarchThreads + threadIdx.x;
   const unsigned lane = threadIdx.x & 31;
   stat_cta_start();
   if (MODE == kModeScene && cta_precull(args, gid)) return;
