@@ -342,7 +342,9 @@ int ensure_attrs() {
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
 struct Workspace {
-  unsigned int *counts;
+  unsigned int *counts;        // per-instance hit counts, then [n_inst]: live chunks, [n_inst+1]: fetch
+  unsigned int *chunk_list;    // scene: live 128-slot chunks
+  uint8_t *chunk_live;
   HitRec *queue;
   uint8_t *nhit;
   float *lrgba, *ldepth;
@@ -359,13 +361,18 @@ size_t ws_layout(int n_inst, long long queue_recs, int layers, long long P, char
     return base ? base + o : nullptr;
   };
   const size_t n = (size_t)(P > 0 ? P : 1);
-  char *counts = take(sizeof(unsigned) * (size_t)(n_inst > 0 ? n_inst : 1));
+  char *counts = take(sizeof(unsigned) * (size_t)((n_inst > 0 ? n_inst : 1) + 2));
+  const size_t n_chunks = (size_t)((P > 0 ? P : 1) + 127) / 128;
+  char *chunk_list = take(sizeof(unsigned) * n_chunks);
+  char *chunk_live = take(n_chunks);
   char *queue = take(sizeof(HitRec) * (size_t)(queue_recs > 0 ? queue_recs : 1));
   char *nhit = take(layers > 0 ? n : 1);
   char *lrgba = take(sizeof(float) * 4 * n * (size_t)layers);
   char *ldepth = take(sizeof(float) * n * (size_t)layers);
   if (w) {
     w->counts = reinterpret_cast<unsigned *>(counts);
+    w->chunk_list = reinterpret_cast<unsigned *>(chunk_list);
+    w->chunk_live = reinterpret_cast<uint8_t *>(chunk_live);
     w->queue = reinterpret_cast<HitRec *>(queue);
     w->nhit = reinterpret_cast<uint8_t *>(nhit);
     w->lrgba = reinterpret_cast<float *>(lrgba);
@@ -864,7 +871,7 @@ int launch_march_shade(int mode, const NolfInstance *ins, int n_inst, const Nolf
   CUDA_TRY(cudaMemcpyAsync(dp, hp, param_bytes(n_inst, n_cams), cudaMemcpyHostToDevice, st));
   if ((rc = ring_release(slot, st))) return rc;
   if (n_rays == 0) return 0;
-  CUDA_TRY(cudaMemsetAsync(w.counts, 0, sizeof(unsigned) * n_inst, st));
+  CUDA_TRY(cudaMemsetAsync(w.counts, 0, sizeof(unsigned) * (n_inst + 2), st));
 
   MarchArgs ma{};
   ma.inst = dp->inst;
@@ -887,10 +894,21 @@ int launch_march_shade(int mode, const NolfInstance *ins, int n_inst, const Nolf
   ma.nhit = w.nhit;
   ma.counters = counters;
   const unsigned grid = (unsigned)((n_rays + kMarchThreads - 1) / kMarchThreads);
+  const bool chunked = mode == kModeScene && n_cams > 0 && tile_stride % kMarchThreads == 0;
   if ((rc = prof_mark(0, st))) return rc;
   if (mode == kModeRays) k_march<kModeRays><<<grid, kMarchThreads, 0, st>>>(ma);
   else if (mode == kModeRect) k_march<kModeRect><<<grid, kMarchThreads, 0, st>>>(ma);
-  else k_march<kModeScene><<<grid, kMarchThreads, 0, st>>>(ma);
+  else if (!chunked) k_march<kModeScene><<<grid, kMarchThreads, 0, st>>>(ma);
+  else {                       // compact the live chunks, then a persistent marcher drains them
+    const long long n_chunks = n_rays / kMarchThreads;
+    ma.chunks = w.chunk_list;
+    ma.n_chunks = w.counts + n_inst;
+    ma.fetch = w.counts + n_inst + 1;
+    k_cull_chunks<<<(unsigned)((n_chunks + 127) / 128), 128, 0, st>>>(ma, n_chunks, w.chunk_live, w.chunk_list,
+                                                                      w.counts + n_inst);
+    CUDA_TRY(cudaGetLastError());
+    k_march_chunks<<<(unsigned)n_chunks, kMarchThreads, 0, st>>>(ma);
+  }
   CUDA_TRY(cudaGetLastError());
   if ((rc = prof_mark(1, st))) return rc;
   if (mode == kModeScene) {
@@ -916,6 +934,7 @@ int launch_march_shade(int mode, const NolfInstance *ins, int n_inst, const Nolf
     ca.out_rgba8 = sout->rgba8;
     ca.out_depth16 = sout->depth16;
     ca.depth_far = (float)sout->depth_far;
+    ca.chunk_live = chunked ? w.chunk_live : nullptr;
     ca.four = (tile_stride % 4 == 0 && n_rays % 4 == 0 && ((uintptr_t)w.nhit & 3) == 0 &&
                ((uintptr_t)sout->rgba8 & 15) == 0 && ((uintptr_t)sout->depth16 & 7) == 0) ? 1 : 0;
     const long long n_thr = ca.four ? n_rays / 4 : n_rays;

@@ -61,6 +61,12 @@ struct MarchArgs {
   uint8_t *out_hit;
   double *out_t_hit, *out_alpha_c, *out_p_h;
   long long *out_samples;
+  // scene mode with 128-slot-aligned tiles: compacted list of the chunks
+  // (128 consecutive slots of one tile) some screen box meets, and the
+  // persistent marcher's work counter
+  const unsigned *chunks;
+  const unsigned *n_chunks;
+  unsigned *fetch;
 };
 
 // Exit parameter of an axis-aligned box [lo, hi] (object coords) along the
@@ -536,11 +542,10 @@ __device__ __forceinline__ HitRec hit_record(const DevAsset &A, const double o[3
 // One thread per ray, every candidate instance marched in scene order by
 // that thread (kModeRays / kModeRect, and the march_rays entry point).
 template <int MODE>
-__global__ void __launch_bounds__(kMarchThreads, NOLF_MARCH_MINB) k_march(MarchArgs args) {
-  const long long gid = (long long)blockIdx.x * kMarchThreads + threadIdx.x;
+__device__ __forceinline__ void march_chunk(const MarchArgs &args, unsigned chunk, bool precull) {
+  const long long gid = (long long)chunk * kMarchThreads + threadIdx.x;
   const unsigned lane = threadIdx.x & 31;
-  stat_cta_start();
-  if (MODE == kModeScene && cta_precull(args, gid)) return;
+  if (MODE == kModeScene && precull && cta_precull(args, gid)) return;
   bool valid = gid < args.n_rays;
   int pix_x = 0, pix_y = 0, cam = 0;
   if (valid) {
@@ -607,10 +612,71 @@ __global__ void __launch_bounds__(kMarchThreads, NOLF_MARCH_MINB) k_march(MarchA
     }
   }
   if (MODE == kModeScene && valid) args.nhit[gid] = (uint8_t)ordinal;
-  stat_cta_end();
   // march_samples counter (lightfield.py:430-431)
   const unsigned warp_samples = __reduce_add_sync(0xffffffffu, samples_total);
   if (lane == 0 && warp_samples && args.counters) atomicAdd(args.counters + 3, (unsigned long long)warp_samples);
+}
+
+// One CTA per 128 slots (rays / rect mode, and scene tiles that are not
+// 128-slot aligned: those pre-cull per CTA).
+template <int MODE>
+__global__ void __launch_bounds__(kMarchThreads, NOLF_MARCH_MINB) k_march(MarchArgs args) {
+  stat_cta_start();
+  march_chunk<MODE>(args, blockIdx.x, true);
+  stat_cta_end();
+}
+
+// Scene chunks (128 slots of one tile) that some instance's screen box
+// meets, compacted into a work list; every other chunk is a miss and is
+// never launched (k_compose reads chunk_live instead of its layer counts).
+__global__ void __launch_bounds__(128) k_cull_chunks(MarchArgs args, long long n_chunks, uint8_t *chunk_live,
+                                                     unsigned *list, unsigned *count) {
+  const long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  bool live = false;
+  if (c < n_chunks) {
+    long long t, local0;
+    split_slot(c * kMarchThreads, args.tile_stride, t, local0);
+    const TileParams tp = args.tiles[t];
+    const int w = tp.x1 - tp.x0, h = tp.y1 - tp.y0;
+    if (local0 < (long long)w * h) {
+      // pixel rectangle of the chunk's valid slots: the bbox of the slot
+      // positions at every 8x4-block start/end (row-major tiles: the rows)
+      const long long l1 = min(local0 + kMarchThreads, (long long)w * h) - 1;
+      int xa = INT_MAX, xb = INT_MIN, ya = INT_MAX, yb = INT_MIN;
+      for (long long l = local0; l <= l1; l += 32) {
+        int x, y;
+        slot_xy(min(l, l1), w, h, x, y);
+        xa = min(xa, x); xb = max(xb, x); ya = min(ya, y); yb = max(yb, y);
+        slot_xy(min((l | 31), l1), w, h, x, y);
+        xa = min(xa, x); xb = max(xb, x); ya = min(ya, y); yb = max(yb, y);
+      }
+      if (yb > ya && !((w & 7) == 0 && (h & 3) == 0)) { xa = 0; xb = w - 1; }   // row-major: rows span the width
+      xa += tp.x0; xb += tp.x0; ya += tp.y0; yb += tp.y0;
+      for (int k = 0; k < args.n_inst && !live; ++k) {
+        const ScreenBox bb = args.cull[k * args.n_cams + tp.cam];
+        live = bb.x0 <= bb.x1 && bb.x0 <= xb && bb.x1 >= xa && bb.y0 <= yb && bb.y1 >= ya;
+      }
+    }
+    chunk_live[c] = live ? 1 : 0;
+  }
+  const unsigned ballot = __ballot_sync(0xffffffffu, live);
+  if (ballot) {
+    const unsigned lane = threadIdx.x & 31;
+    unsigned base = 0;
+    if (lane == __ffs(ballot) - 1) base = atomicAdd(count, (unsigned)__popc(ballot));
+    base = __shfl_sync(0xffffffffu, base, __ffs(ballot) - 1);
+    if (live) list[base + __popc(ballot & ((1u << lane) - 1u))] = (unsigned)c;
+  }
+}
+
+// Scene marcher over the compacted live chunks: one CTA per list entry; the
+// grid is sized for the worst case (every chunk live) and the CTAs past the
+// list's length exit after one load (no tile lookups, no culling, no barrier).
+__global__ void __launch_bounds__(kMarchThreads, NOLF_MARCH_MINB) k_march_chunks(MarchArgs args) {
+  if (blockIdx.x >= *args.n_chunks) return;
+  stat_cta_start();
+  march_chunk<kModeScene>(args, args.chunks[blockIdx.x], false);
+  stat_cta_end();
 }
 
 // ---------------------------------------------------------------- shading
@@ -899,6 +965,7 @@ struct ComposeArgs {
   uint16_t *out_depth16;
   float depth_far;
   int four;                    // 4 slots per thread (tiles && nhit && tile_stride % 4 == 0)
+  const uint8_t *chunk_live;   // scene: per 128-slot chunk, 0 = never marched (all misses)
 };
 
 constexpr int kMaxLayers = 64;
@@ -991,7 +1058,8 @@ __device__ __forceinline__ void compose_one(const ComposeArgs &a, const long lon
   }
   float4 o;
   float od;
-  compose_px(a, p, a.nhit ? (int)a.nhit[p] : a.K, o, od);
+  const bool skip = a.chunk_live && !a.chunk_live[p >> 7];
+  compose_px(a, p, skip ? 0 : (a.nhit ? (int)a.nhit[p] : a.K), o, od);
   compose_store(a, q, o, od);
 }
 
@@ -1003,7 +1071,8 @@ __device__ __forceinline__ void compose_four(const ComposeArgs &a, const long lo
   long long t, local0;
   split_slot(p0, a.tile_stride, t, local0);
   const TileParams tp = a.tiles[t];
-  const uchar4 nh = *reinterpret_cast<const uchar4 *>(a.nhit + p0);
+  const uchar4 nh = (a.chunk_live && !a.chunk_live[p0 >> 7]) ? make_uchar4(0, 0, 0, 0)
+                                                                : *reinterpret_cast<const uchar4 *>(a.nhit + p0);
   const int ns[4] = {nh.x, nh.y, nh.z, nh.w};
   long long q[4];
 #pragma unroll
