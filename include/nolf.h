@@ -134,9 +134,11 @@ typedef struct NolfTile {              /* RayRange rect of one camera */
 } NolfTile;
 
 /* Scene output.  layout 0 writes pixels in TILE-PACKED order: tile t (in the
- * order given) owns pixels [t*tile_stride, t*tile_stride + w_t*h_t), row-major
- * inside the tile (the unit the multi-GPU gather moves); layout 1 writes the
- * row-major frame of each camera.  Any pointer may be NULL to skip it. */
+ * order given) owns slots [t*tile_stride, t*tile_stride + w_t*h_t); inside a
+ * tile whose sides are multiples of 8x4 the slots run over 8x4 pixel blocks
+ * (block-row-major, row-major inside a block), other tiles are row-major
+ * (render.slot_xy / unpack_index); layout 1 writes the row-major frame of
+ * each camera.  Any pointer may be NULL to skip it. */
 typedef struct NolfSceneOut {
     float *rgba;                       /* (.., 4) f32, farm.compose Frame.rgba */
     float *depth;                      /* f32, inf = miss */
@@ -155,6 +157,13 @@ int nolf_abi_version(void);
 const char *nolf_last_error(void);
 
 int nolf_asset_create(const NolfAssetDesc *desc, int device, nolf_asset_t *out);
+/* assetio.read_asset (assetio.py:174-255) natively: the ``.nolf`` container
+ * (optionally gzip-compressed) is parsed, every section's CRC32 checked, the
+ * JSON meta decoded and the asset uploaded; object_to_world (may be NULL)
+ * receives the stored transform (row-major 4x4).  Corrupt input ->
+ * NOLF_EDATA (DataError). */
+int nolf_asset_load(const char *path, int device, nolf_asset_t *out, double object_to_world[16]);
+int nolf_asset_load_mem(const void *data, size_t n, int device, nolf_asset_t *out, double object_to_world[16]);
 int nolf_asset_destroy(nolf_asset_t asset);
 int nolf_asset_set_mlp_mode(nolf_asset_t asset, int mode);
 int64_t nolf_asset_device_bytes(nolf_asset_t asset);

@@ -19,7 +19,7 @@ def __getattr__(name):
     # render entry points import torch lazily (first import can be slow)
     if name in ("render_rays", "render_ray", "render_range", "render_frame", "compose",
                 "compose_device", "render_scene", "SceneRenderer", "frame_tiles", "device_asset",
-                "invalidate", "unpack_index", "slot_xy"):
+                "invalidate", "unpack_index", "slot_xy", "load_device_asset"):
         from . import render
         return getattr(render, name)
     raise AttributeError(name)

@@ -87,6 +87,8 @@ def lib():
         "nolf_abi_version": ([], C.c_int),
         "nolf_last_error": ([], C.c_char_p),
         "nolf_asset_create": ([C.POINTER(AssetDesc), C.c_int, C.POINTER(vp)], C.c_int),
+        "nolf_asset_load": ([C.c_char_p, C.c_int, C.POINTER(vp), C.POINTER(C.c_double)], C.c_int),
+        "nolf_asset_load_mem": ([C.c_char_p, C.c_size_t, C.c_int, C.POINTER(vp), C.POINTER(C.c_double)], C.c_int),
         "nolf_asset_destroy": ([vp], C.c_int),
         "nolf_asset_set_mlp_mode": ([vp, C.c_int], C.c_int),
         "nolf_asset_device_bytes": ([vp], i64),

@@ -12,6 +12,7 @@
 
 #include "../../include/nolf.h"
 #include "nolf_kernels.cuh"
+#include "nolf_load.h"
 #include "nolf_shade_tc.cuh"
 
 using namespace nolf;
@@ -1224,3 +1225,189 @@ extern "C" int nolf_stats_read(unsigned long long *out, int reset) {
   return (int)cudaGetLastError();
 }
 #endif
+
+// ---------------------------------------------------------------- native .nolf loading
+// assetio.read_asset (assetio.py:174-255) without Python: container, CRC32,
+// gzip, meta JSON -> NolfAssetDesc -> nolf_asset_create.
+extern "C" int nolf_asset_load_mem(const void *data, size_t n, int device, nolf_asset_t *out,
+                                   double object_to_world[16]) {
+  using namespace nolf_load;
+  if (!data || !out) return fail(NOLF_EINVAL, "null argument");
+  *out = nullptr;
+  Container c;
+  std::string err;
+  if (!parse_container(std::vector<uint8_t>(static_cast<const uint8_t *>(data), static_cast<const uint8_t *>(data) + n),
+                       c, err))
+    return fail(NOLF_EDATA, "%s", err.c_str());
+  const Json &m = c.meta;
+  auto bad = [&](const char *what) { return fail(NOLF_EDATA, "bad asset meta: %s", what); };
+  NolfAssetDesc d{};
+  // keep-alive storage for the aligned copies handed to nolf_asset_create
+  std::vector<int32_t> den_index, dif_index, tris;
+  std::vector<float> den_cubes, dif_cubes, feats;
+  std::vector<int64_t> offsets;
+  std::vector<double> verts;
+  std::vector<std::vector<float>> hg, mw;
+
+  auto atlas = [&](const char *key, const char *tag, int ch, NolfAtlasDesc &a, std::vector<int32_t> &idx,
+                   std::vector<float> &cubes) -> int {
+    const Json *j = m.get(key);
+    int64_t b, r, nc;
+    if (!inum(j ? j->get("b") : nullptr, b) || !inum(j->get("r"), r) || !inum(j->get("cubes"), nc) || b < 1 || r < 1 ||
+        nc < 0)
+      return bad(key);
+    const size_t s1 = (size_t)r + 1;
+    if (!aligned(c, std::string(tag) + "_index", (size_t)(b * b * b), idx, err) ||
+        !aligned(c, std::string(tag) + "_cubes", (size_t)nc * s1 * s1 * s1 * (size_t)ch, cubes, err))
+      return fail(NOLF_EDATA, "%s", err.c_str());
+    a.b = (int32_t)b;
+    a.r = (int32_t)r;
+    a.channels = ch;
+    a.n_cubes = nc;
+    a.index = idx.data();
+    a.cubes = cubes.empty() ? nullptr : cubes.data();
+    return 0;
+  };
+  int rc;
+  if ((rc = atlas("density_atlas", "den", 1, d.density, den_index, den_cubes))) return rc;
+  if (flag(m.get("has_diffuse_atlas"), false)) {
+    d.has_diffuse_atlas = 1;
+    if ((rc = atlas("diffuse_atlas", "dif", 4, d.diffuse, dif_index, dif_cubes))) return rc;
+  }
+  // PSH (assetio.py: psh meta + psh_offsets int64 + psh_features f32)
+  const Json *pm = m.get("psh");
+  int64_t res, tsz, osz, F;
+  if (!pm || !inum(pm->get("resolution"), res) || !inum(pm->get("table_size"), tsz) ||
+      !inum(pm->get("offset_size"), osz) || !inum(pm->get("features"), F) || F < 1)
+    return bad("psh");
+  const Json *p0 = pm->get("primes_h0"), *p1 = pm->get("primes_h1");
+  if (!p0 || !p1 || p0->kind != Json::Arr || p1->kind != Json::Arr || p0->arr.size() != 3 || p1->arr.size() != 3)
+    return bad("psh primes");
+  for (int k = 0; k < 3; ++k) {
+    int64_t a, b;
+    if (!inum(&p0->arr[k], a) || !inum(&p1->arr[k], b) || a < 0 || b < 0) return bad("psh primes");
+    d.primes_h0[k] = (uint64_t)a;
+    d.primes_h1[k] = (uint64_t)b;
+  }
+  if (!aligned(c, "psh_offsets", (size_t)osz, offsets, err) || !aligned(c, "psh_features", (size_t)(tsz * F), feats, err))
+    return fail(NOLF_EDATA, "%s", err.c_str());
+  d.psh_resolution = (int32_t)res;
+  d.psh_table_size = tsz;
+  d.psh_offset_size = osz;
+  d.psh_offsets = offsets.data();
+  d.psh_features = feats.data();
+  d.psh_features_dim = (int32_t)F;
+  // hash-grid diffuse encoder (encoding.py:415-424 resolutions / dense rows)
+  const Json *em = m.get("diffuse_encoder");
+  int64_t lv, base, hts, fpl;
+  double growth;
+  if (!em || !inum(em->get("levels"), lv) || !inum(em->get("base_resolution"), base) || !num(em->get("growth"), growth) ||
+      !inum(em->get("table_size"), hts) || !inum(em->get("features_per_level"), fpl) || lv < 0 || lv > 16)
+    return bad("diffuse_encoder");
+  d.hg_levels = (int32_t)lv;
+  d.hg_features = (int32_t)fpl;
+  d.hg_table_size = hts;
+  hg.resize((size_t)lv);
+  for (int l = 0; l < lv; ++l) {
+    const int64_t nres = std::max<int64_t>(2, (int64_t)std::floor((double)base * std::pow(growth, (double)l)));
+    const bool dense = (nres + 1) * (nres + 1) * (nres + 1) <= hts;
+    const int64_t rows = dense ? (nres + 1) * (nres + 1) * (nres + 1) : hts;
+    if (!aligned(c, "ed_feat_" + std::to_string(l), (size_t)(rows * fpl), hg[(size_t)l], err))
+      return fail(NOLF_EDATA, "%s", err.c_str());
+    d.hg_resolution[l] = (int32_t)nres;
+    d.hg_dense[l] = dense ? 1 : 0;
+    d.hg_rows[l] = rows;
+    d.hg_feat[l] = hg[(size_t)l].data();
+  }
+  // MLPs (assetio.py mlp meta: widths + heads; sections {tag}_w{i} (out,in), {tag}_b{i})
+  mw.reserve(16);
+  auto mlp = [&](const char *key, const char *tag, NolfMlpDesc &md) -> int {
+    const Json *j = m.get(key);
+    const Json *w = j ? j->get("widths") : nullptr, *h = j ? j->get("heads") : nullptr;
+    if (!w || w->kind != Json::Arr || w->arr.size() < 2 || w->arr.size() > 5 || !h || h->kind != Json::Arr ||
+        h->arr.size() > 8)
+      return bad(key);
+    int64_t wd[5];
+    for (size_t i = 0; i < w->arr.size(); ++i)
+      if (!inum(&w->arr[i], wd[i]) || wd[i] < 1) return bad(key);
+    md.n_layers = (int32_t)w->arr.size() - 1;
+    md.widths[0] = (int32_t)wd[0];
+    for (int i = 0; i < md.n_layers; ++i) {
+      mw.emplace_back();
+      std::vector<float> &W = mw.back();
+      if (!aligned(c, std::string(tag) + "_w" + std::to_string(i), (size_t)(wd[i + 1] * wd[i]), W, err))
+        return fail(NOLF_EDATA, "%s", err.c_str());
+      mw.emplace_back();
+      std::vector<float> &B = mw.back();
+      if (!aligned(c, std::string(tag) + "_b" + std::to_string(i), (size_t)wd[i + 1], B, err))
+        return fail(NOLF_EDATA, "%s", err.c_str());
+      md.widths[i + 1] = (int32_t)wd[i + 1];
+      md.w[i] = mw[mw.size() - 2].data();
+      md.b[i] = B.data();
+    }
+    md.n_heads = (int32_t)h->arr.size();
+    for (size_t i = 0; i < h->arr.size(); ++i) {
+      const Json &e = h->arr[i];
+      int64_t hw;
+      if (e.kind != Json::Arr || e.arr.size() != 2 || e.arr[0].kind != Json::Str || !inum(&e.arr[1], hw))
+        return bad(key);
+      const std::string &act = e.arr[0].str;
+      md.head_act[i] = act == "identity" ? NOLF_HEAD_IDENTITY : act == "sigmoid" ? NOLF_HEAD_SIGMOID
+                     : act == "exponential" ? NOLF_HEAD_EXP : -1;
+      if (md.head_act[i] < 0) return bad("head activation");
+      md.head_w[i] = (int32_t)hw;
+    }
+    return 0;
+  };
+  if ((rc = mlp("specular_mlp", "fs", d.specular)) || (rc = mlp("diffuse_mlp", "fd", d.diffuse_mlp))) return rc;
+  // march params, proxy, wiring, transform
+  const Json *mm = m.get("march");
+  if (!mm || !num(mm->get("step"), d.step) || !num(mm->get("t_stop"), d.t_stop) ||
+      !num(mm->get("alpha_floor"), d.alpha_floor))
+    return bad("march");
+  const Json *px = m.get("proxy");
+  const Json *pmin = px ? px->get("min") : nullptr, *pmax = px ? px->get("max") : nullptr;
+  if (!pmin || !pmax || pmin->kind != Json::Arr || pmax->kind != Json::Arr || pmin->arr.size() != 3 ||
+      pmax->arr.size() != 3)
+    return bad("proxy");
+  for (int k = 0; k < 3; ++k)
+    if (!num(&pmin->arr[k], d.proxy_min[k]) || !num(&pmax->arr[k], d.proxy_max[k])) return bad("proxy");
+  const Json *wi = m.get("wiring");
+  d.use_hit_point = flag(wi ? wi->get("use_hit_point") : nullptr, true);
+  d.use_opacity = flag(wi ? wi->get("use_opacity") : nullptr, true);
+  d.refine_opacity = flag(wi ? wi->get("refine_opacity") : nullptr, true);
+  d.use_tint = flag(wi ? wi->get("use_tint") : nullptr, true);
+  d.use_diffuse_color = flag(wi ? wi->get("use_diffuse_color") : nullptr, true);
+  const Json *tf = m.get("transform");
+  if (!tf || tf->kind != Json::Arr || tf->arr.size() != 16) return bad("transform");
+  double o2w[16];
+  for (int k = 0; k < 16; ++k)
+    if (!num(&tf->arr[k], o2w[k])) return bad("transform");
+  if (const Json *pm2 = m.get("proxy_mesh")) {   // extension sections (nolf_io.py), absent in reference files
+    int64_t nv, nt;
+    if (!inum(pm2->get("vertices"), nv) || !inum(pm2->get("triangles"), nt) || nv < 0 || nt < 0) return bad("proxy_mesh");
+    if (!aligned(c, "mesh_vertices", (size_t)nv * 3, verts, err) || !aligned(c, "mesh_triangles", (size_t)nt * 3, tris, err))
+      return fail(NOLF_EDATA, "%s", err.c_str());
+    d.mesh_vertices = verts.data();
+    d.mesh_n_vertices = nv;
+    d.mesh_triangles = tris.data();
+    d.mesh_n_triangles = nt;
+  }
+  if ((rc = nolf_asset_create(&d, device, out))) return rc;
+  if (object_to_world) memcpy(object_to_world, o2w, sizeof o2w);
+  return 0;
+}
+
+extern "C" int nolf_asset_load(const char *path, int device, nolf_asset_t *out, double object_to_world[16]) {
+  if (!path || !out) return fail(NOLF_EINVAL, "null argument");
+  FILE *f = fopen(path, "rb");
+  if (!f) return fail(NOLF_EDATA, "cannot open %s", path);
+  std::vector<uint8_t> buf;
+  uint8_t tmp[1 << 16];
+  size_t got;
+  while ((got = fread(tmp, 1, sizeof tmp, f)) > 0) buf.insert(buf.end(), tmp, tmp + got);
+  const bool err = ferror(f) != 0;
+  fclose(f);
+  if (err) return fail(NOLF_EDATA, "read error on %s", path);
+  return nolf_asset_load_mem(buf.data(), buf.size(), device, out, object_to_world);
+}

@@ -78,16 +78,25 @@ def bf16_capable(asset) -> bool:
 class DeviceAsset:
     """Owns one nolf_asset_t (device copy of every table of an asset)."""
 
-    def __init__(self, asset, device_index: int):
-        desc, keep = N.asset_desc(asset)
-        h = C.c_void_p()
-        N.check(N.lib().nolf_asset_create(C.byref(desc), int(device_index), C.byref(h)))
-        del keep
+    object_to_world = None        # set for natively loaded assets (load_device_asset)
+
+    def __init__(self, asset, device_index: int, handle=None):
+        if handle is None:
+            desc, keep = N.asset_desc(asset)
+            h = C.c_void_p()
+            N.check(N.lib().nolf_asset_create(C.byref(desc), int(device_index), C.byref(h)))
+            del keep
+        else:
+            h = handle
         self.handle = h
         self.device_index = device_index
         self.nbytes = int(N.lib().nolf_asset_device_bytes(h))
         self.mode = N.MLP_FP32
-        self.bf16_ok = bf16_capable(asset)
+        if asset is not None:
+            self.bf16_ok = bf16_capable(asset)
+        else:                     # ask the library (it validates the tensor-core layout)
+            self.bf16_ok = N.lib().nolf_asset_set_mlp_mode(h, N.MLP_BF16) == 0
+            N.check(N.lib().nolf_asset_set_mlp_mode(h, N.MLP_FP32))
 
     def set_mlp_mode(self, mode: int) -> None:
         if mode != self.mode:
@@ -137,8 +146,30 @@ def _fingerprint(asset, device_index):
     return key, arrays
 
 
+def load_device_asset(path_or_bytes, device_index: int | None = None) -> DeviceAsset:
+    """assetio.read_asset + upload in one native call (nolf_asset_load): the
+    ``.nolf`` file (gzip accepted) is parsed, CRC-checked and uploaded by the
+    library.  The result can be placed in scenes like any asset; its stored
+    transform is ``.object_to_world``."""
+    if device_index is None:
+        _device()
+        device_index = torch().cuda.current_device()
+    h = C.c_void_p()
+    o2w = (C.c_double * 16)()
+    if isinstance(path_or_bytes, (bytes, bytearray, memoryview)):
+        buf = bytes(path_or_bytes)
+        N.check(N.lib().nolf_asset_load_mem(buf, len(buf), int(device_index), C.byref(h), o2w))
+    else:
+        N.check(N.lib().nolf_asset_load(str(path_or_bytes).encode(), int(device_index), C.byref(h), o2w))
+    dev = DeviceAsset(None, device_index, handle=h)
+    dev.object_to_world = np.array(o2w[:], np.float64).reshape(4, 4)
+    return dev
+
+
 def device_asset(asset, device_index: int | None = None) -> DeviceAsset:
     """Upload (or fetch the cached upload of) an asset on a CUDA device."""
+    if isinstance(asset, DeviceAsset):
+        return asset
     if device_index is None:
         _device()
         device_index = torch().cuda.current_device()
