@@ -65,6 +65,9 @@ def parse():
     p.add_argument("--verify", action="store_true",
                    help="rank 0 re-renders the last frame alone and compares bitwise with the "
                         "multi-GPU assembled frame")
+    p.add_argument("--sync", default="flags", choices=["flags", "nccl"],
+                   help="p2p frame completion: flags = peer-mapped u32 flags set/polled by tiny kernels "
+                        "(no collective); nccl = a 1-element all-reduce per frame")
     p.add_argument("--exchange", default="p2p", choices=["p2p", "dma", "gather"],
                    help="N>1 frame composer: compose stores into rank 0's frame over NVLink "
                         "(CUDA IPC peer memory) or NCCL gather + unpack kernel")
@@ -373,7 +376,49 @@ def run_ours(args):
                 raw.append(ptr.value)
         peer_frames = [(p, p + NPX * 4) for p in raw]
 
-    def step(k, fb=0, before_barrier=None):
+    # ---- frame-completion flags (p2p, --sync flags): rank 0 owns done[world]
+    # (peer r sets done[r] = seq after its stores), every peer owns free
+    # (rank 0 sets it = seq once frame seq is consumed, so a peer reuses a
+    # frame buffer only after rank 0 is done with it: double buffering)
+    flags = p2p and args.sync == "flags"
+    seq_box = [0]
+    timeout_flag = torch.zeros(1, dtype=torch.int32, device=dev)
+    if flags:
+        import ctypes
+
+        def alloc_flag(nwords):
+            ptr = ctypes.c_void_p()
+            N.check(N.lib().nolf_device_alloc(4 * nwords, ctypes.byref(ptr)))
+            N.check(N.lib().nolf_memcpy_async(ptr, torch.zeros(nwords, dtype=torch.int32, device=dev).data_ptr(),
+                                              4 * nwords, stream))
+            torch.cuda.synchronize()
+            hh = (ctypes.c_uint8 * 64)()
+            N.check(N.lib().nolf_ipc_get_handle(ptr, ctypes.byref(hh)))
+            return ptr.value, torch.tensor(list(bytes(hh)), dtype=torch.uint8, device=dev)
+
+        def open_flag(h):
+            hh = (ctypes.c_uint8 * 64)(*h.cpu().tolist())
+            ptr = ctypes.c_void_p()
+            N.check(N.lib().nolf_ipc_open_handle(ctypes.byref(hh), ctypes.byref(ptr)))
+            return ptr.value
+
+        own, own_h = alloc_flag(max(world, 1))           # rank 0: done[world]; peers: free
+        hs = [torch.zeros(64, dtype=torch.uint8, device=dev) for _ in range(world)]
+        dist.all_gather(hs, own_h)
+        done_remote = open_flag(hs[0]) if rank != 0 else own
+        free_remote = [open_flag(hs[j]) for j in range(1, world)] if rank == 0 else []
+
+    def release(seq, s):
+        """rank 0: frame seq consumed -> its buffers may be overwritten"""
+        for ptr in free_remote:
+            N.check(N.lib().nolf_flag_set(ptr, seq, s))
+
+    def step(k, fb=0, before_barrier=None, auto_release=True):
+        if p2p and flags:
+            seq_box[0] += 1
+            seq = seq_box[0]
+            if rank != 0 and seq > 2:      # buffer fb held frame seq-2: wait until rank 0 is done
+                N.check(N.lib().nolf_flag_wait(own, 1, seq - 2, timeout_flag.data_ptr(), stream))
         if p2p:
             if dma:
                 # compose into this GPU's own frame (local HBM stores), then
@@ -392,6 +437,16 @@ def run_ours(args):
                       "counters": out["counters"]}
                 R.render(cam_arrays[k % n_cam], my_tiles, n_max, stride, o2, frame_layout=True,
                          peer=(rank != 0))
+            if flags:
+                if rank != 0:
+                    N.check(N.lib().nolf_flag_set(done_remote + 4 * rank, seq, stream))
+                else:                      # every peer's stores for frame seq have landed
+                    N.check(N.lib().nolf_flag_wait(own + 4, world - 1, seq, timeout_flag.data_ptr(), stream))
+                    if before_barrier is not None:
+                        torch.cuda.current_stream().wait_event(before_barrier)
+                    if auto_release:
+                        release(seq, stream)
+                return
             if before_barrier is not None:
                 torch.cuda.current_stream().wait_event(before_barrier)
             dist.all_reduce(token)         # every rank's peer stores have landed
@@ -562,7 +617,8 @@ def run_ours(args):
             # p2p: other ranks write buffer fb^1 at step k+1 once this step's
             # completion collective passes, so rank 0 enters it only after
             # the download of step k-1 (buffer fb^1) finished
-            step(k, fb, before_barrier=done_copy[fb ^ 1] if (p2p and rank == 0) else None)
+            step(k, fb, before_barrier=done_copy[fb ^ 1] if (p2p and rank == 0) else None,
+                 auto_release=False)
             if rank == 0:
                 rendered = torch.cuda.Event()
                 rendered.record(comp)
@@ -574,6 +630,8 @@ def run_ours(args):
                     else:
                         hosts[fb][:NPX * 4].view(NPX, 4).copy_(frames[fb][0], non_blocking=True)
                         hosts[fb][NPX * 4:].view(torch.int16).copy_(frames[fb][1], non_blocking=True)
+                    if flags:              # downloaded: the peers may refill buffer fb
+                        release(seq_box[0], copy_stream.cuda_stream)
                 ev = torch.cuda.Event()
                 ev.record(copy_stream)
                 done_copy[fb] = ev
@@ -701,12 +759,17 @@ def run_ours(args):
         }
         line["config"]["parallelism"] = f"ray-tile x{world}"
         if world > 1:
+            line["config"]["frame_sync"] = (
+                "peer-mapped completion flags (k_flag_set / k_flag_wait, no collective)"
+                if flags else "1-element NCCL all-reduce" if p2p else "NCCL gather")
+            if flags and int(timeout_flag.item()) != 0:
+                line["config"]["frame_sync"] += " -- TIMED OUT (frames incomplete)"
             line["config"]["exchange"] = (
                 "every rank composes its tile rows locally, the copy engine DMAs them into rank 0's "
-                "frame over NVLink (CUDA IPC, strided 2-D copies) + 1-element NCCL all-reduce"
+                "frame over NVLink (CUDA IPC, strided 2-D copies)"
                 if args.exchange == "dma" else
-                "compose epilogue stores into rank 0's frame over NVLink (CUDA IPC peer memory) "
-                "+ 1-element NCCL all-reduce" if p2p else "NCCL gather of encoded tiles + unpack kernel")
+                "compose epilogue stores into rank 0's frame over NVLink (CUDA IPC peer memory)"
+                if p2p else "NCCL gather of encoded tiles + unpack kernel")
         print(json.dumps(line), flush=True)
     if host_map is not None:
         torch.cuda.synchronize()

@@ -238,6 +238,14 @@ int nolf_device_free(void *ptr);
 int nolf_ipc_get_handle(void *ptr, void *handle64);          /* 64-byte handle out */
 int nolf_ipc_open_handle(const void *handle64, void **ptr);  /* peer mapping */
 int nolf_ipc_close_handle(void *ptr);
+/* Frame-completion signalling over NVLink without a collective: set stores
+ * `value` into a (possibly peer-mapped) u32 flag after a system-scope fence
+ * (everything the stream did before is visible first); wait spins on the
+ * device until all n local flags are >= value (sleeping between polls),
+ * bounded: after ~4 s it gives up and sets *timed_out (device u32, may be
+ * NULL).  Both are stream-ordered, no host sync. */
+int nolf_flag_set(uint32_t *flag, uint32_t value, void *stream);
+int nolf_flag_wait(const uint32_t *flags, int32_t n, uint32_t value, uint32_t *timed_out, void *stream);
 int nolf_memcpy_async(void *dst, const void *src, size_t bytes, void *stream);
 int nolf_memcpy2d_async(void *dst, size_t dpitch, const void *src, size_t spitch, size_t width_bytes,
                         size_t height, void *stream);

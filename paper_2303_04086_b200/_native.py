@@ -110,6 +110,8 @@ def lib():
         "nolf_ipc_get_handle": ([vp, vp], C.c_int),
         "nolf_ipc_open_handle": ([vp, C.POINTER(vp)], C.c_int),
         "nolf_ipc_close_handle": ([vp], C.c_int),
+        "nolf_flag_set": ([vp, C.c_uint32, vp], C.c_int),
+        "nolf_flag_wait": ([vp, C.c_int32, C.c_uint32, vp, vp], C.c_int),
         "nolf_memcpy_async": ([vp, vp, C.c_size_t, vp], C.c_int),
         "nolf_memcpy2d_async": ([vp, C.c_size_t, vp, C.c_size_t, C.c_size_t, C.c_size_t, vp], C.c_int),
         "nolf_host_register": ([vp, C.c_size_t, C.POINTER(vp)], C.c_int),

@@ -1151,6 +1151,21 @@ int nolf_ipc_open_handle(const void *handle64, void **ptr) {
   return 0;
 }
 
+int nolf_flag_set(uint32_t *flag, uint32_t value, void *stream) {
+  if (!flag) return fail(NOLF_EINVAL, "null flag");
+  k_flag_set<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(flag, value);
+  CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+int nolf_flag_wait(const uint32_t *flags, int32_t n, uint32_t value, uint32_t *timed_out, void *stream) {
+  if (n < 0 || n > 32 || (n > 0 && !flags)) return fail(NOLF_EINVAL, "flag count %d outside 0..32", n);
+  if (n == 0) return 0;
+  k_flag_wait<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(flags, n, value, timed_out);
+  CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
 int nolf_ipc_close_handle(void *ptr) {
   if (ptr) CUDA_TRY(cudaIpcCloseMemHandle(ptr));
   return 0;

@@ -1147,4 +1147,29 @@ __global__ void __launch_bounds__(256) k_unpack(const uint8_t *gathered, long lo
   depth16[dst] = reinterpret_cast<const uint16_t *>(base + (long long)n_per_rank * tile_stride * 4)[src];
 }
 
+// ---------------------------------------------------------------- cross-GPU flags
+__global__ void k_flag_set(uint32_t *flag, uint32_t value) {
+  __threadfence_system();      // the stream's earlier (peer) stores become visible first
+  *reinterpret_cast<volatile uint32_t *>(flag) = value;
+  __threadfence_system();
+}
+
+__global__ void k_flag_wait(const uint32_t *flags, int n, uint32_t value, uint32_t *timed_out) {
+  const int i = threadIdx.x;
+  bool ok = i >= n;
+  unsigned long long t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  while (!__all_sync(0xffffffffu, ok)) {
+    if (!ok) ok = *reinterpret_cast<const volatile uint32_t *>(flags + i) >= value;
+    unsigned long long now;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+    if (now - t0 > 4000000000ull) {          // bounded: never hang the device
+      if (i == 0 && timed_out) *timed_out = 1u;
+      break;
+    }
+    __nanosleep(200);
+  }
+  __threadfence_system();      // order the peers' data before what follows on this stream
+}
+
 }  // namespace nolf
