@@ -227,14 +227,15 @@ def cpu_sample(scene, cams, tiles, seconds, seed=0, max_tiles=None):
     rng = np.random.default_rng(seed)
     order = rng.permutation(len(tiles))
     rays, t0, used = 0, time.perf_counter(), 0
+    nthr = os.cpu_count()        # explicit: torchrun exports OMP_NUM_THREADS=1
     for t in order:
         c, x0, y0, x1, y1 = (int(v) for v in tiles[t])
         rg, dp = [], []
         for oa, tr in oas:
-            r, d = O.render_rect(oa, cams[c], (x0, y0, x1, y1), transform=tr)
+            r, d = O.render_rect(oa, cams[c], (x0, y0, x1, y1), transform=tr, nthreads=nthr)
             rg.append(r)
             dp.append(d)
-        O.compose(np.stack(rg), np.stack(dp))
+        O.compose(np.stack(rg), np.stack(dp), nthreads=nthr)
         rays += (x1 - x0) * (y1 - y0)
         used += 1
         if time.perf_counter() - t0 >= seconds or (max_tiles and used >= max_tiles):
