@@ -938,7 +938,10 @@ int launch_march_shade(int mode, const NolfInstance *ins, int n_inst, const Nolf
     ca.chunk_live = chunked ? w.chunk_live : nullptr;
     ca.four = (tile_stride % 4 == 0 && n_rays % 4 == 0 && ((uintptr_t)w.nhit & 3) == 0 &&
                ((uintptr_t)sout->rgba8 & 15) == 0 && ((uintptr_t)sout->depth16 & 7) == 0) ? 1 : 0;
-    const long long n_thr = ca.four ? n_rays / 4 : n_rays;
+    if (ca.four && tile_stride % 8 == 0 && ((uintptr_t)w.nhit & 7) == 0 && ((uintptr_t)sout->rgba8 & 31) == 0 &&
+        ((uintptr_t)sout->depth16 & 15) == 0)
+      ca.four = 2;
+    const long long n_thr = ca.four == 2 ? n_rays / 8 : ca.four ? n_rays / 4 : n_rays;
     k_compose<<<(unsigned)((n_thr + 255) / 256), 256, 0, st>>>(ca);
     CUDA_TRY(cudaGetLastError());
     if ((rc = prof_mark(3, st))) return rc;

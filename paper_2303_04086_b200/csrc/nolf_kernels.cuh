@@ -964,7 +964,7 @@ struct ComposeArgs {
   uint8_t *out_rgba8;
   uint16_t *out_depth16;
   float depth_far;
-  int four;                    // 4 slots per thread (tiles && nhit && tile_stride % 4 == 0)
+  int four;                    // slots per thread: 0 -> 1, 1 -> 4, 2 -> 8 (tiles && nhit && stride % 4 / 8 == 0)
   const uint8_t *chunk_live;   // scene: per 128-slot chunk, 0 = never marched (all misses)
 };
 
@@ -1110,9 +1110,59 @@ __device__ __forceinline__ void compose_four(const ComposeArgs &a, const long lo
   }
 }
 
+// Eight consecutive slots per thread (tile_stride % 8 == 0): in an 8x4-block
+// tile they are one 8-pixel row of a block, i.e. 32 contiguous rgba8 bytes
+// and 16 depth16 bytes of the frame -> two 16 B + one 16 B stores, one 8 B
+// layer-count load; anything else goes through the 4-slot path twice.
+__device__ __forceinline__ void compose_eight(const ComposeArgs &a, const long long p0) {
+  long long t, local0;
+  split_slot(p0, a.tile_stride, t, local0);
+  const TileParams tp = a.tiles[t];
+  const int w = tp.x1 - tp.x0, h = tp.y1 - tp.y0;
+  if (a.frame_layout && (w & 7) == 0 && (h & 3) == 0 && local0 < (long long)w * h && !a.out_rgba && !a.out_depth) {
+    const CamParams &cp = a.cams[tp.cam];
+    int x, y;
+    slot_xy(local0, w, h, x, y);
+    const long long q0 = cp.pix_base + (long long)(tp.y0 + y) * cp.width + (tp.x0 + x);
+    if ((q0 & 7) == 0) {
+      const bool live = !a.chunk_live || a.chunk_live[p0 >> 7];
+      const uint2 nh = live ? *reinterpret_cast<const uint2 *>(a.nhit + p0) : make_uint2(0u, 0u);
+      uint4 *r8 = reinterpret_cast<uint4 *>(a.out_rgba8 + q0 * 4);
+      uint4 *d16 = reinterpret_cast<uint4 *>(a.out_depth16 + q0);
+      if ((nh.x | nh.y) == 0) {                 // eight misses
+        if (a.out_rgba8) { r8[0] = make_uint4(0u, 0u, 0u, 0u); r8[1] = make_uint4(0u, 0u, 0u, 0u); }
+        if (a.out_depth16) d16[0] = make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu);
+        return;
+      }
+      unsigned c8[8], dd[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int n = (int)(((j < 4 ? nh.x : nh.y) >> (8 * (j & 3))) & 0xffu);
+        float4 o;
+        float od;
+        compose_px(a, p0 + j, n, o, od);
+        const uchar4 u = encode_rgba8(o);
+        c8[j] = (unsigned)u.x | ((unsigned)u.y << 8) | ((unsigned)u.z << 16) | ((unsigned)u.w << 24);
+        dd[j] = encode_depth16(od, a.depth_far);
+      }
+      if (a.out_rgba8) {
+        r8[0] = make_uint4(c8[0], c8[1], c8[2], c8[3]);
+        r8[1] = make_uint4(c8[4], c8[5], c8[6], c8[7]);
+      }
+      if (a.out_depth16)
+        d16[0] = make_uint4(dd[0] | (dd[1] << 16), dd[2] | (dd[3] << 16), dd[4] | (dd[5] << 16), dd[6] | (dd[7] << 16));
+      return;
+    }
+  }
+  compose_four(a, p0);
+  compose_four(a, p0 + 4);
+}
+
 __global__ void __launch_bounds__(256) k_compose(ComposeArgs a) {
   const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (a.four) {
+  if (a.four == 2) {
+    if (8 * gid < a.n_pix) compose_eight(a, 8 * gid);
+  } else if (a.four) {
     if (4 * gid < a.n_pix) compose_four(a, 4 * gid);
   } else if (gid < a.n_pix) {
     compose_one(a, gid);
