@@ -69,21 +69,6 @@ struct MarchArgs {
   unsigned *fetch;
 };
 
-// Exit parameter of an axis-aligned box [lo, hi] (object coords) along the
-// ray, with faces on the unit-cube boundary pushed to infinity because march
-// positions are clipped to [0,1] (lightfield.py:166).
-// (An estimate only: the skip target is verified exactly, so fp32 is fine.)
-__device__ __forceinline__ double box_exit(const double o[3], const double d[3], const float invf[3],
-                                           const double lo[3], const double hi[3]) {
-  float t = __int_as_float(0x7f800000);
-#pragma unroll
-  for (int k = 0; k < 3; ++k) {
-    if (d[k] > 0.0 && hi[k] < 1.0) t = fminf(t, (float)(hi[k] - o[k]) * invf[k]);
-    else if (d[k] < 0.0 && lo[k] > 0.0) t = fminf(t, (float)(lo[k] - o[k]) * invf[k]);
-  }
-  return (double)t;
-}
-
 // Sample i's clipped position and index cell, exactly as march_rays computes
 // them (t_mid = t_near + (i+0.5)*step ; pos = clip(o + t_mid*d, 0, 1)).
 // CLIP = false when the caller proved every position it will ask for lies in
@@ -231,12 +216,14 @@ __device__ __forceinline__ MarchOut march_ray(const DevAsset &A, const double o[
   const DevAtlas &at = A.den;
   const double delta = A.step;
   const int b = at.b;
-  const double inv_b = 1.0 / (double)b;
-  const double inv_delta = 1.0 / delta;
+  const float inv_bf = 1.0f / (float)b;
+  const float inv_delta_f = (float)(1.0 / delta);
+  const float t_near_f = (float)t_near;
   double best_w = 0.0, trans = 1.0, alpha_c = 0.0, t_hit = r.t_hit;
   int samples = 0;
   // samples before i_start and from t_end on are empty: march [i_start, t_lim)
   const double t_lim = fmin(t_far, t_end);
+  const float t_lim_f = (float)t_lim;
   const double t_stop = A.t_stop;
   int i = i_start;
   const int lr = at.lr;
@@ -277,16 +264,17 @@ __device__ __forceinline__ MarchOut march_ray(const DevAsset &A, const double o[
     }
     if (empty) {
       NOLF_STAT(3, 1);
-      double lo[3], hi[3];
+      // the jump target is an estimate (verified below), so it is computed
+      // in fp32 relative to t_near: box faces, exit and sample index
+      float te = __int_as_float(0x7f800000);
 #pragma unroll
       for (int k = 0; k < 3; ++k) {
-        lo[k] = lo_c[k] > 0 ? lo_c[k] * inv_b : -1.0;       // grid faces: clipped
-        hi[k] = hi_c[k] < b - 1 ? (hi_c[k] + 1) * inv_b : 2.0;  // positions never leave
+        const float ok = (float)o[k];
+        if (invf[k] > 0.f && hi_c[k] < b - 1) te = fminf(te, ((float)(hi_c[k] + 1) * inv_bf - ok) * invf[k]);
+        else if (invf[k] < 0.f && lo_c[k] > 0) te = fminf(te, ((float)lo_c[k] * inv_bf - ok) * invf[k]);
       }
-      double te = box_exit(o, d, invf, lo, hi);
-      double tl = fmin(te, t_lim);
-      double jf = floor((tl - t_near) * inv_delta - 0.5);
-      int j = jf > 2.0e9 ? 2000000000 : (int)jf;
+      const float jf = floorf((fminf(te, t_lim_f) - t_near_f) * inv_delta_f - 0.5f);
+      int j = jf > 2.0e9f ? 2000000000 : (int)jf;
       int next = i + 1;
       for (int attempt = 0; attempt < 2 && j > i; ++attempt, --j) {
         double pj[3];
