@@ -157,6 +157,8 @@ __device__ __forceinline__ void to_object(const double *w2o12, const double ow[3
 // Tracking it with one flag instead of NaN-aware selects is observably
 // identical (every non-NaN value is computed with the same comparisons).
 // inv[] returns 1/d (inf for d == 0) for reuse by the march.
+// HAVE_INV: inv[] already holds 1/d from an earlier slab of the same ray.
+template <bool HAVE_INV = false>
 __device__ __forceinline__ bool slab(const double pmin[3], const double pmax[3], const double o[3],
                                      const double d[3], double &t_near, double &t_far, double inv[3]) {
   const double INF = __longlong_as_double(0x7ff0000000000000ll);
@@ -169,9 +171,9 @@ __device__ __forceinline__ bool slab(const double pmin[3], const double pmax[3],
       const bool inside = (o[k] >= pmin[k]) && (o[k] <= pmax[k]);
       lo = inside ? -INF : INF;
       hi = inside ? INF : -INF;
-      inv[k] = INF;
+      if (!HAVE_INV) inv[k] = INF;
     } else {
-      inv[k] = __ddiv_rn(1.0, d[k]);
+      if (!HAVE_INV) inv[k] = __drcp_rn(d[k]);   // IEEE 1/d, == __ddiv_rn(1.0, d)
       const double t0 = __dmul_rn(__dsub_rn(pmin[k], o[k]), inv[k]);
       const double t1 = __dmul_rn(__dsub_rn(pmax[k], o[k]), inv[k]);
       nan |= (t0 != t0) | (t1 != t1);

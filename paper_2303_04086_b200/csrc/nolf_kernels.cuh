@@ -465,7 +465,6 @@ __device__ __forceinline__ bool prepare_march(const DevInst &I, const DevAsset &
   } else {
     to_object(I.w2o, ow, dw, o, d);
   }
-  double inv_unused[3];
   sp.t_near = 0.0;
   sp.t_far = 0.0;
   sp.i_start = 0;
@@ -484,7 +483,7 @@ __device__ __forceinline__ bool prepare_march(const DevInst &I, const DevAsset &
   // leaves the result bit-identical (empty samples change nothing).
   if (boxhit && sp.t_near < sp.t_far) {
     double ca, cb;
-    if (!slab(A.cull_lo, A.cull_hi, o, d, ca, cb, inv_unused) || A.cull_empty) {
+    if (!slab<true>(A.cull_lo, A.cull_hi, o, d, ca, cb, inv) || A.cull_empty) {
       boxhit = false;                     // never meets an occupied cell: exact miss
     } else {
       const double f = floor((ca - sp.t_near) / A.step - 2.5);
