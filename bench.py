@@ -722,9 +722,12 @@ def run_ours(args):
         caps = sorted(glob.glob(os.path.join(ROOT, "profiles", f"r*_config{args.config}_1gpu*.json")))
         for path in reversed(caps):
             kern_caps = json.load(open(path)).get("kernels", {})
-            hit = [v for k, v in kern_caps.items() if k.split("<")[0] == top]
+            # the march phase is k_cull_chunks + k_march_chunks (k_march<> for unaligned tiles)
+            names_of = {"k_march": ("k_march", "k_march_chunks", "k_cull_chunks"),
+                        "k_shade": ("k_shade", "k_shade_tc"), "k_compose": ("k_compose",)}[top]
+            hit = [v for k, v in kern_caps.items() if k.split("<")[0] in names_of]
             if hit:
-                roof["traffic"] = float(hit[0]["dram_bytes_per_launch"])
+                roof["traffic"] = float(sum(v["dram_bytes_per_launch"] for v in hit))
                 roof["traffic_unit"] = "B/launch (dram__bytes_read.sum + dram__bytes_write.sum)"
                 roof["traffic_source"] = os.path.relpath(path, ROOT)
                 break
