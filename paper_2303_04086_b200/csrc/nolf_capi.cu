@@ -834,6 +834,19 @@ int prof_mark(int i, cudaStream_t st) {
   return 0;
 }
 
+// Live-chunk count of an earlier frame per (workspace, stream): sizes the
+// marcher's grid without a host wait.
+struct LiveEstimate {
+  void *ws = nullptr;
+  long long n_chunks = 0;
+  cudaStream_t st = nullptr;
+  unsigned *host = nullptr;
+  cudaEvent_t ev = nullptr;
+  bool pending = false;
+  long long last = 0;
+};
+thread_local LiveEstimate g_live;
+
 int launch_march_shade(int mode, const NolfInstance *ins, int n_inst, const NolfCamera *cams, int n_cams,
                        const NolfTile *tiles_dev, int n_tiles, TileParams rect, long long n_rays,
                        long long tile_stride, const double *origins, int origin_stride, const double *dirs,
@@ -908,7 +921,31 @@ int launch_march_shade(int mode, const NolfInstance *ins, int n_inst, const Nolf
     k_cull_chunks<<<(unsigned)((n_chunks + 127) / 128), 128, 0, st>>>(ma, n_chunks, w.chunk_live, w.chunk_list,
                                                                       w.counts + n_inst);
     CUDA_TRY(cudaGetLastError());
-    k_march_chunks<<<(unsigned)n_chunks, kMarchThreads, 0, st>>>(ma);
+    // grid from the last live count that has landed on the host (async
+    // read-back of an earlier frame on this workspace; worst case at first)
+    LiveEstimate &le = g_live;
+    if (le.ws != workspace || le.n_chunks != n_chunks || le.st != st) {
+      if (!le.host) {
+        CUDA_TRY(cudaMallocHost(&le.host, sizeof(unsigned)));
+        CUDA_TRY(cudaEventCreateWithFlags(&le.ev, cudaEventDisableTiming));
+      }
+      if (le.pending) CUDA_TRY(cudaEventSynchronize(le.ev));
+      le.ws = workspace;
+      le.n_chunks = n_chunks;
+      le.st = st;
+      le.last = n_chunks;
+      le.pending = false;
+    } else if (le.pending && cudaEventQuery(le.ev) == cudaSuccess) {
+      le.last = *le.host;
+      le.pending = false;
+    }
+    const long long want = (long long)le.last + (long long)le.last / 8 + 2ll * num_sms();
+    k_march_chunks<<<(unsigned)std::max<long long>(1, std::min(n_chunks, want)), kMarchThreads, 0, st>>>(ma);
+    if (!le.pending) {
+      CUDA_TRY(cudaMemcpyAsync(le.host, w.counts + n_inst, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+      CUDA_TRY(cudaEventRecord(le.ev, st));
+      le.pending = true;
+    }
   }
   CUDA_TRY(cudaGetLastError());
   if ((rc = prof_mark(1, st))) return rc;

@@ -656,13 +656,15 @@ __global__ void __launch_bounds__(128) k_cull_chunks(MarchArgs args, long long n
   }
 }
 
-// Scene marcher over the compacted live chunks: one CTA per list entry; the
-// grid is sized for the worst case (every chunk live) and the CTAs past the
-// list's length exit after one load (no tile lookups, no culling, no barrier).
+// Scene marcher over the compacted live chunks: one CTA per list entry.  The
+// host sizes the grid from the live count of an earlier frame (read back
+// asynchronously, never waited for) plus headroom; a grid-stride loop keeps
+// any size correct, and CTAs past the list exit after one load.
 __global__ void __launch_bounds__(kMarchThreads, NOLF_MARCH_MINB) k_march_chunks(MarchArgs args) {
-  if (blockIdx.x >= *args.n_chunks) return;
+  const unsigned n = *args.n_chunks;
   stat_cta_start();
-  march_chunk<kModeScene>(args, args.chunks[blockIdx.x], false);
+  for (unsigned it = blockIdx.x; it < n; it += gridDim.x)   // normally one pass: the grid is sized
+    march_chunk<kModeScene>(args, args.chunks[it], false);  // from the previous frame's count
   stat_cta_end();
 }
 
