@@ -202,3 +202,27 @@ def test_any_grid_matches_oracle(b, r):
     assert np.array_equal(tile.depth, o_depth)
     assert np.abs(tile.rgba - o_rgba).max() <= 1e-6
     assert (cnt.hit_pixels, cnt.march_samples) == (ocnt.hit_pixels, ocnt.march_samples)
+
+
+def test_multi_camera_launch_equals_single_camera_launches():
+    """One launch over the tiles of two cameras (the multi-user batch of
+    BASELINE configs 3/5: compacted live chunks, per-camera frame bases)
+    gives each camera's frame bit for bit as rendering it alone."""
+    import torch
+    from paper_2303_04086_b200.model import orbit_camera
+    _, scene = _scene()
+    cams = [orbit_camera(0.5, 0.6, radius=2.5, size=64, target=(0.2, 0.2, 0.25)),
+            orbit_camera(2.0, 0.3, radius=2.2, size=64, target=(0.1, 0.3, 0.2))]
+    r = R.SceneRenderer(scene)
+    tiles = np.concatenate([R.frame_tiles(64, 64, 32, cam=c) for c in range(2)])
+    out = r.alloc(len(tiles), 1024, want_f32=False, want_u8=True)
+    r.render(cams, torch.from_numpy(tiles).to(r.device), len(tiles), 1024, out, frame_layout=True)
+    both = out["rgba8"][:2 * 64 * 64].cpu().numpy().reshape(2, 64, 64, 4)
+    both_d = out["depth16"][:2 * 64 * 64].cpu().numpy().view(np.uint16).reshape(2, 64, 64)
+    for c in range(2):
+        one = r.alloc(4, 1024, want_f32=False, want_u8=True)
+        t1 = R.frame_tiles(64, 64, 32)
+        r.render([cams[c]], torch.from_numpy(t1).to(r.device), len(t1), 1024, one, frame_layout=True)
+        np.testing.assert_array_equal(both[c], one["rgba8"][:64 * 64].cpu().numpy().reshape(64, 64, 4))
+        np.testing.assert_array_equal(both_d[c], one["depth16"][:64 * 64].cpu().numpy().view(np.uint16).reshape(64, 64))
+    assert (both_d != 65535).sum() > 0
