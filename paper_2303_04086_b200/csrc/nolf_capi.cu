@@ -768,7 +768,10 @@ int run_shade(const DevInst *inst, const long long *qoff, int n_inst, const Work
     }
     const int by_regs = 65536 / (((regs + 7) / 8 * 8) * kTcThreads);
     const int by_smem = (int)((227u * 1024u) / (smem + 1024u));
-    int per_sm = std::max(1, std::min(std::min(by_regs, by_smem), 4));
+#ifndef NOLF_SHADE_CAP
+#define NOLF_SHADE_CAP 4
+#endif
+    int per_sm = std::max(1, std::min(std::min(by_regs, by_smem), NOLF_SHADE_CAP));
     k_shade_tc<<<num_sms() * std::max(per_sm, 1), kTcThreads, smem, st>>>(sa);
   } else {
     k_shade<<<num_sms() * 3, kShadeThreads, kShadeSmem, st>>>(sa);
