@@ -34,7 +34,7 @@ __device__ __forceinline__ double mt_hit(const double *T, const double o[3], con
   const double pz = __dsub_rn(__dmul_rn(d[0], e2y), __dmul_rn(d[1], e2x));
   const double det = __dadd_rn(__dadd_rn(__dmul_rn(e1x, px), __dmul_rn(e1y, py)), __dmul_rn(e1z, pz));
   if (fabs(det) < 1e-300) return -1.0;
-  const double inv = __ddiv_rn(1.0, det);
+  const double inv = __drcp_rn(det);          // IEEE 1/det (== __ddiv_rn(1.0, det))
   const double sx = __dsub_rn(o[0], T[0]), sy = __dsub_rn(o[1], T[1]), sz = __dsub_rn(o[2], T[2]);
   const double u = __dmul_rn(__dadd_rn(__dadd_rn(__dmul_rn(sx, px), __dmul_rn(sy, py)), __dmul_rn(sz, pz)), inv);
   if (u < 0.0 || u > 1.0) return -1.0;
@@ -47,7 +47,25 @@ __device__ __forceinline__ double mt_hit(const double *T, const double o[3], con
   return t >= 0.0 ? t : -1.0;
 }
 
+// Conservative fp32 slab of a node (boxes padded at build time; +-2% in t):
+// entry distance, or +inf when the ray cannot reach a triangle inside
+// before the best hit so far.
+__device__ __forceinline__ float node_entry(const BvhNode &n, float ox, float oy, float oz, float ix, float iy,
+                                            float iz, float best_f) {
+  float t0 = (n.lo[0] - ox) * ix, t1 = (n.hi[0] - ox) * ix;
+  float tmin = fminf(t0, t1), tmax = fmaxf(t0, t1);
+  t0 = (n.lo[1] - oy) * iy; t1 = (n.hi[1] - oy) * iy;
+  tmin = fmaxf(tmin, fminf(t0, t1)); tmax = fminf(tmax, fmaxf(t0, t1));
+  t0 = (n.lo[2] - oz) * iz; t1 = (n.hi[2] - oz) * iz;
+  tmin = fmaxf(tmin, fminf(t0, t1)); tmax = fminf(tmax, fmaxf(t0, t1));
+  if (tmax < 0.0f || tmin > tmax * 1.02f + 1e-6f || tmin > best_f * 1.02f + 1e-6f) return __int_as_float(0x7f800000);
+  return tmin;
+}
+
 // Closest hit over the mesh: t_mesh >= 0, or -1 when the ray misses it.
+// Children are visited near-first (both boxes tested at the parent, the far
+// one pushed with its entry distance and dropped on pop if a closer hit was
+// found meanwhile); pruning only, the fp64 triangle tests decide t.
 __device__ __forceinline__ double mesh_first_hit(const DevMesh &M, const double o[3], const double d[3]) {
   const float ox = (float)o[0], oy = (float)o[1], oz = (float)o[2];
   // finite reciprocals: a zero component gets +-1e30 so (lo - o) * inv is never 0*inf
@@ -55,19 +73,20 @@ __device__ __forceinline__ double mesh_first_hit(const DevMesh &M, const double 
   const float ix = rcp(d[0]), iy = rcp(d[1]), iz = rcp(d[2]);
   double best = -1.0;
   float best_f = __int_as_float(0x7f800000);
-  int stack[48];
+  int stack[32];
+  float stack_t[32];
   int sp = 0;
-  stack[sp++] = 0;
+  {
+    const float te = node_entry(M.nodes[0], ox, oy, oz, ix, iy, iz, best_f);
+    if (te == __int_as_float(0x7f800000)) return -1.0;
+    stack[0] = 0;
+    stack_t[0] = te;
+    sp = 1;
+  }
   while (sp) {
-    const BvhNode n = M.nodes[stack[--sp]];
-    // conservative fp32 slab (boxes padded at build time; +-2% in t)
-    float t0 = (n.lo[0] - ox) * ix, t1 = (n.hi[0] - ox) * ix;
-    float tmin = fminf(t0, t1), tmax = fmaxf(t0, t1);
-    t0 = (n.lo[1] - oy) * iy; t1 = (n.hi[1] - oy) * iy;
-    tmin = fmaxf(tmin, fminf(t0, t1)); tmax = fminf(tmax, fmaxf(t0, t1));
-    t0 = (n.lo[2] - oz) * iz; t1 = (n.hi[2] - oz) * iz;
-    tmin = fmaxf(tmin, fminf(t0, t1)); tmax = fminf(tmax, fmaxf(t0, t1));
-    if (tmax < 0.0f || tmin > tmax * 1.02f + 1e-6f || tmin > best_f * 1.02f + 1e-6f) continue;
+    --sp;
+    if (stack_t[sp] > best_f * 1.02f + 1e-6f) continue;   // a closer hit appeared after the push
+    const BvhNode n = M.nodes[stack[sp]];
     if (n.count > 0) {
       for (int i = 0; i < n.count; ++i) {
         const double t = mt_hit(M.tri + 9ll * (n.first + i), o, d);
@@ -76,9 +95,21 @@ __device__ __forceinline__ double mesh_first_hit(const DevMesh &M, const double 
           best_f = (float)t;
         }
       }
-    } else if (sp < 46) {
-      stack[sp++] = n.first + 1;
-      stack[sp++] = n.first;
+    } else if (sp < 30) {
+      const BvhNode L = M.nodes[n.first], R = M.nodes[n.first + 1];
+      const float tl = node_entry(L, ox, oy, oz, ix, iy, iz, best_f);
+      const float tr = node_entry(R, ox, oy, oz, ix, iy, iz, best_f);
+      const bool hl = tl != __int_as_float(0x7f800000), hr = tr != __int_as_float(0x7f800000);
+      if (hl && hr) {
+        const bool lfirst = tl <= tr;
+        stack[sp] = lfirst ? n.first + 1 : n.first;      // far
+        stack_t[sp++] = lfirst ? tr : tl;
+        stack[sp] = lfirst ? n.first : n.first + 1;      // near on top
+        stack_t[sp++] = lfirst ? tl : tr;
+      } else if (hl || hr) {
+        stack[sp] = hl ? n.first : n.first + 1;
+        stack_t[sp++] = hl ? tl : tr;
+      }
     }
   }
   return best;
