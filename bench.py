@@ -65,6 +65,10 @@ def parse():
     p.add_argument("--verify", action="store_true",
                    help="rank 0 re-renders the last frame alone and compares bitwise with the "
                         "multi-GPU assembled frame")
+    p.add_argument("--prefill", default="on", choices=["on", "off"],
+                   help="frame buffers are pre-set to the miss encoding (memset, on the owning "
+                        "GPU, inside the timed step) so compose skips every chunk no instance "
+                        "can reach; off = compose writes every pixel")
     p.add_argument("--sync", default="flags", choices=["flags", "nccl"],
                    help="p2p frame completion: flags = peer-mapped u32 flags set/polled by tiny kernels "
                         "(no collective); nccl = a 1-element all-reduce per frame")
@@ -409,15 +413,40 @@ def run_ours(args):
         done_remote = open_flag(hs[0]) if rank != 0 else own
         free_remote = [open_flag(hs[j]) for j in range(1, world)] if rank == 0 else []
 
+    # (measured: at 1 GPU the 50 MB memset costs more than compose writing the
+    # dead chunks itself; with peers it saves ~80 % of the NVLink stores)
+    prefill = args.prefill == "on" and flags and not dma
+    last_fb = [0]
+
+    def clear(fb, s):
+        """miss encoding (rgba8 0, depth16 65535) over frame buffer fb, on its owner GPU"""
+        if p2p:
+            rgba_ptr, d_ptr = peer_frames[fb]
+        else:
+            rgba_ptr, d_ptr = frames[fb][0].data_ptr(), frames[fb][1].data_ptr()
+        N.check(N.lib().nolf_memset_async(rgba_ptr, 0, NPX * 4, s))
+        N.check(N.lib().nolf_memset_async(d_ptr, 0xFF, NPX * 2, s))
+
     def release(seq, s):
-        """rank 0: frame seq consumed -> its buffers may be overwritten"""
+        """rank 0: frame seq consumed -> its buffer is re-cleared and may be overwritten"""
+        if prefill:
+            clear(seq % 2, s)
         for ptr in free_remote:
             N.check(N.lib().nolf_flag_set(ptr, seq, s))
+
+    if prefill and (world == 1 or rank == 0):
+        clear(0, stream)
+        clear(1, stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
 
     def step(k, fb=0, before_barrier=None, auto_release=True):
         if p2p and flags:
             seq_box[0] += 1
             seq = seq_box[0]
+            fb = seq % 2                   # the buffer protocol alternates by frame sequence
+            last_fb[0] = fb
             if rank != 0 and seq > 2:      # buffer fb held frame seq-2: wait until rank 0 is done
                 N.check(N.lib().nolf_flag_wait(own, 1, seq - 2, timeout_flag.data_ptr(), stream))
         if p2p:
@@ -437,7 +466,7 @@ def run_ours(args):
                 o2 = {"rgba8": peer_frames[fb][0], "depth16": peer_frames[fb][1],
                       "counters": out["counters"]}
                 R.render(cam_arrays[k % n_cam], my_tiles, n_max, stride, o2, frame_layout=True,
-                         peer=(rank != 0))
+                         peer=(rank != 0), prefilled=prefill)
             if flags:
                 if rank != 0:
                     N.check(N.lib().nolf_flag_set(done_remote + 4 * rank, seq, stream))
@@ -453,9 +482,13 @@ def run_ours(args):
             dist.all_reduce(token)         # every rank's peer stores have landed
             return
         frame, frame_d = frames[fb]
+        last_fb[0] = fb
         if world == 1:             # single GPU: compose writes the frame directly
             out["rgba8"], out["depth16"] = frame, frame_d
-        R.render(cam_arrays[k % n_cam], my_tiles, n_max, stride, out, frame_layout=(world == 1))
+            if prefill:
+                clear(fb, stream)
+        R.render(cam_arrays[k % n_cam], my_tiles, n_max, stride, out, frame_layout=(world == 1),
+                 prefilled=(world == 1 and prefill))
         if world > 1:
             # frame composer: NCCL gather of every rank's encoded tiles, then
             # one unpack kernel writes the row-major frame on rank 0
@@ -489,7 +522,7 @@ def run_ours(args):
         if not args.no_flush:
             flush.fill_(k & 0xFF)                          # evict L2 (untimed)
         ev[k][0].record()
-        step(args.warmup + k)
+        step(args.warmup + k, k % 2)
         ev[k][1].record()
     barrier()
     n_prof = N.lib().nolf_profile_read(kms)
@@ -612,7 +645,7 @@ def run_ours(args):
         t1 = torch.cuda.Event(enable_timing=True)
         t0.record(comp)
         for k in range(args.steps):
-            fb = k % 2
+            fb = (seq_box[0] + 1) % 2 if (p2p and flags) else k % 2   # the buffer step() will use
             if done_copy[fb] is not None:
                 comp.wait_event(done_copy[fb])       # buffer free again
             # p2p: other ranks write buffer fb^1 at step k+1 once this step's
@@ -652,17 +685,20 @@ def run_ours(args):
     verify = None
     if args.verify:
         kv = args.warmup + args.steps - 1
-        step(kv, 0)
+        step(kv, 0, auto_release=False)    # keep the frame until it is read back
+        fbv = last_fb[0]
         barrier()
         if rank == 0:
             import ctypes
             got = torch.empty(NPX * 6, dtype=torch.uint8, device=dev)
             if p2p:
-                N.check(N.lib().nolf_memcpy_async(got.data_ptr(), peer_frames[0][0], NPX * 6,
+                N.check(N.lib().nolf_memcpy_async(got.data_ptr(), peer_frames[fbv][0], NPX * 6,
                                                   torch.cuda.current_stream().cuda_stream))
+                if flags:
+                    release(seq_box[0], torch.cuda.current_stream().cuda_stream)
             else:
-                got[:NPX * 4].copy_(frames[0][0].view(-1))
-                got[NPX * 4:].copy_(frames[0][1].view(torch.uint8).view(-1))
+                got[:NPX * 4].copy_(frames[fbv][0].view(-1))
+                got[NPX * 4:].copy_(frames[fbv][1].view(torch.uint8).view(-1))
             all_tiles = torch.from_numpy(tiles.astype(np.int32)).to(dev)
             ref = {"rgba8": torch.empty((NPX, 4), dtype=torch.uint8, device=dev),
                    "depth16": torch.empty(NPX, dtype=torch.int16, device=dev),

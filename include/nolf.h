@@ -151,6 +151,10 @@ typedef struct NolfSceneOut {
     int32_t peer;                      /* 1: outputs live in another GPU's memory (CUDA IPC
                                           mapping); the compose epilogue stores them over
                                           NVLink and ends with a system-scope fence */
+    int32_t prefilled;                 /* 1: rgba8 / depth16 already hold the miss encoding
+                                          (0 / 65535) for every pixel of these tiles, so
+                                          pixels no instance can reach are not written
+                                          (u8/u16 outputs only; rgba/depth must be NULL) */
 } NolfSceneOut;
 
 int nolf_abi_version(void);
@@ -247,6 +251,7 @@ int nolf_ipc_close_handle(void *ptr);
 int nolf_flag_set(uint32_t *flag, uint32_t value, void *stream);
 int nolf_flag_wait(const uint32_t *flags, int32_t n, uint32_t value, uint32_t *timed_out, void *stream);
 int nolf_memcpy_async(void *dst, const void *src, size_t bytes, void *stream);
+int nolf_memset_async(void *dst, int32_t byte_value, size_t bytes, void *stream);
 int nolf_memcpy2d_async(void *dst, size_t dpitch, const void *src, size_t spitch, size_t width_bytes,
                         size_t height, void *stream);
 /* Page-lock host memory (e.g. a shared-memory frame buffer mapped by every

@@ -67,7 +67,7 @@ class Camera(C.Structure):
 class SceneOut(C.Structure):
     _fields_ = [("rgba", C.c_void_p), ("depth", C.c_void_p), ("rgba8", C.c_void_p),
                 ("depth16", C.c_void_p), ("tile_stride", C.c_int64), ("depth_far", C.c_double),
-                ("layout", C.c_int32), ("peer", C.c_int32)]
+                ("layout", C.c_int32), ("peer", C.c_int32), ("prefilled", C.c_int32)]
 
 
 _lib = None
@@ -111,6 +111,7 @@ def lib():
         "nolf_ipc_open_handle": ([vp, C.POINTER(vp)], C.c_int),
         "nolf_ipc_close_handle": ([vp], C.c_int),
         "nolf_flag_set": ([vp, C.c_uint32, vp], C.c_int),
+        "nolf_memset_async": ([vp, C.c_int32, C.c_size_t, vp], C.c_int),
         "nolf_flag_wait": ([vp, C.c_int32, C.c_uint32, vp, vp], C.c_int),
         "nolf_memcpy_async": ([vp, vp, C.c_size_t, vp], C.c_int),
         "nolf_memcpy2d_async": ([vp, C.c_size_t, vp, C.c_size_t, C.c_size_t, C.c_size_t, vp], C.c_int),

@@ -976,6 +976,7 @@ int launch_march_shade(int mode, const NolfInstance *ins, int n_inst, const Nolf
     ca.out_depth16 = sout->depth16;
     ca.depth_far = (float)sout->depth_far;
     ca.chunk_live = chunked ? w.chunk_live : nullptr;
+    ca.prefilled = (sout->prefilled && !sout->rgba && !sout->depth) ? 1 : 0;
     ca.four = (tile_stride % 4 == 0 && n_rays % 4 == 0 && ((uintptr_t)w.nhit & 3) == 0 &&
                ((uintptr_t)sout->rgba8 & 15) == 0 && ((uintptr_t)sout->depth16 & 7) == 0) ? 1 : 0;
     if (ca.four && tile_stride % 8 == 0 && ((uintptr_t)w.nhit & 7) == 0 && ((uintptr_t)sout->rgba8 & 31) == 0 &&
@@ -1211,6 +1212,13 @@ int nolf_flag_wait(const uint32_t *flags, int32_t n, uint32_t value, uint32_t *t
 
 int nolf_ipc_close_handle(void *ptr) {
   if (ptr) CUDA_TRY(cudaIpcCloseMemHandle(ptr));
+  return 0;
+}
+
+int nolf_memset_async(void *dst, int32_t byte_value, size_t bytes, void *stream) {
+  if (bytes == 0) return 0;
+  if (!dst) return fail(NOLF_EINVAL, "null buffer");
+  CUDA_TRY(cudaMemsetAsync(dst, byte_value, bytes, static_cast<cudaStream_t>(stream)));
   return 0;
 }
 

@@ -955,6 +955,7 @@ struct ComposeArgs {
   float depth_far;
   int four;                    // slots per thread: 0 -> 1, 1 -> 4, 2 -> 8 (tiles && nhit && stride % 4 / 8 == 0)
   const uint8_t *chunk_live;   // scene: per 128-slot chunk, 0 = never marched (all misses)
+  int prefilled;               // outputs already hold the miss encoding: dead chunks are not written
 };
 
 constexpr int kMaxLayers = 64;
@@ -1048,6 +1049,7 @@ __device__ __forceinline__ void compose_one(const ComposeArgs &a, const long lon
   float4 o;
   float od;
   const bool skip = a.chunk_live && !a.chunk_live[p >> 7];
+  if (skip && a.prefilled) return;
   compose_px(a, p, skip ? 0 : (a.nhit ? (int)a.nhit[p] : a.K), o, od);
   compose_store(a, q, o, od);
 }
@@ -1060,8 +1062,9 @@ __device__ __forceinline__ void compose_four(const ComposeArgs &a, const long lo
   long long t, local0;
   split_slot(p0, a.tile_stride, t, local0);
   const TileParams tp = a.tiles[t];
-  const uchar4 nh = (a.chunk_live && !a.chunk_live[p0 >> 7]) ? make_uchar4(0, 0, 0, 0)
-                                                                : *reinterpret_cast<const uchar4 *>(a.nhit + p0);
+  const bool dead4 = a.chunk_live && !a.chunk_live[p0 >> 7];
+  if (dead4 && a.prefilled) return;
+  const uchar4 nh = dead4 ? make_uchar4(0, 0, 0, 0) : *reinterpret_cast<const uchar4 *>(a.nhit + p0);
   const int ns[4] = {nh.x, nh.y, nh.z, nh.w};
   long long q[4];
 #pragma unroll
@@ -1104,6 +1107,7 @@ __device__ __forceinline__ void compose_four(const ComposeArgs &a, const long lo
 // and 16 depth16 bytes of the frame -> two 16 B + one 16 B stores, one 8 B
 // layer-count load; anything else goes through the 4-slot path twice.
 __device__ __forceinline__ void compose_eight(const ComposeArgs &a, const long long p0) {
+  if (a.prefilled && a.chunk_live && !a.chunk_live[p0 >> 7]) return;   // misses already in place
   long long t, local0;
   split_slot(p0, a.tile_stride, t, local0);
   const TileParams tp = a.tiles[t];

@@ -434,7 +434,7 @@ class SceneRenderer:
         return cams
 
     def render(self, cameras, tiles_dev, n_tiles: int, tile_stride: int, out: dict, stream=None,
-               frame_layout: bool = False, peer: bool = False):
+               frame_layout: bool = False, peer: bool = False, prefilled: bool = False):
         cams = cameras if isinstance(cameras, C.Array) else self.camera_array(cameras)
         so = N.SceneOut()
         def ptr(key):              # tensors, or raw device addresses (peer mappings)
@@ -449,6 +449,7 @@ class SceneRenderer:
         so.depth_far = self.depth_far
         so.layout = 1 if frame_layout else 0
         so.peer = 1 if peer else 0
+        so.prefilled = 1 if prefilled else 0
         st = stream if stream is not None else _stream_ptr()
         ws = self._workspace(cams, int(n_tiles) * int(tile_stride))
         N.check(N.lib().nolf_render_scene(self._inst_arr, len(self.insts), cams, len(cams),

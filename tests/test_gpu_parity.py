@@ -226,3 +226,25 @@ def test_multi_camera_launch_equals_single_camera_launches():
         np.testing.assert_array_equal(both[c], one["rgba8"][:64 * 64].cpu().numpy().reshape(64, 64, 4))
         np.testing.assert_array_equal(both_d[c], one["depth16"][:64 * 64].cpu().numpy().view(np.uint16).reshape(64, 64))
     assert (both_d != 65535).sum() > 0
+
+
+def test_prefilled_output_skips_only_unreachable_pixels():
+    """NolfSceneOut.prefilled: with the frame pre-set to the miss encoding,
+    the compose epilogue skips chunks no screen box reaches and the frame is
+    bit-identical to a full write (multi-GPU frame composer, bench.py)."""
+    import torch
+    from paper_2303_04086_b200.model import orbit_camera
+    _, scene = _scene()
+    cam = orbit_camera(0.5, 0.6, radius=2.5, size=256, target=(0.2, 0.2, 0.25))
+    r = R.SceneRenderer(scene)
+    tiles = torch.from_numpy(R.frame_tiles(256, 256, 32)).to(r.device)
+    full = r.alloc(len(tiles), 1024, want_f32=False, want_u8=True)
+    r.render([cam], tiles, len(tiles), 1024, full, frame_layout=True)
+    pre = r.alloc(len(tiles), 1024, want_f32=False, want_u8=True)
+    pre["rgba8"].zero_()
+    pre["depth16"].fill_(-1)
+    r.render([cam], tiles, len(tiles), 1024, pre, frame_layout=True, prefilled=True)
+    n = 256 * 256
+    assert torch.equal(full["rgba8"][:n], pre["rgba8"][:n])
+    assert torch.equal(full["depth16"][:n], pre["depth16"][:n])
+    assert (full["depth16"][:n] != -1).sum().item() > 0
