@@ -781,6 +781,15 @@ def run_ours(args):
         except Exception as e:  # noqa: BLE001
             cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
                    "sample": f"failed: {e}"}
+    # our kernels per timed step on rank 0: k_cull_chunks + k_march_chunks +
+    # k_shade_tc + k_compose (k_march alone when tiles are not 128-slot
+    # aligned), + k_unpack (gather exchange) or k_flag_wait + one k_flag_set
+    # per peer (flag-synchronised p2p exchange)
+    launches_per_step = (4 if stride % 128 == 0 else 3)
+    if world > 1 and not p2p:
+        launches_per_step += 1
+    elif flags:
+        launches_per_step += 1 + (world - 1)
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -789,7 +798,8 @@ def run_ours(args):
             "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference-pipeline assets, "
             "random-init networks)", "config": workload_config(args, desc, W, H, len(scene)),
-            "e2e": e2e, "gpu_launches": (3 + (1 if (world > 1 and not p2p) else 0)) * args.steps, "roofline": roof, "cpu_baseline": cpu,
+            "e2e": e2e, "gpu_launches": launches_per_step * args.steps,
+            "gpu_launches_per_step": launches_per_step, "roofline": roof, "cpu_baseline": cpu,
             "clocks": csum, "verify": verify,
             "rank_kernel_ms": {"fields": ["k_march", "k_shade", "k_compose", "sm_mhz"],
                                "ranks": rank_kernel_ms},

@@ -837,6 +837,42 @@ int prof_mark(int i, cudaStream_t st) {
   return 0;
 }
 
+// A side stream per launching stream (thread-local cache of one): the
+// parameter upload and the live-count read-back run there so the launch
+// stream's kernels never queue behind a PCIe round trip.
+struct Aux {
+  cudaStream_t for_st = nullptr, s = nullptr;
+  cudaEvent_t ev_param = nullptr, ev_cull = nullptr;
+  int device = -1;
+};
+thread_local Aux g_aux;
+
+Aux &aux_for(cudaStream_t st) {
+  Aux &a = g_aux;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!a.s || a.device != dev) {
+    if (a.s) {
+      cudaStreamSynchronize(a.s);
+      cudaStreamDestroy(a.s);
+      cudaEventDestroy(a.ev_param);
+      cudaEventDestroy(a.ev_cull);
+      a.s = nullptr;
+    }
+    cudaError_t e = cudaStreamCreateWithFlags(&a.s, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&a.ev_param, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&a.ev_cull, cudaEventDisableTiming);
+    if (e != cudaSuccess) {
+      g_err = cudaGetErrorString(e);
+      a.s = nullptr;
+      return a;
+    }
+    a.device = dev;
+  }
+  a.for_st = st;
+  return a;
+}
+
 // Live-chunk count of an earlier frame per (workspace, stream): sizes the
 // marcher's grid without a host wait.
 struct LiveEstimate {
@@ -885,9 +921,14 @@ int launch_march_shade(int mode, const NolfInstance *ins, int n_inst, const Nolf
   hp->rect = rect;
   for (int k = 0; k <= n_inst; ++k) hp->qoff[k] = pl.qoff[(size_t)k];
   for (size_t i = 0; i < pl.cull.size(); ++i) hp->cull[i] = pl.cull[i];
-  CUDA_TRY(cudaMemcpyAsync(dp, hp, param_bytes(n_inst, n_cams), cudaMemcpyHostToDevice, st));
-  if ((rc = ring_release(slot, st))) return rc;
-  if (n_rays == 0) return 0;
+  // the parameter block goes up on a side stream (the copy overlaps the
+  // previous frame's kernels); the launch stream waits for it
+  Aux &ax = aux_for(st);
+  if (!ax.s) return fail(NOLF_ECUDA, "aux stream: %s", g_err.c_str());
+  CUDA_TRY(cudaMemcpyAsync(dp, hp, param_bytes(n_inst, n_cams), cudaMemcpyHostToDevice, ax.s));
+  CUDA_TRY(cudaEventRecord(ax.ev_param, ax.s));
+  CUDA_TRY(cudaStreamWaitEvent(st, ax.ev_param, 0));
+  if (n_rays == 0) return ring_release(slot, st);
   CUDA_TRY(cudaMemsetAsync(w.counts, 0, sizeof(unsigned) * (n_inst + 2), st));
 
   MarchArgs ma{};
@@ -944,9 +985,11 @@ int launch_march_shade(int mode, const NolfInstance *ins, int n_inst, const Nolf
     }
     const long long want = (long long)le.last + (long long)le.last / 8 + 2ll * num_sms();
     k_march_chunks<<<(unsigned)std::max<long long>(1, std::min(n_chunks, want)), kMarchThreads, 0, st>>>(ma);
-    if (!le.pending) {
-      CUDA_TRY(cudaMemcpyAsync(le.host, w.counts + n_inst, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
-      CUDA_TRY(cudaEventRecord(le.ev, st));
+    if (!le.pending) {          // read the live count back on the side stream: shading never waits for it
+      CUDA_TRY(cudaEventRecord(ax.ev_cull, st));
+      CUDA_TRY(cudaStreamWaitEvent(ax.s, ax.ev_cull, 0));
+      CUDA_TRY(cudaMemcpyAsync(le.host, w.counts + n_inst, sizeof(unsigned), cudaMemcpyDeviceToHost, ax.s));
+      CUDA_TRY(cudaEventRecord(le.ev, ax.s));
       le.pending = true;
     }
   }
@@ -986,11 +1029,13 @@ int launch_march_shade(int mode, const NolfInstance *ins, int n_inst, const Nolf
     k_compose<<<(unsigned)((n_thr + 255) / 256), 256, 0, st>>>(ca);
     CUDA_TRY(cudaGetLastError());
     if ((rc = prof_mark(3, st))) return rc;
+    if ((rc = ring_release(slot, st))) return rc;   // the block is reusable once this frame is done
   } else {
     if ((rc = run_shade(dp->inst, dp->qoff, n_inst, w, mode, rgba, depth, 0, counters, st, use_tc, phi_smem)))
       return rc;
     if ((rc = prof_mark(2, st))) return rc;
     if ((rc = prof_mark(3, st))) return rc;
+    if ((rc = ring_release(slot, st))) return rc;
   }
   return 0;
 }
