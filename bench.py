@@ -427,12 +427,25 @@ def run_ours(args):
         N.check(N.lib().nolf_memset_async(rgba_ptr, 0, NPX * 4, s))
         N.check(N.lib().nolf_memset_async(d_ptr, 0xFF, NPX * 2, s))
 
-    def release(seq, s):
-        """rank 0: frame seq consumed -> its buffer is re-cleared and may be overwritten"""
+    clear_stream = torch.cuda.Stream(device=dev) if (prefill and rank == 0) else None
+    clear_ev = [None, None]
+
+    def release(seq, ts):
+        """rank 0: frame seq consumed on torch stream ts -> its buffer is re-cleared
+        (side stream, off rank 0's critical path) and may then be overwritten"""
         if prefill:
-            clear(seq % 2, s)
-        for ptr in free_remote:
-            N.check(N.lib().nolf_flag_set(ptr, seq, s))
+            ev = torch.cuda.Event()
+            ev.record(ts)
+            clear_stream.wait_event(ev)
+            clear(seq % 2, clear_stream.cuda_stream)
+            for ptr in free_remote:
+                N.check(N.lib().nolf_flag_set(ptr, seq, clear_stream.cuda_stream))
+            cev = torch.cuda.Event()
+            cev.record(clear_stream)
+            clear_ev[seq % 2] = cev        # rank 0's own next render into this buffer waits
+        else:
+            for ptr in free_remote:
+                N.check(N.lib().nolf_flag_set(ptr, seq, ts.cuda_stream))
 
     if prefill and (world == 1 or rank == 0):
         clear(0, stream)
@@ -465,6 +478,8 @@ def run_ours(args):
             else:
                 o2 = {"rgba8": peer_frames[fb][0], "depth16": peer_frames[fb][1],
                       "counters": out["counters"]}
+                if rank == 0 and clear_ev[fb] is not None:
+                    torch.cuda.current_stream().wait_event(clear_ev[fb])   # buffer re-cleared
                 R.render(cam_arrays[k % n_cam], my_tiles, n_max, stride, o2, frame_layout=True,
                          peer=(rank != 0), prefilled=prefill)
             if flags:
@@ -475,7 +490,7 @@ def run_ours(args):
                     if before_barrier is not None:
                         torch.cuda.current_stream().wait_event(before_barrier)
                     if auto_release:
-                        release(seq, stream)
+                        release(seq, torch.cuda.current_stream())
                 return
             if before_barrier is not None:
                 torch.cuda.current_stream().wait_event(before_barrier)
@@ -665,7 +680,7 @@ def run_ours(args):
                         hosts[fb][:NPX * 4].view(NPX, 4).copy_(frames[fb][0], non_blocking=True)
                         hosts[fb][NPX * 4:].view(torch.int16).copy_(frames[fb][1], non_blocking=True)
                     if flags:              # downloaded: the peers may refill buffer fb
-                        release(seq_box[0], copy_stream.cuda_stream)
+                        release(seq_box[0], copy_stream)
                 ev = torch.cuda.Event()
                 ev.record(copy_stream)
                 done_copy[fb] = ev
@@ -695,7 +710,7 @@ def run_ours(args):
                 N.check(N.lib().nolf_memcpy_async(got.data_ptr(), peer_frames[fbv][0], NPX * 6,
                                                   torch.cuda.current_stream().cuda_stream))
                 if flags:
-                    release(seq_box[0], torch.cuda.current_stream().cuda_stream)
+                    release(seq_box[0], torch.cuda.current_stream())
             else:
                 got[:NPX * 4].copy_(frames[fbv][0].view(-1))
                 got[NPX * 4:].copy_(frames[fbv][1].view(torch.uint8).view(-1))
