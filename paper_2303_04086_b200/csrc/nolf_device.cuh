@@ -289,6 +289,37 @@ __device__ __forceinline__ void atlas_query_cid(const DevAtlas &at, int cid, con
   atlas_trilinear<C>(at, cid, x, out);
 }
 
+// query_atlas with the trilinear weights and sums in fp32 (the bf16 shading
+// path's diffuse term: 2/255 budget); cell / sub-voxel selection as above.
+__device__ __forceinline__ void atlas_query4_f(const DevAtlas &at, int cid, const double x[3], float out[4]) {
+  if (cid < 0) {
+    out[0] = out[1] = out[2] = out[3] = 0.f;
+    return;
+  }
+  int base[3];
+  double frac[3];
+  atlas_subvoxel(at, x, base, frac);
+  const int s = at.s;
+  const float *cube = at.cubes + (size_t)cid * (size_t)(s * s * s * 4);
+  float4 q[8];
+#pragma unroll
+  for (int c = 0; c < 8; ++c)
+    q[c] = __ldg(reinterpret_cast<const float4 *>(
+        cube + (((base[0] + (c & 1)) * s + (base[1] + ((c >> 1) & 1))) * s + (base[2] + ((c >> 2) & 1))) * 4));
+  const float f0 = (float)frac[0], f1 = (float)frac[1], f2 = (float)frac[2];
+  const float g0 = 1.0f - f0, g1 = 1.0f - f1, g2 = 1.0f - f2;
+  float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const float w = ((c & 1) ? f0 : g0) * (((c >> 1) & 1) ? f1 : g1) * (((c >> 2) & 1) ? f2 : g2);
+    a0 = fmaf(w, q[c].x, a0);
+    a1 = fmaf(w, q[c].y, a1);
+    a2 = fmaf(w, q[c].z, a2);
+    a3 = fmaf(w, q[c].w, a3);
+  }
+  out[0] = a0; out[1] = a1; out[2] = a2; out[3] = a3;
+}
+
 template <int C>
 __device__ __forceinline__ void atlas_query(const DevAtlas &at, const double x[3], float out[C]) {
   const int cid = atlas_cell_id(at, x);
@@ -369,6 +400,28 @@ __device__ __forceinline__ void sh_encode(const double d[3], double o[16]) {
   o[15] = M_(M_(C36, x), S_(xx, M_(3.0, yy)));
 #undef M_
 #undef S_
+}
+
+// sh_encode's polynomial in fp32 (inputs of the bf16 MLP path only).
+__device__ __forceinline__ void sh_encode_f(const double dd[3], float o[16]) {
+  const float x = (float)dd[0], y = (float)dd[1], z = (float)dd[2];
+  const float xx = x * x, yy = y * y, zz = z * z;
+  o[0] = 0.28209479177387814f;
+  o[1] = -0.4886025119029199f * y;
+  o[2] = 0.4886025119029199f * z;
+  o[3] = -0.4886025119029199f * x;
+  o[4] = 1.0925484305920792f * x * y;
+  o[5] = -1.0925484305920792f * y * z;
+  o[6] = 0.31539156525252005f * (2.0f * zz - xx - yy);
+  o[7] = -1.0925484305920792f * x * z;
+  o[8] = 0.5462742152960396f * (xx - yy);
+  o[9] = -0.5900435899266435f * y * (3.0f * xx - yy);
+  o[10] = 2.890611442640554f * x * y * z;
+  o[11] = -0.4570457994644658f * y * (4.0f * zz - xx - yy);
+  o[12] = 0.3731763325901154f * z * (2.0f * zz - 3.0f * xx - 3.0f * yy);
+  o[13] = -0.4570457994644658f * x * (4.0f * zz - xx - yy);
+  o[14] = 1.445305721320277f * z * (xx - yy);
+  o[15] = -0.5900435899266435f * x * (xx - 3.0f * yy);
 }
 
 __device__ __forceinline__ float sigmoidf_np(float z) {   // neural._sigmoid in f32

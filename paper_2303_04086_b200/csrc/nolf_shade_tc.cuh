@@ -200,7 +200,28 @@ __device__ __forceinline__ void tc_gather_inputs(const DevAsset &A, const TcSmem
   const int F = FIXED_F ? FIXED_F : A.F;
   int base[3];
   double w8[8];
-  base_weights(rec.p, A.N, base, w8);
+  float w8f[8];
+  if (FIXED_F == 2) {
+    // bf16 path: the corner (integer) addresses exactly as encoding.py, the
+    // weights and sums in fp32 -- they feed bf16 MLP inputs (2/255 budget)
+    float f[3], g[3];
+    const double rd = (double)A.N;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const double scaled = __dmul_rn(rec.p[k], rd);
+      const double fl = floor(scaled);
+      int bb = fl > (double)(A.N - 1) ? A.N - 1 : (int)fl;
+      if (bb < 0) bb = 0;
+      base[k] = bb;
+      f[k] = (float)(scaled - (double)bb);
+      g[k] = 1.0f - f[k];
+    }
+    const float gygz = g[1] * g[2], fygz = f[1] * g[2], gyfz = g[1] * f[2], fyfz = f[1] * f[2];
+    w8f[0] = g[0] * gygz; w8f[1] = f[0] * gygz; w8f[2] = g[0] * fygz; w8f[3] = f[0] * fygz;
+    w8f[4] = g[0] * gyfz; w8f[5] = f[0] * gyfz; w8f[6] = g[0] * fyfz; w8f[7] = f[0] * fyfz;
+  } else {
+    base_weights(rec.p, A.N, base, w8);
+  }
   double es[FIXED_F ? FIXED_F : kTcK0] = {};
   uint32_t slots[8];
   const int s1 = A.N + 1;
@@ -220,14 +241,24 @@ __device__ __forceinline__ void tc_gather_inputs(const DevAsset &A, const TcSmem
     slots[c] = slot >= A.m ? slot - A.m : slot;
   }
   if (FIXED_F == 2) {
-    float2 f[8];               // all 8 gathers in flight before the ordered sum
+    float2 f[8];               // all 8 gathers in flight before the sum
 #pragma unroll
     for (int c = 0; c < 8; ++c) f[c] = __ldg(reinterpret_cast<const float2 *>(A.feat) + slots[c]);
+    float e0 = 0.f, e1 = 0.f;
 #pragma unroll
     for (int c = 0; c < 8; ++c) {
-      es[0] = __dadd_rn(es[0], __dmul_rn((double)f[c].x, w8[c]));
-      es[1] = __dadd_rn(es[1], __dmul_rn((double)f[c].y, w8[c]));
+      e0 = fmaf(f[c].x, w8f[c], e0);
+      e1 = fmaf(f[c].y, w8f[c], e1);
     }
+    x[0] = e0;
+    x[1] = e1;
+    // SH degree 3 of d_obj (core.py:239-261) in fp32
+    float sh[16];
+    sh_encode_f(rec.d, sh);
+#pragma unroll
+    for (int q = 0; q < 16; ++q) x[2 + q] = sh[q];
+    if (A.refine_opacity) x[18] = (float)clampd(rec.alpha_c, 1e-4, 1.0 - 1e-4);
+    return;
   } else {
     for (int c = 0; c < 8; ++c)
       for (int q = 0; q < F; ++q)
@@ -342,7 +373,7 @@ __global__ void __launch_bounds__(kTcThreads) k_shade_tc(ShadeArgs args) {
       }
       if (want_dif) {
         float dv[4];
-        atlas_query_cid<4>(A.dif, dif_cid, rec.p, dv);
+        atlas_query4_f(A.dif, dif_cid, rec.p, dv);
         cd[0] = dv[0]; cd[1] = dv[1]; cd[2] = dv[2];
         tint = dv[3];
       }
@@ -357,17 +388,19 @@ __global__ void __launch_bounds__(kTcThreads) k_shade_tc(ShadeArgs args) {
 #pragma unroll
       for (int j = 0; j < 4; ++j)
         fs_out[j] = A.fs.act[j] == 0 ? z4[j] : (A.fs.act[j] == 1 ? sigmoidf_np(z4[j]) : expf(z4[j]));
-      const double ac = clampd(alpha_c, 1e-4, 1.0 - 1e-4);
-      const double z = (double)fs_out[3];
-      double alpha;
-      if (!A.use_opacity) alpha = clampd(alpha_c, 0.0, 1.0);
-      else if (A.refine_opacity) alpha = sigmoid_np(z + log(ac / (1.0 - ac)));
-      else alpha = sigmoid_np(z);
+      // opacity / combine (lightfield.py:291-336) in fp32: the bf16 path's budget
+      const float ac = (float)clampd(alpha_c, 1e-4, 1.0 - 1e-4);
+      const float z = fs_out[3];
+      float alpha;
+      if (!A.use_opacity) alpha = (float)clampd(alpha_c, 0.0, 1.0);
+      else if (A.refine_opacity) alpha = sigmoidf_np(z + logf(ac / (1.0f - ac)));
+      else alpha = sigmoidf_np(z);
+      const float tf = (float)tint;
       float4 o;
-      o.x = (float)clampd(__dadd_rn(cd[0], __dmul_rn(tint, (double)fs_out[0])), 0.0, 1.0);
-      o.y = (float)clampd(__dadd_rn(cd[1], __dmul_rn(tint, (double)fs_out[1])), 0.0, 1.0);
-      o.z = (float)clampd(__dadd_rn(cd[2], __dmul_rn(tint, (double)fs_out[2])), 0.0, 1.0);
-      o.w = (float)alpha;
+      o.x = fminf(fmaxf(fmaf(tf, fs_out[0], (float)cd[0]), 0.f), 1.f);
+      o.y = fminf(fmaxf(fmaf(tf, fs_out[1], (float)cd[1]), 0.f), 1.f);
+      o.z = fminf(fmaxf(fmaf(tf, fs_out[2], (float)cd[2]), 0.f), 1.f);
+      o.w = alpha;
       float dep = (float)__ddiv_rn(t_obj, I.scale);
       if (o.w <= 0.f) {
         o = make_float4(0.f, 0.f, 0.f, 0.f);
