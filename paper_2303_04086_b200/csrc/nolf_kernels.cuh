@@ -969,6 +969,25 @@ __device__ __forceinline__ void compose_px(const ComposeArgs &a, const long long
   o = make_float4(0.f, 0.f, 0.f, 0.f);
   od = __int_as_float(0x7f800000);
   if (n == 0) return;
+  if (n == 1) {                // one layer: no sort; the same f64 arithmetic as below
+    const float d0 = a.depth[p];
+    if (a.nhit && !(d0 < __int_as_float(0x7f800000))) return;   // missed / alpha <= 0: nothing
+    const float4 c = reinterpret_cast<const float4 *>(a.rgba)[p];
+    const double oc0 = __dadd_rn(0.0, __dmul_rn(1.0, (double)c.x));
+    const double oc1 = __dadd_rn(0.0, __dmul_rn(1.0, (double)c.y));
+    const double oc2 = __dadd_rn(0.0, __dmul_rn(1.0, (double)c.z));
+    const double trans = __dmul_rn(1.0, (double)(1.0f - c.w));
+    if (c.w > a.alpha_vis) od = d0;
+    o.x = (float)clampd(oc0, 0.0, 1.0);
+    o.y = (float)clampd(oc1, 0.0, 1.0);
+    o.z = (float)clampd(oc2, 0.0, 1.0);
+    o.w = (float)clampd(__dsub_rn(1.0, trans), 0.0, 1.0);
+    if (o.w <= 0.f) {
+      o = make_float4(0.f, 0.f, 0.f, 0.f);
+      od = __int_as_float(0x7f800000);
+    }
+    return;
+  }
   float dk[kMaxLayers];
   unsigned char ord[kMaxLayers];
   // stable insertion sort by depth (np.argsort kind="stable")
