@@ -988,6 +988,47 @@ __device__ __forceinline__ void compose_px(const ComposeArgs &a, const long long
     }
     return;
   }
+  if (n <= 4) {                // few layers: the same stable sort and f64 over, in registers
+    float dk4[4];
+    int ord4[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      dk4[k] = __int_as_float(0x7f800000);
+      ord4[k] = k;
+      if (k < n) dk4[k] = a.depth[(long long)k * a.layer_stride + p];
+    }
+    // stable: insertion by strict '>' (np.argsort kind="stable")
+#pragma unroll
+    for (int k = 1; k < 4; ++k)
+#pragma unroll
+      for (int j = k; j > 0; --j)
+        if (j <= k && k < n && dk4[j - 1] > dk4[j]) {
+          const float td = dk4[j - 1]; dk4[j - 1] = dk4[j]; dk4[j] = td;
+          const int to = ord4[j - 1]; ord4[j - 1] = ord4[j]; ord4[j] = to;
+        }
+    double oc0 = 0.0, oc1 = 0.0, oc2 = 0.0, trans = 1.0;
+    bool set = false;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      if (r >= n) break;
+      if (a.nhit && !(dk4[r] < __int_as_float(0x7f800000))) break;
+      const float4 c = reinterpret_cast<const float4 *>(a.rgba)[(long long)ord4[r] * a.layer_stride + p];
+      oc0 = __dadd_rn(oc0, __dmul_rn(trans, (double)c.x));
+      oc1 = __dadd_rn(oc1, __dmul_rn(trans, (double)c.y));
+      oc2 = __dadd_rn(oc2, __dmul_rn(trans, (double)c.z));
+      if (!set && c.w > a.alpha_vis) { od = dk4[r]; set = true; }
+      trans = __dmul_rn(trans, (double)(1.0f - c.w));
+    }
+    o.x = (float)clampd(oc0, 0.0, 1.0);
+    o.y = (float)clampd(oc1, 0.0, 1.0);
+    o.z = (float)clampd(oc2, 0.0, 1.0);
+    o.w = (float)clampd(__dsub_rn(1.0, trans), 0.0, 1.0);
+    if (o.w <= 0.f) {
+      o = make_float4(0.f, 0.f, 0.f, 0.f);
+      od = __int_as_float(0x7f800000);
+    }
+    return;
+  }
   float dk[kMaxLayers];
   unsigned char ord[kMaxLayers];
   // stable insertion sort by depth (np.argsort kind="stable")
