@@ -413,9 +413,15 @@ def run_ours(args):
         done_remote = open_flag(hs[0]) if rank != 0 else own
         free_remote = [open_flag(hs[j]) for j in range(1, world)] if rank == 0 else []
 
-    # (measured: at 1 GPU the 50 MB memset costs more than compose writing the
-    # dead chunks itself; with peers it saves ~80 % of the NVLink stores)
-    prefill = args.prefill == "on" and flags and not dma
+    # Frame buffers are pre-set to the miss encoding by their owner (rank 0 /
+    # the single GPU) so compose stores only chunks some instance reaches
+    # (with peers: ~80 % fewer NVLink stores).  A consumed buffer is queued for
+    # re-clearing; the clear runs on a side stream once the NEXT step has
+    # started (so it overlaps rendering, never the untimed L2 flush), then the
+    # peers' "free" flags are set and the owner's next render into that buffer
+    # waits for it.
+    prefill = args.prefill == "on" and ((flags and not dma) or world == 1)
+    owner = world == 1 or rank == 0
     last_fb = [0]
 
     def clear(fb, s):
@@ -427,27 +433,38 @@ def run_ours(args):
         N.check(N.lib().nolf_memset_async(rgba_ptr, 0, NPX * 4, s))
         N.check(N.lib().nolf_memset_async(d_ptr, 0xFF, NPX * 2, s))
 
-    clear_stream = torch.cuda.Stream(device=dev) if (prefill and rank == 0) else None
+    clear_stream = torch.cuda.Stream(device=dev) if (prefill and owner) else None
     clear_ev = [None, None]
+    pending = []
 
-    def release(seq, ts):
-        """rank 0: frame seq consumed on torch stream ts -> its buffer is re-cleared
-        (side stream, off rank 0's critical path) and may then be overwritten"""
+    def release(fb, seq, ts):
+        """owner: buffer fb (frame seq, None at 1 GPU) consumed on torch stream ts"""
         if prefill:
             ev = torch.cuda.Event()
             ev.record(ts)
-            clear_stream.wait_event(ev)
-            clear(seq % 2, clear_stream.cuda_stream)
-            for ptr in free_remote:
-                N.check(N.lib().nolf_flag_set(ptr, seq, clear_stream.cuda_stream))
-            cev = torch.cuda.Event()
-            cev.record(clear_stream)
-            clear_ev[seq % 2] = cev        # rank 0's own next render into this buffer waits
-        else:
+            pending.append((fb, seq, ev))
+        elif seq is not None:
             for ptr in free_remote:
                 N.check(N.lib().nolf_flag_set(ptr, seq, ts.cuda_stream))
 
-    if prefill and (world == 1 or rank == 0):
+    def flush_pending():
+        if not pending:
+            return
+        start = torch.cuda.Event()
+        start.record(torch.cuda.current_stream())      # inside this step's timed window
+        clear_stream.wait_event(start)
+        for fb, seq, ev in pending:
+            clear_stream.wait_event(ev)
+            clear(fb, clear_stream.cuda_stream)
+            if seq is not None:
+                for ptr in free_remote:
+                    N.check(N.lib().nolf_flag_set(ptr, seq, clear_stream.cuda_stream))
+            cev = torch.cuda.Event()
+            cev.record(clear_stream)
+            clear_ev[fb] = cev
+        pending.clear()
+
+    if prefill and owner:
         clear(0, stream)
         clear(1, stream)
         torch.cuda.synchronize()
@@ -455,6 +472,8 @@ def run_ours(args):
         dist.barrier()
 
     def step(k, fb=0, before_barrier=None, auto_release=True):
+        if prefill and owner:
+            flush_pending()
         if p2p and flags:
             seq_box[0] += 1
             seq = seq_box[0]
@@ -490,7 +509,7 @@ def run_ours(args):
                     if before_barrier is not None:
                         torch.cuda.current_stream().wait_event(before_barrier)
                     if auto_release:
-                        release(seq, torch.cuda.current_stream())
+                        release(fb, seq, torch.cuda.current_stream())
                 return
             if before_barrier is not None:
                 torch.cuda.current_stream().wait_event(before_barrier)
@@ -500,10 +519,12 @@ def run_ours(args):
         last_fb[0] = fb
         if world == 1:             # single GPU: compose writes the frame directly
             out["rgba8"], out["depth16"] = frame, frame_d
-            if prefill:
-                clear(fb, stream)
+            if prefill and clear_ev[fb] is not None:
+                torch.cuda.current_stream().wait_event(clear_ev[fb])   # buffer re-cleared
         R.render(cam_arrays[k % n_cam], my_tiles, n_max, stride, out, frame_layout=(world == 1),
                  prefilled=(world == 1 and prefill))
+        if world == 1 and auto_release:
+            release(fb, None, torch.cuda.current_stream())
         if world > 1:
             # frame composer: NCCL gather of every rank's encoded tiles, then
             # one unpack kernel writes the row-major frame on rank 0
@@ -667,7 +688,7 @@ def run_ours(args):
             # completion collective passes, so rank 0 enters it only after
             # the download of step k-1 (buffer fb^1) finished
             step(k, fb, before_barrier=done_copy[fb ^ 1] if (p2p and rank == 0) else None,
-                 auto_release=False)
+                 auto_release=not (flags or world == 1))
             if rank == 0:
                 rendered = torch.cuda.Event()
                 rendered.record(comp)
@@ -679,8 +700,8 @@ def run_ours(args):
                     else:
                         hosts[fb][:NPX * 4].view(NPX, 4).copy_(frames[fb][0], non_blocking=True)
                         hosts[fb][NPX * 4:].view(torch.int16).copy_(frames[fb][1], non_blocking=True)
-                    if flags:              # downloaded: the peers may refill buffer fb
-                        release(seq_box[0], copy_stream)
+                    if flags or world == 1:   # downloaded: the buffer may be re-cleared / refilled
+                        release(fb, seq_box[0] if flags else None, copy_stream)
                 ev = torch.cuda.Event()
                 ev.record(copy_stream)
                 done_copy[fb] = ev
@@ -710,10 +731,12 @@ def run_ours(args):
                 N.check(N.lib().nolf_memcpy_async(got.data_ptr(), peer_frames[fbv][0], NPX * 6,
                                                   torch.cuda.current_stream().cuda_stream))
                 if flags:
-                    release(seq_box[0], torch.cuda.current_stream())
+                    release(fbv, seq_box[0], torch.cuda.current_stream())
             else:
                 got[:NPX * 4].copy_(frames[fbv][0].view(-1))
                 got[NPX * 4:].copy_(frames[fbv][1].view(torch.uint8).view(-1))
+                if world == 1:
+                    release(fbv, None, torch.cuda.current_stream())
             all_tiles = torch.from_numpy(tiles.astype(np.int32)).to(dev)
             ref = {"rgba8": torch.empty((NPX, 4), dtype=torch.uint8, device=dev),
                    "depth16": torch.empty(NPX, dtype=torch.int16, device=dev),
