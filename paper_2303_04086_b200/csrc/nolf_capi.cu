@@ -1026,7 +1026,16 @@ int launch_march_shade(int mode, const NolfInstance *ins, int n_inst, const Nolf
         ((uintptr_t)sout->depth16 & 15) == 0)
       ca.four = 2;
     const long long n_thr = ca.four == 2 ? n_rays / 8 : ca.four ? n_rays / 4 : n_rays;
-    k_compose<<<(unsigned)((n_thr + 255) / 256), 256, 0, st>>>(ca);
+    if (chunked && ca.prefilled && ca.four == 2) {
+      // misses are already in place: only the live chunks (grid from the
+      // earlier frame's live count, grid-stride for any size)
+      const long long n_chunks = n_rays / kMarchThreads;
+      const long long live = std::min<long long>(n_chunks, g_live.last + g_live.last / 8 + 2ll * num_sms());
+      k_compose_live<<<(unsigned)std::max<long long>(1, (live * 16 + 255) / 256), 256, 0, st>>>(ca, w.chunk_list,
+                                                                                             w.counts + n_inst);
+    } else {
+      k_compose<<<(unsigned)((n_thr + 255) / 256), 256, 0, st>>>(ca);
+    }
     CUDA_TRY(cudaGetLastError());
     if ((rc = prof_mark(3, st))) return rc;
     if ((rc = ring_release(slot, st))) return rc;   // the block is reusable once this frame is done

@@ -1226,6 +1226,19 @@ __global__ void __launch_bounds__(256) k_compose(ComposeArgs a) {
   }                            // the completion collective that follows
 }
 
+// Prefilled outputs: compose only the live chunks, from the compacted list
+// (16 threads x 8 slots per chunk, grid-stride over the list's length).
+__global__ void __launch_bounds__(256) k_compose_live(ComposeArgs a, const unsigned *live_list, const unsigned *count) {
+  const long long total = (long long)count[0] * 16;
+  for (long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x; g < total;
+       g += (long long)gridDim.x * blockDim.x)
+    compose_eight(a, (long long)live_list[g >> 4] * 128 + (g & 15) * 8);
+  if (a.peer) {
+    __syncthreads();
+    if (threadIdx.x == 0) __threadfence_system();
+  }
+}
+
 // Frame assembly after an all-rank gather: rank r's buffer holds n_per_rank
 // tile slots of rgba8 (stride*4 B each) followed by their depth16; slot_tiles
 // lists the tile of every (rank, slot) in rank-major order.
