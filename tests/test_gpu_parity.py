@@ -287,3 +287,47 @@ def test_random_scene_matches_oracle(seed):
     assert np.array_equal(out.depth, o_depth), "depth bits differ from the every-step oracle"
     assert np.abs(out.rgba - o_rgba).max() <= 1e-6
     assert (cnt.hit_pixels, cnt.march_samples) == (ocnt.hit_pixels, ocnt.march_samples)
+
+
+_FULL = {}
+
+
+def _full_size(kind):
+    """A reference-default asset (b=32, r=8, PSH N=64: power-of-two grid path)."""
+    from paper_2303_04086_b200 import synth
+    if kind not in _FULL:
+        _FULL[kind] = synth.make_asset(kind, seed=7, shell_cameras_n=64, shell_image_size=32,
+                                       diffuse_shell_cameras=16, diffuse_shell_image=16)
+    return _FULL[kind]
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_random_full_size_scene_matches_oracle(seed):
+    """As above with reference-default (b=32, r=8, N=64) assets: the integer
+    sub-voxel path, long distance-field jumps and the zero masks at full
+    resolution, against the every-step oracle."""
+    import math
+    from paper_2303_04086_b200.model import orbit_camera
+    rng = np.random.default_rng(200 + seed)
+    scene = []
+    for kind in ("sphere", "box", "two"):
+        m = np.eye(4)
+        th = rng.uniform(0, 2 * math.pi)
+        rot = np.array([[math.cos(th), -math.sin(th), 0], [math.sin(th), math.cos(th), 0], [0, 0, 1]])
+        m[:3, :3] = rot * rng.uniform(0.4, 0.9)
+        m[:3, 3] = rng.uniform(-0.6, 0.6, 3)
+        scene.append((_full_size(kind), m))
+    cam = orbit_camera(rng.uniform(0, 2 * math.pi), rng.uniform(-0.5, 0.8), radius=rng.uniform(1.5, 2.5),
+                       size=96, target=tuple(rng.uniform(0.0, 0.5, 3)))
+    cnt, ocnt = RenderCounters(), RenderCounters()
+    out = R.render_scene(scene, cam, cnt, tile=32)
+    rg, dp = [], []
+    for a, m in scene:
+        r_, d_ = O.render_rect(a, cam, (0, 0, 96, 96), ocnt, transform=m)
+        rg.append(r_)
+        dp.append(d_)
+    o_rgba, o_depth = O.compose(np.stack(rg), np.stack(dp))
+    assert np.isfinite(o_depth).sum() > 50
+    assert np.array_equal(out.depth, o_depth), "depth bits differ from the every-step oracle"
+    assert np.abs(out.rgba - o_rgba).max() <= 1e-6
+    assert (cnt.hit_pixels, cnt.march_samples) == (ocnt.hit_pixels, ocnt.march_samples)
