@@ -362,9 +362,9 @@ size_t ws_layout(int n_inst, long long queue_recs, int layers, long long P, char
     return base ? base + o : nullptr;
   };
   const size_t n = (size_t)(P > 0 ? P : 1);
-  char *counts = take(sizeof(unsigned) * (size_t)((n_inst > 0 ? n_inst : 1) + 2));
+  char *counts = take(sizeof(unsigned) * (size_t)((n_inst > 0 ? n_inst : 1) + 2 + kChunkBuckets));
   const size_t n_chunks = (size_t)((P > 0 ? P : 1) + 127) / 128;
-  char *chunk_list = take(sizeof(unsigned) * n_chunks);
+  char *chunk_list = take(sizeof(unsigned) * n_chunks * kChunkBuckets);
   char *chunk_live = take(n_chunks);
   char *queue = take(sizeof(HitRec) * (size_t)(queue_recs > 0 ? queue_recs : 1));
   char *nhit = take(layers > 0 ? n : 1);
@@ -929,7 +929,7 @@ int launch_march_shade(int mode, const NolfInstance *ins, int n_inst, const Nolf
   CUDA_TRY(cudaEventRecord(ax.ev_param, ax.s));
   CUDA_TRY(cudaStreamWaitEvent(st, ax.ev_param, 0));
   if (n_rays == 0) return ring_release(slot, st);
-  CUDA_TRY(cudaMemsetAsync(w.counts, 0, sizeof(unsigned) * (n_inst + 2), st));
+  CUDA_TRY(cudaMemsetAsync(w.counts, 0, sizeof(unsigned) * (n_inst + 2 + kChunkBuckets), st));
 
   MarchArgs ma{};
   ma.inst = dp->inst;
@@ -961,6 +961,7 @@ int launch_march_shade(int mode, const NolfInstance *ins, int n_inst, const Nolf
     const long long n_chunks = n_rays / kMarchThreads;
     ma.chunks = w.chunk_list;
     ma.n_chunks = w.counts + n_inst;
+    ma.list_stride = n_chunks;
     ma.fetch = w.counts + n_inst + 1;
     k_cull_chunks<<<(unsigned)((n_chunks + 127) / 128), 128, 0, st>>>(ma, n_chunks, w.chunk_live, w.chunk_list,
                                                                       w.counts + n_inst);
@@ -984,6 +985,8 @@ int launch_march_shade(int mode, const NolfInstance *ins, int n_inst, const Nolf
       le.pending = false;
     }
     const long long want = (long long)le.last + (long long)le.last / 8 + 2ll * num_sms();
+    // a launch of only a few waves is bounded by its heaviest CTAs: start them first
+    ma.heavy_first = le.last < 3ll * NOLF_MARCH_MINB * num_sms() ? 1 : 0;
     k_march_chunks<<<(unsigned)std::max<long long>(1, std::min(n_chunks, want)), kMarchThreads, 0, st>>>(ma);
     if (!le.pending) {          // read the live count back on the side stream: shading never waits for it
       CUDA_TRY(cudaEventRecord(ax.ev_cull, st));
@@ -1032,7 +1035,7 @@ int launch_march_shade(int mode, const NolfInstance *ins, int n_inst, const Nolf
       const long long n_chunks = n_rays / kMarchThreads;
       const long long live = std::min<long long>(n_chunks, g_live.last + g_live.last / 8 + 2ll * num_sms());
       k_compose_live<<<(unsigned)std::max<long long>(1, (live * 16 + 255) / 256), 256, 0, st>>>(ca, w.chunk_list,
-                                                                                             w.counts + n_inst);
+                                                                                             w.counts + n_inst, n_chunks);
     } else {
       k_compose<<<(unsigned)((n_thr + 255) / 256), 256, 0, st>>>(ca);
     }

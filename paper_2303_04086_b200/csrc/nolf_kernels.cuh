@@ -64,10 +64,29 @@ struct MarchArgs {
   // scene mode with 128-slot-aligned tiles: compacted list of the chunks
   // (128 consecutive slots of one tile) some screen box meets, and the
   // persistent marcher's work counter
-  const unsigned *chunks;
-  const unsigned *n_chunks;
+  const unsigned *chunks;      // live chunks bucketed by candidate count: bucket b at chunks + b * list_stride
+  const unsigned *n_chunks;    // [0] all live chunks, [2 + b] bucket b's count (b = 1..kChunkBuckets-1)
   unsigned *fetch;
+  long long list_stride;
+  int heavy_first;             // walk the buckets (most candidates first) instead of the spatial list
 };
+
+constexpr int kChunkBuckets = 8;   // candidate-count buckets (the last one: >= 7 instances)
+
+// it-th live chunk: spatial order (list region 0, best cache locality) or
+// heavy-first (most candidate instances first, so the longest CTAs start
+// early and light ones fill the tail -- for launches of only a few waves).
+__device__ __forceinline__ unsigned chunk_at(const unsigned *list, const unsigned *counts, long long stride,
+                                             unsigned it, int heavy_first) {
+  if (!heavy_first) return list[it];
+#pragma unroll
+  for (int b = kChunkBuckets - 1; b >= 1; --b) {
+    const unsigned c = counts[2 + b];
+    if (it < c) return list[(long long)b * stride + it];
+    it -= c;
+  }
+  return 0u;
+}
 
 // Sample i's clipped position and index cell, exactly as march_rays computes
 // them (t_mid = t_near + (i+0.5)*step ; pos = clip(o + t_mid*d, 0, 1)).
@@ -620,6 +639,7 @@ __global__ void __launch_bounds__(128) k_cull_chunks(MarchArgs args, long long n
                                                      unsigned *list, unsigned *count) {
   const long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   bool live = false;
+  int ncand = 0;
   if (c < n_chunks) {
     long long t, local0;
     split_slot(c * kMarchThreads, args.tile_stride, t, local0);
@@ -639,20 +659,30 @@ __global__ void __launch_bounds__(128) k_cull_chunks(MarchArgs args, long long n
       }
       if (yb > ya && !((w & 7) == 0 && (h & 3) == 0)) { xa = 0; xb = w - 1; }   // row-major: rows span the width
       xa += tp.x0; xb += tp.x0; ya += tp.y0; yb += tp.y0;
-      for (int k = 0; k < args.n_inst && !live; ++k) {
+      for (int k = 0; k < args.n_inst; ++k) {
         const ScreenBox bb = args.cull[k * args.n_cams + tp.cam];
-        live = bb.x0 <= bb.x1 && bb.x0 <= xb && bb.x1 >= xa && bb.y0 <= yb && bb.y1 >= ya;
+        ncand += (bb.x0 <= bb.x1 && bb.x0 <= xb && bb.x1 >= xa && bb.y0 <= yb && bb.y1 >= ya) ? 1 : 0;
       }
+      live = ncand > 0;
     }
     chunk_live[c] = live ? 1 : 0;
   }
+  const unsigned lane = threadIdx.x & 31;
   const unsigned ballot = __ballot_sync(0xffffffffu, live);
   if (ballot) {
-    const unsigned lane = threadIdx.x & 31;
-    unsigned base = 0;
-    if (lane == __ffs(ballot) - 1) base = atomicAdd(count, (unsigned)__popc(ballot));
-    base = __shfl_sync(0xffffffffu, base, __ffs(ballot) - 1);
-    if (live) list[base + __popc(ballot & ((1u << lane) - 1u))] = (unsigned)c;
+    unsigned sbase = 0;        // spatial list (region 0) and the total
+    if (lane == __ffs(ballot) - 1) sbase = atomicAdd(count, (unsigned)__popc(ballot));
+    sbase = __shfl_sync(0xffffffffu, sbase, __ffs(ballot) - 1);
+    if (live) list[sbase + __popc(ballot & ((1u << lane) - 1u))] = (unsigned)c;
+    if (live) {                // and this chunk's candidate-count bucket (regions 1..)
+      const int b = min(ncand, kChunkBuckets - 1);
+      const unsigned peers = __match_any_sync(ballot, b);
+      const int leader = __ffs(peers) - 1;
+      unsigned base = 0;
+      if ((int)lane == leader) base = atomicAdd(count + 2 + b, (unsigned)__popc(peers));
+      base = __shfl_sync(peers, base, leader);
+      list[(long long)b * n_chunks + base + __popc(peers & ((1u << lane) - 1u))] = (unsigned)c;
+    }
   }
 }
 
@@ -664,7 +694,7 @@ __global__ void __launch_bounds__(kMarchThreads, NOLF_MARCH_MINB) k_march_chunks
   const unsigned n = *args.n_chunks;
   stat_cta_start();
   for (unsigned it = blockIdx.x; it < n; it += gridDim.x)   // normally one pass: the grid is sized
-    march_chunk<kModeScene>(args, args.chunks[it], false);  // from the previous frame's count
+    march_chunk<kModeScene>(args, chunk_at(args.chunks, args.n_chunks, args.list_stride, it, args.heavy_first), false);
   stat_cta_end();
 }
 
@@ -1228,11 +1258,12 @@ __global__ void __launch_bounds__(256) k_compose(ComposeArgs a) {
 
 // Prefilled outputs: compose only the live chunks, from the compacted list
 // (16 threads x 8 slots per chunk, grid-stride over the list's length).
-__global__ void __launch_bounds__(256) k_compose_live(ComposeArgs a, const unsigned *live_list, const unsigned *count) {
+__global__ void __launch_bounds__(256) k_compose_live(ComposeArgs a, const unsigned *live_list, const unsigned *count,
+                                                      long long list_stride) {
   const long long total = (long long)count[0] * 16;
   for (long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x; g < total;
        g += (long long)gridDim.x * blockDim.x)
-    compose_eight(a, (long long)live_list[g >> 4] * 128 + (g & 15) * 8);
+    compose_eight(a, (long long)live_list[g >> 4] * 128 + (g & 15) * 8);   // spatial list
   if (a.peer) {
     __syncthreads();
     if (threadIdx.x == 0) __threadfence_system();
