@@ -986,7 +986,8 @@ int launch_march_shade(int mode, const NolfInstance *ins, int n_inst, const Nolf
     }
     const long long want = (long long)le.last + (long long)le.last / 8 + 2ll * num_sms();
     // a launch of only a few waves is bounded by its heaviest CTAs: start them first
-    ma.heavy_first = le.last < 3ll * NOLF_MARCH_MINB * num_sms() ? 1 : 0;
+    static const long long heavy_waves = getenv("NOLF_HEAVY_WAVES") ? atoll(getenv("NOLF_HEAVY_WAVES")) : 3;
+    ma.heavy_first = le.last < heavy_waves * NOLF_MARCH_MINB * num_sms() ? 1 : 0;
     k_march_chunks<<<(unsigned)std::max<long long>(1, std::min(n_chunks, want)), kMarchThreads, 0, st>>>(ma);
     if (!le.pending) {          // read the live count back on the side stream: shading never waits for it
       CUDA_TRY(cudaEventRecord(ax.ev_cull, st));
