@@ -798,7 +798,7 @@ def run_ours(args):
             kern_caps = json.load(open(path)).get("kernels", {})
             # the march phase is k_cull_chunks + k_march_chunks (k_march<> for unaligned tiles)
             names_of = {"k_march": ("k_march", "k_march_chunks", "k_cull_chunks"),
-                        "k_shade": ("k_shade", "k_shade_tc"), "k_compose": ("k_compose",)}[top]
+                        "k_shade": ("k_shade", "k_shade_tc"), "k_compose": ("k_compose", "k_compose_live")}[top]
             hit = [v for k, v in kern_caps.items() if k.split("<")[0] in names_of]
             if hit:
                 roof["traffic"] = float(sum(v["dram_bytes_per_launch"] for v in hit))
