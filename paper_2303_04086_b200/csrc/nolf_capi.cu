@@ -963,9 +963,6 @@ int launch_march_shade(int mode, const NolfInstance *ins, int n_inst, const Nolf
     ma.n_chunks = w.counts + n_inst;
     ma.list_stride = n_chunks;
     ma.fetch = w.counts + n_inst + 1;
-    k_cull_chunks<<<(unsigned)((n_chunks + 127) / 128), 128, 0, st>>>(ma, n_chunks, w.chunk_live, w.chunk_list,
-                                                                      w.counts + n_inst);
-    CUDA_TRY(cudaGetLastError());
     // grid from the last live count that has landed on the host (async
     // read-back of an earlier frame on this workspace; worst case at first)
     LiveEstimate &le = g_live;
@@ -988,9 +985,12 @@ int launch_march_shade(int mode, const NolfInstance *ins, int n_inst, const Nolf
     // a launch of only a few waves is bounded by its heaviest CTAs: start them first
     static const long long heavy_waves = getenv("NOLF_HEAVY_WAVES") ? atoll(getenv("NOLF_HEAVY_WAVES")) : 3;
     ma.heavy_first = le.last < heavy_waves * NOLF_MARCH_MINB * num_sms() ? 1 : 0;
+    k_cull_chunks<<<(unsigned)((n_chunks + 127) / 128), 128, 0, st>>>(ma, n_chunks, w.chunk_live, w.chunk_list,
+                                                                      w.counts + n_inst);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaEventRecord(ax.ev_cull, st));   // the live count is final here
     k_march_chunks<<<(unsigned)std::max<long long>(1, std::min(n_chunks, want)), kMarchThreads, 0, st>>>(ma);
     if (!le.pending) {          // read the live count back on the side stream: shading never waits for it
-      CUDA_TRY(cudaEventRecord(ax.ev_cull, st));
       CUDA_TRY(cudaStreamWaitEvent(ax.s, ax.ev_cull, 0));
       CUDA_TRY(cudaMemcpyAsync(le.host, w.counts + n_inst, sizeof(unsigned), cudaMemcpyDeviceToHost, ax.s));
       CUDA_TRY(cudaEventRecord(le.ev, ax.s));

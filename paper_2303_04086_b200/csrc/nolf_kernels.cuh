@@ -659,9 +659,10 @@ __global__ void __launch_bounds__(128) k_cull_chunks(MarchArgs args, long long n
       }
       if (yb > ya && !((w & 7) == 0 && (h & 3) == 0)) { xa = 0; xb = w - 1; }   // row-major: rows span the width
       xa += tp.x0; xb += tp.x0; ya += tp.y0; yb += tp.y0;
-      for (int k = 0; k < args.n_inst; ++k) {
+      for (int k = 0; k < args.n_inst; ++k) {   // count them only when the buckets are used
         const ScreenBox bb = args.cull[k * args.n_cams + tp.cam];
         ncand += (bb.x0 <= bb.x1 && bb.x0 <= xb && bb.x1 >= xa && bb.y0 <= yb && bb.y1 >= ya) ? 1 : 0;
+        if (ncand && !args.heavy_first) break;
       }
       live = ncand > 0;
     }
@@ -674,7 +675,7 @@ __global__ void __launch_bounds__(128) k_cull_chunks(MarchArgs args, long long n
     if (lane == __ffs(ballot) - 1) sbase = atomicAdd(count, (unsigned)__popc(ballot));
     sbase = __shfl_sync(0xffffffffu, sbase, __ffs(ballot) - 1);
     if (live) list[sbase + __popc(ballot & ((1u << lane) - 1u))] = (unsigned)c;
-    if (live) {                // and this chunk's candidate-count bucket (regions 1..)
+    if (live && args.heavy_first) {   // and this chunk's candidate-count bucket (regions 1..)
       const int b = min(ncand, kChunkBuckets - 1);
       const unsigned peers = __match_any_sync(ballot, b);
       const int leader = __ffs(peers) - 1;
