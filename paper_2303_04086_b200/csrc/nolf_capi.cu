@@ -651,6 +651,9 @@ int nolf_asset_create(const NolfAssetDesc *d, int device, nolf_asset_t *out) {
   H.t_stop = d->t_stop;
   H.alpha_floor = d->alpha_floor;
   if (!(H.step > 0.0)) return bail(fail(NOLF_EINVAL, "march step must be positive"));
+  H.inv_step = 1.0 / H.step;
+  H.inv_step_f = (float)(1.0 / H.step);
+  H.inv_b_f = 1.0f / (float)H.den.b;
   for (int k = 0; k < 3; ++k) {
     H.pmin[k] = d->proxy_min[k];
     H.pmax[k] = d->proxy_max[k];

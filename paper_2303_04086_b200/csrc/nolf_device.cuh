@@ -68,6 +68,8 @@ struct DevAsset {              // LightFieldAsset (lightfield.py:217-248)
   const float *hg_feat[kMaxLevels];
   DevMlp fs, fd;
   double step, t_stop, alpha_floor;
+  double inv_step;             // 1 / step: only for conservative sample-index bounds (margins absorb its rounding)
+  float inv_step_f, inv_b_f;   // fp32 1/step and 1/b: the march's jump estimates (verified exactly)
   double pmin[3], pmax[3];
   int use_hit_point, use_opacity, refine_opacity, use_tint, use_diffuse_color;
   int mlp_mode;

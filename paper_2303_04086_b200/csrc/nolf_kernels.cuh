@@ -235,8 +235,8 @@ __device__ __forceinline__ MarchOut march_ray(const DevAsset &A, const double o[
   const DevAtlas &at = A.den;
   const double delta = A.step;
   const int b = at.b;
-  const float inv_bf = 1.0f / (float)b;
-  const float inv_delta_f = (float)(1.0 / delta);
+  const float inv_bf = A.inv_b_f;
+  const float inv_delta_f = A.inv_step_f;
   const float t_near_f = (float)t_near;
   double best_w = 0.0, trans = 1.0, alpha_c = 0.0, t_hit = r.t_hit;
   int samples = 0;
@@ -505,7 +505,7 @@ __device__ __forceinline__ bool prepare_march(const DevInst &I, const DevAsset &
     if (!slab<true>(A.cull_lo, A.cull_hi, o, d, ca, cb, inv) || A.cull_empty) {
       boxhit = false;                     // never meets an occupied cell: exact miss
     } else {
-      const double f = floor((ca - sp.t_near) / A.step - 2.5);
+      const double f = floor((ca - sp.t_near) * A.inv_step - 2.5);   // 2-sample margins absorb the rounding
       sp.i_start = f > 0.0 ? (f < 2.0e9 ? (int)f : 2000000000) : 0;
       sp.t_end = cb + 2.0 * A.step;
     }
@@ -513,7 +513,7 @@ __device__ __forceinline__ bool prepare_march(const DevInst &I, const DevAsset &
   if (boxhit) {
     // every sample the march can visit has index in [i_start, i_hi]
     const double lim = fmin(sp.t_far, sp.t_end);
-    const double hf = floor((lim - sp.t_near) / A.step) + 2.0;
+    const double hf = floor((lim - sp.t_near) * A.inv_step) + 2.0;
     sp.noclip = sp.t_near < lim && hf < 2.0e9 && samples_inside_unit(o, d, sp.t_near, A.step, sp.i_start, (int)hf);
   }
   return boxhit;
