@@ -72,6 +72,9 @@ def parse():
     p.add_argument("--sync", default="flags", choices=["flags", "nccl"],
                    help="p2p frame completion: flags = peer-mapped u32 flags set/polled by tiny kernels "
                         "(no collective); nccl = a 1-element all-reduce per frame")
+    p.add_argument("--frames", type=int, default=3,
+                   help="p2p + flags: frame buffers in rank 0's ring (a peer renders frame seq once "
+                        "frame seq - frames was consumed and re-cleared)")
     p.add_argument("--exchange", default="p2p", choices=["p2p", "dma", "gather"],
                    help="N>1 frame composer: compose stores into rank 0's frame over NVLink "
                         "(CUDA IPC peer memory) or NCCL gather + unpack kernel")
@@ -359,14 +362,15 @@ def run_ours(args):
     bands_dev = row_bands(world, rank, n_views, W, H, T) if dma else []
     peer_frames = []
     token = torch.zeros(1, dtype=torch.float32, device=dev)
+    NB = max(2, args.frames) if (p2p and args.sync == "flags") else 2   # frame buffers in the ring
     if p2p:
         import ctypes
         FB = NPX * 6
-        hbuf = torch.zeros(2 * 64, dtype=torch.uint8, device=dev)
+        hbuf = torch.zeros(NB * 64, dtype=torch.uint8, device=dev)
         raw = []
         if rank == 0:
-            hh = (ctypes.c_uint8 * 128)()
-            for i in range(2):
+            hh = (ctypes.c_uint8 * (64 * NB))()
+            for i in range(NB):
                 ptr = ctypes.c_void_p()
                 N.check(N.lib().nolf_device_alloc(FB, ctypes.byref(ptr)))
                 N.check(N.lib().nolf_ipc_get_handle(ptr, ctypes.byref(hh, 64 * i)))
@@ -374,8 +378,8 @@ def run_ours(args):
             hbuf.copy_(torch.tensor(list(bytes(hh)), dtype=torch.uint8))
         dist.broadcast(hbuf, src=0)
         if rank != 0:
-            hh = (ctypes.c_uint8 * 128)(*hbuf.cpu().tolist())
-            for i in range(2):
+            hh = (ctypes.c_uint8 * (64 * NB))(*hbuf.cpu().tolist())
+            for i in range(NB):
                 ptr = ctypes.c_void_p()
                 N.check(N.lib().nolf_ipc_open_handle(ctypes.byref(hh, 64 * i), ctypes.byref(ptr)))
                 raw.append(ptr.value)
@@ -384,7 +388,7 @@ def run_ours(args):
     # ---- frame-completion flags (p2p, --sync flags): rank 0 owns done[world]
     # (peer r sets done[r] = seq after its stores), every peer owns free
     # (rank 0 sets it = seq once frame seq is consumed, so a peer reuses a
-    # frame buffer only after rank 0 is done with it: double buffering)
+    # frame buffer only after rank 0 is done with it: a ring of --frames buffers)
     flags = p2p and args.sync == "flags"
     seq_box = [0]
     timeout_flag = torch.zeros(1, dtype=torch.int32, device=dev)
@@ -434,7 +438,7 @@ def run_ours(args):
         N.check(N.lib().nolf_memset_async(d_ptr, 0xFF, NPX * 2, s))
 
     clear_stream = torch.cuda.Stream(device=dev) if (prefill and owner) else None
-    clear_ev = [None, None]
+    clear_ev = [None] * NB
     pending = []
 
     def release(fb, seq, ts):
@@ -465,8 +469,8 @@ def run_ours(args):
         pending.clear()
 
     if prefill and owner:
-        clear(0, stream)
-        clear(1, stream)
+        for i in range(NB if p2p else 2):
+            clear(i, stream)
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -477,10 +481,10 @@ def run_ours(args):
         if p2p and flags:
             seq_box[0] += 1
             seq = seq_box[0]
-            fb = seq % 2                   # the buffer protocol alternates by frame sequence
+            fb = seq % NB                  # the buffer ring rotates by frame sequence
             last_fb[0] = fb
-            if rank != 0 and seq > 2:      # buffer fb held frame seq-2: wait until rank 0 is done
-                N.check(N.lib().nolf_flag_wait(own, 1, seq - 2, timeout_flag.data_ptr(), stream))
+            if rank != 0 and seq > NB:     # buffer fb held frame seq-NB: wait until rank 0 is done
+                N.check(N.lib().nolf_flag_wait(own, 1, seq - NB, timeout_flag.data_ptr(), stream))
         if p2p:
             if dma:
                 # compose into this GPU's own frame (local HBM stores), then
@@ -560,6 +564,7 @@ def run_ours(args):
         ev[k][0].record()
         step(args.warmup + k, k % 2)
         ev[k][1].record()
+    host_ms = (time.perf_counter() - h0) * 1e3 / args.steps   # host enqueue rate (diagnostic)
     barrier()
     n_prof = N.lib().nolf_profile_read(kms)
     if n_prof < 0:
@@ -573,7 +578,7 @@ def run_ours(args):
     t = torch.tensor([t_local], dtype=torch.float64, device=dev)
     # per-rank kernel time (march + shade + compose per step), for imbalance
     csum = clk.summary()
-    kr = torch.tensor(list(kern / args.steps) + [csum["sm_mhz"] or 0.0], dtype=torch.float64, device=dev)
+    kr = torch.tensor(list(kern / args.steps) + [csum["sm_mhz"] or 0.0, host_ms], dtype=torch.float64, device=dev)
     rank_kernel_ms = [[round(float(v), 4) for v in kr.tolist()]]
     if world > 1:
         allk = [torch.zeros_like(kr) for _ in range(world)]
@@ -670,24 +675,24 @@ def run_ours(args):
         # stream; a copy stream downloads it to pinned host memory while
         # step k+1 renders.  Timed from the first render to the last byte on
         # the host (device events on both streams).
-        hosts = [torch.empty((NPX * 6,), dtype=torch.uint8, pin_memory=True) for _ in range(2)]
+        hosts = [torch.empty((NPX * 6,), dtype=torch.uint8, pin_memory=True) for _ in range(NB)]
         copy_stream = torch.cuda.Stream(device=dev)
         comp = torch.cuda.current_stream()
         for k in range(2):
             step(k, k % 2)
         barrier()
-        done_copy = [None, None]
+        done_copy = [None] * NB
         t0 = torch.cuda.Event(enable_timing=True)
         t1 = torch.cuda.Event(enable_timing=True)
         t0.record(comp)
         for k in range(args.steps):
-            fb = (seq_box[0] + 1) % 2 if (p2p and flags) else k % 2   # the buffer step() will use
+            fb = (seq_box[0] + 1) % NB if (p2p and flags) else k % 2   # the buffer step() will use
             if done_copy[fb] is not None:
                 comp.wait_event(done_copy[fb])       # buffer free again
             # p2p: other ranks write buffer fb^1 at step k+1 once this step's
             # completion collective passes, so rank 0 enters it only after
             # the download of step k-1 (buffer fb^1) finished
-            step(k, fb, before_barrier=done_copy[fb ^ 1] if (p2p and rank == 0) else None,
+            step(k, fb, before_barrier=done_copy[(fb - 1) % NB] if (p2p and rank == 0) else None,
                  auto_release=not (flags or world == 1))
             if rank == 0:
                 rendered = torch.cuda.Event()
@@ -839,7 +844,7 @@ def run_ours(args):
             "e2e": e2e, "gpu_launches": launches_per_step * args.steps,
             "gpu_launches_per_step": launches_per_step, "roofline": roof, "cpu_baseline": cpu,
             "clocks": csum, "verify": verify,
-            "rank_kernel_ms": {"fields": ["k_march", "k_shade", "k_compose", "sm_mhz"],
+            "rank_kernel_ms": {"fields": ["k_march", "k_shade", "k_compose", "sm_mhz", "host_enqueue_ms"],
                                "ranks": rank_kernel_ms},
             "per_frame": {"march_samples": S, "hits": Hh, "pixels": npix},
             "step_ms": {"p50": float(np.percentile(step_ms, 50)), "p90": float(np.percentile(step_ms, 90)),
