@@ -2,6 +2,7 @@
 
   render_rays(asset, origins, dirs, counters=None)   lightfield.py:400-456
   render_ray(asset, ray, counters=None)              lightfield.py:459-463
+  march_rays(asset, origins, dirs)                   lightfield.py:129-186, 418-425
   render_range(asset, ray_range, counters=None)      renderer.py:63-93
   render_frame(scene, camera, counters=None)         renderer.py:96-107
   compose(frames, asset_order=None, alpha_vis=0.5)   farm.py:129-172
@@ -21,6 +22,7 @@ import ctypes as C
 import time
 import zlib
 from collections import OrderedDict
+from typing import NamedTuple
 
 import numpy as np
 
@@ -269,6 +271,41 @@ def render_rays(asset, origins, dirs, counters=None):
     out = rgba.cpu().numpy(), depth.cpu().numpy()
     _merge(counters, cnt)
     return out
+
+
+class MarchResult(NamedTuple):
+    """lightfield.MarchResult (lightfield.py:101-110) minus the transmittance."""
+    hit: np.ndarray          # (B,) bool
+    t_hit: np.ndarray        # (B,) f64, inf on a miss
+    alpha_c: np.ndarray      # (B,) f64
+    samples: np.ndarray      # (B,) i64 active samples
+    p_h: np.ndarray          # (B,3) f64 clip(o + t_hit d, 0, 1), 0 on a miss
+
+
+def march_rays(asset, origins, dirs) -> MarchResult:
+    """The march alone, as render_rays runs it (lightfield.py:418-425): OBJECT-
+    space rays, t_near / t_far from the asset's proxy box, then march_rays
+    (lightfield.py:129-186) on the CUDA marcher (nolf_march_rays)."""
+    t = torch()
+    origins = np.asarray(origins, dtype=np.float64)
+    dirs = np.asarray(dirs, dtype=np.float64)
+    if origins.ndim != 2 or origins.shape[1] != 3 or dirs.shape != origins.shape:
+        raise errors.DomainError("origins and dirs must both be (B,3)")
+    n = len(origins)
+    dev = _device()
+    o = t.from_numpy(np.ascontiguousarray(origins)).to(dev)
+    d = t.from_numpy(np.ascontiguousarray(dirs)).to(dev)
+    hit = t.zeros(n, dtype=t.uint8, device=dev)
+    t_hit = t.empty(n, dtype=t.float64, device=dev)
+    alpha = t.empty(n, dtype=t.float64, device=dev)
+    samples = t.empty(n, dtype=t.int64, device=dev)
+    p_h = t.empty((n, 3), dtype=t.float64, device=dev)
+    if n:
+        N.check(N.lib().nolf_march_rays(device_asset(asset).handle, o.data_ptr(), 1, d.data_ptr(), n,
+                                        hit.data_ptr(), t_hit.data_ptr(), alpha.data_ptr(), samples.data_ptr(),
+                                        p_h.data_ptr(), None, 0, _stream_ptr()))
+    return MarchResult(hit.cpu().numpy().astype(bool), t_hit.cpu().numpy(), alpha.cpu().numpy(),
+                       samples.cpu().numpy(), p_h.cpu().numpy())
 
 
 def render_ray(asset, ray, counters=None):

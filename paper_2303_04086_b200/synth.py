@@ -116,15 +116,9 @@ def shell_cameras(n_cameras=512, image_size=32, radius=2.0, fov_deg=60.0):
 
 def collect_hit_points_gpu(atlas: CubeAtlas, march: MarchParams, n_cameras=512, image_size=32):
     """Hit points of the sweep, marched by nolf_march_rays on the GPU."""
-    import ctypes as C
-
-    import torch
-
-    from . import _native as N
     from . import render as R
 
     probe = march_only_asset(atlas, march)
-    dev = R.device_asset(probe)
     cams = shell_cameras(n_cameras, image_size)
     # camera_dirs on the host with numpy (identical bits to core.camera_dirs)
     px, py = np.meshgrid(np.arange(image_size), np.arange(image_size))
@@ -138,22 +132,8 @@ def collect_hit_points_gpu(atlas: CubeAtlas, march: MarchParams, n_cameras=512, 
         d = d / np.linalg.norm(d, axis=-1, keepdims=True)
         dirs.append(d)
         origins.append(np.broadcast_to(cam.position, d.shape))
-    dirs = np.concatenate(dirs)
-    origins = np.ascontiguousarray(np.concatenate(origins))
-    n = len(dirs)
-    device = R._device()
-    o = torch.from_numpy(origins).to(device)
-    d = torch.from_numpy(np.ascontiguousarray(dirs)).to(device)
-    hit = torch.empty(n, dtype=torch.uint8, device=device)
-    t_hit = torch.empty(n, dtype=torch.float64, device=device)
-    alpha = torch.empty(n, dtype=torch.float64, device=device)
-    samples = torch.empty(n, dtype=torch.int64, device=device)
-    p_h = torch.empty((n, 3), dtype=torch.float64, device=device)
-    N.check(N.lib().nolf_march_rays(dev.handle, o.data_ptr(), 1, d.data_ptr(), n, hit.data_ptr(),
-                                    t_hit.data_ptr(), alpha.data_ptr(), samples.data_ptr(),
-                                    p_h.data_ptr(), None, 0, R._stream_ptr()))
-    h = hit.cpu().numpy().astype(bool)
-    return p_h.cpu().numpy()[h]
+    res = R.march_rays(probe, np.concatenate(origins), np.concatenate(dirs))
+    return res.p_h[res.hit]
 
 
 def voxelize(points: np.ndarray, resolution: int, dilate: int = 1) -> np.ndarray:
