@@ -1038,8 +1038,13 @@ int launch_march_shade(int mode, const NolfInstance *ins, int n_inst, const Nolf
       // earlier frame's live count, grid-stride for any size)
       const long long n_chunks = n_rays / kMarchThreads;
       const long long live = std::min<long long>(n_chunks, g_live.last + g_live.last / 8 + 2ll * num_sms());
-      k_compose_live<<<(unsigned)std::max<long long>(1, (live * 16 + 255) / 256), 256, 0, st>>>(ca, w.chunk_list,
-                                                                                             w.counts + n_inst, n_chunks);
+      // 8 slots per thread, or 4 when that leaves under ~1024 threads per SM
+      static const int g_env = getenv("NOLF_COMPOSE_G") ? atoi(getenv("NOLF_COMPOSE_G")) : 0;
+      const int G = g_env == 4 || g_env == 8 ? g_env : (live * 16 >= 1024ll * num_sms() ? 8 : 4);
+      const long long threads = live * (128 / G);
+      const unsigned cgrid = (unsigned)std::max<long long>(1, (threads + 255) / 256);
+      if (G == 8) k_compose_live<8><<<cgrid, 256, 0, st>>>(ca, w.chunk_list, w.counts + n_inst, n_chunks);
+      else k_compose_live<4><<<cgrid, 256, 0, st>>>(ca, w.chunk_list, w.counts + n_inst, n_chunks);
     } else {
       k_compose<<<(unsigned)((n_thr + 255) / 256), 256, 0, st>>>(ca);
     }

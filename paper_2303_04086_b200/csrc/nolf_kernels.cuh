@@ -1259,12 +1259,19 @@ __global__ void __launch_bounds__(256) k_compose(ComposeArgs a) {
 
 // Prefilled outputs: compose only the live chunks, from the compacted list
 // (16 threads x 8 slots per chunk, grid-stride over the list's length).
+// G slots per thread (8 or 4): a launch over few live chunks (a multi-GPU
+// shard) uses 4 so twice the threads hide the layer-read latency.
+template <int G>
 __global__ void __launch_bounds__(256) k_compose_live(ComposeArgs a, const unsigned *live_list, const unsigned *count,
                                                       long long list_stride) {
-  const long long total = (long long)count[0] * 16;
+  constexpr int per_chunk = 128 / G;
+  const long long total = (long long)count[0] * per_chunk;
   for (long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x; g < total;
-       g += (long long)gridDim.x * blockDim.x)
-    compose_eight(a, (long long)live_list[g >> 4] * 128 + (g & 15) * 8);   // spatial list
+       g += (long long)gridDim.x * blockDim.x) {
+    const long long p0 = (long long)live_list[g / per_chunk] * 128 + (g % per_chunk) * G;   // spatial list
+    if (G == 8) compose_eight(a, p0);
+    else compose_four(a, p0);
+  }
   if (a.peer) {
     __syncthreads();
     if (threadIdx.x == 0) __threadfence_system();
