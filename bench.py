@@ -798,7 +798,11 @@ def run_ours(args):
     # capture of this config (profiles/, `ncu --set full`, per launch)
     try:
         import glob
-        caps = sorted(glob.glob(os.path.join(ROOT, "profiles", f"r*_config{args.config}_1gpu*.json")))
+        def _ver(path):              # r01_config4_1gpu_v10 after _v9 (numeric, not lexical)
+            import re
+            m = re.search(r"r(\d+)_config\d+_1gpu(?:_v(\d+))?\.json$", path)
+            return (int(m.group(1)), int(m.group(2) or 0)) if m else (0, 0)
+        caps = sorted(glob.glob(os.path.join(ROOT, "profiles", f"r*_config{args.config}_1gpu*.json")), key=_ver)
         for path in reversed(caps):
             kern_caps = json.load(open(path)).get("kernels", {})
             # the march phase is k_cull_chunks + k_march_chunks (k_march<> for unaligned tiles)
