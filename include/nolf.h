@@ -153,7 +153,8 @@ typedef struct NolfSceneOut {
                                           NVLink and ends with a system-scope fence */
     int32_t prefilled;                 /* 1: rgba8 / depth16 already hold the miss encoding
                                           (0 / 65535) for every pixel of these tiles, so
-                                          pixels no instance can reach are not written
+                                          miss pixels are not written (chunks no screen
+                                          box reaches, runs of 4 / 8 misses)
                                           (u8/u16 outputs only; rgba/depth must be NULL) */
 } NolfSceneOut;
 

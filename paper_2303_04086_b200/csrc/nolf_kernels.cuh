@@ -1163,6 +1163,7 @@ __device__ __forceinline__ void compose_four(const ComposeArgs &a, const long lo
   const bool run = q[0] >= 0 && (q[0] & 3) == 0 && q[1] == q[0] + 1 && q[2] == q[0] + 2 && q[3] == q[0] + 3 &&
                    !a.out_rgba && !a.out_depth;
   if (run && (ns[0] | ns[1] | ns[2] | ns[3]) == 0) {     // common case: four misses
+    if (a.prefilled) return;                              // the miss encoding is already there
     if (a.out_rgba8) reinterpret_cast<uint4 *>(a.out_rgba8)[q[0] >> 2] = make_uint4(0u, 0u, 0u, 0u);
     if (a.out_depth16) reinterpret_cast<uint2 *>(a.out_depth16)[q[0] >> 2] = make_uint2(0xffffffffu, 0xffffffffu);
     return;
@@ -1214,6 +1215,7 @@ __device__ __forceinline__ void compose_eight(const ComposeArgs &a, const long l
       uint4 *r8 = reinterpret_cast<uint4 *>(a.out_rgba8 + q0 * 4);
       uint4 *d16 = reinterpret_cast<uint4 *>(a.out_depth16 + q0);
       if ((nh.x | nh.y) == 0) {                 // eight misses
+        if (a.prefilled) return;                // the miss encoding is already there
         if (a.out_rgba8) { r8[0] = make_uint4(0u, 0u, 0u, 0u); r8[1] = make_uint4(0u, 0u, 0u, 0u); }
         if (a.out_depth16) d16[0] = make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu);
         return;
