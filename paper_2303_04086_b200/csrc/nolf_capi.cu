@@ -764,13 +764,15 @@ int run_shade(const DevInst *inst, const long long *qoff, int n_inst, const Work
     // resident CTAs per SM from registers and shared memory (TMEM: 64 columns
     // each, never the limit below 8)
     static int regs = 0;
+    static size_t static_smem = 0;
     if (!regs) {
       cudaFuncAttributes fa{};
       CUDA_TRY(cudaFuncGetAttributes(&fa, k_shade_tc));
       regs = fa.numRegs > 0 ? fa.numRegs : 168;
+      static_smem = fa.sharedSizeBytes;
     }
     const int by_regs = 65536 / (((regs + 7) / 8 * 8) * kTcThreads);
-    const int by_smem = (int)((227u * 1024u) / (smem + 1024u));
+    const int by_smem = (int)((227u * 1024u) / (smem + static_smem + 1024u));
 #ifndef NOLF_SHADE_CAP
 #define NOLF_SHADE_CAP 4
 #endif

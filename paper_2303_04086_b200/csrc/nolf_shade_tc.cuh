@@ -281,6 +281,8 @@ __global__ void __launch_bounds__(kTcThreads) k_shade_tc(ShadeArgs args) {
   const TcSmemPtrs S = tc_carve(smem_raw);
   const int tid = threadIdx.x, warp = tid >> 5;
   if (warp == 0) tc::tmem_alloc<64>(S.tmem_slot);
+  __shared__ DevAsset s_asset;
+  __shared__ double s_scale;
   if (tid == 0) {
     tc::mbar_init(S.bar_mma, 1);
     tc::mbar_init(S.bar_tma, 1);
@@ -338,9 +340,16 @@ __global__ void __launch_bounds__(kTcThreads) k_shade_tc(ShadeArgs args) {
       }
     }
     if (k >= args.n_inst) break;
-    const DevInst &I = args.inst[k];
-    const DevAsset &A = *I.a;
+    // the instance's asset record, copied to shared memory once per instance:
+    // the tile loop's field reads are then shared-memory loads, not generic
+    // loads that miss a gather-thrashed L1
+    const DevAsset &A = s_asset;
     if (k != cur) {
+      __syncthreads();
+      const uint32_t *src = reinterpret_cast<const uint32_t *>(args.inst[k].a);
+      uint32_t *dst = reinterpret_cast<uint32_t *>(&s_asset);
+      for (int q = tid; q < (int)(sizeof(DevAsset) / 4); q += kTcThreads) dst[q] = __ldg(src + q);
+      if (tid == 0) s_scale = args.inst[k].scale;
       __syncthreads();
       tc_stage_asset(A, S, tma_phase, tid, phi_smem);
       tab_smem = 6 * (A.N + 1) <= (int)kTcTabMax;
@@ -401,7 +410,7 @@ __global__ void __launch_bounds__(kTcThreads) k_shade_tc(ShadeArgs args) {
       o.y = fminf(fmaxf(fmaf(tf, fs_out[1], (float)cd[1]), 0.f), 1.f);
       o.z = fminf(fmaxf(fmaf(tf, fs_out[2], (float)cd[2]), 0.f), 1.f);
       o.w = alpha;
-      float dep = (float)__ddiv_rn(t_obj, I.scale);
+      float dep = (float)__ddiv_rn(t_obj, s_scale);
       if (o.w <= 0.f) {
         o = make_float4(0.f, 0.f, 0.f, 0.f);
         dep = __int_as_float(0x7f800000);
