@@ -62,11 +62,11 @@ __device__ __forceinline__ void tc_mlp_rows(uint8_t *A, const uint8_t *W, const 
   tc::tmem_ld32(trow + 0, h);
   tc::tmem_ld32(trow + 32, h + 32);
   // bias + ReLU, re-quantise as the layer-1 A operand (K=64)
-  uint8_t *rowp = A + (tid >> 3) * 128 + (tid & 7) * 16;
+  const uint32_t rowa = aA + (tid >> 3) * 128 + (tid & 7) * 16, fpa = tc::smem_u32(fp);
 #pragma unroll
   for (int c = 0; c < 8; ++c) {
     float v[8];
-    const float4 bA = reinterpret_cast<const float4 *>(fp)[2 * c], bB = reinterpret_cast<const float4 *>(fp)[2 * c + 1];
+    const float4 bA = tc::lds128(fpa + 32 * c), bB = tc::lds128(fpa + 32 * c + 16);
     const float bb[8] = {bA.x, bA.y, bA.z, bA.w, bB.x, bB.y, bB.z, bB.w};
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
@@ -78,7 +78,7 @@ __device__ __forceinline__ void tc_mlp_rows(uint8_t *A, const uint8_t *W, const 
     q.y = tc::pack_bf16(v[2], v[3]);
     q.z = tc::pack_bf16(v[4], v[5]);
     q.w = tc::pack_bf16(v[6], v[7]);
-    *reinterpret_cast<uint4 *>(rowp + c * 2048) = q;
+    tc::sts128(rowa + c * 2048, q);
   }
   tc::tc_fence_before();
   tc::fence_async_smem();
@@ -100,32 +100,34 @@ __device__ __forceinline__ void tc_mlp_rows(uint8_t *A, const uint8_t *W, const 
   tc::tc_fence_before();
   // ---- layer 2 (fp32, CUDA cores): 64 -> 4, sequential in the hidden index;
   // W2 is staged hidden-major ([o][4]) so one 16 B load feeds the 4 outputs
-  const float4 *b1 = reinterpret_cast<const float4 *>(fp + 64), *w2 = reinterpret_cast<const float4 *>(fp + 128);
-  const float *b2 = fp + 128 + 256;
+  // b1 at fp + 64, W2 at fp + 128, b2 at fp + 384 (floats)
   float acc[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
   for (int o4 = 0; o4 < 16; ++o4) {
-    const float4 bv = b1[o4];
+    const float4 bv = tc::lds128(fpa + 256 + 16 * o4);
     const float bb[4] = {bv.x, bv.y, bv.z, bv.w};
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       const int o = 4 * o4 + e;
       float z = h[o] + bb[e];
       z = z > 0.f ? z : 0.f;
-      const float4 wv = w2[o];
+      const float4 wv = tc::lds128(fpa + 512 + 16 * o);
       acc[0] = fmaf(z, wv.x, acc[0]);
       acc[1] = fmaf(z, wv.y, acc[1]);
       acc[2] = fmaf(z, wv.z, acc[2]);
       acc[3] = fmaf(z, wv.w, acc[3]);
     }
   }
-#pragma unroll
-  for (int j = 0; j < 4; ++j) out4[j] = acc[j] + b2[j];
+  const float4 b2 = tc::lds128(fpa + 1536);
+  out4[0] = acc[0] + b2.x;
+  out4[1] = acc[1] + b2.y;
+  out4[2] = acc[2] + b2.z;
+  out4[3] = acc[3] + b2.w;
 }
 
 // Write one bf16 input row (n values of x, zero padded to kTcK0) to A.
 __device__ __forceinline__ void tc_write_x(uint8_t *A, int tid, const float *x, int n) {
-  uint8_t *rowp = A + (tid >> 3) * 128 + (tid & 7) * 16;
+  const uint32_t rowa = tc::smem_u32(A) + (tid >> 3) * 128 + (tid & 7) * 16;
 #pragma unroll
   for (int c = 0; c < kTcK0 / 8; ++c) {
     float v[8];
@@ -136,7 +138,7 @@ __device__ __forceinline__ void tc_write_x(uint8_t *A, int tid, const float *x, 
     q.y = tc::pack_bf16(v[2], v[3]);
     q.z = tc::pack_bf16(v[4], v[5]);
     q.w = tc::pack_bf16(v[6], v[7]);
-    *reinterpret_cast<uint4 *>(rowp + c * 2048) = q;
+    tc::sts128(rowa + c * 2048, q);
   }
 }
 
@@ -195,7 +197,7 @@ __device__ __forceinline__ void tc_stage_asset(const DevAsset &A, const TcSmemPt
 // direction, and the clamped opacity when refining.  FIXED_F = 2 makes every
 // index static (the row stays in registers); 0 = any F (local array).
 template <int FIXED_F>
-__device__ __forceinline__ void tc_gather_inputs(const DevAsset &A, const TcSmemPtrs &S, const uint32_t *tab,
+__device__ __forceinline__ void tc_gather_inputs(const DevAsset &A, const TcSmemPtrs &S, bool tab_smem,
                                                  bool phi_smem, const HitRec &rec, float x[kTcK0]) {
   const int F = FIXED_F ? FIXED_F : A.F;
   int base[3];
@@ -225,18 +227,20 @@ __device__ __forceinline__ void tc_gather_inputs(const DevAsset &A, const TcSmem
   double es[FIXED_F ? FIXED_F : kTcK0] = {};
   uint32_t slots[8];
   const int s1 = A.N + 1;
+  const uint32_t taba = tc::smem_u32(S.tab), phia = tc::smem_u32(S.phi);
+  auto tab = [&](int i) -> uint32_t { return tab_smem ? tc::lds32(taba + 4u * (uint32_t)i) : __ldg(A.tab + i); };
 #pragma unroll
   for (int c = 0; c < 8; ++c) {
     const int xx = base[0] + (c & 1), yy = base[1] + ((c >> 1) & 1), zz = base[2] + ((c >> 2) & 1);
-    uint32_t h0 = tab[xx] + tab[s1 + yy];
+    uint32_t h0 = tab(xx) + tab(s1 + yy);
     h0 = h0 >= A.m ? h0 - A.m : h0;
-    h0 += tab[2 * s1 + zz];
+    h0 += tab(2 * s1 + zz);
     h0 = h0 >= A.m ? h0 - A.m : h0;
-    uint32_t h1 = tab[3 * s1 + xx] + tab[4 * s1 + yy];
+    uint32_t h1 = tab(3 * s1 + xx) + tab(4 * s1 + yy);
     h1 = h1 >= A.mphi ? h1 - A.mphi : h1;
-    h1 += tab[5 * s1 + zz];
+    h1 += tab(5 * s1 + zz);
     h1 = h1 >= A.mphi ? h1 - A.mphi : h1;
-    const uint32_t off = phi_smem ? (uint32_t)reinterpret_cast<const uint16_t *>(S.phi)[h1] : __ldg(A.phi + h1);
+    const uint32_t off = phi_smem ? tc::lds16(phia + 2u * h1) : __ldg(A.phi + h1);
     uint32_t slot = h0 + off;
     slots[c] = slot >= A.m ? slot - A.m : slot;
   }
@@ -369,14 +373,13 @@ __global__ void __launch_bounds__(kTcThreads) k_shade_tc(ShadeArgs args) {
       t_obj = rec.t_obj;
       out_idx = rec.out_idx;
       ordinal = rec.ordinal;
-      const uint32_t *tab = tab_smem ? S.tab : A.tab;
       const bool want_dif = A.use_diffuse_color && A.has_dif;
       const int dif_cid = want_dif ? atlas_cell_id(A.dif, rec.p) : -1;   // overlaps the PSH gather
       if (A.F == 2) {            // the common layout: every input index is static -> registers
-        tc_gather_inputs<2>(A, S, tab, phi_smem, rec, x);
+        tc_gather_inputs<2>(A, S, tab_smem, phi_smem, rec, x);
       } else {
         float xl[kTcK0] = {};
-        tc_gather_inputs<0>(A, S, tab, phi_smem, rec, xl);
+        tc_gather_inputs<0>(A, S, tab_smem, phi_smem, rec, xl);
 #pragma unroll
         for (int q = 0; q < kTcK0; ++q) x[q] = xl[q];
       }
