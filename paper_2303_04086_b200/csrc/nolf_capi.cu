@@ -626,9 +626,35 @@ int nolf_asset_create(const NolfAssetDesc *d, int device, nolf_asset_t *out) {
       for (int i = 0; i < in; ++i) put(0, o, i, d->specular.w[0][o * in + i]);
     for (int o = 0; o < 64; ++o)
       for (int i = 0; i < 64; ++i) put(kTcW0 / 2, o, i, d->specular.w[1][o * 64 + i]);
-    uint16_t *tw;
-    if ((rc = A->upload(wt.data(), wt.size(), &tw))) return bail(rc);
-    H.tc_w = reinterpret_cast<const uint8_t *>(tw);
+    // the shader's shared-memory image after the bf16 weights: the fp32
+    // block (b0, b1, W2 hidden-major [o][4], b2) and the PSH residue tables
+    // when they fit, so one TMA bulk copy stages all of it
+    const int nt = 6 * (H.N + 1);
+    const size_t tab_bytes = nt <= (int)kTcTabMax ? ((size_t)nt * 4 + 15) / 16 * 16 : 0;
+    std::vector<uint8_t> img(kTcWBytes + kTcF32 * 4 + tab_bytes, 0);
+    memcpy(img.data(), wt.data(), kTcWBytes);
+    std::vector<float> fpb(kTcF32, 0.f);
+    for (int q = 0; q < kTcF32; ++q) {
+      if (q < 64) fpb[q] = d->specular.b[0][q];
+      else if (q < 128) fpb[q] = d->specular.b[1][q - 64];
+      else if (q < 128 + 256) fpb[q] = d->specular.w[2][((q - 128) & 3) * 64 + ((q - 128) >> 2)];
+      else fpb[q] = d->specular.b[2][q - 384];
+    }
+    memcpy(img.data() + kTcWBytes, fpb.data(), kTcF32 * 4);
+    if (tab_bytes) {
+      std::vector<uint32_t> tab((size_t)nt);
+      const int s1 = H.N + 1;
+      for (int a = 0; a < 3; ++a)
+        for (int x = 0; x < s1; ++x) {
+          tab[(size_t)a * s1 + x] = (uint32_t)(((uint64_t)x * d->primes_h0[a]) % (uint64_t)H.m);
+          tab[(size_t)(3 + a) * s1 + x] = (uint32_t)(((uint64_t)x * d->primes_h1[a]) % (uint64_t)H.mphi);
+        }
+      memcpy(img.data() + kTcWBytes + kTcF32 * 4, tab.data(), (size_t)nt * 4);
+    }
+    uint8_t *tw;
+    if ((rc = A->upload(img.data(), img.size(), &tw))) return bail(rc);
+    H.tc_w = tw;
+    H.tc_w_bytes = (uint32_t)img.size();
   }
   if (d->psh_table_size <= 65536) {
     const size_t n16 = ((size_t)d->psh_offset_size + 7) / 8 * 8;

@@ -75,6 +75,9 @@ struct DevAsset {              // LightFieldAsset (lightfield.py:217-248)
   int mlp_mode;
   // tensor-core shading tables (NOLF_MLP_BF16)
   const uint8_t *tc_w;         // bf16 W0 [64 x 32] then W1 [64 x 64], UMMA K-major layout
+                               // then the fp32 block (b0, b1, W2 [o][4], b2) and the PSH
+                               // residue tables: the shader's smem image, one bulk copy
+  uint32_t tc_w_bytes;
   const uint16_t *phi16;       // Phi narrowed to u16 (m <= 65536), else null
   uint32_t phi16_bytes;        // padded to 16 B for the TMA bulk copy
   DevMesh mesh;                // triangle-mesh proxy (nodes == null: slab only)

@@ -170,24 +170,14 @@ __device__ __forceinline__ TcSmemPtrs tc_carve(uint8_t *raw) {
 __device__ __forceinline__ void tc_stage_asset(const DevAsset &A, const TcSmemPtrs &S, uint32_t &tma_phase,
                                                int tid, bool &phi_smem) {
   phi_smem = A.phi16 != nullptr && A.phi16_bytes <= kTcPhiMax;
+  // one bulk copy: bf16 weights, fp32 block and residue tables (the host
+  // laid them out as the shared-memory image, tc_w_bytes), plus Phi
   if (tid == 0) {
-    const uint32_t bytes = kTcWBytes + (phi_smem ? A.phi16_bytes : 0u);
+    const uint32_t bytes = A.tc_w_bytes + (phi_smem ? A.phi16_bytes : 0u);
     tc::mbar_arrive_expect_tx(S.bar_tma, bytes);
-    tc::bulk_g2s(S.W, A.tc_w, kTcWBytes, S.bar_tma);
+    tc::bulk_g2s(S.W, A.tc_w, A.tc_w_bytes, S.bar_tma);
     if (phi_smem) tc::bulk_g2s(S.phi, A.phi16, A.phi16_bytes, S.bar_tma);
   }
-  const float *P = A.fs.params;
-  for (int q = tid; q < kTcF32; q += kTcThreads) {
-    float v;
-    if (q < 64) v = P[MlpOff::b0 + q];
-    else if (q < 128) v = P[MlpOff::b1 + q - 64];
-    else if (q < 128 + 256) v = P[MlpOff::wl + ((q - 128) & 3) * 64 + ((q - 128) >> 2)];   // [o][4]
-    else v = P[MlpOff::bl + q - 384];
-    S.fp[q] = v;
-  }
-  const int nt = 6 * (A.N + 1);
-  if (nt <= (int)kTcTabMax)
-    for (int q = tid; q < nt; q += kTcThreads) S.tab[q] = A.tab[q];
   tc::mbar_wait(S.bar_tma, tma_phase);
   tma_phase ^= 1;
 }
