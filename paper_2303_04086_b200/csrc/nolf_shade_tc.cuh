@@ -219,16 +219,25 @@ __device__ __forceinline__ void tc_gather_inputs(const DevAsset &A, const TcSmem
   const int s1 = A.N + 1;
   const uint32_t taba = tc::smem_u32(S.tab), phia = tc::smem_u32(S.phi);
   auto tab = [&](int i) -> uint32_t { return tab_smem ? tc::lds32(taba + 4u * (uint32_t)i) : __ldg(A.tab + i); };
+  // the 8 corners touch only 2 residues per (table, axis): load those 12
+  // once (the volatile shared loads are never merged by the compiler)
+  uint32_t rt[6][2];
+#pragma unroll
+  for (int j = 0; j < 6; ++j) {
+    const int ax = j % 3;
+    rt[j][0] = tab(j * s1 + base[ax]);
+    rt[j][1] = tab(j * s1 + base[ax] + 1);
+  }
 #pragma unroll
   for (int c = 0; c < 8; ++c) {
-    const int xx = base[0] + (c & 1), yy = base[1] + ((c >> 1) & 1), zz = base[2] + ((c >> 2) & 1);
-    uint32_t h0 = tab(xx) + tab(s1 + yy);
+    const int cx = c & 1, cy = (c >> 1) & 1, cz = (c >> 2) & 1;
+    uint32_t h0 = rt[0][cx] + rt[1][cy];
     h0 = h0 >= A.m ? h0 - A.m : h0;
-    h0 += tab(2 * s1 + zz);
+    h0 += rt[2][cz];
     h0 = h0 >= A.m ? h0 - A.m : h0;
-    uint32_t h1 = tab(3 * s1 + xx) + tab(4 * s1 + yy);
+    uint32_t h1 = rt[3][cx] + rt[4][cy];
     h1 = h1 >= A.mphi ? h1 - A.mphi : h1;
-    h1 += tab(5 * s1 + zz);
+    h1 += rt[5][cz];
     h1 = h1 >= A.mphi ? h1 - A.mphi : h1;
     const uint32_t off = phi_smem ? tc::lds16(phia + 2u * h1) : __ldg(A.phi + h1);
     uint32_t slot = h0 + off;
