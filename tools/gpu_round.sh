@@ -1,11 +1,12 @@
 # Round-end GPU check: gpu tests, smoke, bench lines for every BASELINE config + reference arm, ncu launch list and full capture.
-# usage: gpurun --timeout 3000 -- bash tools/gpu_round.sh   (outputs under gpurun_out/r12_*)
+# usage: gpurun --timeout 3000 -- bash tools/gpu_round.sh   (outputs under gpurun_out/$P_*, P defaults to r13)
 set -x
+P=${P:-r13}
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
-timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/r12_pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/r12_pytest_gpu.log
-timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > gpurun_out/r12_smoke.log 2>&1
-for c in 4 1 2 3 5; do timeout 400 python bench.py --config $c > gpurun_out/r12_bench_cfg$c.json 2> gpurun_out/r12_bench_cfg$c.err; done
-timeout 400 python bench.py --impl reference > gpurun_out/r12_bench_ref.json 2> gpurun_out/r12_bench_ref.err
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/r12_launches.csv python bench.py --steps 2 --warmup 3 > gpurun_out/r12_ncu_launch.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k "regex:^k_(cull_chunks|march_chunks|shade_tc|compose_live)" -c 4 -o gpurun_out/r12_cfg4 python bench.py --steps 1 --warmup 3 > gpurun_out/r12_ncu_full.log 2>&1
-tail -3 gpurun_out/r12_pytest_gpu.log; cat gpurun_out/r12_smoke.log | tail -2; cat gpurun_out/r12_bench_cfg4.json
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/${P}_pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/${P}_pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > gpurun_out/${P}_smoke.log 2>&1
+for c in 4 1 2 3 5; do timeout 400 python bench.py --config $c > gpurun_out/${P}_bench_cfg$c.json 2> gpurun_out/${P}_bench_cfg$c.err; done
+timeout 400 python bench.py --impl reference > gpurun_out/${P}_bench_ref.json 2> gpurun_out/${P}_bench_ref.err
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/${P}_launches.csv python bench.py --steps 2 --warmup 3 > gpurun_out/${P}_ncu_launch.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k "regex:^k_(cull_chunks|march_chunks|shade_tc|compose_live)" -c 4 -o gpurun_out/${P}_cfg4 python bench.py --steps 1 --warmup 3 > gpurun_out/${P}_ncu_full.log 2>&1
+tail -3 gpurun_out/${P}_pytest_gpu.log; cat gpurun_out/${P}_smoke.log | tail -2; cat gpurun_out/${P}_bench_cfg4.json
