@@ -35,6 +35,9 @@ sys.path.insert(0, ROOT)
 
 METRIC = "Mrays/s and fps at 4K for multi-asset i-NOLF scene at 1/2/4/8 B200 vs CPU ref"
 UNIT = "Mrays/s"
+# what the path computes in: f64 ray setup / march / PSH addressing / compose,
+# bf16 x bf16 -> fp32 specular MLP on tcgen05 (--mlp fp32: CUDA-core fp32)
+DTYPE = "f64+bf16"
 CACHE_DIR = os.environ.get("NOLF_BENCH_CACHE", "/tmp/nolf_bench_assets")
 
 
@@ -44,6 +47,9 @@ def parse():
     p.add_argument("--steps", type=int, default=200)
     p.add_argument("--warmup", type=int, default=10)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--build-assets", action="store_true",
+                   help="only build / cache the config's synthetic assets (the reference arm runs "
+                        "this in a child process so its own process never loads the product)")
     p.add_argument("--config", type=int, default=4, choices=[1, 2, 3, 4, 5])
     p.add_argument("--width", type=int, default=3840)
     p.add_argument("--height", type=int, default=2160)
@@ -82,9 +88,12 @@ def parse():
 
 
 # ------------------------------------------------------------------ scene
-def build_scene(n_assets):
-    """Config-4 scene; cached as .nolf files so repeated runs on a box reuse it."""
-    from paper_2303_04086_b200 import nolf_io, synth
+def build_scene(n_assets, cache_only=False):
+    """Config-4 scene; cached as .nolf files so repeated runs on a box reuse it.
+    cache_only: never synthesise (the reference arm reads files only; its
+    assets were built beforehand in a separate process, see run_reference)."""
+    from paper_2303_04086_b200 import nolf_io
+    from tools import synth
     os.makedirs(CACHE_DIR, exist_ok=True)
     cache, assets = {}, []
     for i in range(n_assets):
@@ -92,6 +101,8 @@ def build_scene(n_assets):
         path = os.path.join(CACHE_DIR, f"zodiac_{kind}_{i}_b32r8n64.nolf")
         if os.path.exists(path):
             a = nolf_io.read_asset(path)
+        elif cache_only:
+            raise RuntimeError(f"asset cache miss: {path}")
         else:
             a = synth.make_asset(kind, seed=i, cache=cache)
             tmp = f"{path}.{os.getpid()}.tmp"
@@ -102,11 +113,11 @@ def build_scene(n_assets):
 
 
 def camera_for_step(k, width, height):
-    from paper_2303_04086_b200 import synth
+    from tools import synth
     return synth.zodiac_camera(width, height, azimuth=0.3 + 0.005 * k)
 
 
-def workload(args):
+def workload(args, cache_only=False):
     """(scene, views(k) -> [Camera], W, H, description) of a BASELINE config.
 
     1: single asset, one 256x256 view           (orbit_camera(0.8, 0.3, 2.0))
@@ -118,18 +129,18 @@ def workload(args):
     Each step moves the viewpoints slightly (azimuth + 0.005 k)."""
     import math as m
 
-    from paper_2303_04086_b200 import synth
+    from tools import synth
     from paper_2303_04086_b200.model import Camera, orbit_camera
     c = args.config
     if c == 2:
         import dataclasses
-        a = dataclasses.replace(build_scene(1)[0][0], proxy_mesh=synth.icosphere(radius=0.3, level=3))
+        a = dataclasses.replace(build_scene(1, cache_only)[0][0], proxy_mesh=synth.icosphere(radius=0.3, level=3))
         W, H = 1920, 1080
         return [(a, np.eye(4))], (lambda k: [orbit_camera(0.8 + 0.005 * k, 0.3, radius=2.0, width=W,
                                                           height=H)]), W, H, \
             "BASELINE config 2: single asset, mesh proxy (1280-triangle icosphere, BVH), 1920x1080"
     if c in (1, 3):
-        scene = build_scene(1)[:1]
+        scene = build_scene(1, cache_only)[:1]
         scene = [(scene[0][0], np.eye(4))]
         if c == 1:
             W = H = 256
@@ -139,7 +150,7 @@ def workload(args):
         return scene, (lambda k: [orbit_camera(2 * m.pi * v / 16 + 0.005 * k, 0.3, radius=1.5, width=W,
                                                height=H) for v in range(16)]), W, H, \
             "BASELINE config 3: single asset at 3840x2160, 16 simultaneous viewpoints"
-    scene = build_scene(args.assets)
+    scene = build_scene(args.assets, cache_only)
     if c == 5:
         W = H = 2160
 
@@ -225,42 +236,114 @@ class Clocks:
 
 
 # ------------------------------------------------------------------ CPU reference (oracle port)
-def cpu_sample(scene, cams, tiles, seconds, seed=0, max_tiles=None):
+def cpu_sample(scene, cams, tiles, seconds, seed=0, max_tiles=None, keep=None):
     """Render + compose random 32x32 tiles with the C oracle (the reference's
     algorithm restated, every fixed march step evaluated) on all host cores
-    until ``seconds`` elapse; returns (rays, elapsed, tiles used)."""
+    until ``seconds`` elapse; returns (rays, elapsed, tiles used).  ``keep``
+    (dict): also collect every tile's composed (rgba, depth) by tile index
+    and the summed RenderCounters (the verify leg's reference frame)."""
     from oracle import oracle as O
+    from paper_2303_04086_b200.model import RenderCounters
     oas = [(O.Asset(a), tr) for a, tr in scene]
     rng = np.random.default_rng(seed)
     order = rng.permutation(len(tiles))
     rays, t0, used = 0, time.perf_counter(), 0
     nthr = os.cpu_count()        # explicit: torchrun exports OMP_NUM_THREADS=1
+    cnt = RenderCounters() if keep is not None else None
     for t in order:
         c, x0, y0, x1, y1 = (int(v) for v in tiles[t])
         rg, dp = [], []
         for oa, tr in oas:
-            r, d = O.render_rect(oa, cams[c], (x0, y0, x1, y1), transform=tr, nthreads=nthr)
+            r, d = O.render_rect(oa, cams[c], (x0, y0, x1, y1), counters=cnt, transform=tr, nthreads=nthr)
             rg.append(r)
             dp.append(d)
-        O.compose(np.stack(rg), np.stack(dp), nthreads=nthr)
+        out = O.compose(np.stack(rg), np.stack(dp), nthreads=nthr)
+        if keep is not None:
+            keep[int(t)] = out
         rays += (x1 - x0) * (y1 - y0)
         used += 1
         if time.perf_counter() - t0 >= seconds or (max_tiles and used >= max_tiles):
             break
+    if keep is not None:
+        keep["counters"] = cnt
     return rays, time.perf_counter() - t0, used
 
 
+def verify_vs_oracle(R, N, cams, tiles, my_tiles, n_max, stride, W, H, n_views, kept, mlp):
+    """The timed launch path's frame vs the oracle's (N=1): the same camera
+    re-rendered (1) into a prefilled encode_frame buffer exactly as a timed
+    step does (same launch sizes, so the same auto-selected variants) and
+    (2) with f32 outputs through the same march / shade path; compared on
+    every tile the oracle rendered: depth bits, hit pattern, counters
+    (when the oracle covered the whole frame), rgba within the MLP mode's
+    tolerance, encode_frame bytes."""
+    import torch
+    from oracle import oracle as O
+    dev = my_tiles.device
+    NPX = n_views * H * W
+    enc = {"rgba8": torch.zeros((NPX, 4), dtype=torch.uint8, device=dev),
+           "depth16": torch.full((NPX,), -1, dtype=torch.int16, device=dev),
+           "counters": torch.zeros(4, dtype=torch.int64, device=dev)}
+    R.render(cams, my_tiles, n_max, stride, enc, frame_layout=True, prefilled=True)
+    variant = R.last_launch()
+    f32 = R.alloc(n_max, stride, want_f32=True, want_u8=False)
+    R.render(cams, my_tiles, n_max, stride, f32, frame_layout=True)
+    torch.cuda.synchronize()
+    g_rgba = f32["rgba"][:NPX].cpu().numpy().reshape(n_views, H, W, 4)
+    g_depth = f32["depth"][:NPX].cpu().numpy().reshape(n_views, H, W)
+    g_r8 = enc["rgba8"].cpu().numpy().reshape(n_views, H, W, 4)
+    g_d16 = enc["depth16"].cpu().numpy().view(np.uint16).reshape(n_views, H, W)
+    cnt = f32["counters"].cpu().numpy()
+    rgba_err, lsb, depth_bad, d16_bad, covered, px = 0.0, 0, 0, 0, 0, 0
+    for t, (o_rgba, o_depth) in ((k, v) for k, v in kept.items() if k != "counters"):
+        c, x0, y0, x1, y1 = (int(v) for v in tiles[t])
+        gr, gd = g_rgba[c, y0:y1, x0:x1], g_depth[c, y0:y1, x0:x1]
+        rgba_err = max(rgba_err, float(np.abs(gr.astype(np.float64) - o_rgba).max()))
+        depth_bad += int((~((gd == o_depth) | (np.isinf(gd) & np.isinf(o_depth)))).sum())
+        e8, e16 = O.encode_frame(o_rgba, o_depth)
+        lsb = max(lsb, int(np.abs(g_r8[c, y0:y1, x0:x1].astype(np.int32) - e8).max()))
+        d16_bad += int((g_d16[c, y0:y1, x0:x1] != e16).sum())
+        covered += int(np.isfinite(o_depth).sum())
+        px += o_depth.size
+    oc = kept["counters"]
+    full = px == NPX
+    tol = 1e-3 if mlp == "fp32" else 2.0 / 255.0
+    # fp32: every depth bit equal; bf16: compose's alpha_vis = 0.5 test may flip
+    # on layers whose alpha is within the MLP's error of 0.5 (a few pixels)
+    depth_ok = depth_bad == 0 if mlp == "fp32" else depth_bad <= max(3, covered // 500)
+    counters_ok = (not full) or (int(cnt[2]) == oc.hit_pixels and int(cnt[3]) == oc.march_samples)
+    return {
+        "what": "timed launch path (same camera as the last timed step) vs the C oracle (pinned to the "
+                "reference goldens, every march step evaluated) on every tile the cpu_baseline leg rendered",
+        "launch_variant": variant, "tiles_checked": len(kept) - 1, "pixels_checked": px,
+        "full_frame": full, "covered_pixels": covered,
+        "depth_mismatched_px": depth_bad, "depth16_mismatched_px": d16_bad,
+        "rgba_max_abs_err": rgba_err, "rgba_tol": tol, "rgba8_max_lsb": lsb,
+        "counters": {"gpu_hits": int(cnt[2]), "gpu_march_samples": int(cnt[3]),
+                     "oracle_hits": oc.hit_pixels if full else None,
+                     "oracle_march_samples": oc.march_samples if full else None},
+        "pass": bool(depth_ok and counters_ok and rgba_err <= tol and lsb <= (1 if mlp == "fp32" else 3)),
+    }
+
+
 def run_reference(args):
+    """The reference arm: the reference's algorithm (the C oracle port of
+    radfarm's render_rays + compose, every fixed march step evaluated) on the
+    box's host cores.  Nothing of the product is loaded in this process: the
+    synthetic assets are built (or found cached) by a child process first,
+    and this process only reads the .nolf files (pure Python) and maps the
+    oracle library."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
+    cmd = [sys.executable, os.path.abspath(__file__), "--build-assets", "--config", str(args.config),
+           "--assets", str(args.assets)]
+    env = {k: v for k, v in os.environ.items() if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK")}
+    subprocess.run(cmd, check=True, env=env, stdout=subprocess.DEVNULL)
     from oracle import oracle as O
-    from paper_2303_04086_b200.render import frame_tiles
+    from paper_2303_04086_b200.render import frame_tiles   # numpy only; no native library
     O.build()
-    import torch
-    if torch.cuda.is_available():
-        torch.cuda.set_device(0)        # asset synthesis only; the timed path is CPU
-    scene, views, W, H, desc = workload(args)
+    scene, views, W, H, desc = workload(args, cache_only=True)
     n_views = len(views(0))
     tiles = np.concatenate([frame_tiles(W, H, args.tile, cam=v) for v in range(n_views)])
     cores = os.cpu_count()
@@ -278,16 +361,31 @@ def run_reference(args):
     sample = (f"{args.steps} steps x {per_step_tiles} random {args.tile}x{args.tile} tiles of "
               f"{desc} ({len(scene)} assets each, oracle render + compose on {cores} threads), "
               f"extrapolated to Mrays/s")
+    cfg = workload_config(args, desc, W, H, len(scene))
+    cfg["workload"] = (f"{desc}, {args.tile}x{args.tile} ray tiles: render_rays of every asset + "
+                       f"compose (f32 frame; no encode_frame), CPU")
+    cfg["parallelism"] = f"{cores} host threads (OpenMP over rays)"
+    cfg.pop("mlp", None)
+    cfg.pop("partition", None)
+    cfg.pop("l2", None)
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": el / args.steps * 1e3, "fps": value * 1e6 / npix,
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": workload_config(args, desc, W, H, len(scene)),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64+fp32",
+        "data": "synthetic", "config": cfg,
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
                          "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
+
+
+def build_assets(args):
+    """--build-assets: synthesise (or find cached) the config's assets, then exit."""
+    import torch
+    if torch.cuda.is_available():
+        torch.cuda.set_device(0)
+    workload(args)
 
 
 def workload_config(args, desc, W, H, n_assets):
@@ -819,8 +917,12 @@ def run_ours(args):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        # the oracle renders the last timed step's camera: timed as the CPU
+        # baseline, and kept as the reference frame the timed path is verified on
+        kv = args.warmup + args.steps - 1
+        kept = {}
         try:
-            rays, el, used = cpu_sample(scene, views(0), tiles, args.cpu_seconds)
+            rays, el, used = cpu_sample(scene, views(kv), tiles, args.cpu_seconds, keep=kept)
             cpu = {"value": rays / el / 1e6, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
                    "sample": f"{used} of {len(tiles)} random {T}x{T} tiles ({len(scene)} assets "
                              f"each), oracle render + compose on {os.cpu_count()} OpenMP threads, "
@@ -828,6 +930,13 @@ def run_ours(args):
         except Exception as e:  # noqa: BLE001
             cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
                    "sample": f"failed: {e}"}
+        if len(kept) > 1:
+            vo = verify_vs_oracle(R, N, cam_arrays[kv % n_cam], tiles, my_tiles, n_max, stride, W, H,
+                                  n_views, kept, args.mlp)
+            if verify is None:
+                verify = vo
+            else:
+                verify["oracle"] = vo
     # our kernels per timed step on rank 0: k_cull_chunks + k_march_chunks +
     # k_shade_tc + k_compose (k_march alone when tiles are not 128-slot
     # aligned), + k_unpack (gather exchange) or k_flag_wait + one k_flag_set
@@ -843,7 +952,7 @@ def run_ours(args):
             "warmup": args.warmup, "ms_per_step": t_max / args.steps * 1e3,
             "fps": args.steps * n_views / t_max, "views_per_step": n_views,
             "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference-pipeline assets, "
+            "vs_baseline": None, "dtype": DTYPE if args.mlp == "bf16" else "f64+fp32", "data": "synthetic (reference-pipeline assets, "
             "random-init networks)", "config": workload_config(args, desc, W, H, len(scene)),
             "e2e": e2e, "gpu_launches": launches_per_step * args.steps,
             "gpu_launches_per_step": launches_per_step, "roofline": roof, "cpu_baseline": cpu,
@@ -894,7 +1003,9 @@ def run_ours(args):
 
 def main():
     args = parse()
-    if args.impl == "reference":
+    if args.build_assets:
+        build_assets(args)
+    elif args.impl == "reference":
         run_reference(args)
     else:
         run_ours(args)

@@ -31,7 +31,8 @@
  *
  * Error mapping in the host mirror (errors.py of the reference):
  *   NOLF_EINVAL -> DomainError, NOLF_ESTATE -> StateError,
- *   NOLF_EDATA -> DataError, NOLF_ECUDA / NOLF_ENOMEM -> RuntimeError.
+ *   NOLF_EDATA -> DataError, NOLF_ECAPACITY -> CapacityError,
+ *   NOLF_ECUDA / NOLF_ENOMEM -> RuntimeError.
  */
 #ifndef NOLF_H_
 #define NOLF_H_
@@ -51,6 +52,7 @@ extern "C" {
 #define NOLF_EDATA -3
 #define NOLF_ECUDA -4
 #define NOLF_ENOMEM -5
+#define NOLF_ECAPACITY -6   /* work was dropped on the device (see nolf_check_errors) */
 
 #define NOLF_HEAD_IDENTITY 0
 #define NOLF_HEAD_SIGMOID 1
@@ -210,6 +212,40 @@ int nolf_march_rays(nolf_asset_t asset, const double *origins, int32_t origin_st
  * neural.py:89-108) at n object-space points -> (n, 4) post-activation
  * (c_d, t); what bake_diffuse_cubes caches (lightfield.py:547-576). */
 int nolf_eval_diffuse(nolf_asset_t asset, const double *points, int64_t n, float *out, void *stream);
+
+/* Launch-variant knobs of the calling thread (defaults are the measured
+ * best; the timed variants are selected by launch size, so tests force each
+ * one to run it against the oracle).  Results never depend on them. */
+#define NOLF_OPT_MARCH_ORDER 1    /* 0 auto, 1 live chunks in spatial order, 2 heaviest first */
+#define NOLF_OPT_COMPOSE_SLOTS 2  /* live-chunk compose slots per thread: 0 auto, 4 or 8 */
+#define NOLF_OPT_HEAVY_WAVES 3    /* auto order: heaviest-first below this many CTA waves (3) */
+int nolf_set_option(int32_t key, int64_t value);
+
+/* Device-side failures fail loudly.  The kernels count (never silently
+ * blend) work they had to drop: hit records beyond an instance's queue, hits
+ * beyond a pixel's compose layers, scene tiles outside their camera's frame
+ * (or larger than tile_stride), BVH traversals deeper than the stack -- all
+ * impossible for valid inputs.  The counters are read back asynchronously
+ * after every render call; an increase makes the NEXT render call on the
+ * thread return NOLF_ECAPACITY.  nolf_check_errors synchronises `stream`
+ * and reports at once (NOLF_ECAPACITY, message in nolf_last_error). */
+int nolf_check_errors(void *stream);
+
+/* The variants the calling thread's last render call launched: info[0] = 1
+ * when live 128-slot chunks were compacted and marched (k_cull_chunks +
+ * k_march_chunks), info[1] = 1 heaviest-first / 0 spatial order, info[2] =
+ * live-chunk compose slots per thread (4 / 8; 0 = full-frame k_compose),
+ * info[3] = 1 bf16 tcgen05 shading (k_shade_tc) / 0 fp32 (k_shade). */
+int nolf_last_launch(int32_t info[4]);
+
+/* Parity read-back (debug): while slots != NULL, every render call on the
+ * calling thread makes its shading kernel (k_shade / k_shade_tc) store the
+ * 8 PSH corner slots it gathered for each shaded hit -- PshTable.corner_slots
+ * (encoding.py:130-140), corner order CORNERS (encoding.py:34-37) -- to
+ * slots[8*row + c] (u32, DEVICE), row = the hit's output row (render_rays /
+ * render_rect) or layer*P + slot (render_scene's compose layers); rows >=
+ * capacity_rows are not written.  NULL turns it off. */
+int nolf_debug_psh_slots(uint32_t *slots, int64_t capacity_rows);
 
 /* Per-kernel timing: while enabled, every render call of the calling thread
  * records CUDA events on its stream around k_march, k_shade, k_compose (up to

@@ -18,8 +18,10 @@ LIB_NAME = "libnolf_b200.so"
 LIB_PATH = os.environ.get("NOLF_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)),
                                                      LIB_NAME)
 
-NOLF_EINVAL, NOLF_ESTATE, NOLF_EDATA, NOLF_ECUDA, NOLF_ENOMEM = -1, -2, -3, -4, -5
+NOLF_EINVAL, NOLF_ESTATE, NOLF_EDATA, NOLF_ECUDA, NOLF_ENOMEM, NOLF_ECAPACITY = -1, -2, -3, -4, -5, -6
 HEAD_ACT = {"identity": 0, "sigmoid": 1, "exponential": 2}
+# nolf_set_option keys (include/nolf.h)
+OPT_MARCH_ORDER, OPT_COMPOSE_SLOTS, OPT_HEAVY_WAVES = 1, 2, 3
 MLP_FP32, MLP_BF16 = 0, 1
 
 
@@ -104,6 +106,10 @@ def lib():
         "nolf_march_rays": ([vp, vp, i32, vp, i64, vp, vp, vp, vp, vp, vp, C.c_size_t, vp], C.c_int),
         "nolf_eval_diffuse": ([vp, vp, i64, vp, vp], C.c_int),
         "nolf_profile": ([C.c_int], C.c_int),
+        "nolf_debug_psh_slots": ([vp, i64], C.c_int),
+        "nolf_set_option": ([i32, i64], C.c_int),
+        "nolf_last_launch": ([vp], C.c_int),
+        "nolf_check_errors": ([vp], C.c_int),
         "nolf_mlp_eval": ([vp, C.c_int, vp, i64, vp, vp], C.c_int),
         "nolf_device_alloc": ([C.c_size_t, C.POINTER(vp)], C.c_int),
         "nolf_device_free": ([vp], C.c_int),
@@ -141,6 +147,8 @@ def check(rc: int) -> None:
         raise errors.StateError(msg)
     if rc == NOLF_EDATA:
         raise errors.DataError(msg)
+    if rc == NOLF_ECAPACITY:
+        raise errors.CapacityError(msg)
     raise RuntimeError(f"nolf error {rc}: {msg}")
 
 

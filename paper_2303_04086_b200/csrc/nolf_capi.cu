@@ -257,6 +257,22 @@ int upload_mesh(NolfAsset *A, const NolfAssetDesc &d, DevMesh *out) {
   }
   B.nodes.push_back(BvhNode{});
   B.build(0, 0, nt);
+  // traversal keeps one far child per level on a 32-entry stack
+  // (nolf_mesh.cuh): median splits give depth ceil(log2(nt / 4)) <= 28
+  {
+    std::vector<std::pair<int, int>> st{{0, 0}};
+    int depth = 0;
+    while (!st.empty()) {
+      const auto [nd, dd] = st.back();
+      st.pop_back();
+      depth = std::max(depth, dd);
+      if (B.nodes[(size_t)nd].count == 0) {
+        st.push_back({B.nodes[(size_t)nd].first, dd + 1});
+        st.push_back({B.nodes[(size_t)nd].first + 1, dd + 1});
+      }
+    }
+    if (depth > 28) return fail(NOLF_EINVAL, "mesh proxy: BVH depth %d exceeds the traversal stack", depth);
+  }
   std::vector<double> tri(9ull * nt);
   for (int i = 0; i < nt; ++i)
     for (int v = 0; v < 3; ++v)
@@ -768,10 +784,114 @@ size_t nolf_scene_workspace_bytes(const NolfInstance *inst, int32_t n_inst, cons
 
 namespace {
 
+// Launch-variant knobs (nolf_set_option), per thread; defaults from the
+// environment (NOLF_HEAVY_WAVES, NOLF_COMPOSE_G) at first use.
+struct Options {
+  long long heavy_waves = 3;   // marcher launches below this many CTA waves go heaviest-chunk-first
+  int march_order = 0;         // 0 auto, 1 spatial list, 2 heavy-first buckets
+  int compose_slots = 0;       // live-chunk compose slots per thread: 0 auto, 4, 8
+  bool init = false;
+};
+thread_local Options g_opt;
+
+Options &options() {
+  if (!g_opt.init) {
+    if (const char *e = getenv("NOLF_HEAVY_WAVES")) g_opt.heavy_waves = atoll(e);
+    if (const char *e = getenv("NOLF_COMPOSE_G")) g_opt.compose_slots = atoi(e);
+    g_opt.init = true;
+  }
+  return g_opt;
+}
+
+// Sticky device error counters (kErr*, nolf_kernels.cuh) per device, read
+// back asynchronously after every render call on a side stream; an increase
+// fails the next call on this thread (or nolf_check_errors) with
+// NOLF_ECAPACITY -- the dropped work is never silently blended.
+struct ErrState {
+  unsigned *dev = nullptr;     // [kNumErr] device counters (monotone)
+  unsigned *host = nullptr;    // pinned mirror
+  cudaEvent_t ev = nullptr, ev_done = nullptr;
+  bool pending = false;
+  unsigned seen[kNumErr] = {0, 0, 0, 0};
+};
+constexpr int kMaxDevices = 64;
+thread_local ErrState g_errs[kMaxDevices];
+
+int cur_device() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return dev >= 0 && dev < kMaxDevices ? dev : 0;
+}
+
+int err_state(ErrState **out) {
+  ErrState &E = g_errs[cur_device()];
+  if (!E.dev) {
+    CUDA_TRY(cudaMalloc(&E.dev, sizeof(unsigned) * kNumErr));
+    CUDA_TRY(cudaMemset(E.dev, 0, sizeof(unsigned) * kNumErr));
+    CUDA_TRY(cudaMallocHost(&E.host, sizeof(unsigned) * kNumErr));
+    memset(E.host, 0, sizeof(unsigned) * kNumErr);
+    CUDA_TRY(cudaEventCreateWithFlags(&E.ev, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventCreateWithFlags(&E.ev_done, cudaEventDisableTiming));
+  }
+  *out = &E;
+  return 0;
+}
+
+int report_errors(ErrState &E) {
+  const char *what[kNumErr] = {"hit records dropped: an instance's hit queue overflowed",
+                               "hits dropped: more hits than compose layers at a pixel",
+                               "scene tiles skipped: outside their camera's frame, larger than tile_stride or "
+                               "naming a missing camera",
+                               "BVH nodes dropped: traversal stack overflow"};
+  for (int i = 0; i < kNumErr; ++i)
+    if (E.host[i] != E.seen[i]) {
+      const unsigned n = E.host[i] - E.seen[i];
+      for (int j = 0; j < kNumErr; ++j) E.seen[j] = E.host[j];
+      return fail(NOLF_ECAPACITY, "%u %s (device error counter %d)", n, what[i], i);
+    }
+  return 0;
+}
+
+// Non-blocking: fold in the last read-back if it has landed.
+int poll_errors() {
+  ErrState *E;
+  int rc;
+  if ((rc = err_state(&E))) return rc;
+  if (E->pending && cudaEventQuery(E->ev_done) == cudaSuccess) {
+    E->pending = false;
+    return report_errors(*E);
+  }
+  return 0;
+}
+
+// Queue a read-back of the counters after the work on st (side stream aux).
+int post_errors(cudaStream_t st, cudaStream_t aux) {
+  ErrState *E;
+  int rc;
+  if ((rc = err_state(&E))) return rc;
+  if (E->pending) return 0;
+  CUDA_TRY(cudaEventRecord(E->ev, st));
+  CUDA_TRY(cudaStreamWaitEvent(aux, E->ev, 0));
+  CUDA_TRY(cudaMemcpyAsync(E->host, E->dev, sizeof(unsigned) * kNumErr, cudaMemcpyDeviceToHost, aux));
+  CUDA_TRY(cudaEventRecord(E->ev_done, aux));
+  E->pending = true;
+  return 0;
+}
+
+// nolf_last_launch: the variants the calling thread's last scene launch ran
+// {chunked live-chunk march, heavy_first, compose slots per thread (0 = k_compose), mlp bf16}
+thread_local int32_t g_last_launch[4] = {0, 0, 0, 0};
+
+// nolf_debug_psh_slots: PSH-slot read-back buffer of the calling thread
+thread_local uint32_t *g_dbg_slots = nullptr;
+thread_local long long g_dbg_rows = 0;
+
 int run_shade(const DevInst *inst, const long long *qoff, int n_inst, const Workspace &w, int mode, float *rgba,
               float *depth, long long layer_stride, unsigned long long *counters, cudaStream_t st, bool use_tc,
               uint32_t phi_smem_bytes) {
   ShadeArgs sa{};
+  sa.dbg_slots = g_dbg_slots;
+  sa.dbg_rows = g_dbg_rows;
   sa.inst = inst;
   sa.n_inst = n_inst;
   sa.queue = w.queue;
@@ -928,6 +1048,10 @@ int launch_march_shade(int mode, const NolfInstance *ins, int n_inst, const Nolf
   if (mode == kModeScene && n_inst > 255) return fail(NOLF_EINVAL, "too many layers");
   for (int k = 0; k < n_inst; ++k)
     if (!ins[k].asset) return fail(NOLF_EINVAL, "null asset instance");
+  int rc0;
+  if ((rc0 = poll_errors())) return rc0;    // an earlier launch dropped work: fail loudly
+  ErrState *errs;
+  if ((rc0 = err_state(&errs))) return rc0;
   std::vector<CamParams> hcams((size_t)std::max(n_cams, 1));
   fill_cams(cams, n_cams, hcams.data());
   thread_local Plan pl;
@@ -962,6 +1086,8 @@ int launch_march_shade(int mode, const NolfInstance *ins, int n_inst, const Nolf
   if (n_rays == 0) return ring_release(slot, st);
   CUDA_TRY(cudaMemsetAsync(w.counts, 0, sizeof(unsigned) * (n_inst + 2 + kChunkBuckets), st));
 
+  g_last_launch[0] = g_last_launch[1] = g_last_launch[2] = 0;
+  g_last_launch[3] = use_tc ? 1 : 0;
   MarchArgs ma{};
   ma.inst = dp->inst;
   ma.n_inst = n_inst;
@@ -982,8 +1108,11 @@ int launch_march_shade(int mode, const NolfInstance *ins, int n_inst, const Nolf
   ma.depth = depth;
   ma.nhit = w.nhit;
   ma.counters = counters;
+  ma.max_layers = pl.layers;
+  ma.errors = errs->dev;
   const unsigned grid = (unsigned)((n_rays + kMarchThreads - 1) / kMarchThreads);
   const bool chunked = mode == kModeScene && n_cams > 0 && tile_stride % kMarchThreads == 0;
+  g_last_launch[0] = chunked ? 1 : 0;
   if ((rc = prof_mark(0, st))) return rc;
   if (mode == kModeRays) k_march<kModeRays><<<grid, kMarchThreads, 0, st>>>(ma);
   else if (mode == kModeRect) k_march<kModeRect><<<grid, kMarchThreads, 0, st>>>(ma);
@@ -1013,9 +1142,12 @@ int launch_march_shade(int mode, const NolfInstance *ins, int n_inst, const Nolf
       le.pending = false;
     }
     const long long want = (long long)le.last + (long long)le.last / 8 + 2ll * num_sms();
-    // a launch of only a few waves is bounded by its heaviest CTAs: start them first
-    static const long long heavy_waves = getenv("NOLF_HEAVY_WAVES") ? atoll(getenv("NOLF_HEAVY_WAVES")) : 3;
-    ma.heavy_first = le.last < heavy_waves * NOLF_MARCH_MINB * num_sms() ? 1 : 0;
+    // a launch of only a few waves is bounded by its heaviest CTAs: start them
+    // first (NOLF_OPT_MARCH_ORDER forces either order)
+    const Options &opt = options();
+    ma.heavy_first = opt.march_order == 1 ? 0 : opt.march_order == 2 ? 1
+                   : (le.last < opt.heavy_waves * NOLF_MARCH_MINB * num_sms() ? 1 : 0);
+    g_last_launch[1] = ma.heavy_first;
     k_cull_chunks<<<(unsigned)((n_chunks + 127) / 128), 128, 0, st>>>(ma, n_chunks, w.chunk_live, w.chunk_list,
                                                                       w.counts + n_inst);
     CUDA_TRY(cudaGetLastError());
@@ -1045,6 +1177,7 @@ int launch_march_shade(int mode, const NolfInstance *ins, int n_inst, const Nolf
     ca.tiles = reinterpret_cast<const TileParams *>(tiles_dev);
     ca.tile_stride = tile_stride;
     ca.cams = dp->cams;
+    ca.n_cams = n_cams;
     ca.frame_layout = sout->layout;
     ca.peer = sout->peer;
     ca.alpha_vis = (float)alpha_vis;
@@ -1067,8 +1200,9 @@ int launch_march_shade(int mode, const NolfInstance *ins, int n_inst, const Nolf
       const long long n_chunks = n_rays / kMarchThreads;
       const long long live = std::min<long long>(n_chunks, g_live.last + g_live.last / 8 + 2ll * num_sms());
       // 8 slots per thread, or 4 when that leaves under ~1024 threads per SM
-      static const int g_env = getenv("NOLF_COMPOSE_G") ? atoi(getenv("NOLF_COMPOSE_G")) : 0;
-      const int G = g_env == 4 || g_env == 8 ? g_env : (live * 16 >= 1024ll * num_sms() ? 8 : 4);
+      const int g_opt = options().compose_slots;
+      const int G = g_opt == 4 || g_opt == 8 ? g_opt : (live * 16 >= 1024ll * num_sms() ? 8 : 4);
+      g_last_launch[2] = G;
       const long long threads = live * (128 / G);
       const unsigned cgrid = (unsigned)std::max<long long>(1, (threads + 255) / 256);
       if (G == 8) k_compose_live<8><<<cgrid, 256, 0, st>>>(ca, w.chunk_list, w.counts + n_inst, n_chunks);
@@ -1086,7 +1220,7 @@ int launch_march_shade(int mode, const NolfInstance *ins, int n_inst, const Nolf
     if ((rc = prof_mark(3, st))) return rc;
     if ((rc = ring_release(slot, st))) return rc;
   }
-  return 0;
+  return post_errors(st, ax.s);
 }
 
 }  // namespace
@@ -1166,6 +1300,10 @@ int nolf_march_rays(nolf_asset_t asset, const double *origins, int32_t origin_st
   ma.out_p_h = p_h;
   unsigned long long *dummy = nullptr;
   ma.counters = dummy;
+  ErrState *errs;
+  if ((rc = poll_errors())) return rc;
+  if ((rc = err_state(&errs))) return rc;
+  ma.errors = errs->dev;
   k_march<kModeRays><<<(unsigned)((n + 127) / 128), 128, 0, st>>>(ma);
   CUDA_TRY(cudaGetLastError());
   return 0;
@@ -1207,6 +1345,50 @@ int nolf_mlp_eval(nolf_asset_t asset, int mode, const float *x, int64_t n, float
     return fail(NOLF_EINVAL, "unknown MLP mode %d", mode);
   }
   CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+int nolf_set_option(int32_t key, int64_t value) {
+  Options &o = options();
+  switch (key) {
+    case NOLF_OPT_MARCH_ORDER:
+      if (value < 0 || value > 2) return fail(NOLF_EINVAL, "march order %lld outside 0..2", (long long)value);
+      o.march_order = (int)value;
+      return 0;
+    case NOLF_OPT_COMPOSE_SLOTS:
+      if (value != 0 && value != 4 && value != 8) return fail(NOLF_EINVAL, "compose slots must be 0, 4 or 8");
+      o.compose_slots = (int)value;
+      return 0;
+    case NOLF_OPT_HEAVY_WAVES:
+      if (value < 0) return fail(NOLF_EINVAL, "heavy waves must be >= 0");
+      o.heavy_waves = value;
+      return 0;
+    default:
+      return fail(NOLF_EINVAL, "unknown option %d", key);
+  }
+}
+
+int nolf_check_errors(void *stream) {
+  ErrState *E;
+  int rc;
+  if ((rc = err_state(&E))) return rc;
+  CUDA_TRY(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
+  if (E->pending) CUDA_TRY(cudaEventSynchronize(E->ev_done));
+  E->pending = false;
+  CUDA_TRY(cudaMemcpy(E->host, E->dev, sizeof(unsigned) * kNumErr, cudaMemcpyDeviceToHost));
+  return report_errors(*E);
+}
+
+int nolf_last_launch(int32_t *info) {
+  if (!info) return fail(NOLF_EINVAL, "null argument");
+  for (int i = 0; i < 4; ++i) info[i] = g_last_launch[i];
+  return 0;
+}
+
+int nolf_debug_psh_slots(uint32_t *slots, int64_t capacity_rows) {
+  if (slots && capacity_rows < 0) return fail(NOLF_EINVAL, "negative capacity");
+  g_dbg_slots = slots;
+  g_dbg_rows = slots ? capacity_rows : 0;
   return 0;
 }
 

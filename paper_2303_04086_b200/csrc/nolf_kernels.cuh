@@ -69,7 +69,28 @@ struct MarchArgs {
   unsigned *fetch;
   long long list_stride;
   int heavy_first;             // walk the buckets (most candidates first) instead of the spatial list
+  int max_layers;              // scene mode: compose layers per pixel slot in the workspace
+  unsigned *errors;            // sticky device error counters (kErr*), never NULL
 };
+
+// Device error counters (nolf_capi.cu reads them back and fails loudly):
+// a hit record that did not fit its instance's queue, a hit beyond the
+// pixel's compose layers, a scene tile outside its camera's frame (or larger
+// than tile_stride, or naming a missing camera), a BVH traversal deeper than
+// its stack.  Each is impossible for valid inputs (the host sizes queues and
+// layers from the screen boxes); they guard against invalid ones, and the
+// offending work is dropped instead of writing out of bounds.
+enum { kErrQueue = 0, kErrLayers = 1, kErrTile = 2, kErrBvh = 3, kNumErr = 4 };
+
+// A scene tile the kernels may address: a non-empty rect inside its camera's
+// frame with no more pixels than a tile slot holds.
+__device__ __forceinline__ bool tile_valid(const TileParams &tp, const CamParams *cams, int n_cams,
+                                           long long stride) {
+  if (tp.cam < 0 || tp.cam >= n_cams) return false;
+  const CamParams &c = cams[tp.cam];
+  return tp.x0 >= 0 && tp.y0 >= 0 && tp.x1 > tp.x0 && tp.y1 > tp.y0 && tp.x1 <= c.width && tp.y1 <= c.height &&
+         (long long)(tp.x1 - tp.x0) * (tp.y1 - tp.y0) <= stride;
+}
 
 constexpr int kChunkBuckets = 8;   // candidate-count buckets (the last one: >= 7 instances)
 
@@ -394,6 +415,10 @@ __device__ __forceinline__ bool slot_pixel(const MarchArgs &args, long long gid,
   long long t = 0, local = gid;
   if (MODE != kModeRect) split_slot(gid, args.tile_stride, t, local);
   const TileParams tp = args.tiles[t];
+  if (MODE == kModeScene && !tile_valid(tp, args.cams, args.n_cams, args.tile_stride)) {
+    if (local == 0) atomicAdd(args.errors + kErrTile, 1u);
+    return false;
+  }
   const int w = tp.x1 - tp.x0, h = tp.y1 - tp.y0;
   if (local >= (long long)w * h) return false;
   cam = tp.cam;
@@ -477,7 +502,7 @@ struct MarchSpan {
 
 __device__ __forceinline__ bool prepare_march(const DevInst &I, const DevAsset &A, bool raw_rays, const double ow[3],
                                               const double dw[3], double o[3], double d[3], double inv[3],
-                                              MarchSpan &sp) {
+                                              MarchSpan &sp, unsigned *errors) {
   if (raw_rays) {
 #pragma unroll
     for (int q = 0; q < 3; ++q) { o[q] = ow[q]; d[q] = dw[q]; }
@@ -490,7 +515,7 @@ __device__ __forceinline__ bool prepare_march(const DevInst &I, const DevAsset &
   sp.noclip = false;
   bool boxhit = slab(A.pmin, A.pmax, o, d, sp.t_near, sp.t_far, inv);
   if (boxhit && A.mesh.nodes) {          // mesh proxy: march from its first hit
-    const double tm = mesh_first_hit(A.mesh, o, d);
+    const double tm = mesh_first_hit(A.mesh, o, d, errors + kErrBvh);
     if (tm < 0.0) boxhit = false;
     else sp.t_near = tm;
   }
@@ -583,7 +608,7 @@ __device__ __forceinline__ void march_chunk(const MarchArgs &args, unsigned chun
       NOLF_STAT(0, 1);
       double ow[3], dw[3];     // rebuilt per candidate instead of held across the march
       world_ray<MODE>(args, gid, cam, pix_x, pix_y, ow, dw);
-      if (prepare_march(I, A, args.raw_rays, ow, dw, o, d, inv, sp)) {
+      if (prepare_march(I, A, args.raw_rays, ow, dw, o, d, inv, sp, args.errors)) {
         NOLF_STAT(2, 1);
         const float invf[3] = {(float)inv[0], (float)inv[1], (float)inv[2]};
         mr = run_march(A, o, d, invf, sp, args.use_zmask);
@@ -603,6 +628,12 @@ __device__ __forceinline__ void march_chunk(const MarchArgs &args, unsigned chun
       }
       continue;
     }
+    // a pixel never has more hits than compose layers (the host bounds the
+    // layers by the screen-box overlap); a violation is counted and dropped
+    if (MODE == kModeScene && hit && (int)ordinal >= args.max_layers) {
+      atomicAdd(args.errors + kErrLayers, 1u);
+      hit = false;
+    }
     // warp-aggregated queue append (one atomic per warp per instance)
     const unsigned ballot = __ballot_sync(0xffffffffu, hit);
     if (ballot) {
@@ -611,9 +642,12 @@ __device__ __forceinline__ void march_chunk(const MarchArgs &args, unsigned chun
       base = __shfl_sync(0xffffffffu, base, __ffs(ballot) - 1);
       if (hit) {
         const unsigned pos = base + __popc(ballot & ((1u << lane) - 1u));
-        if ((long long)pos < args.qoff[k + 1] - args.qoff[k])
+        if ((long long)pos < args.qoff[k + 1] - args.qoff[k]) {
           args.queue[args.qoff[k] + pos] = hit_record(A, o, d, sp.t_near, mr, (uint32_t)gid, ordinal);
-        ++ordinal;
+          ++ordinal;           // the layer exists only if its record does
+        } else {
+          atomicAdd(args.errors + kErrQueue, 1u);
+        }
       }
     }
   }
@@ -645,7 +679,9 @@ __global__ void __launch_bounds__(128) k_cull_chunks(MarchArgs args, long long n
     split_slot(c * kMarchThreads, args.tile_stride, t, local0);
     const TileParams tp = args.tiles[t];
     const int w = tp.x1 - tp.x0, h = tp.y1 - tp.y0;
-    if (local0 < (long long)w * h) {
+    const bool tv = tile_valid(tp, args.cams, args.n_cams, args.tile_stride);
+    if (!tv && local0 == 0) atomicAdd(args.errors + kErrTile, 1u);
+    if (tv && local0 < (long long)w * h) {
       // pixel rectangle of the chunk's valid slots: the bbox of the slot
       // positions at every 8x4-block start/end (row-major tiles: the rows)
       const long long l1 = min(local0 + kMarchThreads, (long long)w * h) - 1;
@@ -712,6 +748,8 @@ struct ShadeArgs {
   long long layer_stride;      // scene: P
   int tile_order;              // 0 round-robin tiles over CTAs, 1 blocked ranges
   unsigned long long *counters;
+  uint32_t *dbg_slots;         // debug (nolf_debug_psh_slots): 8 PSH slots per output row, or NULL
+  long long dbg_rows;          // rows dbg_slots holds
 };
 
 constexpr int kShadeThreads = 128;
@@ -828,10 +866,14 @@ __global__ void __launch_bounds__(kShadeThreads) k_shade(ShadeArgs args) {
     double w8[8];
     base_weights(rec.p, A.N, base, w8);
     double es0 = 0.0, es1 = 0.0, es_rest[2] = {0.0, 0.0};
+    const long long orow = args.mode == kModeScene ? (long long)rec.ordinal * args.layer_stride + rec.out_idx
+                                                   : (long long)rec.out_idx;
+    uint32_t *dbg = (args.dbg_slots && orow < args.dbg_rows) ? args.dbg_slots + 8 * orow : nullptr;
 #pragma unroll
     for (int c = 0; c < 8; ++c) {
       const uint32_t slot = psh_slot(A.tab, A.phi, A.N, A.m, A.mphi, base[0] + (c & 1),
                                      base[1] + ((c >> 1) & 1), base[2] + ((c >> 2) & 1));
+      if (dbg) dbg[c] = slot;
       if (A.F == 2) {
         const float2 f = __ldg(reinterpret_cast<const float2 *>(A.feat) + slot);
         es0 = __dadd_rn(es0, __dmul_rn((double)f.x, w8[c]));
@@ -893,10 +935,8 @@ __global__ void __launch_bounds__(kShadeThreads) k_shade(ShadeArgs args) {
       out = make_float4(0.f, 0.f, 0.f, 0.f);
       dep = __int_as_float(0x7f800000);
     }
-    const long long o = args.mode == kModeScene ? (long long)rec.ordinal * args.layer_stride + rec.out_idx
-                                                : (long long)rec.out_idx;
-    reinterpret_cast<float4 *>(args.rgba)[o] = out;
-    args.depth[o] = dep;
+    reinterpret_cast<float4 *>(args.rgba)[orow] = out;
+    args.depth[orow] = dep;
   }
   // fs_evals, fd_evals, hit_pixels (lightfield.py:299-301, 324-325)
   const unsigned lane = tid & 31;
@@ -975,7 +1015,8 @@ struct ComposeArgs {
   long long layer_stride;      // P
   const TileParams *tiles;     // scene mode: skip padding slots (NULL => none)
   long long tile_stride;
-  const CamParams *cams;       // frame layout: camera sizes / output bases
+  const CamParams *cams;       // scene mode: camera sizes / output bases (tile validation, frame layout)
+  int n_cams;
   int frame_layout;            // 0: outputs tile-packed at p ; 1: row-major frame per camera
   int peer;                    // outputs are a peer GPU's memory: fence system-wide at the end
   float alpha_vis;             // compared in f32 (numpy 2 weak scalar)
@@ -1115,6 +1156,7 @@ __device__ __forceinline__ long long compose_dst(const ComposeArgs &a, const Til
                                                  long long p) {
   const int w = tp.x1 - tp.x0, h = tp.y1 - tp.y0;
   if (local >= (long long)w * h) return -1;
+  if (!tile_valid(tp, a.cams, a.n_cams, a.tile_stride)) return -1;   // never marched (kErrTile)
   if (!a.frame_layout) return p;
   const CamParams &cp = a.cams[tp.cam];
   int x, y;
@@ -1204,7 +1246,8 @@ __device__ __forceinline__ void compose_eight(const ComposeArgs &a, const long l
   split_slot(p0, a.tile_stride, t, local0);
   const TileParams tp = a.tiles[t];
   const int w = tp.x1 - tp.x0, h = tp.y1 - tp.y0;
-  if (a.frame_layout && (w & 7) == 0 && (h & 3) == 0 && local0 < (long long)w * h && !a.out_rgba && !a.out_depth) {
+  if (a.frame_layout && (w & 7) == 0 && (h & 3) == 0 && local0 < (long long)w * h && !a.out_rgba && !a.out_depth &&
+      tile_valid(tp, a.cams, a.n_cams, a.tile_stride)) {
     const CamParams &cp = a.cams[tp.cam];
     int x, y;
     slot_xy(local0, w, h, x, y);

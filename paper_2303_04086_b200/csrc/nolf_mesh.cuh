@@ -66,7 +66,11 @@ __device__ __forceinline__ float node_entry(const BvhNode &n, float ox, float oy
 // Children are visited near-first (both boxes tested at the parent, the far
 // one pushed with its entry distance and dropped on pop if a closer hit was
 // found meanwhile); pruning only, the fp64 triangle tests decide t.
-__device__ __forceinline__ double mesh_first_hit(const DevMesh &M, const double o[3], const double d[3]) {
+// The host builds median-split trees of depth <= 28 (nolf_capi.cu
+// upload_mesh), so the stack (one far child per level) never fills; a deeper
+// tree would be counted in *err_overflow and its nodes dropped.
+__device__ __forceinline__ double mesh_first_hit(const DevMesh &M, const double o[3], const double d[3],
+                                                 unsigned *err_overflow) {
   const float ox = (float)o[0], oy = (float)o[1], oz = (float)o[2];
   // finite reciprocals: a zero component gets +-1e30 so (lo - o) * inv is never 0*inf
   auto rcp = [](double x) { const float f = (float)x; return 1.0f / copysignf(fmaxf(fabsf(f), 1e-30f), f); };
@@ -95,7 +99,9 @@ __device__ __forceinline__ double mesh_first_hit(const DevMesh &M, const double 
           best_f = (float)t;
         }
       }
-    } else if (sp < 30) {
+    } else if (sp >= 30) {
+      atomicAdd(err_overflow, 1u);
+    } else {
       const BvhNode L = M.nodes[n.first], R = M.nodes[n.first + 1];
       const float tl = node_entry(L, ox, oy, oz, ix, iy, iz, best_f);
       const float tr = node_entry(R, ox, oy, oz, ix, iy, iz, best_f);

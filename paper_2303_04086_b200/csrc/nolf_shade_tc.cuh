@@ -188,7 +188,8 @@ __device__ __forceinline__ void tc_stage_asset(const DevAsset &A, const TcSmemPt
 // index static (the row stays in registers); 0 = any F (local array).
 template <int FIXED_F>
 __device__ __forceinline__ void tc_gather_inputs(const DevAsset &A, const TcSmemPtrs &S, bool tab_smem,
-                                                 bool phi_smem, const HitRec &rec, float x[kTcK0]) {
+                                                 bool phi_smem, const HitRec &rec, float x[kTcK0],
+                                                 uint32_t *dbg_slots) {
   const int F = FIXED_F ? FIXED_F : A.F;
   int base[3];
   double w8[8];
@@ -242,6 +243,10 @@ __device__ __forceinline__ void tc_gather_inputs(const DevAsset &A, const TcSmem
     const uint32_t off = phi_smem ? tc::lds16(phia + 2u * h1) : __ldg(A.phi + h1);
     uint32_t slot = h0 + off;
     slots[c] = slot >= A.m ? slot - A.m : slot;
+  }
+  if (dbg_slots) {             // debug read-back of the addresses the gathers below use
+#pragma unroll
+    for (int c = 0; c < 8; ++c) dbg_slots[c] = slots[c];
   }
   if (FIXED_F == 2) {
     float2 f[8];               // all 8 gathers in flight before the sum
@@ -372,13 +377,16 @@ __global__ void __launch_bounds__(kTcThreads) k_shade_tc(ShadeArgs args) {
       t_obj = rec.t_obj;
       out_idx = rec.out_idx;
       ordinal = rec.ordinal;
+      const long long orow = args.mode == kModeScene ? (long long)ordinal * args.layer_stride + out_idx
+                                                     : (long long)out_idx;
+      uint32_t *dbg = (args.dbg_slots && orow < args.dbg_rows) ? args.dbg_slots + 8 * orow : nullptr;
       const bool want_dif = A.use_diffuse_color && A.has_dif;
       const int dif_cid = want_dif ? atlas_cell_id(A.dif, rec.p) : -1;   // overlaps the PSH gather
       if (A.F == 2) {            // the common layout: every input index is static -> registers
-        tc_gather_inputs<2>(A, S, tab_smem, phi_smem, rec, x);
+        tc_gather_inputs<2>(A, S, tab_smem, phi_smem, rec, x, dbg);
       } else {
         float xl[kTcK0] = {};
-        tc_gather_inputs<0>(A, S, tab_smem, phi_smem, rec, xl);
+        tc_gather_inputs<0>(A, S, tab_smem, phi_smem, rec, xl, dbg);
 #pragma unroll
         for (int q = 0; q < kTcK0; ++q) x[q] = xl[q];
       }

@@ -223,6 +223,12 @@ def _instance(asset, transform=None) -> N.Instance:
     return inst
 
 
+def check_device_errors(stream=None) -> None:
+    """Synchronise and raise CapacityError if any launch on this thread had
+    to drop work on the device (nolf_check_errors)."""
+    N.check(N.lib().nolf_check_errors(stream if stream is not None else _stream_ptr()))
+
+
 def _merge(counters, cnt_dev):
     if counters is None:
         return
@@ -231,6 +237,43 @@ def _merge(counters, cnt_dev):
     counters.fd_evals += int(c[1])
     counters.hit_pixels += int(c[2])
     counters.march_samples += int(c[3])
+
+
+# ------------------------------------------------------------------ test / debug hooks
+def set_option(key: int, value: int) -> None:
+    """Force a launch variant (nolf_set_option; _native.OPT_*) on this thread."""
+    N.check(N.lib().nolf_set_option(int(key), int(value)))
+
+
+def last_launch() -> dict:
+    """Variants of this thread's last render launch (nolf_last_launch)."""
+    info = (C.c_int32 * 4)()
+    N.check(N.lib().nolf_last_launch(info))
+    return {"chunked": bool(info[0]), "march_order": "heavy-first" if info[1] else "spatial",
+            "compose_slots": int(info[2]), "shade": "k_shade_tc (bf16)" if info[3] else "k_shade (fp32)"}
+
+
+class debug_psh_slots:
+    """While active, the shading kernels of this thread's render calls store
+    the 8 PSH corner slots each hit gathered (nolf_debug_psh_slots):
+    ``.slots()`` -> (rows, 8) int64 host array, -1 where no hit was shaded.
+    Row = output row (render_rays / render_range) or layer * P + slot
+    (render_scene)."""
+
+    def __init__(self, rows: int):
+        t = torch()
+        self.buf = t.full((max(int(rows), 1), 8), -1, dtype=t.int32, device=_device())
+
+    def __enter__(self):
+        N.check(N.lib().nolf_debug_psh_slots(self.buf.data_ptr(), len(self.buf)))
+        return self
+
+    def __exit__(self, *exc):
+        N.check(N.lib().nolf_debug_psh_slots(None, 0))
+
+    def slots(self):
+        torch().cuda.synchronize()
+        return self.buf.cpu().numpy().astype(np.int64)
 
 
 # ------------------------------------------------------------------ reference API
@@ -269,6 +312,7 @@ def render_rays(asset, origins, dirs, counters=None):
                                      rgba.data_ptr(), depth.data_ptr(), cnt.data_ptr(), ws.data_ptr(),
                                      ws.numel(), _stream_ptr()))
     out = rgba.cpu().numpy(), depth.cpu().numpy()
+    check_device_errors()
     _merge(counters, cnt)
     return out
 
@@ -304,8 +348,10 @@ def march_rays(asset, origins, dirs) -> MarchResult:
         N.check(N.lib().nolf_march_rays(device_asset(asset).handle, o.data_ptr(), 1, d.data_ptr(), n,
                                         hit.data_ptr(), t_hit.data_ptr(), alpha.data_ptr(), samples.data_ptr(),
                                         p_h.data_ptr(), None, 0, _stream_ptr()))
-    return MarchResult(hit.cpu().numpy().astype(bool), t_hit.cpu().numpy(), alpha.cpu().numpy(),
-                       samples.cpu().numpy(), p_h.cpu().numpy())
+    res = MarchResult(hit.cpu().numpy().astype(bool), t_hit.cpu().numpy(), alpha.cpu().numpy(),
+                      samples.cpu().numpy(), p_h.cpu().numpy())
+    check_device_errors()
+    return res
 
 
 def render_ray(asset, ray, counters=None):
@@ -333,6 +379,7 @@ def render_range(asset, ray_range, counters=None):
                                      depth.data_ptr(), cnt.data_ptr(), ws.data_ptr(), ws.numel(),
                                      _stream_ptr()))
     tile = TYPES["Tile"](x0=x0, y0=y0, rgba=rgba.cpu().numpy(), depth=depth.cpu().numpy())
+    check_device_errors()
     c = cnt.cpu().numpy()
     before_fs, before_hits = counters.fs_evals, counters.hit_pixels
     _merge(counters, cnt)
@@ -494,6 +541,12 @@ class SceneRenderer:
                                           self.alpha_vis, out["counters"].data_ptr(),
                                           ws.data_ptr(), ws.numel(), st))
 
+    def check(self, stream=None) -> None:
+        """Synchronise; CapacityError if a render dropped work on the device
+        (invalid tiles, ...).  Renders also fail on the call after one that
+        dropped work, once its asynchronous error read-back has landed."""
+        check_device_errors(stream)
+
 
 def slot_xy(local, w: int, h: int):
     """(x, y) inside a w x h tile of packed slot ``local`` (nolf_kernels.cuh:slot_xy)."""
@@ -535,6 +588,7 @@ def render_scene(scene, camera, counters=None, tile: int = 32):
     npx = camera.width * camera.height
     rgba = out["rgba"][:npx].reshape(camera.height, camera.width, 4)
     depth = out["depth"][:npx].reshape(camera.height, camera.width)
+    check_device_errors()
     _merge(counters, out["counters"])
     return Frame(width=camera.width, height=camera.height, rgba=rgba.cpu().numpy(),
                  depth=depth.cpu().numpy())

@@ -3,6 +3,7 @@ tests/golden/make_golden.py from the reference)."""
 
 import dataclasses
 import glob
+import hashlib
 import os
 
 import numpy as np
@@ -45,3 +46,33 @@ def camera(g):
     fx, fy, cx, cy = g["intr"]
     w, h = g["size"]
     return Camera(pose=g["pose"], fx=fx, fy=fy, cx=cx, cy=cy, width=int(w), height=int(h))
+
+
+def sha(a) -> str:
+    """SHA-256 of an array's dtype, shape and bytes."""
+    a = np.ascontiguousarray(a)
+    return hashlib.sha256(a.dtype.str.encode() + str(a.shape).encode() + a.tobytes()).hexdigest()
+
+
+def asset_digests(asset) -> dict:
+    """SHA-256 of every asset array the synth restatement must reproduce
+    exactly (name -> hex); diffuse cubes are compared by cube_sums instead."""
+    d = {
+        "density_index": sha(asset.density_atlas.index),
+        "density_cubes": sha(asset.density_atlas.cubes),
+        "psh_offsets": sha(np.asarray(asset.psh.offsets, np.int64)),
+        "psh_features": sha(asset.psh_features),
+        "diffuse_index": sha(asset.diffuse_atlas.index),
+    }
+    for tag, m in (("fs", asset.specular_mlp), ("fd", asset.diffuse_mlp)):
+        for i, (w, b) in enumerate(zip(m.weights, m.biases)):
+            d[f"{tag}_w{i}"] = sha(w)
+            d[f"{tag}_b{i}"] = sha(b)
+    for i, f in enumerate(asset.diffuse_features):
+        d[f"ed_feat_{i}"] = sha(f)
+    return d
+
+
+def cube_sums(cubes) -> np.ndarray:
+    """Per-cube f64 sums (the diffuse cubes' fingerprint)."""
+    return np.asarray(cubes, np.float64).reshape(len(cubes), -1).sum(axis=1)

@@ -1,0 +1,160 @@
+"""Parity at the reference's own scale (b=32, r=8, PSH N=64: pipeline.py:32-33,
+lightfield.py:585-586) -- the configuration the benchmark times.
+
+Goldens: tests/golden/make_golden_fullsize.py ran the reference pipeline for
+BASELINE config 1 (sphere, seed 0, 256x256, far and close views) and for
+config 4's 12-asset zodiac scene (480x270, the bench's step-0 camera).  The
+assets are rebuilt on the GPU box by tools/synth.py (the bench's asset
+factory); their SHA-256 digests must equal the reference-built arrays', so
+every render below runs on provably the reference's assets.
+
+Bars: depth bits, hit pattern, counters and PSH slots bit-exact; rgba
+<= 1e-3 (fp32 MLP) / <= 2/255 (bf16 tcgen05 MLP).  The zodiac frame also goes
+through the timed launch variants (spatial-order live-chunk march,
+k_compose_live<8> into a prefilled encode_frame buffer) and the others."""
+
+import os
+import sys
+
+import numpy as np
+import pytest
+
+from golden_util import asset_digests, camera, cube_sums, load
+from oracle import oracle as O
+from paper_2303_04086_b200 import _native as N
+from paper_2303_04086_b200 import render as R
+from paper_2303_04086_b200.model import RayRange, RenderCounters
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+TOL = {"fp32": 1e-3, "bf16": 2.0 / 255.0}
+
+
+def _check_digests(a, g, prefix=""):
+    names = [str(x) for x in g[f"{prefix}digest_names"]]
+    want = dict(zip(names, (str(x) for x in g[f"{prefix}digests"])))
+    got = asset_digests(a)
+    bad = [k for k in names if got.get(k) != want[k]]
+    assert not bad, f"{prefix}asset arrays differ from the reference-built ones: {bad}"
+    assert tuple(a.diffuse_atlas.cubes.shape) == tuple(g[f"{prefix}diffuse_cubes_shape"])
+    # diffuse cubes: fp32 MLP (sequential FMA) vs OpenBLAS sgemm, <= 2e-6 per value
+    np.testing.assert_allclose(cube_sums(a.diffuse_atlas.cubes), g[f"{prefix}diffuse_cube_sums"],
+                               rtol=0, atol=4e-3)
+
+
+@pytest.fixture(scope="module")
+def config1():
+    from tools import synth
+    g = load("fullsize_config1.npz")
+    a = synth.make_asset("sphere", seed=0)
+    _check_digests(a, g)
+    return a, g
+
+
+@pytest.mark.parametrize("mode", ["fp32", "bf16"])
+@pytest.mark.parametrize("view", ["", "close_"])
+def test_config1_reference_scale(config1, mode, view):
+    a, g0 = config1
+    g = {k[len(view):]: v for k, v in g0.items() if k.startswith(view)} if view else g0
+    cam = camera(g)
+    R.set_mlp_mode(mode)
+    try:
+        cnt = RenderCounters()
+        with R.debug_psh_slots(cam.width * cam.height) as dbg:
+            tile, _ = R.render_range(a, RayRange(cam, 0, 0, cam.width, cam.height), cnt)
+        slots = dbg.slots()
+    finally:
+        R.set_mlp_mode("fp32")
+    rgba, depth = tile.rgba.reshape(-1, 4), tile.depth.reshape(-1)
+    fin = np.isfinite(g["depth"])
+    assert np.array_equal(np.isfinite(depth), fin), "hit pattern differs"
+    assert np.array_equal(depth[fin], g["depth"][fin]), "depth bits (hit sample index) differ"
+    assert [cnt.fs_evals, cnt.fd_evals, cnt.hit_pixels, cnt.march_samples] == g["counters"].tolist()
+    assert np.array_equal(slots[g["hit_rows"]], g["psh_slots"]), "PSH addresses differ"
+    err = float(np.abs(rgba.astype(np.float64) - g["rgba"]).max())
+    assert err <= TOL[mode], f"{mode}: max |rgba - reference| = {err}"
+    print(f"config1 {view or 'far_'}{mode}: {len(g['hit_rows'])} hits, max rgba err {err:.3g}")
+
+
+@pytest.fixture(scope="module")
+def zodiac():
+    sys.path.insert(0, ROOT)
+    import bench
+    g = load("fullsize_zodiac.npz")
+    scene = bench.build_scene(12)          # the bench's own asset cache / factory
+    for i, (a, tr) in enumerate(scene):
+        _check_digests(a, g, prefix=f"a{i}_")
+        assert np.array_equal(tr, g["transforms"][i])
+    return scene, g
+
+
+def _render_zodiac(scene, cam, mode, order=0, slots=0, encode=False):
+    import torch
+    R.set_mlp_mode(mode)
+    R.set_option(N.OPT_MARCH_ORDER, order)
+    R.set_option(N.OPT_COMPOSE_SLOTS, slots)
+    try:
+        r = R.SceneRenderer(scene)
+        tiles = R.frame_tiles(cam.width, cam.height, 32)
+        dev = r.device
+        npx = cam.width * cam.height
+        if encode:                        # the bench's output: prefilled encode_frame RAW frame
+            out = {"rgba8": torch.zeros((npx, 4), dtype=torch.uint8, device=dev),
+                   "depth16": torch.full((npx,), -1, dtype=torch.int16, device=dev),
+                   "counters": torch.zeros(4, dtype=torch.int64, device=dev)}
+        else:
+            out = r.alloc(len(tiles), 1024, want_f32=True, want_u8=False)
+        r.render([cam], torch.from_numpy(tiles).to(dev), len(tiles), 1024, out, frame_layout=True,
+                 prefilled=encode)
+        torch.cuda.synchronize()
+        cnt = out["counters"].cpu().numpy()
+        if encode:
+            return (out["rgba8"].cpu().numpy().reshape(cam.height, cam.width, 4),
+                    out["depth16"].cpu().numpy().view(np.uint16).reshape(cam.height, cam.width), cnt)
+        return (out["rgba"][:npx].cpu().numpy().reshape(cam.height, cam.width, 4),
+                out["depth"][:npx].cpu().numpy().reshape(cam.height, cam.width), cnt)
+    finally:
+        R.set_mlp_mode("fp32")
+        R.set_option(N.OPT_MARCH_ORDER, 0)
+        R.set_option(N.OPT_COMPOSE_SLOTS, 0)
+
+
+def _check_composed_depth(depth, ref, mode, miss=np.inf):
+    """Composed depth = the first layer with alpha > alpha_vis (farm.py:156).
+    fp32: bit-exact.  bf16: a layer whose alpha lies within the MLP's error
+    of 0.5 may cross the threshold, so a few pixels (<= 0.2 % of the covered
+    ones) may take another layer's depth; every other pixel is bit-exact."""
+    bad = ~((depth == ref) | ((depth != depth) & (ref != ref)))
+    covered = int((ref != miss).sum())
+    if mode == "fp32":
+        assert not bad.any(), f"composed depth differs at {int(bad.sum())} pixels"
+    else:
+        assert int(bad.sum()) <= max(3, covered // 500), f"composed depth differs at {int(bad.sum())} pixels"
+
+
+@pytest.mark.parametrize("mode", ["fp32", "bf16"])
+@pytest.mark.parametrize("order", [1, 2])
+def test_zodiac_scene_reference_scale(zodiac, mode, order):
+    scene, g = zodiac
+    cam = camera(g)
+    rgba, depth, cnt = _render_zodiac(scene, cam, mode, order=order)
+    _check_composed_depth(depth, g["depth"], mode)
+    # hits and march samples over all 12 assets (RenderCounters of render_frame)
+    assert int(cnt[2]) == int(g["counters"][2]) and int(cnt[3]) == int(g["counters"][3])
+    err = float(np.abs(rgba.astype(np.float64) - g["rgba"]).max())
+    assert err <= TOL[mode], f"{mode}: max |rgba - reference| = {err}"
+
+
+@pytest.mark.parametrize("mode,order,slots", [("bf16", 1, 8), ("bf16", 2, 4), ("fp32", 1, 8)])
+def test_zodiac_encoded_frame_timed_variants(zodiac, mode, order, slots):
+    """The bench's timed path at 1 GPU: live chunks marched in spatial order
+    (heavy_first = 0) and composed by k_compose_live<8> into a prefilled
+    encode_frame buffer; every variant vs encode_frame of the reference frame."""
+    scene, g = zodiac
+    cam = camera(g)
+    r8, d16, cnt = _render_zodiac(scene, cam, mode, order=order, slots=slots, encode=True)
+    e8, e16 = O.encode_frame(g["rgba"], g["depth"])
+    _check_composed_depth(d16.astype(np.float64), e16.astype(np.float64), mode, miss=65535.0)
+    lsb = int(np.abs(r8.astype(np.int32) - e8.astype(np.int32)).max())
+    assert lsb <= (1 if mode == "fp32" else 3), f"rgba8 off by {lsb} LSB"
+    assert int(cnt[3]) == int(g["counters"][3])

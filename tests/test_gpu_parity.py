@@ -189,7 +189,7 @@ def test_any_grid_matches_oracle(b, r):
     """The march has an integer sub-voxel path for power-of-two b and r (the
     reference defaults) and the general fp64 path otherwise: both must match
     the oracle bit for bit on depth / counters (rgba to 1e-6)."""
-    from paper_2303_04086_b200 import synth
+    from tools import synth
     from paper_2303_04086_b200.model import orbit_camera
     a = synth.make_asset("sphere", 5, b=b, r=r, psh_resolution=16, diffuse_levels=3,
                          diffuse_table=2 ** 10, shell_cameras_n=12, shell_image_size=16,
@@ -294,7 +294,7 @@ _FULL = {}
 
 def _full_size(kind):
     """A reference-default asset (b=32, r=8, PSH N=64: power-of-two grid path)."""
-    from paper_2303_04086_b200 import synth
+    from tools import synth
     if kind not in _FULL:
         _FULL[kind] = synth.make_asset(kind, seed=7, shell_cameras_n=64, shell_image_size=32,
                                        diffuse_shell_cameras=16, diffuse_shell_image=16)

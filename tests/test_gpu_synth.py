@@ -5,7 +5,7 @@ import numpy as np
 import pytest
 
 from golden_util import asset, load
-from paper_2303_04086_b200 import synth
+from tools import synth
 
 pytestmark = pytest.mark.gpu
 SEEDS = {"sphere": 3, "box": 1, "two": 2}

@@ -11,7 +11,8 @@ import pytest
 
 from golden_util import asset
 from oracle import oracle as O
-from paper_2303_04086_b200 import nolf_io, synth
+from paper_2303_04086_b200 import nolf_io
+from tools import synth
 from paper_2303_04086_b200.model import RayRange, orbit_camera
 
 

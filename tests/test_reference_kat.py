@@ -22,7 +22,7 @@ import pytest
 from golden_util import asset as golden_asset
 from oracle import oracle as O
 from paper_2303_04086_b200.model import Frame, MarchParams, RenderCounters
-from paper_2303_04086_b200.synth import bake_density, march_only_asset
+from tools.synth import bake_density, march_only_asset
 
 gpu = pytest.mark.gpu
 

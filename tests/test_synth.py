@@ -6,7 +6,7 @@ import numpy as np
 import pytest
 
 from golden_util import asset, load
-from paper_2303_04086_b200 import synth
+from tools import synth
 
 SEEDS = {"sphere": 3, "box": 1, "two": 2}
 TOY = dict(b=16, r=4, psh_resolution=16, diffuse_levels=3, diffuse_table=2 ** 10)

@@ -20,8 +20,9 @@ rows and weights; diffuse cubes to fp32 MLP rounding):
   bake_diffuse_cubes          lightfield.py:547-576 + atlas.py:129-155
                               (diffuse network evaluated on the GPU)
 
-Asset production is offline work in the reference; here it only feeds the
-benchmark and the full-size parity tests.
+Asset production is offline work in the reference (out
+of scope); this module is bench / test support, not part of the product
+package.  It only feeds the benchmark and the full-size parity tests.
 """
 
 from __future__ import annotations
@@ -30,8 +31,8 @@ import math
 
 import numpy as np
 
-from . import errors
-from .model import (Camera, CubeAtlas, HashGridEncoder, LightFieldAsset, MarchParams, Mlp,
+from paper_2303_04086_b200 import errors
+from paper_2303_04086_b200.model import (Camera, CubeAtlas, HashGridEncoder, LightFieldAsset, MarchParams, Mlp,
                     ModelWiring, PshTable, look_at)
 
 # ------------------------------------------------------------------ densities
@@ -116,7 +117,7 @@ def shell_cameras(n_cameras=512, image_size=32, radius=2.0, fov_deg=60.0):
 
 def collect_hit_points_gpu(atlas: CubeAtlas, march: MarchParams, n_cameras=512, image_size=32):
     """Hit points of the sweep, marched by nolf_march_rays on the GPU."""
-    from . import render as R
+    from paper_2303_04086_b200 import render as R
 
     probe = march_only_asset(atlas, march)
     cams = shell_cameras(n_cameras, image_size)
@@ -341,8 +342,8 @@ def bake_diffuse_gpu(asset, mask: np.ndarray) -> CubeAtlas:
     """bake_diffuse_cubes with the diffuse network evaluated by nolf_eval_diffuse."""
     import torch
 
-    from . import _native as N
-    from . import render as R
+    from paper_2303_04086_b200 import _native as N
+    from paper_2303_04086_b200 import render as R
 
     b = asset.density_atlas.base_resolution
     r = asset.density_atlas.cube_resolution
