@@ -284,8 +284,9 @@ def verify_vs_oracle(R, N, cams, tiles, my_tiles, n_max, stride, W, H, n_views, 
     enc = {"rgba8": torch.zeros((NPX, 4), dtype=torch.uint8, device=dev),
            "depth16": torch.full((NPX,), -1, dtype=torch.int16, device=dev),
            "counters": torch.zeros(4, dtype=torch.int64, device=dev)}
+    from paper_2303_04086_b200 import render as RM
     R.render(cams, my_tiles, n_max, stride, enc, frame_layout=True, prefilled=True)
-    variant = R.last_launch()
+    variant = RM.last_launch()
     f32 = R.alloc(n_max, stride, want_f32=True, want_u8=False)
     R.render(cams, my_tiles, n_max, stride, f32, frame_layout=True)
     torch.cuda.synchronize()

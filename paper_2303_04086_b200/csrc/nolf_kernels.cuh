@@ -109,6 +109,8 @@ __device__ __forceinline__ unsigned chunk_at(const unsigned *list, const unsigne
   return 0u;
 }
 
+__device__ __forceinline__ double t_stop_of(const DevAsset &A) { return A.t_stop; }
+
 // Sample i's clipped position and index cell, exactly as march_rays computes
 // them (t_mid = t_near + (i+0.5)*step ; pos = clip(o + t_mid*d, 0, 1)).
 // CLIP = false when the caller proved every position it will ask for lies in
@@ -367,6 +369,134 @@ __device__ __forceinline__ MarchOut march_ray(const DevAsset &A, const double o[
   return r;
 }
 
+// ---------------------------------------------------------------- power-of-two grids
+// The reference defaults (b = 32, r = 8) make the sub-voxel grid G = b*r a
+// power of two, so the march runs in GRID UNITS: with oG = o*G and dG = d*G
+// (exact: scaling by a power of two), every sample position
+//   xg = clip(fl(oG + fl(t_mid * dG)), 0, G) == clip(fl(o + fl(t_mid * d)), 0, 1) * G
+// bit for bit (rounding commutes with power-of-two scaling; no sub-normals or
+// overflow at these magnitudes).  Then
+//   gi   = floor(xg)            = low word of fl_rd(xg + 2^52)   (0 <= xg < 2^52)
+//   cell = min(gi >> lr, b - 1) , base = gi - (cell << lr), frac = xg - floor(xg)
+// except at xg == G (pos == 1.0: cell b-1, base r-1, frac 1.0), which is
+// exactly atlas.py:162-172's floor / clip / subtract sequence without a single
+// fp64 <-> int conversion.  t_mid = t_near + (i + 0.5) * step with (i + 0.5)
+// carried as a double (exact for i < 2^52).
+__device__ __forceinline__ int floor_grid(double xg) {    // 0 <= xg < 2^52
+  return __double2loint(__dadd_rd(xg, 4503599627370496.0));
+}
+__device__ __forceinline__ double frac_grid(double xg) {  // xg - floor(xg), exact
+  return __dsub_rn(xg, __dsub_rn(__dadd_rd(xg, 4503599627370496.0), 4503599627370496.0));
+}
+
+template <bool CLIP>
+__device__ __forceinline__ double grid_pos(const double oG[3], const double dG[3], double t_mid, double G, int k) {
+  const double v = __dadd_rn(oG[k], __dmul_rn(t_mid, dG[k]));
+  return CLIP ? (v < 0.0 ? 0.0 : (v > G ? G : v)) : v;
+}
+
+template <bool CLIP>
+__device__ __forceinline__ MarchOut march_p2(const DevAsset &A, const double oG[3], const double dG[3],
+                                             const float invG[3], double t_near, double t_far, bool use_zmask,
+                                             int i_start, double t_end) {
+  MarchOut r;
+  r.alpha_c = 0.0;
+  r.t_hit = __longlong_as_double(0x7ff0000000000000ll);
+  r.samples = 0;
+  r.hit = false;
+  if (!(t_near < t_far)) return r;
+  const DevAtlas &at = A.den;
+  const double delta = A.step;
+  const int b = at.b, lr = at.lr, rr = at.r;
+  const int Gi = b << lr;
+  const double G = (double)Gi;
+  const double t_lim = fmin(t_far, t_end);
+  double best_w = 0.0, trans = 1.0, alpha_c = 0.0, t_hit = r.t_hit;
+  int samples = 0;
+  int i = i_start;
+  double ti = (double)i_start + 0.5;          // i + 0.5, exact
+  for (;;) {
+    const double t_mid = __dadd_rn(t_near, __dmul_rn(ti, delta));
+    if (!(t_mid < t_lim)) break;
+    double xg[3];
+    int gi[3], cell[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      xg[k] = grid_pos<CLIP>(oG, dG, t_mid, G, k);
+      gi[k] = floor_grid(xg[k]);
+      cell[k] = min(gi[k] >> lr, b - 1);
+    }
+    const int ci = (cell[0] * b + cell[1]) * b + cell[2];
+    const int dist = __ldg(at.dist + ci);
+    if (dist > 0) {            // every cell within Chebyshev radius dist-1 is empty: jump (verified)
+      int lo_c[3], hi_c[3];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        lo_c[k] = max(cell[k] - (dist - 1), 0);
+        hi_c[k] = min(cell[k] + (dist - 1), b - 1);
+      }
+      // fp32 estimate of the last sample before the empty box's exit
+      float te = __int_as_float(0x7f800000);
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        const float ok = (float)oG[k];
+        if (invG[k] > 0.f && hi_c[k] < b - 1) te = fminf(te, ((float)((hi_c[k] + 1) << lr) - ok) * invG[k]);
+        else if (invG[k] < 0.f && lo_c[k] > 0) te = fminf(te, ((float)(lo_c[k] << lr) - ok) * invG[k]);
+      }
+      const float jf = floorf((fminf(te, (float)t_lim) - (float)t_near) * A.inv_step_f - 0.5f);
+      int j = jf > 2.0e9f ? 2000000000 : (int)jf;
+      int next = i + 1;
+      for (int attempt = 0; attempt < 2 && j > i; ++attempt, --j) {
+        const double tj = __dadd_rn(t_near, __dmul_rn((double)j + 0.5, delta));
+        bool inside = tj < t_lim;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          const int cj = min(floor_grid(grid_pos<CLIP>(oG, dG, tj, G, k)) >> lr, b - 1);
+          inside = inside && cj >= lo_c[k] && cj <= hi_c[k];
+        }
+        if (inside) { next = j + 1; break; }
+      }
+      ti = next == i + 1 ? ti + 1.0 : (double)next + 0.5;
+      i = next;
+      continue;
+    }
+    const int cid = __ldg(at.index + ci);
+    int base[3];
+    double frac[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      base[k] = gi[k] - (cell[k] << lr);
+      frac[k] = frac_grid(xg[k]);
+      if (gi[k] >= Gi) { base[k] = rr - 1; frac[k] = 1.0; }   // pos == 1.0 (clipped to the far face)
+    }
+    ++samples;
+    const int bit = (((base[0] << lr) + base[1]) << lr) + base[2];
+    // the sub-voxel's 8 corners: one 32-byte sector (bricks); all-zero corners
+    // give sigma = +0 exactly (absorb 1, w 0): only the sample count changes
+    const float4 *bp = at.bricks + (((size_t)cid << (3 * lr)) + (size_t)bit) * 2;
+    const float4 qa = __ldg(bp), qb = __ldg(bp + 1);
+    const bool zero = qa.x == 0.f && qa.y == 0.f && qa.z == 0.f && qa.w == 0.f && qb.x == 0.f && qb.y == 0.f &&
+                      qb.z == 0.f && qb.w == 0.f;
+    if (!(use_zmask && zero)) {
+      const float s = trilinear8(qa, qb, frac);
+      const double sigma = (double)s;
+      const double absorb = exp(__dmul_rn(-sigma, delta));
+      const double w = __dmul_rn(trans, __dsub_rn(1.0, absorb));
+      if (w > best_w) { best_w = w; t_hit = t_mid; }
+      alpha_c = __dadd_rn(alpha_c, w);
+      trans = __dmul_rn(trans, absorb);
+      if (!(trans > t_stop_of(A))) break;
+    }
+    ++i;
+    ti += 1.0;
+  }
+  r.alpha_c = alpha_c;
+  r.samples = samples;
+  r.hit = alpha_c > A.alpha_floor;
+  r.t_hit = r.hit ? t_hit : __longlong_as_double(0x7ff0000000000000ll);
+  return r;
+}
+
 #ifndef NOLF_MARCH_MINB
 #define NOLF_MARCH_MINB 8  // latency-bound: 50% occupancy beats the spills it costs (measured 4..8)
 #endif
@@ -544,27 +674,48 @@ __device__ __forceinline__ bool prepare_march(const DevInst &I, const DevAsset &
   return boxhit;
 }
 
+// o, d: the object-space ray; power-of-two grids march in grid units, so
+// there o and d arrive already scaled by G (prepare_for_march) and invf is
+// 1/(d*G) -- see march_p2.
 __device__ __forceinline__ MarchOut run_march(const DevAsset &A, const double o[3], const double d[3],
                                               const float invf[3], const MarchSpan &sp, bool use_zmask) {
-  if (A.den.lr >= 0) {         // power-of-two grid: integer sub-voxel addressing
-    if (sp.noclip) return march_ray<false, true>(A, o, d, invf, sp.t_near, sp.t_far, use_zmask, sp.i_start, sp.t_end);
-    return march_ray<true, true>(A, o, d, invf, sp.t_near, sp.t_far, use_zmask, sp.i_start, sp.t_end);
+  if (A.den.lr >= 0) {
+    if (sp.noclip) return march_p2<false>(A, o, d, invf, sp.t_near, sp.t_far, use_zmask, sp.i_start, sp.t_end);
+    return march_p2<true>(A, o, d, invf, sp.t_near, sp.t_far, use_zmask, sp.i_start, sp.t_end);
   }
   if (sp.noclip) return march_ray<false, false>(A, o, d, invf, sp.t_near, sp.t_far, use_zmask, sp.i_start, sp.t_end);
   return march_ray<true, false>(A, o, d, invf, sp.t_near, sp.t_far, use_zmask, sp.i_start, sp.t_end);
 }
 
-// Hit record for the shading pass (lightfield.py:433-445).
-__device__ __forceinline__ HitRec hit_record(const DevAsset &A, const double o[3], const double d[3], double t_near,
-                                             const MarchOut &mr, uint32_t out_idx, uint32_t ordinal) {
+// Grid units for power-of-two atlases (exact scaling, see march_p2): o, d and
+// 1/d are multiplied / divided by G in place; returns the factor that maps
+// positions back to object space (1/G, or 1 for the general path).
+__device__ __forceinline__ double to_grid_units(const DevAsset &A, double o[3], double d[3], float invf[3]) {
+  if (A.den.lr < 0) return 1.0;
+  const double G = (double)(A.den.b << A.den.lr);
+  const float igf = 1.0f / (float)G;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    o[k] = __dmul_rn(o[k], G);
+    d[k] = __dmul_rn(d[k], G);
+    invf[k] *= igf;
+  }
+  return 1.0 / G;
+}
+
+// Hit record for the shading pass (lightfield.py:433-445).  o, d in units
+// scaled by 1/unit (to_grid_units): positions and the direction are mapped
+// back exactly (power-of-two factors).
+__device__ __forceinline__ HitRec hit_record(const DevAsset &A, const double o[3], const double d[3], double unit,
+                                             double t_near, const MarchOut &mr, uint32_t out_idx, uint32_t ordinal) {
   HitRec rec;
   double t_obj = mr.t_hit;
   if (!A.use_hit_point) t_obj = t_near;   // ablation: shade at the proxy entry (lightfield.py:438-445)
 #pragma unroll
-  for (int q = 0; q < 3; ++q) rec.p[q] = clamp01(__dadd_rn(o[q], __dmul_rn(t_obj, d[q])));
+  for (int q = 0; q < 3; ++q) rec.p[q] = clamp01(__dmul_rn(__dadd_rn(o[q], __dmul_rn(t_obj, d[q])), unit));
   rec.alpha_c = mr.alpha_c;
   rec.t_obj = t_obj;
-  rec.d[0] = d[0]; rec.d[1] = d[1]; rec.d[2] = d[2];
+  rec.d[0] = __dmul_rn(d[0], unit); rec.d[1] = __dmul_rn(d[1], unit); rec.d[2] = __dmul_rn(d[2], unit);
   rec.out_idx = out_idx;
   rec.ordinal = ordinal;
   return rec;
@@ -600,6 +751,7 @@ __device__ __forceinline__ void march_chunk(const MarchArgs &args, unsigned chun
     const DevAsset &A = *I.a;
     bool hit = false;
     double o[3], d[3], inv[3];
+    double unit = 1.0;
     MarchSpan sp{0.0, 0.0, 0.0, 0, false};
     MarchOut mr{0.0, __longlong_as_double(0x7ff0000000000000ll), 0, false};
     const bool live = (lane_mask >> k) & 1ull;
@@ -610,7 +762,8 @@ __device__ __forceinline__ void march_chunk(const MarchArgs &args, unsigned chun
       world_ray<MODE>(args, gid, cam, pix_x, pix_y, ow, dw);
       if (prepare_march(I, A, args.raw_rays, ow, dw, o, d, inv, sp, args.errors)) {
         NOLF_STAT(2, 1);
-        const float invf[3] = {(float)inv[0], (float)inv[1], (float)inv[2]};
+        float invf[3] = {(float)inv[0], (float)inv[1], (float)inv[2]};
+        unit = to_grid_units(A, o, d, invf);
         mr = run_march(A, o, d, invf, sp, args.use_zmask);
         samples_total += (unsigned)mr.samples;
         hit = mr.hit;
@@ -624,7 +777,7 @@ __device__ __forceinline__ void march_chunk(const MarchArgs &args, unsigned chun
         args.out_samples[gid] = mr.samples;
 #pragma unroll
         for (int q = 0; q < 3; ++q)
-          args.out_p_h[3 * gid + q] = hit ? clamp01(__dadd_rn(o[q], __dmul_rn(mr.t_hit, d[q]))) : 0.0;
+          args.out_p_h[3 * gid + q] = hit ? clamp01(__dmul_rn(__dadd_rn(o[q], __dmul_rn(mr.t_hit, d[q])), unit)) : 0.0;
       }
       continue;
     }
@@ -643,7 +796,7 @@ __device__ __forceinline__ void march_chunk(const MarchArgs &args, unsigned chun
       if (hit) {
         const unsigned pos = base + __popc(ballot & ((1u << lane) - 1u));
         if ((long long)pos < args.qoff[k + 1] - args.qoff[k]) {
-          args.queue[args.qoff[k] + pos] = hit_record(A, o, d, sp.t_near, mr, (uint32_t)gid, ordinal);
+          args.queue[args.qoff[k] + pos] = hit_record(A, o, d, unit, sp.t_near, mr, (uint32_t)gid, ordinal);
           ++ordinal;           // the layer exists only if its record does
         } else {
           atomicAdd(args.errors + kErrQueue, 1u);

@@ -59,11 +59,12 @@ def test_missing_camera_raises():
 
 
 def test_duplicated_tiles_overflow_the_hit_queue():
-    """Every tile listed 6 times: each pixel is marched 6 times, so the hit
-    records exceed the queue the host sized from the screen box."""
+    """Every tile listed 40 times: each pixel is marched 40 times, so the hit
+    records exceed the queue the host sized from the screen box (at most the
+    frame's 4096 pixels)."""
     a = asset("toy_sphere")
     cam = orbit_camera(0.8, 0.3, radius=1.2, size=64)
-    tiles = np.concatenate([R.frame_tiles(64, 64, 32)] * 6)
+    tiles = np.concatenate([R.frame_tiles(64, 64, 32)] * 40)
     r, _ = _render([(a, np.eye(4))], cam, tiles)
     with pytest.raises(errors.CapacityError, match="hit queue"):
         r.check()

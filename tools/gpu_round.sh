@@ -1,9 +1,9 @@
 # Round-end GPU check: gpu tests, smoke, bench lines for every BASELINE config + reference arm, ncu launch list and full capture.
-# usage: gpurun --timeout 3000 -- bash tools/gpu_round.sh   (outputs under gpurun_out/$P_*, P defaults to r02)
+# usage: gpurun --timeout 3000 -- bash tools/gpu_round.sh [prefix] [steps]   (outputs under gpurun_out/<prefix>_*)
 # STEPS selects parts: t (pytest) s (smoke) b (bench cfg4) a (all configs) r (reference arm) n (ncu)
 set -x
-P=${P:-r02}
-STEPS=${STEPS:-tsbarn}
+P=${1:-${P:-r02}}
+STEPS=${2:-${STEPS:-tsbarn}}
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
 case $STEPS in *t*) timeout 1500 python -m pytest tests -m gpu -x -q -rf --durations=15 > gpurun_out/${P}_pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/${P}_pytest_gpu.log;; esac
 case $STEPS in *s*) timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > gpurun_out/${P}_smoke.log 2>&1;; esac
