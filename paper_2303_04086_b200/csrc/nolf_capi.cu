@@ -158,26 +158,9 @@ int upload_atlas(NolfAsset *A, const NolfAtlasDesc &d, int channels, DevAtlas *o
   out->zwords = words;
   auto pow2 = [](int v) { return v > 0 && (v & (v - 1)) == 0; };
   out->lr = -1;
-  out->bricks = nullptr;
   if (pow2(b) && pow2(r) && (int64_t)b * r < (1 << 30)) {
     out->lr = 0;
     while ((1 << out->lr) < r) ++out->lr;
-    if (channels == 1) {       // density: sub-voxel corner bricks for the march
-      const size_t per = (size_t)r * r * r * 8;
-      std::vector<float> br((size_t)std::max<int64_t>(d.n_cubes, 1) * per, 0.f);
-      for (int64_t c = 0; c < d.n_cubes; ++c) {
-        const float *cube = d.cubes + (size_t)c * s * s * s;
-        float *dst = br.data() + (size_t)c * per;
-        for (int x = 0; x < r; ++x)
-          for (int y = 0; y < r; ++y)
-            for (int z = 0; z < r; ++z)
-              for (int q = 0; q < 8; ++q)
-                *dst++ = cube[((size_t)(x + (q & 1)) * s + (y + ((q >> 1) & 1))) * s + (z + ((q >> 2) & 1))];
-      }
-      float4 *bp;
-      if ((rc = A->upload(reinterpret_cast<const float4 *>(br.data()), br.size() / 4, &bp))) return rc;
-      out->bricks = bp;
-    }
   }
   return 0;
 }

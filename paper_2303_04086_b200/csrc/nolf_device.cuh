@@ -24,32 +24,8 @@ struct DevAtlas {              // CubeAtlas (atlas.py:25-51)
   const uint32_t *zmask;       // per cube, r^3 bits: sub-voxel whose 8 corners are all 0
   int zwords;                  // 32-bit words per cube
   int lr;                      // log2(r) when b and r are both powers of two, else -1
-  // power-of-two density atlases: the 8 trilinear corners of every sub-voxel
-  // stored contiguously (CORNERS order, one 32-byte sector per sample:
-  // float4 x 2 per sub-voxel, sub-voxel (x*r + y)*r + z of cube cid at
-  // (cid * r^3 + sub-voxel) * 2) -- 5.6x the cube bytes, 1 sector per march
-  // sample instead of 8 scattered corners (null: not built)
-  const float4 *bricks;
 };
 
-// query_atlas's trilinear sum (atlas.py:176-184) over one sub-voxel's 8
-// corners held in registers: w_c = (wx * wy) * wz in f64, acc += w_c * q_c in
-// corner order, cast to f32.
-__device__ __forceinline__ float trilinear8(const float4 qa, const float4 qb, const double frac[3]) {
-  const double g0 = __dsub_rn(1.0, frac[0]), g1 = __dsub_rn(1.0, frac[1]), g2 = __dsub_rn(1.0, frac[2]);
-  const double w00 = __dmul_rn(g0, g1), w10 = __dmul_rn(frac[0], g1);
-  const double w01 = __dmul_rn(g0, frac[1]), w11 = __dmul_rn(frac[0], frac[1]);
-  double acc = 0.0;
-  acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(w00, g2), (double)qa.x));
-  acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(w10, g2), (double)qa.y));
-  acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(w01, g2), (double)qa.z));
-  acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(w11, g2), (double)qa.w));
-  acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(w00, frac[2]), (double)qb.x));
-  acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(w10, frac[2]), (double)qb.y));
-  acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(w01, frac[2]), (double)qb.z));
-  acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(w11, frac[2]), (double)qb.w));
-  return (float)acc;
-}
 
 // Fully fused MLP parameter block (neural.py:29-108), fp32, padded:
 //   w0t [kInp][kHid]  (layer-0 weights TRANSPOSED: in-major)

@@ -418,6 +418,13 @@ __device__ __forceinline__ MarchOut march_p2(const DevAsset &A, const double oG[
   for (;;) {
     const double t_mid = __dadd_rn(t_near, __dmul_rn(ti, delta));
     if (!(t_mid < t_lim)) break;
+    NOLF_STAT(7, 1);
+#if defined(NOLF_STATS) && defined(NOLF_STATS_CTR)
+    {
+      const unsigned am = __activemask();
+      if ((threadIdx.x & 31) == (unsigned)(__ffs(am) - 1)) { NOLF_STAT(9, 1); NOLF_STAT(10, __popc(am)); }
+    }
+#endif
     double xg[3];
     int gi[3], cell[3];
 #pragma unroll
@@ -429,6 +436,7 @@ __device__ __forceinline__ MarchOut march_p2(const DevAsset &A, const double oG[
     const int ci = (cell[0] * b + cell[1]) * b + cell[2];
     const int dist = __ldg(at.dist + ci);
     if (dist > 0) {            // every cell within Chebyshev radius dist-1 is empty: jump (verified)
+      NOLF_STAT(3, 1);
       int lo_c[3], hi_c[3];
 #pragma unroll
       for (int k = 0; k < 3; ++k) {
@@ -471,14 +479,12 @@ __device__ __forceinline__ MarchOut march_p2(const DevAsset &A, const double oG[
     }
     ++samples;
     const int bit = (((base[0] << lr) + base[1]) << lr) + base[2];
-    // the sub-voxel's 8 corners: one 32-byte sector (bricks); all-zero corners
-    // give sigma = +0 exactly (absorb 1, w 0): only the sample count changes
-    const float4 *bp = at.bricks + (((size_t)cid << (3 * lr)) + (size_t)bit) * 2;
-    const float4 qa = __ldg(bp), qb = __ldg(bp + 1);
-    const bool zero = qa.x == 0.f && qa.y == 0.f && qa.z == 0.f && qa.w == 0.f && qb.x == 0.f && qb.y == 0.f &&
-                      qb.z == 0.f && qb.w == 0.f;
-    if (!(use_zmask && zero)) {
-      const float s = trilinear8(qa, qb, frac);
+    // sub-voxel whose 8 corner densities are all 0: sigma = +0 exactly, so
+    // absorb = exp(-0) = 1, w = 0 -- only the active-sample count changes
+    if (!(use_zmask && ((__ldg(at.zmask + (unsigned)(cid * at.zwords + (bit >> 5))) >> (bit & 31)) & 1u))) {
+      NOLF_STAT(6, 1);
+      float s;
+      atlas_trilinear_at<1>(at, cid, base, frac, &s);
       const double sigma = (double)s;
       const double absorb = exp(__dmul_rn(-sigma, delta));
       const double w = __dmul_rn(trans, __dsub_rn(1.0, absorb));

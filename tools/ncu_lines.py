@@ -1,21 +1,26 @@
-"""Top source lines of one kernel in an ncu capture (needs -lineinfo)."""
-import csv, subprocess, sys, io
-rep, kern = sys.argv[1], sys.argv[2]
-n = int(sys.argv[3]) if len(sys.argv) > 3 else 40
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "-k", f"regex:{kern}", "--print-source", "cuda,sass"],
-                     capture_output=True, text=True).stdout
-rows = list(csv.reader(io.StringIO(out)))
-cur = None; data = {}
+"""Per-source-line totals of an ncu capture (needs -lineinfo builds):
+instructions executed and warp-stall samples, hottest first.
+
+usage: ncu -i rep.ncu-rep -k regex:KERNEL --page source --csv --print-source cuda,sass > x.csv
+       python tools/ncu_lines.py x.csv [N]
+"""
+import csv
+import sys
+
+rows = list(csv.reader(open(sys.argv[1])))
+n = int(sys.argv[2]) if len(sys.argv) > 2 else 50
+items, fname = [], "?"
 for r in rows:
-    if len(r) >= 2 and r[0] == "File Path": cur = r[1].split("/")[-1]; continue
-    if len(r) > 8 and r[0] not in ("", "Line No"):
+    if len(r) >= 2 and r[0] == "File Path":
+        fname = r[1].split("/")[-1]
+        continue
+    if len(r) > 8 and r[0].isdigit():
         try:
-            key = (cur, r[0])
-            a = data.setdefault(key, [0, 0, r[1][:100]])
-            a[0] += int(r[6] or 0); a[1] += int(r[7] or 0)
+            items.append((int(r[7] or 0), int(r[4] or 0), fname, int(r[0]), r[1].strip()[:90]))
         except ValueError:
             pass
-tot = sum(v[0] for v in data.values()) or 1; toti = sum(v[1] for v in data.values()) or 1
-print("samples", tot, "warp-instr", toti)
-for (f, l), (s, i, src) in sorted(data.items(), key=lambda kv: -kv[1][0])[:n]:
-    print(f"{s/tot*100:5.1f}% {i/toti*100:5.1f}%i {f[:14]}:{l:>4} {src}")
+te = sum(i[0] for i in items) or 1
+ts = sum(i[1] for i in items) or 1
+print(f"total warp instructions {te}, stall samples {ts}")
+for e, s, f, ln, src in sorted(items, key=lambda x: -x[1])[:n]:
+    print(f"{100 * e / te:5.1f}% inst {100 * s / ts:5.1f}% stall  {f}:{ln:<5} {src}")
