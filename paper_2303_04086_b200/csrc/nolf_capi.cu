@@ -348,7 +348,8 @@ int ensure_attrs() {
   if (!done) {
     CUDA_TRY(cudaFuncSetAttribute(k_shade, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kShadeSmem));
     CUDA_TRY(cudaFuncSetAttribute(k_eval_diffuse, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kShadeSmem));
-    CUDA_TRY(cudaFuncSetAttribute(k_shade_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTcSmem));
+    CUDA_TRY(cudaFuncSetAttribute(k_shade_tc<kShadeTG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)tc_smem_bytes(kShadeTG, kTcPhiMax)));
     CUDA_TRY(cudaFuncSetAttribute(k_mlp_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTcSmem));
     CUDA_TRY(cudaFuncSetAttribute(k_mlp_fp32, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kShadeSmem));
     done = true;
@@ -906,24 +907,23 @@ int run_shade(const DevInst *inst, const long long *qoff, int n_inst, const Work
     // dynamic smem sized to the largest Phi the launch stages (not the 64 KB
     // worst case) so more CTAs fit per SM
     sa.tile_order = 1;               // blocked tile ranges per CTA
-    const size_t smem = kTcSmem - kTcPhiMax + phi_smem_bytes;
-    // resident CTAs per SM from registers and shared memory (TMEM: 64 columns
-    // each, never the limit below 8)
+    const size_t smem = tc_smem_bytes(kShadeTG, phi_smem_bytes);
+    // resident CTAs per SM from registers and shared memory (TMEM: 64
+    // columns per tile group, never the limit here)
     static int regs = 0;
     static size_t static_smem = 0;
     if (!regs) {
       cudaFuncAttributes fa{};
-      CUDA_TRY(cudaFuncGetAttributes(&fa, k_shade_tc));
+      CUDA_TRY(cudaFuncGetAttributes(&fa, k_shade_tc<kShadeTG>));
       regs = fa.numRegs > 0 ? fa.numRegs : 168;
       static_smem = fa.sharedSizeBytes;
     }
-    const int by_regs = 65536 / (((regs + 7) / 8 * 8) * kTcThreads);
+    const int threads = 128 * kShadeTG;
+    const int by_regs = 65536 / (((regs + 7) / 8 * 8) * threads);
     const int by_smem = (int)((227u * 1024u) / (smem + static_smem + 1024u));
-#ifndef NOLF_SHADE_CAP
-#define NOLF_SHADE_CAP 4
-#endif
-    int per_sm = std::max(1, std::min(std::min(by_regs, by_smem), NOLF_SHADE_CAP));
-    k_shade_tc<<<num_sms() * std::max(per_sm, 1), kTcThreads, smem, st>>>(sa);
+    const int by_tmem = 512 / (64 * kShadeTG);
+    const int per_sm = std::max(1, std::min(std::min(by_regs, by_smem), by_tmem));
+    k_shade_tc<kShadeTG><<<num_sms() * per_sm, threads, smem, st>>>(sa);
   } else {
     k_shade<<<num_sms() * 3, kShadeThreads, kShadeSmem, st>>>(sa);
   }

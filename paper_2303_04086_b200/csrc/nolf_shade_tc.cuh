@@ -37,17 +37,19 @@ constexpr uint32_t kTcTabMax = 776;          // residue tables 6*(N+1) for N <= 
 constexpr uint32_t kTcSmem = 1024 + kTcA + kTcWBytes + kTcF32 * 4 + kTcTabMax * 4 + 64 + kTcPhiMax;
 
 // Two layers on tcgen05 for the 128 rows already written to A (layer-0 input,
-// bf16, K-major); returns this thread's 4 pre-head outputs (fp32).
+// bf16, K-major) by one 128-thread tile group (named barrier `bar_id`,
+// group thread gt, TMEM columns [tmem, tmem+64)); returns this thread's 4
+// pre-head outputs (fp32).  TMEM is read back 16 columns at a time so the
+// hidden layer never occupies more than 16 registers.
 __device__ __forceinline__ void tc_mlp_rows(uint8_t *A, const uint8_t *W, const float *fp, uint32_t tmem,
-                                            uint64_t *bar, uint32_t &phase, int tid, float out4[4]) {
+                                            uint64_t *bar, uint32_t &phase, int gt, int bar_id, float out4[4]) {
   const uint32_t aA = tc::smem_u32(A), aW0 = tc::smem_u32(W), aW1 = aW0 + kTcW0;
   constexpr uint32_t idesc = tc::idesc_bf16_f32(128, 64);
-  const int warp = tid >> 5;
-  const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
+  const uint32_t trow = tmem + ((uint32_t)((gt >> 5) * 32) << 16);   // this warp's TMEM lane quadrant
   // ---- layer 0: D = X[128x32] * W0[64x32]^T
   tc::fence_async_smem();
-  __syncthreads();
-  if (tid == 0) {
+  tc::bar_sync(bar_id, 128);
+  if (gt == 0) {
     tc::tc_fence_after();
 #pragma unroll
     for (int s = 0; s < kTcK0 / 16; ++s)
@@ -58,33 +60,36 @@ __device__ __forceinline__ void tc_mlp_rows(uint8_t *A, const uint8_t *W, const 
   tc::mbar_wait(bar, phase);
   phase ^= 1;
   tc::tc_fence_after();
-  float h[64];
-  tc::tmem_ld32(trow + 0, h);
-  tc::tmem_ld32(trow + 32, h + 32);
-  // bias + ReLU, re-quantise as the layer-1 A operand (K=64)
-  const uint32_t rowa = aA + (tid >> 3) * 128 + (tid & 7) * 16, fpa = tc::smem_u32(fp);
+  // bias + ReLU, re-quantised as the layer-1 A operand (K=64), 16 columns at a time
+  const uint32_t rowa = aA + (gt >> 3) * 128 + (gt & 7) * 16, fpa = tc::smem_u32(fp);
 #pragma unroll
-  for (int c = 0; c < 8; ++c) {
-    float v[8];
-    const float4 bA = tc::lds128(fpa + 32 * c), bB = tc::lds128(fpa + 32 * c + 16);
-    const float bb[8] = {bA.x, bA.y, bA.z, bA.w, bB.x, bB.y, bB.z, bB.w};
+  for (int c4 = 0; c4 < 4; ++c4) {
+    uint32_t r[16];
+    tc::tmem_ld16(trow + 16 * c4, r);
 #pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      const float z = h[8 * c + e] + bb[e];
-      v[e] = z > 0.f ? z : 0.f;
+    for (int hcol = 0; hcol < 2; ++hcol) {
+      const int c = 2 * c4 + hcol;
+      const float4 bA = tc::lds128(fpa + 32 * c), bB = tc::lds128(fpa + 32 * c + 16);
+      const float bb[8] = {bA.x, bA.y, bA.z, bA.w, bB.x, bB.y, bB.z, bB.w};
+      float v[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const float z = __uint_as_float(r[8 * hcol + e]) + bb[e];
+        v[e] = z > 0.f ? z : 0.f;
+      }
+      uint4 q;
+      q.x = tc::pack_bf16(v[0], v[1]);
+      q.y = tc::pack_bf16(v[2], v[3]);
+      q.z = tc::pack_bf16(v[4], v[5]);
+      q.w = tc::pack_bf16(v[6], v[7]);
+      tc::sts128(rowa + c * 2048, q);
     }
-    uint4 q;
-    q.x = tc::pack_bf16(v[0], v[1]);
-    q.y = tc::pack_bf16(v[2], v[3]);
-    q.z = tc::pack_bf16(v[4], v[5]);
-    q.w = tc::pack_bf16(v[6], v[7]);
-    tc::sts128(rowa + c * 2048, q);
   }
   tc::tc_fence_before();
   tc::fence_async_smem();
-  __syncthreads();
+  tc::bar_sync(bar_id, 128);
   // ---- layer 1: D = H1[128x64] * W1[64x64]^T (reuses the TMEM columns)
-  if (tid == 0) {
+  if (gt == 0) {
     tc::tc_fence_after();
 #pragma unroll
     for (int s = 0; s < 4; ++s)
@@ -95,29 +100,33 @@ __device__ __forceinline__ void tc_mlp_rows(uint8_t *A, const uint8_t *W, const 
   tc::mbar_wait(bar, phase);
   phase ^= 1;
   tc::tc_fence_after();
-  tc::tmem_ld32(trow + 0, h);
-  tc::tmem_ld32(trow + 32, h + 32);
-  tc::tc_fence_before();
   // ---- layer 2 (fp32, CUDA cores): 64 -> 4, sequential in the hidden index;
   // W2 is staged hidden-major ([o][4]) so one 16 B load feeds the 4 outputs
   // b1 at fp + 64, W2 at fp + 128, b2 at fp + 384 (floats)
   float acc[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-  for (int o4 = 0; o4 < 16; ++o4) {
-    const float4 bv = tc::lds128(fpa + 256 + 16 * o4);
-    const float bb[4] = {bv.x, bv.y, bv.z, bv.w};
+  for (int c4 = 0; c4 < 4; ++c4) {
+    uint32_t r[16];
+    tc::tmem_ld16(trow + 16 * c4, r);
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const int o = 4 * o4 + e;
-      float z = h[o] + bb[e];
-      z = z > 0.f ? z : 0.f;
-      const float4 wv = tc::lds128(fpa + 512 + 16 * o);
-      acc[0] = fmaf(z, wv.x, acc[0]);
-      acc[1] = fmaf(z, wv.y, acc[1]);
-      acc[2] = fmaf(z, wv.z, acc[2]);
-      acc[3] = fmaf(z, wv.w, acc[3]);
+    for (int q4 = 0; q4 < 4; ++q4) {
+      const int o4 = 4 * c4 + q4;
+      const float4 bv = tc::lds128(fpa + 256 + 16 * o4);
+      const float bb[4] = {bv.x, bv.y, bv.z, bv.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int o = 4 * o4 + e;
+        float z = __uint_as_float(r[4 * q4 + e]) + bb[e];
+        z = z > 0.f ? z : 0.f;
+        const float4 wv = tc::lds128(fpa + 512 + 16 * o);
+        acc[0] = fmaf(z, wv.x, acc[0]);
+        acc[1] = fmaf(z, wv.y, acc[1]);
+        acc[2] = fmaf(z, wv.z, acc[2]);
+        acc[3] = fmaf(z, wv.w, acc[3]);
+      }
     }
   }
+  tc::tc_fence_before();
   const float4 b2 = tc::lds128(fpa + 1536);
   out4[0] = acc[0] + b2.x;
   out4[1] = acc[1] + b2.y;
@@ -126,8 +135,8 @@ __device__ __forceinline__ void tc_mlp_rows(uint8_t *A, const uint8_t *W, const 
 }
 
 // Write one bf16 input row (n values of x, zero padded to kTcK0) to A.
-__device__ __forceinline__ void tc_write_x(uint8_t *A, int tid, const float *x, int n) {
-  const uint32_t rowa = tc::smem_u32(A) + (tid >> 3) * 128 + (tid & 7) * 16;
+__device__ __forceinline__ void tc_write_x(uint8_t *A, int gt, const float *x, int n) {
+  const uint32_t rowa = tc::smem_u32(A) + (gt >> 3) * 128 + (gt & 7) * 16;
 #pragma unroll
   for (int c = 0; c < kTcK0 / 8; ++c) {
     float v[8];
@@ -143,23 +152,28 @@ __device__ __forceinline__ void tc_write_x(uint8_t *A, int tid, const float *x, 
 }
 
 struct TcSmemPtrs {
-  uint8_t *A, *W;
+  uint8_t *A, *W;              // A: the tile groups' operand tiles, kTcA bytes each
   float *fp;
   uint32_t *tab;
-  uint64_t *bar_mma, *bar_tma;
+  uint64_t *bar_mma, *bar_tma; // bar_mma: one per tile group
   uint32_t *tmem_slot;
   uint8_t *phi;
 };
 
-__device__ __forceinline__ TcSmemPtrs tc_carve(uint8_t *raw) {
+// Shared-memory carve-up for `groups` 128-thread tile groups (1 KB aligned).
+__host__ __device__ constexpr uint32_t tc_smem_bytes(int groups, uint32_t phi_bytes) {
+  return 1024 + groups * kTcA + kTcWBytes + kTcF32 * 4 + kTcTabMax * 4 + 64 + phi_bytes;
+}
+
+__device__ __forceinline__ TcSmemPtrs tc_carve(uint8_t *raw, int groups = 1) {
   uint8_t *base = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
   TcSmemPtrs p;
   p.A = base;
-  p.W = p.A + kTcA;
+  p.W = p.A + groups * kTcA;
   p.fp = reinterpret_cast<float *>(p.W + kTcWBytes);
   p.tab = reinterpret_cast<uint32_t *>(p.fp + kTcF32);
   p.bar_mma = reinterpret_cast<uint64_t *>(p.tab + kTcTabMax);
-  p.bar_tma = p.bar_mma + 1;
+  p.bar_tma = p.bar_mma + groups;
   p.tmem_slot = reinterpret_cast<uint32_t *>(p.bar_tma + 1);
   p.phi = reinterpret_cast<uint8_t *>(p.bar_mma) + 64;
   return p;
@@ -280,105 +294,27 @@ __device__ __forceinline__ void tc_gather_inputs(const DevAsset &A, const TcSmem
   if (A.refine_opacity) x[F + 16] = (float)clampd(rec.alpha_c, 1e-4, 1.0 - 1e-4);
 }
 
-#ifdef NOLF_SHADE_MINB
-__global__ void __launch_bounds__(kTcThreads, NOLF_SHADE_MINB) k_shade_tc(ShadeArgs args) {
-#else
-__global__ void __launch_bounds__(kTcThreads) k_shade_tc(ShadeArgs args) {
-#endif
-  extern __shared__ uint8_t smem_raw[];
-  const TcSmemPtrs S = tc_carve(smem_raw);
-  const int tid = threadIdx.x, warp = tid >> 5;
-  if (warp == 0) tc::tmem_alloc<64>(S.tmem_slot);
-  __shared__ DevAsset s_asset;
-  __shared__ double s_scale;
-  if (tid == 0) {
-    tc::mbar_init(S.bar_mma, 1);
-    tc::mbar_init(S.bar_tma, 1);
-    tc::mbar_fence_init();
-  }
-  tc::tc_fence_before();
-  __syncthreads();
-  tc::tc_fence_after();
-  const uint32_t tmem = *S.tmem_slot;
-  uint32_t mma_phase = 0, tma_phase = 0;
-  int cur = -1;
-  bool phi_smem = false, tab_smem = false;
-  unsigned long long n_fs = 0;
-  // tile order: blocked ranges per CTA (args.tile_order == 1) or round-robin
-  long long total_tiles = 0;
-  for (int q = 0; q < args.n_inst; ++q)
-    total_tiles += (min((long long)args.counts[q], args.qoff[q + 1] - args.qoff[q]) + kTcThreads - 1) / kTcThreads;
-  const bool blocked = args.tile_order == 1;
-  const long long tile_lo = blocked ? total_tiles * blockIdx.x / gridDim.x : blockIdx.x;
-  const long long tile_hi = blocked ? total_tiles * (blockIdx.x + 1) / gridDim.x : total_tiles;
-  const long long tile_step = blocked ? 1 : gridDim.x;
-  // (instance, tile-in-instance) of tile_lo, found once; blocked ranges then
-  // advance incrementally instead of rescanning the per-instance counts
-  int k_run = 0;
-  long long t_run = tile_lo;
-  unsigned cnt_run = 0;
-  long long nt_run = 0;
-  for (; k_run < args.n_inst; ++k_run) {
-    cnt_run = min((long long)args.counts[k_run], args.qoff[k_run + 1] - args.qoff[k_run]);
-    nt_run = (cnt_run + kTcThreads - 1) / kTcThreads;
-    if (t_run < nt_run) break;
-    t_run -= nt_run;
-  }
-  for (long long tile = tile_lo; tile < tile_hi; tile += tile_step) {
-    int k = 0;
-    long long t = tile;
-    unsigned cnt = 0;
-    if (blocked) {
-      while (k_run < args.n_inst && t_run >= nt_run) {     // next non-empty instance
-        t_run -= nt_run;
-        if (++k_run < args.n_inst) {
-          cnt_run = min((long long)args.counts[k_run], args.qoff[k_run + 1] - args.qoff[k_run]);
-          nt_run = (cnt_run + kTcThreads - 1) / kTcThreads;
-        }
-      }
-      k = k_run;
-      t = t_run++;
-      cnt = cnt_run;
-    } else {
-      for (; k < args.n_inst; ++k) {
-        cnt = min((long long)args.counts[k], args.qoff[k + 1] - args.qoff[k]);
-        const long long nt = (cnt + kTcThreads - 1) / kTcThreads;
-        if (t < nt) break;
-        t -= nt;
-      }
-    }
-    if (k >= args.n_inst) break;
-    // the instance's asset record, copied to shared memory once per instance:
-    // the tile loop's field reads are then shared-memory loads, not generic
-    // loads that miss a gather-thrashed L1
-    const DevAsset &A = s_asset;
-    if (k != cur) {
-      __syncthreads();
-      const uint32_t *src = reinterpret_cast<const uint32_t *>(args.inst[k].a);
-      uint32_t *dst = reinterpret_cast<uint32_t *>(&s_asset);
-      for (int q = tid; q < (int)(sizeof(DevAsset) / 4); q += kTcThreads) dst[q] = __ldg(src + q);
-      if (tid == 0) s_scale = args.inst[k].scale;
-      __syncthreads();
-      tc_stage_asset(A, S, tma_phase, tid, phi_smem);
-      tab_smem = 6 * (A.N + 1) <= (int)kTcTabMax;
-      __syncthreads();
-      cur = k;
-    }
-    const long long r = t * kTcThreads + tid;
-    const bool valid = r < cnt;
+// Shading of one 128-hit tile by one tile group (group thread gt owns row
+// gt): gather -> bf16 operand tile -> two tcgen05 layers -> fp32 layer 2,
+// heads and the combine (lightfield.py:267-336, 446-455).  Only the values
+// the epilogue needs stay in registers across the MMA chain.
+template <int TG>
+__device__ __forceinline__ void tc_shade_tile(const ShadeArgs &args, const DevAsset &A, const TcSmemPtrs &S,
+                                              uint8_t *Ag, uint32_t tmem_g, uint64_t *bar_g, uint32_t &mma_phase,
+                                              int gt, int bar_id, bool tab_smem, bool phi_smem, double scale,
+                                              const HitRec *recs, long long r, unsigned cnt,
+                                              unsigned long long &n_fs) {
+  const bool valid = r < cnt;
+  float cd0 = 0.f, cd1 = 0.f, cd2 = 0.f, tint = 1.f, aterm = 0.f, dep = 0.f;
+  long long orow = 0;
+  {
     float x[kTcK0];
 #pragma unroll
     for (int q = 0; q < kTcK0; ++q) x[q] = 0.f;
-    double cd[3] = {0.0, 0.0, 0.0}, tint = 1.0, alpha_c = 0.0, t_obj = 0.0;
-    uint32_t out_idx = 0, ordinal = 0;
     if (valid) {
-      const HitRec rec = args.queue[args.qoff[k] + r];
-      alpha_c = rec.alpha_c;
-      t_obj = rec.t_obj;
-      out_idx = rec.out_idx;
-      ordinal = rec.ordinal;
-      const long long orow = args.mode == kModeScene ? (long long)ordinal * args.layer_stride + out_idx
-                                                     : (long long)out_idx;
+      const HitRec rec = recs[r];
+      orow = args.mode == kModeScene ? (long long)rec.ordinal * args.layer_stride + rec.out_idx
+                                     : (long long)rec.out_idx;
       uint32_t *dbg = (args.dbg_slots && orow < args.dbg_rows) ? args.dbg_slots + 8 * orow : nullptr;
       const bool want_dif = A.use_diffuse_color && A.has_dif;
       const int dif_cid = want_dif ? atlas_cell_id(A.dif, rec.p) : -1;   // overlaps the PSH gather
@@ -393,43 +329,114 @@ __global__ void __launch_bounds__(kTcThreads) k_shade_tc(ShadeArgs args) {
       if (want_dif) {
         float dv[4];
         atlas_query4_f(A.dif, dif_cid, rec.p, dv);
-        cd[0] = dv[0]; cd[1] = dv[1]; cd[2] = dv[2];
+        cd0 = dv[0]; cd1 = dv[1]; cd2 = dv[2];
         tint = dv[3];
       }
-      if (!A.use_tint) tint = 0.5;
+      if (!A.use_tint) tint = 0.5f;
+      // opacity input of the combine (lightfield.py:305-310), fp32 (bf16 path budget)
+      if (!A.use_opacity) {
+        aterm = (float)clampd(rec.alpha_c, 0.0, 1.0);
+      } else if (A.refine_opacity) {
+        const float ac = (float)clampd(rec.alpha_c, 1e-4, 1.0 - 1e-4);
+        aterm = logf(ac / (1.0f - ac));
+      }
+      dep = (float)__ddiv_rn(rec.t_obj, scale);
       ++n_fs;
     }
-    tc_write_x(S.A, tid, x, kTcK0);   // unused inputs are 0 (W0 is zero-padded too)
-    float z4[4];
-    tc_mlp_rows(S.A, S.W, S.fp, tmem, S.bar_mma, mma_phase, tid, z4);
-    if (valid) {
-      float fs_out[4];
+    tc_write_x(Ag, gt, x, kTcK0);   // unused inputs are 0 (W0 is zero-padded too)
+  }
+  float z4[4];
+  tc_mlp_rows(Ag, S.W, S.fp, tmem_g, bar_g, mma_phase, gt, bar_id, z4);
+  if (valid) {
+    float fs_out[4];
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
-        fs_out[j] = A.fs.act[j] == 0 ? z4[j] : (A.fs.act[j] == 1 ? sigmoidf_np(z4[j]) : expf(z4[j]));
-      // opacity / combine (lightfield.py:291-336) in fp32: the bf16 path's budget
-      const float ac = (float)clampd(alpha_c, 1e-4, 1.0 - 1e-4);
-      const float z = fs_out[3];
-      float alpha;
-      if (!A.use_opacity) alpha = (float)clampd(alpha_c, 0.0, 1.0);
-      else if (A.refine_opacity) alpha = sigmoidf_np(z + logf(ac / (1.0f - ac)));
-      else alpha = sigmoidf_np(z);
-      const float tf = (float)tint;
-      float4 o;
-      o.x = fminf(fmaxf(fmaf(tf, fs_out[0], (float)cd[0]), 0.f), 1.f);
-      o.y = fminf(fmaxf(fmaf(tf, fs_out[1], (float)cd[1]), 0.f), 1.f);
-      o.z = fminf(fmaxf(fmaf(tf, fs_out[2], (float)cd[2]), 0.f), 1.f);
-      o.w = alpha;
-      float dep = (float)__ddiv_rn(t_obj, s_scale);
-      if (o.w <= 0.f) {
-        o = make_float4(0.f, 0.f, 0.f, 0.f);
-        dep = __int_as_float(0x7f800000);
-      }
-      const long long q = args.mode == kModeScene ? (long long)ordinal * args.layer_stride + out_idx
-                                                  : (long long)out_idx;
-      reinterpret_cast<float4 *>(args.rgba)[q] = o;
-      args.depth[q] = dep;
+    for (int j = 0; j < 4; ++j)
+      fs_out[j] = A.fs.act[j] == 0 ? z4[j] : (A.fs.act[j] == 1 ? sigmoidf_np(z4[j]) : expf(z4[j]));
+    float alpha;
+    if (!A.use_opacity) alpha = aterm;
+    else if (A.refine_opacity) alpha = sigmoidf_np(fs_out[3] + aterm);
+    else alpha = sigmoidf_np(fs_out[3]);
+    float4 o;
+    o.x = fminf(fmaxf(fmaf(tint, fs_out[0], cd0), 0.f), 1.f);
+    o.y = fminf(fmaxf(fmaf(tint, fs_out[1], cd1), 0.f), 1.f);
+    o.z = fminf(fmaxf(fmaf(tint, fs_out[2], cd2), 0.f), 1.f);
+    o.w = alpha;
+    if (o.w <= 0.f) {            // lightfield.py:453-455
+      o = make_float4(0.f, 0.f, 0.f, 0.f);
+      dep = __int_as_float(0x7f800000);
     }
+    reinterpret_cast<float4 *>(args.rgba)[orow] = o;
+    args.depth[orow] = dep;
+  }
+}
+
+// bf16 tcgen05 shading: TG tile groups of 128 threads per CTA, each with its
+// own operand tile, TMEM columns and MMA barrier, sharing one staged copy of
+// the asset's tables (TMA) -- while one group waits on its gathers the
+// other's MMA chain and epilogue run, and the staged tables cost shared
+// memory once per CTA.  Tiles (128 hit records of one instance) are dealt
+// to the CTAs in blocked ranges; inside an instance the groups take
+// alternate tiles.
+#ifndef NOLF_SHADE_TG
+#define NOLF_SHADE_TG 1
+#endif
+constexpr int kShadeTG = NOLF_SHADE_TG;
+
+template <int TG>
+__global__ void __launch_bounds__(128 * TG, TG == 1 ? 4 : (TG == 2 ? 3 : 2)) k_shade_tc(ShadeArgs args) {
+  extern __shared__ uint8_t smem_raw[];
+  const TcSmemPtrs S = tc_carve(smem_raw, TG);
+  const int tid = threadIdx.x, warp = tid >> 5, g = tid >> 7, gt = tid & 127;
+  if (warp == 0) tc::tmem_alloc<64 * TG>(S.tmem_slot);
+  __shared__ DevAsset s_asset;
+  __shared__ double s_scale;
+  if (tid == 0) {
+#pragma unroll
+    for (int q = 0; q < TG; ++q) tc::mbar_init(S.bar_mma + q, 1);
+    tc::mbar_init(S.bar_tma, 1);
+    tc::mbar_fence_init();
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem_g = *S.tmem_slot + 64u * (uint32_t)g;
+  uint8_t *Ag = S.A + g * kTcA;
+  uint32_t mma_phase = 0, tma_phase = 0;
+  bool phi_smem = false, tab_smem = false;
+  unsigned long long n_fs = 0;
+  long long total_tiles = 0;
+  for (int q = 0; q < args.n_inst; ++q)
+    total_tiles += (min((long long)args.counts[q], args.qoff[q + 1] - args.qoff[q]) + 127) / 128;
+  const long long tile_lo = total_tiles * blockIdx.x / gridDim.x;
+  const long long tile_hi = total_tiles * (blockIdx.x + 1) / gridDim.x;
+  // walk the instances overlapping [tile_lo, tile_hi)
+  long long t_skip = tile_lo, left = tile_hi - tile_lo;
+  for (int k = 0; k < args.n_inst && left > 0; ++k) {
+    const unsigned cnt = (unsigned)min((long long)args.counts[k], args.qoff[k + 1] - args.qoff[k]);
+    const long long nt = (cnt + 127) / 128;
+    if (t_skip >= nt) { t_skip -= nt; continue; }
+    const long long first = t_skip, n_here = min(nt - first, left);
+    t_skip = 0;
+    left -= n_here;
+    // the instance's asset record and tables, once per CTA (record as shared
+    // memory: the tile loop's field reads never miss a gather-thrashed L1)
+    __syncthreads();
+    {
+      const uint32_t *src = reinterpret_cast<const uint32_t *>(args.inst[k].a);
+      uint32_t *dst = reinterpret_cast<uint32_t *>(&s_asset);
+      for (int q = tid; q < (int)(sizeof(DevAsset) / 4); q += 128 * TG) dst[q] = __ldg(src + q);
+      if (tid == 0) s_scale = args.inst[k].scale;
+    }
+    __syncthreads();
+    const DevAsset &A = s_asset;
+    tc_stage_asset(A, S, tma_phase, tid, phi_smem);
+    tab_smem = 6 * (A.N + 1) <= (int)kTcTabMax;
+    __syncthreads();
+    const HitRec *recs = args.queue + args.qoff[k];
+    const double scale = s_scale;
+    for (long long q = g; q < n_here; q += TG)
+      tc_shade_tile<TG>(args, A, S, Ag, tmem_g, S.bar_mma + g, mma_phase, gt, 1 + g, tab_smem, phi_smem, scale,
+                        recs, (first + q) * 128 + gt, cnt, n_fs);
   }
   const unsigned lane = tid & 31;
 #pragma unroll
@@ -440,7 +447,7 @@ __global__ void __launch_bounds__(kTcThreads) k_shade_tc(ShadeArgs args) {
   }
   tc::tc_fence_before();
   __syncthreads();
-  if (warp == 0) tc::tmem_free<64>(tmem);
+  if (warp == 0) tc::tmem_free<64 * TG>(*S.tmem_slot);
 }
 
 // The specular MLP alone on n input rows (numerics tests): X (n, in) f32 ->
@@ -472,7 +479,7 @@ __global__ void __launch_bounds__(kTcThreads) k_mlp_tc(const DevAsset *Ap, const
     for (int i = 0; i < in; ++i) x[i] = r < n ? X[r * in + i] : 0.f;
     tc_write_x(S.A, tid, x, r < n ? in : 0);
     float z4[4];
-    tc_mlp_rows(S.A, S.W, S.fp, tmem, S.bar_mma, mma_phase, tid, z4);
+    tc_mlp_rows(S.A, S.W, S.fp, tmem, S.bar_mma, mma_phase, tid, 1, z4);
     if (r < n)
       for (int j = 0; j < 4; ++j)
         out[r * 4 + j] = A.fs.act[j] == 0 ? z4[j] : (A.fs.act[j] == 1 ? sigmoidf_np(z4[j]) : expf(z4[j]));
