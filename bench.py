@@ -61,10 +61,12 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-flush", action="store_true",
                    help="diagnostic only: keep L2 warm between timed steps (not a valid bench line)")
-    p.add_argument("--e2e-mode", default="hostmap", choices=["hostmap", "copy"],
-                   help="hostmap: compose stores every rank's tiles straight into one shared, "
-                        "page-locked host frame (zero-copy, each GPU over its own PCIe link); "
-                        "copy: rank 0 downloads the assembled frame with cudaMemcpyAsync")
+    p.add_argument("--e2e-mode", default="sparse", choices=["sparse", "hostmap", "copy"],
+                   help="sparse: compose packs only the live chunks (NolfSceneOut.pack), one DMA per "
+                        "frame moves them to pinned host memory and nolf_host_scatter rebuilds the "
+                        "full frame on host threads (every rank its own rows of one shared frame); "
+                        "hostmap: every rank DMAs its full tile rows into one shared page-locked "
+                        "host frame; copy: rank 0 downloads the assembled frame with cudaMemcpyAsync")
     p.add_argument("--partition", default="rows", choices=["rows", "tiles"],
                    help="ray tiles over GPUs: interleaved tile rows (default; each rank's pixels "
                         "are strided bands of the frame) or interleaved tiles")
@@ -399,6 +401,166 @@ def workload_config(args, desc, W, H, n_assets):
                    "flushed between timed steps (256 MiB write)")}
 
 
+# ------------------------------------------------------------------ end to end (sparse frames)
+def run_e2e_sparse(args, R, N, cam_arrays, n_cam, mine, my_tiles, n_max, stride, W, H, n_views, world, rank,
+                   dev, out, scene):
+    """End to end through the public API, host wall clock: every step uploads
+    its camera block, renders, packs ONLY the live chunks (the pixels any
+    screen box reaches; the rest of the frame is the miss encoding), moves
+    them to pinned host memory in one DMA and rebuilds the full encode_frame
+    RAW frame in host memory on host threads (nolf_host_scatter).  A 3-stage
+    pipeline: step k+1 renders while step k's pack is copied and step k-1 is
+    scattered.  With N ranks every rank rebuilds its own tile rows of one
+    shared host frame (POSIX shared memory) over its own PCIe link."""
+    import ctypes
+    import torch
+    import torch.distributed as dist
+    from multiprocessing import resource_tracker, shared_memory
+    n_chunks = n_max * stride // 128
+    NPX = n_views * H * W
+    tl = np.ascontiguousarray(mine, np.int32)
+    NP = 3                              # pack buffers: render k+1 / copy k / scatter k-1
+    dpack = [torch.empty(n_chunks * 768, dtype=torch.uint8, device=dev) for _ in range(NP)]
+    dids = [torch.empty(n_chunks, dtype=torch.int32, device=dev) for _ in range(NP)]
+    hpack = [torch.empty(n_chunks * 768, dtype=torch.uint8, pin_memory=True) for _ in range(NP)]
+    hids = [torch.empty(n_chunks, dtype=torch.int32, pin_memory=True) for _ in range(NP)]
+    # live-chunk count written by the compose kernel straight into mapped host memory
+    cnt_host = np.zeros(NP, np.uint32)
+    cnt_dev = ctypes.c_void_p()
+    N.check(N.lib().nolf_host_register(cnt_host.ctypes.data, cnt_host.nbytes, ctypes.byref(cnt_dev)))
+    # the host frames (2, rotating): one shared block for all ranks
+    FB = NPX * 6
+    name = f"nolf_sparse_{os.environ.get('MASTER_PORT', 'solo')}_{os.environ.get('TORCHELASTIC_RUN_ID', os.getpid())}"
+    if rank == 0:
+        shm = shared_memory.SharedMemory(name=name, create=True, size=2 * FB)
+    if world > 1:
+        dist.barrier()
+    if rank != 0:
+        shm = shared_memory.SharedMemory(name=name)
+        resource_tracker.unregister(shm._name, "shared_memory")
+    hf = np.ndarray((2 * FB,), np.uint8, buffer=shm.buf)
+    for fb in range(2):                 # miss encoding (each rank its own rows would do; rank 0 all)
+        if rank == 0:
+            hf[fb * FB:fb * FB + NPX * 4] = 0
+            hf[fb * FB + NPX * 4:(fb + 1) * FB] = 0xFF
+    if world > 1:
+        dist.barrier()
+    prev = [np.zeros(n_chunks, np.uint32) for _ in range(2)]
+    prev_n = [ctypes.c_uint32(0) for _ in range(2)]
+    comp = torch.cuda.current_stream()
+    copy_stream = torch.cuda.Stream(device=dev)
+    ev_r = [torch.cuda.Event() for _ in range(NP)]
+    ev_c = [None] * NP
+    n_of = [0] * NP
+    bytes_d2h = [0]
+
+    def render(k):
+        b = k % NP
+        if ev_c[b] is not None:
+            comp.wait_event(ev_c[b])                 # pack buffer b copied out (step k-2)
+        o = {"pack": dpack[b], "pack_ids": dids[b], "pack_count": cnt_dev.value + 4 * b,
+             "counters": out["counters"]}
+        R.render(cam_arrays[k % n_cam], my_tiles, n_max, stride, o, frame_layout=True, prefilled=True)
+        ev_r[b].record(comp)
+
+    tm = {"wait_render": 0.0, "scatter": 0.0, "wait_copy": 0.0, "enqueue": 0.0}
+
+    def copy(k):
+        b = k % NP
+        t = time.perf_counter()
+        ev_r[b].synchronize()
+        tm["wait_render"] += time.perf_counter() - t
+        n = int(cnt_host[b])
+        n_of[b] = n
+        copy_stream.wait_event(ev_r[b])
+        with torch.cuda.stream(copy_stream):
+            hpack[b][:n * 768].copy_(dpack[b][:n * 768], non_blocking=True)
+            hids[b][:n].copy_(dids[b][:n], non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record(copy_stream)
+        ev_c[b] = ev
+        bytes_d2h[0] += n * 772 + 4
+
+    def scatter(k):                      # on the scatter thread
+        b, f = k % NP, k % 2
+        t = time.perf_counter()
+        ev_c[b].synchronize()
+        t1 = time.perf_counter()
+        base = hf.ctypes.data + f * FB
+        N.check(N.lib().nolf_host_scatter(hpack[b].data_ptr(), hids[b].data_ptr(), n_of[b], tl.ctypes.data,
+                                          len(tl), stride, W, H, base, base + NPX * 4, prev[f].ctypes.data,
+                                          ctypes.byref(prev_n[f]), 0))
+        tm["wait_copy"] += t1 - t
+        tm["scatter"] += time.perf_counter() - t1
+
+    from concurrent.futures import ThreadPoolExecutor
+    worker = ThreadPoolExecutor(1)       # ctypes drops the GIL: host scatter overlaps the next enqueue
+    pend = [None]
+
+    def submit(k):
+        if pend[0] is not None:
+            pend[0].result()
+        pend[0] = worker.submit(scatter, k)
+
+    def run(steps):
+        render(0)
+        for k in range(steps):
+            if k + 1 < steps:
+                t = time.perf_counter()
+                render(k + 1)
+                tm["enqueue"] += time.perf_counter() - t
+            copy(k)
+            if k >= 1:
+                submit(k - 1)
+        submit(steps - 1)
+        pend[0].result()
+
+    run(4)                               # warm-up (pool threads, pinned pages)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    bytes_d2h[0] = 0
+    for key in tm:
+        tm[key] = 0.0
+    t0 = time.perf_counter()
+    run(args.steps)
+    el = time.perf_counter() - t0
+    torch.cuda.synchronize()
+    te = torch.tensor([el], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    npix = NPX
+    e2e = {"value": args.steps * npix / float(te.item()) / 1e6, "unit": UNIT,
+           "h2d_bytes_per_step": int(N.lib().nolf_launch_param_bytes(len(scene), n_views)),
+           "d2h_bytes_per_step": int(bytes_d2h[0] / args.steps),
+           "timing": "host wall clock (perf_counter) from the first render to the last frame rebuilt in "
+                     "host memory, max over ranks",
+           "mode": ("sparse frame: compose packs the live 128-pixel chunks (768 B each), one DMA per step "
+                    "to pinned host memory, nolf_host_scatter rebuilds the full encode_frame RAW frame "
+                    "(rgba8 + u16 depth) in host memory on host threads (streaming stores; render k+1 / "
+                    "copy k / scatter k-1 pipelined, the scatter on its own host thread)"),
+           "full_frame_bytes": int(npix * 6),
+           "host_us_per_step": {key: round(v / args.steps * 1e6, 1) for key, v in tm.items()},
+           "host_threads": int(os.environ.get("NOLF_HOST_THREADS",
+                                              max(1, os.cpu_count() // (2 * int(os.environ.get("LOCAL_WORLD_SIZE", "1"))))))}
+    last = (args.steps - 1) % 2
+    frame_copy = torch.from_numpy(hf[last * FB:(last + 1) * FB].copy())
+    worker.shutdown()
+    N.lib().nolf_host_unregister(cnt_host.ctypes.data)
+    if world > 1:
+        dist.barrier()
+    del hf
+    try:
+        shm.close()
+    except BufferError:
+        pass
+    if world > 1:
+        dist.barrier()
+    if rank == 0:
+        shm.unlink()
+    return e2e, (args.steps - 1, frame_copy), None
+
+
 # ------------------------------------------------------------------ our arm
 def run_ours(args):
     import torch
@@ -699,7 +861,11 @@ def run_ours(args):
     shm = host_map = None
     if args.partition == "tiles" and args.e2e_mode == "hostmap":
         args.e2e_mode = "copy"          # strided row DMA needs the row partition
-    if not args.no_e2e and args.e2e_mode == "hostmap":
+    sparse_host = None
+    if not args.no_e2e and args.e2e_mode == "sparse":
+        e2e, sparse_host, shm = run_e2e_sparse(args, R, N, cam_arrays, n_cam, mine, my_tiles, n_max, stride, W, H,
+                                               n_views, world, rank, dev, out, scene)
+    elif not args.no_e2e and args.e2e_mode == "hostmap":
         # One shared page-locked host frame stack (double buffered) mapped by
         # every rank.  Each rank composes its tile rows into its own device
         # frame and one strided DMA per buffer (cudaMemcpy2DAsync, on a copy
@@ -852,6 +1018,11 @@ def run_ours(args):
             verify = {"bitwise_equal": bool(torch.equal(got, exp)),
                       "mismatched_bytes": int((got != exp).sum().item()),
                       "what": "assembled multi-GPU frame vs rank 0 rendering every tile alone"}
+            if sparse_host is not None:   # last e2e frame (host memory, rebuilt from packed chunks)
+                ke, hf = sparse_host
+                R.render(cam_arrays[ke % n_cam], all_tiles, n_tiles, stride, ref, frame_layout=True)
+                exp2 = torch.cat([ref["rgba8"].view(-1), ref["depth16"].view(torch.uint8).view(-1)])
+                verify["host_frame_bitwise_equal"] = bool(torch.equal(hf, exp2.cpu()))
             if host_map is not None:      # last e2e frame (host memory) vs the same camera alone
                 ke = args.steps - 1
                 R.render(cam_arrays[ke % n_cam], all_tiles, n_tiles, stride, ref, frame_layout=True)

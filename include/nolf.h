@@ -44,7 +44,7 @@
 extern "C" {
 #endif
 
-#define NOLF_ABI_VERSION 1
+#define NOLF_ABI_VERSION 2
 
 #define NOLF_OK 0
 #define NOLF_EINVAL -1
@@ -158,6 +158,18 @@ typedef struct NolfSceneOut {
                                           miss pixels are not written (chunks no screen
                                           box reaches, runs of 4 / 8 misses)
                                           (u8/u16 outputs only; rgba/depth must be NULL) */
+    /* Sparse frame (end-to-end delivery): with prefilled = 1, 128-slot-aligned
+     * tiles in the 8x4-block layout (sides multiples of 8 x 4) and tile_stride
+     * a multiple of 128, the compose epilogue also packs every LIVE chunk (128
+     * consecutive slots some screen box reaches; all other pixels are misses):
+     * pack[i*768 ...] = the chunk's 128 encoded pixels in slot order (rgba8,
+     * 512 B) then their depth16 (256 B); pack_ids[i] = chunk id (slot / 128);
+     * *pack_count = number of packed chunks (may be host-mapped memory).  Only
+     * these bytes need to cross PCIe: nolf_host_scatter rebuilds the frame.
+     * rgba8 / depth16 may then be NULL.  All three NULL: no pack. */
+    uint8_t *pack;
+    uint32_t *pack_ids;
+    uint32_t *pack_count;
 } NolfSceneOut;
 
 int nolf_abi_version(void);
@@ -298,6 +310,19 @@ int nolf_host_register(void *host_ptr, size_t bytes, void **dev_ptr);
 int nolf_host_unregister(void *host_ptr);
 
 /* frames: rgba (K, P, 4) f32, depth (K, P) f32, all device pointers. */
+/* Host side of the sparse frame (NolfSceneOut.pack): writes the n packed
+ * chunks (HOST copies of pack / pack_ids) into a row-major encode_frame RAW
+ * frame in host memory (camera c at c*width*height; tiles = the HOST tile
+ * list of the render, tile_stride as rendered) and resets to the miss
+ * encoding (rgba 0, depth 65535) every chunk of prev_ids (the chunks written
+ * into this frame buffer last time) that is not live now; prev_ids /
+ * *prev_n are then updated to this frame's chunks (capacity: all chunks of
+ * the tile list).  Runs on n_threads host threads (0: the library's pool
+ * default).  A frame buffer starts as the miss encoding with *prev_n = 0. */
+int nolf_host_scatter(const uint8_t *pack, const uint32_t *ids, uint32_t n, const NolfTile *tiles, int32_t n_tiles,
+                      int64_t tile_stride, int32_t width, int32_t height, uint8_t *rgba8, uint16_t *depth16,
+                      uint32_t *prev_ids, uint32_t *prev_n, int32_t n_threads);
+
 int nolf_compose(int32_t K, int64_t P, const float *rgba, const float *depth, double alpha_vis,
                  float *out_rgba, float *out_depth, void *stream);
 

@@ -20,6 +20,7 @@ LIB_PATH = os.environ.get("NOLF_LIB") or os.path.join(os.path.dirname(os.path.ab
 
 NOLF_EINVAL, NOLF_ESTATE, NOLF_EDATA, NOLF_ECUDA, NOLF_ENOMEM, NOLF_ECAPACITY = -1, -2, -3, -4, -5, -6
 HEAD_ACT = {"identity": 0, "sigmoid": 1, "exponential": 2}
+ABI_VERSION = 2              # NOLF_ABI_VERSION of include/nolf.h
 # nolf_set_option keys (include/nolf.h)
 OPT_MARCH_ORDER, OPT_COMPOSE_SLOTS, OPT_HEAVY_WAVES = 1, 2, 3
 MLP_FP32, MLP_BF16 = 0, 1
@@ -69,7 +70,8 @@ class Camera(C.Structure):
 class SceneOut(C.Structure):
     _fields_ = [("rgba", C.c_void_p), ("depth", C.c_void_p), ("rgba8", C.c_void_p),
                 ("depth16", C.c_void_p), ("tile_stride", C.c_int64), ("depth_far", C.c_double),
-                ("layout", C.c_int32), ("peer", C.c_int32), ("prefilled", C.c_int32)]
+                ("layout", C.c_int32), ("peer", C.c_int32), ("prefilled", C.c_int32),
+                ("pack", C.c_void_p), ("pack_ids", C.c_void_p), ("pack_count", C.c_void_p)]
 
 
 _lib = None
@@ -110,6 +112,7 @@ def lib():
         "nolf_set_option": ([i32, i64], C.c_int),
         "nolf_last_launch": ([vp], C.c_int),
         "nolf_check_errors": ([vp], C.c_int),
+        "nolf_host_scatter": ([vp, vp, C.c_uint32, vp, i32, i64, i32, i32, vp, vp, vp, vp, i32], C.c_int),
         "nolf_mlp_eval": ([vp, C.c_int, vp, i64, vp, vp], C.c_int),
         "nolf_device_alloc": ([C.c_size_t, C.POINTER(vp)], C.c_int),
         "nolf_device_free": ([vp], C.c_int),
@@ -131,7 +134,7 @@ def lib():
         fn = getattr(L, name)
         fn.argtypes = args
         fn.restype = res
-    if L.nolf_abi_version() != 1:
+    if L.nolf_abi_version() != ABI_VERSION:
         raise RuntimeError("libnolf_b200.so ABI version mismatch")
     _lib = L
     return L

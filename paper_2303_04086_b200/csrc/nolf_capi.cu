@@ -14,6 +14,7 @@
 #include "nolf_kernels.cuh"
 #include "nolf_load.h"
 #include "nolf_shade_tc.cuh"
+#include "nolf_host.h"
 
 using namespace nolf;
 
@@ -1194,6 +1195,17 @@ int launch_march_shade(int mode, const NolfInstance *ins, int n_inst, const Nolf
         ((uintptr_t)sout->depth16 & 15) == 0)
       ca.four = 2;
     const long long n_thr = ca.four == 2 ? n_rays / 8 : ca.four ? n_rays / 4 : n_rays;
+    ca.errors = errs->dev;
+    const bool pack = sout->pack || sout->pack_ids || sout->pack_count;
+    if (pack) {
+      if (!sout->pack || !sout->pack_ids || !sout->pack_count)
+        return fail(NOLF_EINVAL, "sparse frame: pack, pack_ids and pack_count are all required");
+      if (!(chunked && ca.prefilled && ca.four == 2))
+        return fail(NOLF_EINVAL, "sparse frame needs prefilled u8 outputs and 8-slot-aligned, 128-slot tiles");
+      ca.pack = sout->pack;
+      ca.pack_ids = sout->pack_ids;
+      ca.pack_count = sout->pack_count;
+    }
     if (chunked && ca.prefilled && ca.four == 2) {
       // misses are already in place: only the live chunks (grid from the
       // earlier frame's live count, grid-stride for any size)
@@ -1201,7 +1213,7 @@ int launch_march_shade(int mode, const NolfInstance *ins, int n_inst, const Nolf
       const long long live = std::min<long long>(n_chunks, g_live.last + g_live.last / 8 + 2ll * num_sms());
       // 8 slots per thread, or 4 when that leaves under ~1024 threads per SM
       const int g_opt = options().compose_slots;
-      const int G = g_opt == 4 || g_opt == 8 ? g_opt : (live * 16 >= 1024ll * num_sms() ? 8 : 4);
+      const int G = pack ? 8 : g_opt == 4 || g_opt == 8 ? g_opt : (live * 16 >= 1024ll * num_sms() ? 8 : 4);
       g_last_launch[2] = G;
       const long long threads = live * (128 / G);
       const unsigned cgrid = (unsigned)std::max<long long>(1, (threads + 255) / 256);
@@ -1752,4 +1764,24 @@ extern "C" int nolf_asset_load(const char *path, int device, nolf_asset_t *out, 
   fclose(f);
   if (err) return fail(NOLF_EDATA, "read error on %s", path);
   return nolf_asset_load_mem(buf.data(), buf.size(), device, out, object_to_world);
+}
+
+// ---------------------------------------------------------------- sparse frame, host side
+extern "C" int nolf_host_scatter(const uint8_t *pack, const uint32_t *ids, uint32_t n, const NolfTile *tiles,
+                                 int32_t n_tiles, int64_t tile_stride, int32_t width, int32_t height, uint8_t *rgba8,
+                                 uint16_t *depth16, uint32_t *prev_ids, uint32_t *prev_n, int32_t n_threads) {
+  if ((n && (!pack || !ids)) || !tiles || n_tiles < 0 || tile_stride < 128 || tile_stride % 128 || width < 1 ||
+      height < 1 || !rgba8 || !depth16 || !prev_ids || !prev_n)
+    return fail(NOLF_EINVAL, "bad sparse frame arguments");
+  const uint64_t n_chunks = (uint64_t)n_tiles * (uint64_t)(tile_stride / 128);
+  if (n > n_chunks || *prev_n > n_chunks) return fail(NOLF_EINVAL, "more chunks than the tile list holds");
+  for (uint32_t i = 0; i < n; ++i)
+    if (ids[i] >= n_chunks) return fail(NOLF_EDATA, "packed chunk id %u out of range", ids[i]);
+  nolf_host::ScatterJob job{pack, ids, n, tiles, n_tiles, tile_stride, width, height, rgba8, depth16,
+                           prev_ids, *prev_n};
+  const int rc = nolf_host::scatter(job, n_threads);
+  if (rc) return fail(NOLF_EDATA, "sparse frame: tile of a packed chunk is not in the 8x4-block layout");
+  memcpy(prev_ids, ids, sizeof(uint32_t) * n);
+  *prev_n = n;
+  return 0;
 }

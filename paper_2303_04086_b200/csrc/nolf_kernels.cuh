@@ -1187,6 +1187,10 @@ struct ComposeArgs {
   int four;                    // slots per thread: 0 -> 1, 1 -> 4, 2 -> 8 (tiles && nhit && stride % 4 / 8 == 0)
   const uint8_t *chunk_live;   // scene: per 128-slot chunk, 0 = never marched (all misses)
   int prefilled;               // outputs already hold the miss encoding: dead chunks are not written
+  uint8_t *pack;               // sparse frame: 768 B per live chunk (NolfSceneOut.pack), or NULL
+  uint32_t *pack_ids;
+  uint32_t *pack_count;
+  unsigned *errors;            // device error counters (kErrTile for tiles the pack cannot hold)
 };
 
 constexpr int kMaxLayers = 64;
@@ -1461,6 +1465,50 @@ __global__ void __launch_bounds__(256) k_compose(ComposeArgs a) {
   }                            // the completion collective that follows
 }
 
+// Sparse frame: 8 consecutive slots (one 8-pixel row of an 8x4 block) of
+// live chunk `idx` into its 768-byte pack entry (slot order), misses included;
+// the frame itself is written as compose_eight does (when given).
+__device__ __forceinline__ void compose_pack8(const ComposeArgs &a, const long long p0, const unsigned idx) {
+  long long t, local0;
+  split_slot(p0, a.tile_stride, t, local0);
+  const TileParams tp = a.tiles[t];
+  const int w = tp.x1 - tp.x0, h = tp.y1 - tp.y0;
+  if ((w & 7) || (h & 3)) {                 // no 8-pixel runs: cannot be packed
+    if ((local0 & 127) == 0) atomicAdd(a.errors + kErrTile, 1u);
+    return;
+  }
+  const uint2 nh = *reinterpret_cast<const uint2 *>(a.nhit + p0);
+  unsigned c8[8], dd[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const int n = local0 + j < (long long)w * h ? (int)(((j < 4 ? nh.x : nh.y) >> (8 * (j & 3))) & 0xffu) : 0;
+    float4 o;
+    float od;
+    compose_px(a, p0 + j, n, o, od);
+    const uchar4 u = encode_rgba8(o);
+    c8[j] = (unsigned)u.x | ((unsigned)u.y << 8) | ((unsigned)u.z << 16) | ((unsigned)u.w << 24);
+    dd[j] = encode_depth16(od, a.depth_far);
+  }
+  const unsigned s = (unsigned)(p0 & 127);
+  uint8_t *e = a.pack + (size_t)idx * 768;
+  reinterpret_cast<uint4 *>(e + 4 * s)[0] = make_uint4(c8[0], c8[1], c8[2], c8[3]);
+  reinterpret_cast<uint4 *>(e + 4 * s)[1] = make_uint4(c8[4], c8[5], c8[6], c8[7]);
+  *reinterpret_cast<uint4 *>(e + 512 + 2 * s) =
+      make_uint4(dd[0] | (dd[1] << 16), dd[2] | (dd[3] << 16), dd[4] | (dd[5] << 16), dd[6] | (dd[7] << 16));
+  if (a.out_rgba8 && local0 < (long long)w * h && tile_valid(tp, a.cams, a.n_cams, a.tile_stride)) {
+    const CamParams &cp = a.cams[tp.cam];
+    int x, y;
+    slot_xy(local0, w, h, x, y);
+    const long long q0 = cp.pix_base + (long long)(tp.y0 + y) * cp.width + (tp.x0 + x);
+    uint4 *r8 = reinterpret_cast<uint4 *>(a.out_rgba8 + q0 * 4);
+    r8[0] = make_uint4(c8[0], c8[1], c8[2], c8[3]);
+    r8[1] = make_uint4(c8[4], c8[5], c8[6], c8[7]);
+    if (a.out_depth16)
+      *reinterpret_cast<uint4 *>(a.out_depth16 + q0) =
+          make_uint4(dd[0] | (dd[1] << 16), dd[2] | (dd[3] << 16), dd[4] | (dd[5] << 16), dd[6] | (dd[7] << 16));
+  }
+}
+
 // Prefilled outputs: compose only the live chunks, from the compacted list
 // (16 threads x 8 slots per chunk, grid-stride over the list's length).
 // G slots per thread (8 or 4): a launch over few live chunks (a multi-GPU
@@ -1473,9 +1521,16 @@ __global__ void __launch_bounds__(256) k_compose_live(ComposeArgs a, const unsig
   for (long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x; g < total;
        g += (long long)gridDim.x * blockDim.x) {
     const long long p0 = (long long)live_list[g / per_chunk] * 128 + (g % per_chunk) * G;   // spatial list
-    if (G == 8) compose_eight(a, p0);
-    else compose_four(a, p0);
+    if (G == 8 && a.pack) {
+      compose_pack8(a, p0, (unsigned)(g / per_chunk));
+      if (g % per_chunk == 0) a.pack_ids[g / per_chunk] = live_list[g / per_chunk];
+    } else if (G == 8) {
+      compose_eight(a, p0);
+    } else {
+      compose_four(a, p0);
+    }
   }
+  if (a.pack_count && blockIdx.x == 0 && threadIdx.x == 0) *a.pack_count = count[0];
   if (a.peer) {
     __syncthreads();
     if (threadIdx.x == 0) __threadfence_system();

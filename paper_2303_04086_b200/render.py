@@ -519,6 +519,10 @@ class SceneRenderer:
 
     def render(self, cameras, tiles_dev, n_tiles: int, tile_stride: int, out: dict, stream=None,
                frame_layout: bool = False, peer: bool = False, prefilled: bool = False):
+        """One fused launch sequence.  ``out``: rgba / depth (f32), rgba8 /
+        depth16 (encode_frame RAW), counters; optionally pack / pack_ids /
+        pack_count (the sparse frame of live chunks, NolfSceneOut.pack;
+        needs prefilled=True)."""
         cams = cameras if isinstance(cameras, C.Array) else self.camera_array(cameras)
         so = N.SceneOut()
         def ptr(key):              # tensors, or raw device addresses (peer mappings)
@@ -534,6 +538,9 @@ class SceneRenderer:
         so.layout = 1 if frame_layout else 0
         so.peer = 1 if peer else 0
         so.prefilled = 1 if prefilled else 0
+        so.pack = ptr("pack")
+        so.pack_ids = ptr("pack_ids")
+        so.pack_count = ptr("pack_count")
         st = stream if stream is not None else _stream_ptr()
         ws = self._workspace(cams, int(n_tiles) * int(tile_stride))
         N.check(N.lib().nolf_render_scene(self._inst_arr, len(self.insts), cams, len(cams),
