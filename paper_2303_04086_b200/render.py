@@ -542,11 +542,20 @@ class SceneRenderer:
         so.pack_ids = ptr("pack_ids")
         so.pack_count = ptr("pack_count")
         st = stream if stream is not None else _stream_ptr()
-        ws = self._workspace(cams, int(n_tiles) * int(tile_stride))
-        N.check(N.lib().nolf_render_scene(self._inst_arr, len(self.insts), cams, len(cams),
-                                          tiles_dev.data_ptr(), int(n_tiles), C.byref(so),
-                                          self.alpha_vis, out["counters"].data_ptr(),
-                                          ws.data_ptr(), ws.numel(), st))
+        P = int(n_tiles) * int(tile_stride)
+        # the library sizes the launch itself and refuses a short workspace:
+        # only then is the plan computed here too (grow, retry)
+        ws = self._ws if self._ws is not None else self._workspace(cams, P)
+        lib = N.lib()
+
+        def launch(ws):
+            return lib.nolf_render_scene(self._inst_arr, len(self.insts), cams, len(cams), tiles_dev.data_ptr(),
+                                         int(n_tiles), C.byref(so), self.alpha_vis, out["counters"].data_ptr(),
+                                         ws.data_ptr(), ws.numel(), st)
+        rc = launch(ws)
+        if rc == N.NOLF_EINVAL and b"workspace too small" in lib.nolf_last_error():
+            rc = launch(self._workspace(cams, P))
+        N.check(rc)
 
     def check(self, stream=None) -> None:
         """Synchronise; CapacityError if a render dropped work on the device

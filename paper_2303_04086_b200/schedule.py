@@ -185,6 +185,12 @@ class FarmAssigner:
         self.cache = {}            # shared_key -> expiry
         self.assembly = None       # (born_tick, expected set)
         self.session = None
+        # what the last tick did, for an executor (farm.GpuFarm): the frame
+        # being assembled, tasks served from the tile cache, a finished frame
+        self.frame = None          # {"index", "camera", "order", "transforms", "tasks": {id: Task}}
+        self.frame_index = -1
+        self.last_cache_hits = []  # [Task]
+        self.last_finished = None  # {"frame": <self.frame>, "timed_out": set of task ids}
 
     def open(self, width, height, fx, fy, cx, cy, target_fps, scene=None):
         scene = scene if scene is not None else [(n, np.eye(4)) for n in sorted(self.proxies)]
@@ -204,6 +210,9 @@ class FarmAssigner:
         s = self.session
         cam = s.camera()
         expected = set()
+        self.frame_index += 1
+        self.frame = {"index": self.frame_index, "camera": cam, "order": [n for n, _ in s.scene],
+                      "transforms": {n: np.asarray(tr, np.float64) for n, tr in s.scene}, "tasks": {}}
         for name, tr in s.scene:
             proxy = self.proxies[name]
             cls, skip = classify_task(estimate_nhit(proxy, tr, cam), self.thr)
@@ -222,6 +231,7 @@ class FarmAssigner:
                          (name, pose_key, rect, cam.width, cam.height))
                 expected.add(t.task_id)
                 s.pending.append(t)
+                self.frame["tasks"][t.task_id] = t
         self.assembly = [self.tick_index, expected]
 
     # scheduler.py:283-367 for one session
@@ -283,6 +293,8 @@ class FarmAssigner:
     def tick(self, now: float):
         """One master tick; returns [(task_id, asset, rect, class, rays, worker, skip)]."""
         s = self.session
+        self.last_cache_hits = []
+        self.last_finished = None
         if s.pose is not None and self.assembly is None and not s.pending and s.target_time <= now:
             self._build()
         # _dedup_and_cache (single session: only cache hits can occur)
@@ -291,6 +303,7 @@ class FarmAssigner:
             for t in list(s.pending):
                 if not t.skip and t.shared_key in self.cache:
                     s.pending.remove(t)
+                    self.last_cache_hits.append(t)
                     if self.assembly is not None:
                         self.assembly[1].discard(t.task_id)
         dispatched = self._dispatch(self._schedule(now))
@@ -306,6 +319,7 @@ class FarmAssigner:
             born, expected = self.assembly
             timed_out = self.tick_index - born >= self.timeout and expected
             if not expected or timed_out:
+                self.last_finished = {"frame": self.frame, "timed_out": set(expected) if timed_out else set()}
                 if timed_out:
                     s.pending = [t for t in s.pending if t.task_id not in expected]
                 completion = max(0.0, now - born * self.tick_s)
