@@ -532,7 +532,8 @@ int oracle_compose(int K, int64_t P, const float *rgba, const float *depth, doub
 #pragma omp parallel for num_threads(nthreads) schedule(static)
 #endif
     for (int64_t p = 0; p < P; ++p) {
-        int order[64];
+        int order_small[64];
+        int *order = K <= 64 ? order_small : (int *)malloc(sizeof(int) * (size_t)K);
         /* stable argsort by depth (NaN never produced upstream) */
         for (int k = 0; k < K; ++k) {
             int j = k;
@@ -556,6 +557,7 @@ int oracle_compose(int K, int64_t P, const float *rgba, const float *depth, doub
         o[3] = (float)clampd(1.0 - trans, 0.0, 1.0);
         out_depth[p] = od;
         if (o[3] <= 0.f) { o[0] = o[1] = o[2] = o[3] = 0.f; out_depth[p] = INFINITY; }
+        if (order != order_small) free(order);
     }
     return 0;
 }

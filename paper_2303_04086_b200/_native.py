@@ -130,7 +130,10 @@ def lib():
         "nolf_launch_param_bytes": ([i32, i32], C.c_size_t),
         "nolf_unpack_gathered": ([vp, i32, i32, i64, vp, i32, i32, vp, vp, vp], C.c_int),
     }
+    experiment = bool(os.environ.get("NOLF_LIB"))   # another build (A/B): may predate some entry points
     for name, (args, res) in sig.items():
+        if experiment and not hasattr(L, name):
+            continue
         fn = getattr(L, name)
         fn.argtypes = args
         fn.restype = res

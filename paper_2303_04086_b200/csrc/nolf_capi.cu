@@ -22,6 +22,12 @@ namespace {
 
 thread_local std::string g_err;
 
+// Restores the caller's current device when it goes out of scope.
+struct DeviceRestore {
+  int dev;
+  ~DeviceRestore() { cudaSetDevice(dev); }
+};
+
 int fail(int code, const char *fmt, ...) {
   char buf[512];
   va_list ap;
@@ -38,8 +44,8 @@ int fail(int code, const char *fmt, ...) {
     if (e_ != cudaSuccess) return fail(NOLF_ECUDA, "%s: %s", #x, cudaGetErrorString(e_)); \
   } while (0)
 
-constexpr int kMaxInst = 64;
-constexpr int kMaxCams = 32;
+constexpr int kMaxInst = 255;    // compose layers per pixel are counted in a u8
+constexpr int kMaxCams = 4096;
 
 }  // namespace
 
@@ -330,22 +336,26 @@ int pack_mlp(NolfAsset *A, const NolfMlpDesc &m, DevMlp *out, const char *what) 
   return rc;
 }
 
-int g_num_sms = 0;
-
-int num_sms() {
-  if (!g_num_sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-    if (g_num_sms <= 0) g_num_sms = 148;
+int num_sms() {                 // per device (a process may drive several)
+  static int sms[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (!sms[dev]) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    sms[dev] = v > 0 ? v : 148;
   }
-  return g_num_sms;
+  return sms[dev];
 }
 
 constexpr size_t kShadeSmem = (size_t)(2 * MlpOff::total + kInp * kShadeThreads) * sizeof(float);
 
-int ensure_attrs() {
-  static bool done = false;
+int ensure_attrs() {            // function attributes are per device
+  static bool done_dev[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  bool &done = done_dev[dev >= 0 && dev < 64 ? dev : 0];
   if (!done) {
     CUDA_TRY(cudaFuncSetAttribute(k_shade, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kShadeSmem));
     CUDA_TRY(cudaFuncSetAttribute(k_eval_diffuse, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kShadeSmem));
@@ -419,17 +429,46 @@ int run_shade(const DevInst *inst, const long long *qoff, int n_inst, const Work
 
 // Per-launch instance / camera tables live in a device-side parameter block.
 namespace {
+// Packed per launch (only what the launch uses crosses PCIe):
+//   inst[n_inst] | cams[n_cams] | rect | qoff[n_inst + 1] | cull[n_inst * n_cams]
 struct ParamBlock {
-  DevInst inst[kMaxInst];
-  CamParams cams[kMaxCams];
-  TileParams rect;
-  long long qoff[kMaxInst + 1];          // hit-queue offset of every instance
-  ScreenBox cull[kMaxInst * kMaxCams];   // only the used prefix is copied
+  DevInst *inst;
+  CamParams *cams;
+  TileParams *rect;
+  long long *qoff;                       // hit-queue offset of every instance
+  ScreenBox *cull;
 };
 
-size_t param_bytes(int n_inst, int n_cams) {   // cull tail is n_inst x n_cams
-  return offsetof(ParamBlock, cull) + sizeof(ScreenBox) * (size_t)n_inst * (size_t)(n_cams > 0 ? n_cams : 1);
+struct ParamLayout {
+  size_t inst, cams, rect, qoff, cull, total;
+};
+
+ParamLayout param_layout(int n_inst, int n_cams) {
+  ParamLayout L;
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    const size_t o = off;
+    off = (off + bytes + 15) / 16 * 16;
+    return o;
+  };
+  const size_t nc = (size_t)(n_cams > 0 ? n_cams : 1);
+  L.inst = take(sizeof(DevInst) * (size_t)n_inst);
+  L.cams = take(sizeof(CamParams) * nc);
+  L.rect = take(sizeof(TileParams));
+  L.qoff = take(sizeof(long long) * (size_t)(n_inst + 1));
+  L.cull = take(sizeof(ScreenBox) * (size_t)n_inst * nc);
+  L.total = off;
+  return L;
 }
+
+ParamBlock param_view(void *base, const ParamLayout &L) {
+  char *b = static_cast<char *>(base);
+  return ParamBlock{reinterpret_cast<DevInst *>(b + L.inst), reinterpret_cast<CamParams *>(b + L.cams),
+                    reinterpret_cast<TileParams *>(b + L.rect), reinterpret_cast<long long *>(b + L.qoff),
+                    reinterpret_cast<ScreenBox *>(b + L.cull)};
+}
+
+size_t param_bytes(int n_inst, int n_cams) { return param_layout(n_inst, n_cams).total; }
 
 // Conservative image rectangle of an instance's culling box (occupied cells,
 // see nolf_asset_create) for one camera.
@@ -563,7 +602,10 @@ const char *nolf_last_error(void) { return g_err.c_str(); }
 int nolf_asset_create(const NolfAssetDesc *d, int device, nolf_asset_t *out) {
   if (!d || !out) return fail(NOLF_EINVAL, "null argument");
   *out = nullptr;
+  int prev_dev = 0;
+  CUDA_TRY(cudaGetDevice(&prev_dev));
   CUDA_TRY(cudaSetDevice(device));
+  DeviceRestore restore_{prev_dev};   // the caller's current device on every exit
   NolfAsset *A = new NolfAsset();
   A->device = device;
   DevAsset &H = A->host;
@@ -746,7 +788,10 @@ int nolf_asset_create(const NolfAssetDesc *d, int device, nolf_asset_t *out) {
 
 int nolf_asset_destroy(nolf_asset_t a) {
   if (!a) return 0;
+  int prev_dev = 0;
+  cudaGetDevice(&prev_dev);
   cudaSetDevice(a->device);
+  DeviceRestore restore_{prev_dev};
   delete a;
   return 0;
 }
@@ -936,36 +981,45 @@ int run_shade(const DevInst *inst, const long long *qoff, int n_inst, const Work
 // are written with cudaMemcpyAsync from pinned staging on the caller's
 // stream, so consecutive launches on one stream never race.
 struct ParamRing {
-  ParamBlock *host = nullptr;
-  ParamBlock *dev = nullptr;
+  char *host = nullptr;
+  char *dev = nullptr;
+  size_t slot_bytes = 0;
   int slots = 0, next = 0;
   cudaEvent_t *done = nullptr;
 };
-thread_local ParamRing g_ring;
+thread_local ParamRing g_rings[kMaxDevices];   // per device: kernels read their own GPU's copy
 
-int ring_acquire(ParamBlock **h, ParamBlock **d, int *slot) {
-  ParamRing &R = g_ring;
-  if (!R.host) {
-    R.slots = 8;
-    CUDA_TRY(cudaMallocHost(&R.host, sizeof(ParamBlock) * R.slots));
-    CUDA_TRY(cudaMalloc(&R.dev, sizeof(ParamBlock) * R.slots));
-    R.done = new cudaEvent_t[R.slots];
-    for (int i = 0; i < R.slots; ++i) {
-      CUDA_TRY(cudaEventCreateWithFlags(&R.done[i], cudaEventDisableTiming));
-      CUDA_TRY(cudaEventRecord(R.done[i], 0));
+// A staging slot of at least `bytes` (the ring grows -- after draining --
+// when a launch needs more than any before).
+int ring_acquire(size_t bytes, char **h, char **d, int *slot) {
+  ParamRing &R = g_rings[cur_device()];
+  if (!R.host || bytes > R.slot_bytes) {
+    if (R.host) {
+      for (int i = 0; i < R.slots; ++i) CUDA_TRY(cudaEventSynchronize(R.done[i]));
+      cudaFreeHost(R.host);
+      cudaFree(R.dev);
+    } else {
+      R.slots = 8;
+      R.done = new cudaEvent_t[R.slots];
+      for (int i = 0; i < R.slots; ++i) CUDA_TRY(cudaEventCreateWithFlags(&R.done[i], cudaEventDisableTiming));
     }
+    R.slot_bytes = std::max<size_t>((bytes + 255) / 256 * 256, 16384);
+    CUDA_TRY(cudaMallocHost(&R.host, R.slot_bytes * R.slots));
+    CUDA_TRY(cudaMalloc(&R.dev, R.slot_bytes * R.slots));
+    for (int i = 0; i < R.slots; ++i) CUDA_TRY(cudaEventRecord(R.done[i], 0));
+    R.next = 0;
   }
   int s = R.next;
   R.next = (R.next + 1) % R.slots;
   CUDA_TRY(cudaEventSynchronize(R.done[s]));   // host staging slot free again
-  *h = R.host + s;
-  *d = R.dev + s;
+  *h = R.host + (size_t)s * R.slot_bytes;
+  *d = R.dev + (size_t)s * R.slot_bytes;
   *slot = s;
   return 0;
 }
 
 int ring_release(int slot, cudaStream_t st) {
-  CUDA_TRY(cudaEventRecord(g_ring.done[slot], st));
+  CUDA_TRY(cudaEventRecord(g_rings[cur_device()].done[slot], st));
   return 0;
 }
 
@@ -1047,8 +1101,13 @@ int launch_march_shade(int mode, const NolfInstance *ins, int n_inst, const Nolf
   if (n_cams > kMaxCams) return fail(NOLF_EINVAL, "camera count %d > %d", n_cams, kMaxCams);
   if (!counters) return fail(NOLF_EINVAL, "counters pointer required");
   if (mode == kModeScene && n_inst > 255) return fail(NOLF_EINVAL, "too many layers");
-  for (int k = 0; k < n_inst; ++k)
+  const int dev_now = cur_device();
+  for (int k = 0; k < n_inst; ++k) {
     if (!ins[k].asset) return fail(NOLF_EINVAL, "null asset instance");
+    if (ins[k].asset->device != dev_now)
+      return fail(NOLF_EINVAL, "instance %d: asset lives on device %d, the current device is %d", k,
+                  ins[k].asset->device, dev_now);
+  }
   int rc0;
   if ((rc0 = poll_errors())) return rc0;    // an earlier launch dropped work: fail loudly
   ErrState *errs;
@@ -1062,9 +1121,12 @@ int launch_march_shade(int mode, const NolfInstance *ins, int n_inst, const Nolf
   if ((rc = ensure_attrs())) return rc;
   Workspace w;
   ws_layout(n_inst, pl.qoff[(size_t)n_inst], pl.layers, n_rays, static_cast<char *>(workspace), &w);
-  ParamBlock *hp, *dp;
+  const ParamLayout PL = param_layout(n_inst, n_cams);
+  char *hraw, *draw;
   int slot;
-  if ((rc = ring_acquire(&hp, &dp, &slot))) return rc;
+  if ((rc = ring_acquire(PL.total, &hraw, &draw, &slot))) return rc;
+  ParamBlock hb = param_view(hraw, PL), db = param_view(draw, PL);
+  ParamBlock *hp = &hb, *dp = &db;
   bool use_tc = true;
   uint32_t phi_smem = 0;
   for (int k = 0; k < n_inst; ++k) {
@@ -1074,14 +1136,14 @@ int launch_march_shade(int mode, const NolfInstance *ins, int n_inst, const Nolf
     if (H.phi16 && H.phi16_bytes <= kTcPhiMax) phi_smem = std::max(phi_smem, H.phi16_bytes);
   }
   for (int c = 0; c < n_cams; ++c) hp->cams[c] = hcams[(size_t)c];
-  hp->rect = rect;
+  *hp->rect = rect;
   for (int k = 0; k <= n_inst; ++k) hp->qoff[k] = pl.qoff[(size_t)k];
   for (size_t i = 0; i < pl.cull.size(); ++i) hp->cull[i] = pl.cull[i];
   // the parameter block goes up on a side stream (the copy overlaps the
   // previous frame's kernels); the launch stream waits for it
   Aux &ax = aux_for(st);
   if (!ax.s) return fail(NOLF_ECUDA, "aux stream: %s", g_err.c_str());
-  CUDA_TRY(cudaMemcpyAsync(dp, hp, param_bytes(n_inst, n_cams), cudaMemcpyHostToDevice, ax.s));
+  CUDA_TRY(cudaMemcpyAsync(draw, hraw, PL.total, cudaMemcpyHostToDevice, ax.s));
   CUDA_TRY(cudaEventRecord(ax.ev_param, ax.s));
   CUDA_TRY(cudaStreamWaitEvent(st, ax.ev_param, 0));
   if (n_rays == 0) return ring_release(slot, st);
@@ -1097,7 +1159,7 @@ int launch_march_shade(int mode, const NolfInstance *ins, int n_inst, const Nolf
   ma.dirs = dirs;
   ma.n_rays = n_rays;
   ma.cams = dp->cams;
-  ma.tiles = mode == kModeScene ? reinterpret_cast<const TileParams *>(tiles_dev) : &dp->rect;
+  ma.tiles = mode == kModeScene ? reinterpret_cast<const TileParams *>(tiles_dev) : dp->rect;
   ma.tile_stride = tile_stride;
   ma.cull = n_cams > 0 ? dp->cull : nullptr;
   ma.use_zmask = 1;
@@ -1117,6 +1179,7 @@ int launch_march_shade(int mode, const NolfInstance *ins, int n_inst, const Nolf
   if ((rc = prof_mark(0, st))) return rc;
   if (mode == kModeRays) k_march<kModeRays><<<grid, kMarchThreads, 0, st>>>(ma);
   else if (mode == kModeRect) k_march<kModeRect><<<grid, kMarchThreads, 0, st>>>(ma);
+  else if (!chunked && n_inst > 64) k_march<kModeScene, true><<<grid, kMarchThreads, 0, st>>>(ma);
   else if (!chunked) k_march<kModeScene><<<grid, kMarchThreads, 0, st>>>(ma);
   else {                       // compact the live chunks, then a persistent marcher drains them
     const long long n_chunks = n_rays / kMarchThreads;
@@ -1153,7 +1216,9 @@ int launch_march_shade(int mode, const NolfInstance *ins, int n_inst, const Nolf
                                                                       w.counts + n_inst);
     CUDA_TRY(cudaGetLastError());
     CUDA_TRY(cudaEventRecord(ax.ev_cull, st));   // the live count is final here
-    k_march_chunks<<<(unsigned)std::max<long long>(1, std::min(n_chunks, want)), kMarchThreads, 0, st>>>(ma);
+    const unsigned mgrid = (unsigned)std::max<long long>(1, std::min(n_chunks, want));
+    if (n_inst > 64) k_march_chunks<true><<<mgrid, kMarchThreads, 0, st>>>(ma);
+    else k_march_chunks<false><<<mgrid, kMarchThreads, 0, st>>>(ma);
     if (!le.pending) {          // read the live count back on the side stream: shading never waits for it
       CUDA_TRY(cudaStreamWaitEvent(ax.s, ax.ev_cull, 0));
       CUDA_TRY(cudaMemcpyAsync(le.host, w.counts + n_inst, sizeof(unsigned), cudaMemcpyDeviceToHost, ax.s));
@@ -1287,15 +1352,18 @@ int nolf_march_rays(nolf_asset_t asset, const double *origins, int32_t origin_st
   (void)workspace;
   (void)ws_bytes;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  ParamBlock *hp, *dp;
+  const ParamLayout PL = param_layout(1, 0);
+  char *hraw, *draw;
   int slot, rc;
-  if ((rc = ring_acquire(&hp, &dp, &slot))) return rc;
+  if ((rc = ring_acquire(PL.total, &hraw, &draw, &slot))) return rc;
+  ParamBlock hb = param_view(hraw, PL), db = param_view(draw, PL);
+  ParamBlock *hp = &hb, *dp = &db;
   memset(&hp->inst[0], 0, sizeof(DevInst));
   hp->inst[0].a = asset->dev;
   hp->inst[0].scale = 1.0;
   hp->qoff[0] = 0;
   hp->qoff[1] = 0;
-  CUDA_TRY(cudaMemcpyAsync(dp, hp, param_bytes(1, 0), cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemcpyAsync(draw, hraw, PL.total, cudaMemcpyHostToDevice, st));
   if ((rc = ring_release(slot, st))) return rc;
   MarchArgs ma{};
   ma.inst = dp->inst;
@@ -1541,7 +1609,6 @@ int nolf_host_unregister(void *host_ptr) {
 int nolf_compose(int32_t K, int64_t P, const float *rgba, const float *depth, double alpha_vis, float *out_rgba,
                  float *out_depth, void *stream) {
   if (K < 1) return fail(NOLF_EINVAL, "compose needs at least one frame");
-  if (K > kMaxLayers) return fail(NOLF_EINVAL, "compose: %d frames > %d", K, kMaxLayers);
   if (P == 0) return 0;
   if (!rgba || !depth || !out_rgba || !out_depth) return fail(NOLF_EINVAL, "null buffer");
   ComposeArgs ca{};
@@ -1583,8 +1650,32 @@ extern "C" int nolf_stats_read(unsigned long long *out, int reset) {
 // ---------------------------------------------------------------- native .nolf loading
 // assetio.read_asset (assetio.py:174-255) without Python: container, CRC32,
 // gzip, meta JSON -> NolfAssetDesc -> nolf_asset_create.
+// Bounded products of untrusted meta fields: false if any factor is
+// negative or the product exceeds `limit` (no int64 overflow on the way).
+static bool checked_product(std::initializer_list<int64_t> f, int64_t limit, int64_t &out) {
+  int64_t p = 1;
+  for (int64_t v : f) {
+    if (v < 0 || (v > 0 && p > limit / v)) return false;
+    p *= v;
+  }
+  out = p;
+  return p <= limit;
+}
+
+static int asset_load_mem(const void *data, size_t n, int device, nolf_asset_t *out, double object_to_world[16]);
+
 extern "C" int nolf_asset_load_mem(const void *data, size_t n, int device, nolf_asset_t *out,
                                    double object_to_world[16]) {
+  try {                        // nothing may escape the C ABI (bad_alloc on a hostile size, ...)
+    return asset_load_mem(data, n, device, out, object_to_world);
+  } catch (const std::exception &e) {
+    return fail(NOLF_EDATA, "asset load failed: %s", e.what());
+  } catch (...) {
+    return fail(NOLF_EDATA, "asset load failed");
+  }
+}
+
+static int asset_load_mem(const void *data, size_t n, int device, nolf_asset_t *out, double object_to_world[16]) {
   using namespace nolf_load;
   if (!data || !out) return fail(NOLF_EINVAL, "null argument");
   *out = nullptr;
@@ -1606,13 +1697,16 @@ extern "C" int nolf_asset_load_mem(const void *data, size_t n, int device, nolf_
   auto atlas = [&](const char *key, const char *tag, int ch, NolfAtlasDesc &a, std::vector<int32_t> &idx,
                    std::vector<float> &cubes) -> int {
     const Json *j = m.get(key);
-    int64_t b, r, nc;
-    if (!inum(j ? j->get("b") : nullptr, b) || !inum(j->get("r"), r) || !inum(j->get("cubes"), nc) || b < 1 || r < 1 ||
-        nc < 0)
+    int64_t b, r, nc, ncell, ncube;
+    if (!inum(j ? j->get("b") : nullptr, b) || !inum(j->get("r"), r) || !inum(j->get("cubes"), nc) || b < 1 ||
+        b > 1024 || r < 1 || r > 64 || nc < 0)
       return bad(key);
-    const size_t s1 = (size_t)r + 1;
-    if (!aligned(c, std::string(tag) + "_index", (size_t)(b * b * b), idx, err) ||
-        !aligned(c, std::string(tag) + "_cubes", (size_t)nc * s1 * s1 * s1 * (size_t)ch, cubes, err))
+    const int64_t s1 = r + 1;
+    if (!checked_product({b, b, b}, 1ll << 30, ncell) || nc > ncell ||
+        !checked_product({nc, s1, s1, s1, (int64_t)ch}, 1ll << 34, ncube))
+      return bad(key);
+    if (!aligned(c, std::string(tag) + "_index", (size_t)ncell, idx, err) ||
+        !aligned(c, std::string(tag) + "_cubes", (size_t)ncube, cubes, err))
       return fail(NOLF_EDATA, "%s", err.c_str());
     a.b = (int32_t)b;
     a.r = (int32_t)r;
@@ -1632,7 +1726,8 @@ extern "C" int nolf_asset_load_mem(const void *data, size_t n, int device, nolf_
   const Json *pm = m.get("psh");
   int64_t res, tsz, osz, F;
   if (!pm || !inum(pm->get("resolution"), res) || !inum(pm->get("table_size"), tsz) ||
-      !inum(pm->get("offset_size"), osz) || !inum(pm->get("features"), F) || F < 1)
+      !inum(pm->get("offset_size"), osz) || !inum(pm->get("features"), F) || F < 1 || F > 4 || res < 1 ||
+      res > (1 << 20) || tsz < 1 || tsz >= (1ll << 30) || osz < 1 || osz >= (1ll << 30))
     return bad("psh");
   const Json *p0 = pm->get("primes_h0"), *p1 = pm->get("primes_h1");
   if (!p0 || !p1 || p0->kind != Json::Arr || p1->kind != Json::Arr || p0->arr.size() != 3 || p1->arr.size() != 3)
@@ -1656,14 +1751,18 @@ extern "C" int nolf_asset_load_mem(const void *data, size_t n, int device, nolf_
   int64_t lv, base, hts, fpl;
   double growth;
   if (!em || !inum(em->get("levels"), lv) || !inum(em->get("base_resolution"), base) || !num(em->get("growth"), growth) ||
-      !inum(em->get("table_size"), hts) || !inum(em->get("features_per_level"), fpl) || lv < 0 || lv > 16)
+      !inum(em->get("table_size"), hts) || !inum(em->get("features_per_level"), fpl) || lv < 0 || lv > 16 ||
+      base < 1 || base > 4096 || !(growth >= 1.0 && growth <= 16.0) || hts < 1 || hts >= (1ll << 30) || fpl < 1 ||
+      fpl > 8)
     return bad("diffuse_encoder");
   d.hg_levels = (int32_t)lv;
   d.hg_features = (int32_t)fpl;
   d.hg_table_size = hts;
   hg.resize((size_t)lv);
   for (int l = 0; l < lv; ++l) {
-    const int64_t nres = std::max<int64_t>(2, (int64_t)std::floor((double)base * std::pow(growth, (double)l)));
+    const double fres = std::floor((double)base * std::pow(growth, (double)l));
+    if (!(fres < 1e6)) return bad("diffuse_encoder resolution");
+    const int64_t nres = std::max<int64_t>(2, (int64_t)fres);
     const bool dense = (nres + 1) * (nres + 1) * (nres + 1) <= hts;
     const int64_t rows = dense ? (nres + 1) * (nres + 1) * (nres + 1) : hts;
     if (!aligned(c, "ed_feat_" + std::to_string(l), (size_t)(rows * fpl), hg[(size_t)l], err))
@@ -1683,7 +1782,7 @@ extern "C" int nolf_asset_load_mem(const void *data, size_t n, int device, nolf_
       return bad(key);
     int64_t wd[5];
     for (size_t i = 0; i < w->arr.size(); ++i)
-      if (!inum(&w->arr[i], wd[i]) || wd[i] < 1) return bad(key);
+      if (!inum(&w->arr[i], wd[i]) || wd[i] < 1 || wd[i] > 4096) return bad(key);
     md.n_layers = (int32_t)w->arr.size() - 1;
     md.widths[0] = (int32_t)wd[0];
     for (int i = 0; i < md.n_layers; ++i) {
@@ -1739,7 +1838,9 @@ extern "C" int nolf_asset_load_mem(const void *data, size_t n, int device, nolf_
     if (!num(&tf->arr[k], o2w[k])) return bad("transform");
   if (const Json *pm2 = m.get("proxy_mesh")) {   // extension sections (nolf_io.py), absent in reference files
     int64_t nv, nt;
-    if (!inum(pm2->get("vertices"), nv) || !inum(pm2->get("triangles"), nt) || nv < 0 || nt < 0) return bad("proxy_mesh");
+    if (!inum(pm2->get("vertices"), nv) || !inum(pm2->get("triangles"), nt) || nv < 0 || nt < 0 || nv >= (1ll << 30) ||
+        nt >= (1ll << 30))
+      return bad("proxy_mesh");
     if (!aligned(c, "mesh_vertices", (size_t)nv * 3, verts, err) || !aligned(c, "mesh_triangles", (size_t)nt * 3, tris, err))
       return fail(NOLF_EDATA, "%s", err.c_str());
     d.mesh_vertices = verts.data();

@@ -571,12 +571,14 @@ __device__ __forceinline__ bool slot_pixel(const MarchArgs &args, long long gid,
 
 // Instances whose conservative screen box covers this lane's pixel (all
 // instances without culling).  Warp-collective.
+// Instances g0 .. g0+63 (bit k - g0).
 template <int MODE>
 __device__ __forceinline__ unsigned long long candidate_mask(const MarchArgs &args, bool valid, int pix_x, int pix_y,
-                                                             int cam, unsigned lane) {
+                                                             int cam, unsigned lane, int g0) {
   unsigned long long lane_mask = 0;
+  const int g1 = min(args.n_inst, g0 + 64);
   if (MODE == kModeRays || !args.cull) {
-    if (valid) lane_mask = args.n_inst >= 64 ? ~0ull : ((1ull << args.n_inst) - 1ull);
+    if (valid) lane_mask = g1 - g0 >= 64 ? ~0ull : ((1ull << (g1 - g0)) - 1ull);
     return lane_mask;
   }
   const int cmin = __reduce_min_sync(0xffffffffu, valid ? cam : INT_MAX);
@@ -588,10 +590,10 @@ __device__ __forceinline__ unsigned long long candidate_mask(const MarchArgs &ar
     const int xmax = __reduce_max_sync(0xffffffffu, valid ? pix_x : INT_MIN);
     const int ymin = __reduce_min_sync(0xffffffffu, valid ? pix_y : INT_MAX);
     const int ymax = __reduce_max_sync(0xffffffffu, valid ? pix_y : INT_MIN);
-    for (int base = 0; base < args.n_inst; base += 32) {
+    for (int base = g0; base < g1; base += 32) {
       const int k = base + (int)lane;
       ScreenBox bb{1, 1, 0, 0};
-      if (k < args.n_inst) bb = args.cull[k * args.n_cams + cmin];
+      if (k < g1) bb = args.cull[k * args.n_cams + cmin];
       unsigned cand = __ballot_sync(0xffffffffu, bb.x0 <= xmax && bb.x1 >= xmin && bb.y0 <= ymax && bb.y1 >= ymin &&
                                                      bb.x0 <= bb.x1);
       while (cand) {
@@ -599,13 +601,13 @@ __device__ __forceinline__ unsigned long long candidate_mask(const MarchArgs &ar
         cand &= cand - 1;
         const int x0 = __shfl_sync(0xffffffffu, bb.x0, j), x1 = __shfl_sync(0xffffffffu, bb.x1, j);
         const int y0 = __shfl_sync(0xffffffffu, bb.y0, j), y1 = __shfl_sync(0xffffffffu, bb.y1, j);
-        if (valid && pix_x >= x0 && pix_x <= x1 && pix_y >= y0 && pix_y <= y1) lane_mask |= 1ull << (base + j);
+        if (valid && pix_x >= x0 && pix_x <= x1 && pix_y >= y0 && pix_y <= y1) lane_mask |= 1ull << (base - g0 + j);
       }
     }
   } else if (valid) {
-    for (int k = 0; k < args.n_inst; ++k) {
+    for (int k = g0; k < g1; ++k) {
       const ScreenBox bb = args.cull[k * args.n_cams + cam];
-      if (pix_x >= bb.x0 && pix_x <= bb.x1 && pix_y >= bb.y0 && pix_y <= bb.y1) lane_mask |= 1ull << k;
+      if (pix_x >= bb.x0 && pix_x <= bb.x1 && pix_y >= bb.y0 && pix_y <= bb.y1) lane_mask |= 1ull << (k - g0);
     }
   }
   return lane_mask;
@@ -636,9 +638,10 @@ struct MarchSpan {
   bool noclip;
 };
 
-__device__ __forceinline__ bool prepare_march(const DevInst &I, const DevAsset &A, bool raw_rays, const double ow[3],
-                                              const double dw[3], double o[3], double d[3], double inv[3],
-                                              MarchSpan &sp, unsigned *errors) {
+// (1) per lane: object-space ray and proxy-box slab
+__device__ __forceinline__ bool prepare_slab(const DevInst &I, const DevAsset &A, bool raw_rays, const double ow[3],
+                                             const double dw[3], double o[3], double d[3], double inv[3],
+                                             MarchSpan &sp) {
   if (raw_rays) {
 #pragma unroll
     for (int q = 0; q < 3; ++q) { o[q] = ow[q]; d[q] = dw[q]; }
@@ -649,21 +652,23 @@ __device__ __forceinline__ bool prepare_march(const DevInst &I, const DevAsset &
   sp.t_far = 0.0;
   sp.i_start = 0;
   sp.noclip = false;
-  bool boxhit = slab(A.pmin, A.pmax, o, d, sp.t_near, sp.t_far, inv);
-  if (boxhit && A.mesh.nodes) {          // mesh proxy: march from its first hit
-    const double tm = mesh_first_hit(A.mesh, o, d, errors + kErrBvh);
-    if (tm < 0.0) boxhit = false;
-    else sp.t_near = tm;
-  }
+  return slab(A.pmin, A.pmax, o, d, sp.t_near, sp.t_far, inv);
+}
+
+// (2) per lane, after the (warp-cooperative) mesh first hit
+__device__ __forceinline__ bool prepare_clip(const DevAsset &A, const double o[3], const double d[3],
+                                             const double inv[3], MarchSpan &sp) {
+  bool boxhit = true;
   sp.t_end = sp.t_far;
-  if (boxhit) NOLF_STAT(1, 1);
+  NOLF_STAT(1, 1);
   // Clip the march to the ray's span in the culling box (occupied cells
   // grown by one cell): every sample outside it lies in an empty cell, so
   // starting 2 samples before the entry and stopping 2 after the exit
   // leaves the result bit-identical (empty samples change nothing).
-  if (boxhit && sp.t_near < sp.t_far) {
+  if (sp.t_near < sp.t_far) {
     double ca, cb;
-    if (!slab<true>(A.cull_lo, A.cull_hi, o, d, ca, cb, inv) || A.cull_empty) {
+    double inv_c[3] = {inv[0], inv[1], inv[2]};
+    if (!slab<true>(A.cull_lo, A.cull_hi, o, d, ca, cb, inv_c) || A.cull_empty) {
       boxhit = false;                     // never meets an occupied cell: exact miss
     } else {
       const double f = floor((ca - sp.t_near) * A.inv_step - 2.5);   // 2-sample margins absorb the rounding
@@ -729,7 +734,9 @@ __device__ __forceinline__ HitRec hit_record(const DevAsset &A, const double o[3
 
 // One thread per ray, every candidate instance marched in scene order by
 // that thread (kModeRays / kModeRect, and the march_rays entry point).
-template <int MODE>
+// GROUPS: more than 64 instances (candidate masks per group of 64); the
+// common case compiles without the group loop.
+template <int MODE, bool GROUPS = false>
 __device__ __forceinline__ void march_chunk(const MarchArgs &args, unsigned chunk, bool precull) {
   const long long gid = (long long)chunk * kMarchThreads + threadIdx.x;
   const unsigned lane = threadIdx.x & 31;
@@ -746,12 +753,15 @@ __device__ __forceinline__ void march_chunk(const MarchArgs &args, unsigned chun
   unsigned samples_total = 0;  // per lane (< 2^32: at most n_inst * samples per ray)
   unsigned ordinal = 0;
   // candidates OR-ed over the warp so the instance loop below is
-  // warp-uniform (ascending = scene order, so layer ordinals match)
-  const unsigned long long lane_mask = candidate_mask<MODE>(args, valid, pix_x, pix_y, cam, lane);
+  // warp-uniform (ascending = scene order, so layer ordinals match); in
+  // groups of 64 instances
+  for (int g0 = 0; g0 < (GROUPS ? args.n_inst : 1); g0 += 64) {
+  const unsigned long long lane_mask = candidate_mask<MODE>(args, valid, pix_x, pix_y, cam, lane, g0);
   unsigned long long wmask = ((unsigned long long)__reduce_or_sync(0xffffffffu, (unsigned)(lane_mask >> 32)) << 32) |
                              __reduce_or_sync(0xffffffffu, (unsigned)lane_mask);
   while (wmask) {
-    const int k = __ffsll((long long)wmask) - 1;
+    const int kb = __ffsll((long long)wmask) - 1;
+    const int k = g0 + kb;
     wmask &= wmask - 1;
     const DevInst &I = args.inst[k];
     const DevAsset &A = *I.a;
@@ -760,20 +770,33 @@ __device__ __forceinline__ void march_chunk(const MarchArgs &args, unsigned chun
     double unit = 1.0;
     MarchSpan sp{0.0, 0.0, 0.0, 0, false};
     MarchOut mr{0.0, __longlong_as_double(0x7ff0000000000000ll), 0, false};
-    const bool live = (lane_mask >> k) & 1ull;
+    const bool live = (lane_mask >> kb) & 1ull;
     if (lane == 0) NOLF_STAT(8, 1);
+    bool boxhit = false;
     if (live) {
       NOLF_STAT(0, 1);
       double ow[3], dw[3];     // rebuilt per candidate instead of held across the march
       world_ray<MODE>(args, gid, cam, pix_x, pix_y, ow, dw);
-      if (prepare_march(I, A, args.raw_rays, ow, dw, o, d, inv, sp, args.errors)) {
-        NOLF_STAT(2, 1);
-        float invf[3] = {(float)inv[0], (float)inv[1], (float)inv[2]};
-        unit = to_grid_units(A, o, d, invf);
-        mr = run_march(A, o, d, invf, sp, args.use_zmask);
-        samples_total += (unsigned)mr.samples;
-        hit = mr.hit;
+      boxhit = prepare_slab(I, A, args.raw_rays, ow, dw, o, d, inv, sp);
+    }
+    if (A.mesh.nodes) {        // mesh proxy (warp-uniform: k is): march from its first hit
+#ifdef NOLF_MESH_PER_THREAD
+      const double tm = boxhit ? mesh_first_hit(A.mesh, o, d, args.errors + kErrBvh) : -1.0;
+#else
+      const double tm = mesh_first_hit_warp(A.mesh, o, d, boxhit, args.errors + kErrBvh);
+#endif
+      if (boxhit) {
+        if (tm < 0.0) boxhit = false;
+        else sp.t_near = tm;
       }
+    }
+    if (boxhit && prepare_clip(A, o, d, inv, sp)) {
+      NOLF_STAT(2, 1);
+      float invf[3] = {(float)inv[0], (float)inv[1], (float)inv[2]};
+      unit = to_grid_units(A, o, d, invf);
+      mr = run_march(A, o, d, invf, sp, args.use_zmask);
+      samples_total += (unsigned)mr.samples;
+      hit = mr.hit;
     }
     if (args.out_hit) {        // march_rays outputs (MarchResult, lightfield.py:101-110)
       if (live) {
@@ -810,6 +833,7 @@ __device__ __forceinline__ void march_chunk(const MarchArgs &args, unsigned chun
       }
     }
   }
+  }  // instance groups
   if (MODE == kModeScene && valid) args.nhit[gid] = (uint8_t)ordinal;
   // march_samples counter (lightfield.py:430-431)
   const unsigned warp_samples = __reduce_add_sync(0xffffffffu, samples_total);
@@ -818,10 +842,10 @@ __device__ __forceinline__ void march_chunk(const MarchArgs &args, unsigned chun
 
 // One CTA per 128 slots (rays / rect mode, and scene tiles that are not
 // 128-slot aligned: those pre-cull per CTA).
-template <int MODE>
+template <int MODE, bool GROUPS = false>
 __global__ void __launch_bounds__(kMarchThreads, NOLF_MARCH_MINB) k_march(MarchArgs args) {
   stat_cta_start();
-  march_chunk<MODE>(args, blockIdx.x, true);
+  march_chunk<MODE, GROUPS>(args, blockIdx.x, true);
   stat_cta_end();
 }
 
@@ -886,11 +910,13 @@ __global__ void __launch_bounds__(128) k_cull_chunks(MarchArgs args, long long n
 // host sizes the grid from the live count of an earlier frame (read back
 // asynchronously, never waited for) plus headroom; a grid-stride loop keeps
 // any size correct, and CTAs past the list exit after one load.
+template <bool GROUPS = false>
 __global__ void __launch_bounds__(kMarchThreads, NOLF_MARCH_MINB) k_march_chunks(MarchArgs args) {
   const unsigned n = *args.n_chunks;
   stat_cta_start();
   for (unsigned it = blockIdx.x; it < n; it += gridDim.x)   // normally one pass: the grid is sized
-    march_chunk<kModeScene>(args, chunk_at(args.chunks, args.n_chunks, args.list_stride, it, args.heavy_first), false);
+    march_chunk<kModeScene, GROUPS>(args, chunk_at(args.chunks, args.n_chunks, args.list_stride, it, args.heavy_first),
+                                    false);
   stat_cta_end();
 }
 
@@ -1252,6 +1278,41 @@ __device__ __forceinline__ void compose_px(const ComposeArgs &a, const long long
       oc1 = __dadd_rn(oc1, __dmul_rn(trans, (double)c.y));
       oc2 = __dadd_rn(oc2, __dmul_rn(trans, (double)c.z));
       if (!set && c.w > a.alpha_vis) { od = dk4[r]; set = true; }
+      trans = __dmul_rn(trans, (double)(1.0f - c.w));
+    }
+    o.x = (float)clampd(oc0, 0.0, 1.0);
+    o.y = (float)clampd(oc1, 0.0, 1.0);
+    o.z = (float)clampd(oc2, 0.0, 1.0);
+    o.w = (float)clampd(__dsub_rn(1.0, trans), 0.0, 1.0);
+    if (o.w <= 0.f) {
+      o = make_float4(0.f, 0.f, 0.f, 0.f);
+      od = __int_as_float(0x7f800000);
+    }
+    return;
+  }
+  if (n > kMaxLayers) {        // many layers: stable order by repeated selection, no per-thread arrays
+    double oc0 = 0.0, oc1 = 0.0, oc2 = 0.0, trans = 1.0;
+    bool set = false;
+    float last_d = -__int_as_float(0x7f800000);
+    int last_k = -1;
+    for (int r = 0; r < n; ++r) {
+      // next (depth, index) in lexicographic order after (last_d, last_k)
+      float bd = 0.f;
+      int bk = -1;
+      for (int k = 0; k < n; ++k) {
+        const float dv = a.depth[(long long)k * a.layer_stride + p];
+        const bool after = dv > last_d || (dv == last_d && k > last_k);
+        if (after && (bk < 0 || dv < bd)) { bd = dv; bk = k; }
+      }
+      if (bk < 0) break;
+      last_d = bd;
+      last_k = bk;
+      if (a.nhit && !(bd < __int_as_float(0x7f800000))) break;
+      const float4 c = reinterpret_cast<const float4 *>(a.rgba)[(long long)bk * a.layer_stride + p];
+      oc0 = __dadd_rn(oc0, __dmul_rn(trans, (double)c.x));
+      oc1 = __dadd_rn(oc1, __dmul_rn(trans, (double)c.y));
+      oc2 = __dadd_rn(oc2, __dmul_rn(trans, (double)c.z));
+      if (!set && c.w > a.alpha_vis) { od = bd; set = true; }
       trans = __dmul_rn(trans, (double)(1.0f - c.w));
     }
     o.x = (float)clampd(oc0, 0.0, 1.0);

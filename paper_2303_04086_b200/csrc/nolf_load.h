@@ -50,6 +50,8 @@ class JsonParser {
 
  private:
   const char *p_, *e_;
+  int depth_ = 0;
+  static constexpr int kMaxDepth = 64;     // the meta schema nests 4 deep; bound the recursion
   void ws() {
     while (p_ < e_ && (*p_ == ' ' || *p_ == '\n' || *p_ == '\r' || *p_ == '\t')) ++p_;
   }
@@ -92,6 +94,12 @@ class JsonParser {
     return true;
   }
   bool value(Json &v) {
+    if (++depth_ > kMaxDepth) return false;
+    const bool ok = value_in(v);
+    --depth_;
+    return ok;
+  }
+  bool value_in(Json &v) {
     ws();
     if (p_ >= e_) return false;
     const char c = *p_;

@@ -121,4 +121,71 @@ __device__ __forceinline__ double mesh_first_hit(const DevMesh &M, const double 
   return best;
 }
 
+// Warp-cooperative variant (all 32 lanes call it; `active` lanes have a ray
+// to test): the warp walks ONE node stack (in shared memory, uniform), each
+// node is fetched once per warp and tested against every lane's ray, a
+// subtree is entered when any lane's ray can reach it, and a leaf's
+// triangles are tested by the lanes that reach it, each against its own ray
+// with the same fp64 Moller-Trumbore.  Every lane ends with the minimum t
+// over all triangles its ray hits -- the same value as mesh_first_hit, since
+// pruning only ever skips boxes that cannot hold a closer hit for that lane.
+// Children are pushed in the order most lanes would visit them (near first).
+constexpr int kMeshWarps = 4;          // warps per CTA of the marcher (kMarchThreads / 32)
+
+__device__ __forceinline__ double mesh_first_hit_warp(const DevMesh &M, const double o[3], const double d[3],
+                                                      bool active, unsigned *err_overflow) {
+  __shared__ int s_stack[kMeshWarps][32];
+  const unsigned lane = threadIdx.x & 31;
+  int *stack = s_stack[(threadIdx.x >> 5) & (kMeshWarps - 1)];
+  const float ox = active ? (float)o[0] : 0.f, oy = active ? (float)o[1] : 0.f, oz = active ? (float)o[2] : 0.f;
+  auto rcp = [](double x) { const float f = (float)x; return 1.0f / copysignf(fmaxf(fabsf(f), 1e-30f), f); };
+  const float ix = active ? rcp(d[0]) : 1.f, iy = active ? rcp(d[1]) : 1.f, iz = active ? rcp(d[2]) : 1.f;
+  const float INFF = __int_as_float(0x7f800000);
+  double best = -1.0;
+  float best_f = INFF;
+  if (!__any_sync(0xffffffffu, active && node_entry(M.nodes[0], ox, oy, oz, ix, iy, iz, best_f) != INFF)) return -1.0;
+  if (lane == 0) stack[0] = 0;
+  int sp = 1;                              // warp-uniform
+  __syncwarp();
+  while (sp) {
+    --sp;
+    const int ni = stack[sp];
+    __syncwarp();                          // read before any push below overwrites the slot
+    const BvhNode n = M.nodes[ni];
+    const bool in = active && node_entry(n, ox, oy, oz, ix, iy, iz, best_f) != INFF;
+    if (!__any_sync(0xffffffffu, in)) continue;
+    if (n.count > 0) {
+      if (in) {
+        for (int i = 0; i < n.count; ++i) {
+          const double t = mt_hit(M.tri + 9ll * (n.first + i), o, d);
+          if (t >= 0.0 && (best < 0.0 || t < best)) {
+            best = t;
+            best_f = (float)t;
+          }
+        }
+      }
+    } else if (sp >= 30) {
+      if (lane == 0) atomicAdd(err_overflow, 1u);
+    } else {
+      const BvhNode L = M.nodes[n.first], R = M.nodes[n.first + 1];
+      const float tl = in ? node_entry(L, ox, oy, oz, ix, iy, iz, best_f) : INFF;
+      const float tr = in ? node_entry(R, ox, oy, oz, ix, iy, iz, best_f) : INFF;
+      const bool hl = tl != INFF, hr = tr != INFF;
+      const unsigned bl = __ballot_sync(0xffffffffu, hl), br = __ballot_sync(0xffffffffu, hr);
+      const int votes_l = __popc(__ballot_sync(0xffffffffu, hl && (!hr || tl <= tr)));
+      const int votes_r = __popc(__ballot_sync(0xffffffffu, hr && (!hl || tr < tl)));
+      const int nearc = votes_l >= votes_r ? n.first : n.first + 1, farc = nearc == n.first ? n.first + 1 : n.first;
+      const bool near_hit = nearc == n.first ? bl != 0u : br != 0u;
+      const bool far_hit = farc == n.first ? bl != 0u : br != 0u;
+      if (lane == 0) {
+        if (far_hit) stack[sp] = farc;
+        if (near_hit) stack[sp + (far_hit ? 1 : 0)] = nearc;
+      }
+      sp += (far_hit ? 1 : 0) + (near_hit ? 1 : 0);
+      __syncwarp();
+    }
+  }
+  return best;
+}
+
 }  // namespace nolf

@@ -101,3 +101,32 @@ def test_native_load_renders_like_python_load(name):
     assert outs[0][2][3] > 0                      # samples were marched
     if name == "toy_sphere":
         assert np.isfinite(outs[0][1]).sum() > 0
+
+
+@pytest.mark.parametrize("path,value", [
+    (("density_atlas", "b"), 1 << 20),          # b^3 overflows the cell count
+    (("density_atlas", "r"), 100000),
+    (("density_atlas", "cubes"), 1 << 40),
+    (("psh", "table_size"), 1 << 40),
+    (("psh", "features"), 1 << 33),
+    (("diffuse_encoder", "base_resolution"), 1 << 40),
+    (("specular_mlp", "widths"), [19, 1 << 40, 64, 4]),
+])
+def test_hostile_meta_sizes_are_data_errors(path, value):
+    """Untrusted meta sizes are bounded before any multiplication or
+    allocation: NOLF_EDATA, never an overflowed size or an exception across
+    the C ABI."""
+    import json
+    sec = nolf_io.unpack_sections(_raw())
+    meta = json.loads(sec["meta"])
+    meta[path[0]][path[1]] = value
+    sec["meta"] = json.dumps(meta).encode()
+    rc, err = _load_mem(nolf_io.pack_sections(sec))
+    assert rc == N.NOLF_EDATA, err
+
+
+def test_deeply_nested_meta_is_a_data_error():
+    sec = nolf_io.unpack_sections(_raw())
+    sec["meta"] = b"[" * 100000 + b"]" * 100000
+    rc, err = _load_mem(nolf_io.pack_sections(sec))
+    assert rc == N.NOLF_EDATA, err

@@ -115,3 +115,29 @@ def test_encode_frame_restatement_matches_reference():
     r8, d16 = O.encode_frame(s["rgba"], s["depth"])
     np.testing.assert_array_equal(r8, g["scene_rgba8"])
     np.testing.assert_array_equal(d16, g["scene_depth16"])
+
+
+def test_compose_any_number_of_frames():
+    """farm.compose takes any K (farm.py:129-172): 100 frames with depth
+    ties and inf / zero-alpha layers vs a direct numpy restatement."""
+    rng = np.random.default_rng(9)
+    K, P = 100, 64
+    a = rng.uniform(0, 1, (K, P)).astype(np.float32)
+    a[rng.uniform(size=(K, P)) < 0.3] = 0
+    rgba = np.concatenate([rng.uniform(0, 1, (K, P, 3)).astype(np.float32) * a[..., None], a[..., None]], -1)
+    depth = np.where(a > 0, rng.choice([1.0, 1.5, 2.0], (K, P)), np.inf).astype(np.float32)
+    o, d = O.compose(rgba, depth)
+    for p in range(P):
+        order = np.argsort(depth[:, p], kind="stable")
+        oc, T, od = np.zeros(3), 1.0, np.float32(np.inf)
+        for k in order:
+            oc += T * rgba[k, p, :3].astype(np.float64)
+            if np.isinf(od) and rgba[k, p, 3] > np.float32(0.5):
+                od = depth[k, p]
+            T *= np.float64(np.float32(1.0) - rgba[k, p, 3])
+        want = np.concatenate([np.clip(oc, 0, 1), [np.clip(1 - T, 0, 1)]]).astype(np.float32)
+        if want[3] <= 0:
+            want[:] = 0
+            od = np.float32(np.inf)
+        np.testing.assert_array_equal(o[p], want)
+        assert d[p] == od
