@@ -309,6 +309,17 @@ int nolf_memcpy2d_async(void *dst, size_t dpitch, const void *src, size_t spitch
 int nolf_host_register(void *host_ptr, size_t bytes, void **dev_ptr);
 int nolf_host_unregister(void *host_ptr);
 
+/* protocol.encode_frame (protocol.py:256-279): quantisation of an f32 frame
+ * (DEVICE rgba (n,4) / depth (n)) to rgba8 = clip(round(255 x)) and u16 depth
+ * = round(min(d, far) / far * 65534), 65535 for misses; and ENC_DEFLATE's
+ * zlib stream (HOST, zlib compress2 at `level`, the reference uses 6:
+ * byte-identical to Python's zlib.compress(data, 6) when both use the same
+ * zlib, see nolf_zlib_version).  dst NULL: *dst_len = the size bound. */
+int nolf_encode_frame(const float *rgba, const float *depth, int64_t n, double depth_far, uint8_t *rgba8,
+                      uint16_t *depth16, void *stream);
+int nolf_deflate(const void *src, size_t n, int32_t level, void *dst, size_t *dst_len);
+const char *nolf_zlib_version(void);
+
 /* frames: rgba (K, P, 4) f32, depth (K, P) f32, all device pointers. */
 /* Host side of the sparse frame (NolfSceneOut.pack): writes the n packed
  * chunks (HOST copies of pack / pack_ids) into a row-major encode_frame RAW

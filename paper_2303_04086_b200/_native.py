@@ -112,6 +112,9 @@ def lib():
         "nolf_set_option": ([i32, i64], C.c_int),
         "nolf_last_launch": ([vp], C.c_int),
         "nolf_check_errors": ([vp], C.c_int),
+        "nolf_encode_frame": ([vp, vp, i64, dbl, vp, vp, vp], C.c_int),
+        "nolf_deflate": ([vp, C.c_size_t, i32, vp, C.POINTER(C.c_size_t)], C.c_int),
+        "nolf_zlib_version": ([], C.c_char_p),
         "nolf_host_scatter": ([vp, vp, C.c_uint32, vp, i32, i64, i32, i32, vp, vp, vp, vp, i32], C.c_int),
         "nolf_mlp_eval": ([vp, C.c_int, vp, i64, vp, vp], C.c_int),
         "nolf_device_alloc": ([C.c_size_t, C.POINTER(vp)], C.c_int),

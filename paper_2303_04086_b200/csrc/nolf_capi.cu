@@ -1606,6 +1606,35 @@ int nolf_host_unregister(void *host_ptr) {
   return 0;
 }
 
+int nolf_encode_frame(const float *rgba, const float *depth, int64_t n, double depth_far, uint8_t *rgba8,
+                      uint16_t *depth16, void *stream) {
+  if (n < 0 || !(depth_far > 0.0)) return fail(NOLF_EINVAL, "bad frame encode arguments");
+  if (n == 0) return 0;
+  if (!rgba || !depth || !rgba8 || !depth16) return fail(NOLF_EINVAL, "null buffer");
+  if ((uintptr_t)rgba & 15) return fail(NOLF_EINVAL, "rgba must be 16-byte aligned");
+  const long long blocks = std::min<long long>((n + 255) / 256, (long long)num_sms() * 16);
+  k_encode_frame<<<(unsigned)blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      reinterpret_cast<const float4 *>(rgba), depth, n, (float)depth_far, reinterpret_cast<uchar4 *>(rgba8), depth16);
+  CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+int nolf_deflate(const void *src, size_t n, int32_t level, void *dst, size_t *dst_len) {
+  if ((n && !src) || !dst_len || level < -1 || level > 9) return fail(NOLF_EINVAL, "bad deflate arguments");
+  const size_t bound = compressBound((uLong)n);
+  if (!dst) {
+    *dst_len = bound;
+    return 0;
+  }
+  uLongf out = (uLongf)*dst_len;
+  const int z = compress2(static_cast<Bytef *>(dst), &out, static_cast<const Bytef *>(src), (uLong)n, level);
+  if (z != Z_OK) return fail(z == Z_BUF_ERROR ? NOLF_EINVAL : NOLF_ENOMEM, "zlib compress2 failed (%d)", z);
+  *dst_len = (size_t)out;
+  return 0;
+}
+
+const char *nolf_zlib_version(void) { return zlibVersion(); }
+
 int nolf_compose(int32_t K, int64_t P, const float *rgba, const float *depth, double alpha_vis, float *out_rgba,
                  float *out_depth, void *stream) {
   if (K < 1) return fail(NOLF_EINVAL, "compose needs at least one frame");

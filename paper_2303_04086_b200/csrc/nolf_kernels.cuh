@@ -1375,6 +1375,15 @@ __device__ __forceinline__ uint16_t encode_depth16(const float od, const float f
   return isfinite(od) ? (uint16_t)rintf(fminf(od, far) / far * 65534.0f) : (uint16_t)65535;
 }
 
+// protocol.encode_frame (protocol.py:256-266) of a whole f32 frame.
+__global__ void __launch_bounds__(256) k_encode_frame(const float4 *rgba, const float *depth, long long n,
+                                                      float far, uchar4 *rgba8, uint16_t *depth16) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    rgba8[i] = encode_rgba8(rgba[i]);
+    depth16[i] = encode_depth16(depth[i], far);
+  }
+}
+
 // Output index of slot p (-1 for tile padding).
 __device__ __forceinline__ long long compose_dst(const ComposeArgs &a, const TileParams &tp, long long local,
                                                  long long p) {

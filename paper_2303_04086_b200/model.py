@@ -104,6 +104,24 @@ class Frame:
                    np.full((height, width), DEPTH_MISS, np.float32))
 
 
+# protocol.py:36-37 frame encodings
+ENC_RAW = 0
+ENC_DEFLATE = 1
+
+
+@dataclass
+class FrameData:
+    """protocol.FrameData (protocol.py:71-80): an encoded frame message."""
+    pose_seq: int
+    frame_index: int
+    encoding: int
+    width: int
+    height: int
+    depth_far: float
+    rgba: bytes
+    depth: bytes
+
+
 @dataclass
 class MarchParams:
     step: float

@@ -28,12 +28,12 @@ import numpy as np
 
 from . import _native as N
 from . import errors
-from .model import Frame, RayRange, RenderCounters, Tile, uniform_scale_of
+from .model import ENC_DEFLATE, ENC_RAW, Frame, FrameData, RayRange, RenderCounters, Tile, uniform_scale_of
 
 _torch = None
 
 # Result types; shim.install() swaps in the reference's own Tile / Frame.
-OWN_TYPES = {"Frame": Frame, "Tile": Tile}
+OWN_TYPES = {"Frame": Frame, "Tile": Tile, "FrameData": FrameData}
 TYPES = dict(OWN_TYPES)
 
 
@@ -435,6 +435,40 @@ def compose_device(rgba, depth, alpha_vis: float = 0.5):
                                  float(alpha_vis), out_rgba.data_ptr(), out_depth.data_ptr(),
                                  _stream_ptr()))
     return out_rgba, out_depth
+
+
+def encode_frame(frame, encoding: int = ENC_RAW, depth_far: float = 10.0):
+    """protocol.encode_frame (protocol.py:256-279): rgba8 + u16 depth
+    quantised on the GPU (nolf_encode_frame, the compose epilogue's
+    arithmetic), ENC_DEFLATE streams by zlib level 6 in the library
+    (nolf_deflate) -> the reference's FrameData."""
+    if encoding not in (ENC_RAW, ENC_DEFLATE):
+        raise errors.ProtocolError(f"unknown frame encoding {encoding}")
+    t = torch()
+    dev = _device()
+    h, w = frame.height, frame.width
+    rgba = t.from_numpy(np.ascontiguousarray(frame.rgba, np.float32).reshape(-1, 4)).to(dev)
+    depth = t.from_numpy(np.ascontiguousarray(frame.depth, np.float32).reshape(-1)).to(dev)
+    r8 = t.empty((h * w, 4), dtype=t.uint8, device=dev)
+    d16 = t.empty((h * w,), dtype=t.int16, device=dev)
+    N.check(N.lib().nolf_encode_frame(rgba.data_ptr(), depth.data_ptr(), h * w, float(depth_far), r8.data_ptr(),
+                                      d16.data_ptr(), _stream_ptr()))
+    rgba_b = r8.cpu().numpy().tobytes()
+    depth_b = d16.cpu().numpy().view("<u2").tobytes()
+    if encoding == ENC_DEFLATE:
+        rgba_b, depth_b = deflate(rgba_b), deflate(depth_b)
+    return TYPES["FrameData"](pose_seq=0, frame_index=0, encoding=encoding, width=w, height=h,
+                              depth_far=depth_far, rgba=rgba_b, depth=depth_b)
+
+
+def deflate(data: bytes, level: int = 6) -> bytes:
+    """zlib.compress(data, level) by the library's zlib (nolf_deflate)."""
+    lib = N.lib()
+    cap = C.c_size_t(0)
+    N.check(lib.nolf_deflate(data, len(data), level, None, C.byref(cap)))
+    buf = C.create_string_buffer(cap.value)
+    N.check(lib.nolf_deflate(data, len(data), level, buf, C.byref(cap)))
+    return buf.raw[:cap.value]
 
 
 # ------------------------------------------------------------------ fast path

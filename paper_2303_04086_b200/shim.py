@@ -12,6 +12,8 @@ each binding site is patched explicitly:
                                                  cli.py:137 imports it lazily)
   radfarm.pipeline.render_range                 (pipeline.py:25, used :139)
   radfarm.bench.render_range                    (bench.py:27, used :235)
+  radfarm.protocol.encode_frame                 (protocol.py:256)
+  radfarm.farm.encode_frame                     (bound farm.py:30, used tick :587)
 
 Results are returned as the reference's own ``Tile`` / ``Frame`` classes and
 errors are raised as the reference's own exception classes.
@@ -35,6 +37,8 @@ _BINDINGS = [
     ("radfarm.farm", "compose", render.compose),
     ("radfarm.pipeline", "render_range", render.render_range),
     ("radfarm.bench", "render_range", render.render_range),
+    ("radfarm.protocol", "encode_frame", render.encode_frame),
+    ("radfarm.farm", "encode_frame", render.encode_frame),
 ]
 
 
@@ -48,6 +52,7 @@ def install() -> list:
     rend = importlib.import_module("radfarm.renderer")
     render.TYPES["Frame"] = core.Frame
     render.TYPES["Tile"] = rend.Tile
+    render.TYPES["FrameData"] = importlib.import_module("radfarm.protocol").FrameData
     done = []
     for mod_name, attr, fn in _BINDINGS:
         mod = importlib.import_module(mod_name)

@@ -19,7 +19,7 @@ REF = "/root/reference/pkg/src"
 sys.path.insert(0, REF)
 
 from radfarm.core import Frame  # noqa: E402
-from radfarm.protocol import encode_frame  # noqa: E402
+from radfarm.protocol import ENC_DEFLATE, encode_frame  # noqa: E402
 
 
 def enc(rgba, depth, far=10.0):
@@ -39,8 +39,16 @@ def main():
     depth[::5, ::3] = np.inf
     depth[1, :4] = [0.0, 10.0, 10.5, 5.0]
     r8, r16 = enc(rgba, depth)
+    # ENC_DEFLATE (protocol.py:265-267): the zlib streams themselves
+    h, w = g["depth"].shape
+    fz = encode_frame(Frame(width=w, height=h, rgba=g["rgba"], depth=g["depth"]), ENC_DEFLATE)
+    sz = encode_frame(Frame(width=16, height=16, rgba=rgba, depth=depth), ENC_DEFLATE, 7.5)
     np.savez_compressed(os.path.join(HERE, "encode.npz"), scene_rgba8=s8, scene_depth16=s16,
-                        syn_rgba=rgba, syn_depth=depth, syn_rgba8=r8, syn_depth16=r16)
+                        syn_rgba=rgba, syn_depth=depth, syn_rgba8=r8, syn_depth16=r16,
+                        scene_deflate_rgba=np.frombuffer(fz.rgba, np.uint8),
+                        scene_deflate_depth=np.frombuffer(fz.depth, np.uint8),
+                        syn_deflate_rgba=np.frombuffer(sz.rgba, np.uint8),
+                        syn_deflate_depth=np.frombuffer(sz.depth, np.uint8))
     print("done")
 
 

@@ -429,3 +429,20 @@ def test_more_than_32_cameras_in_one_launch():
         r.render([cams[c]], torch.from_numpy(t1).to(r.device), 1, 1024, one, frame_layout=True)
         np.testing.assert_array_equal(allf[c], one["rgba8"][:1024].cpu().numpy().reshape(32, 32, 4))
     r.check()
+
+
+def test_encode_frame_vs_reference():
+    """render.encode_frame (protocol.encode_frame, protocol.py:256-279), RAW
+    and ENC_DEFLATE, byte-equal to the reference's messages (encode.npz)."""
+    from paper_2303_04086_b200.model import ENC_DEFLATE, ENC_RAW
+    g, _ = _scene()
+    enc = load("encode.npz")
+    h, w = g["depth"].shape
+    fr = Frame(width=w, height=h, rgba=g["rgba"], depth=g["depth"])
+    raw = R.encode_frame(fr, ENC_RAW)
+    assert raw.rgba == enc["scene_rgba8"].tobytes() and raw.depth == enc["scene_depth16"].astype("<u2").tobytes()
+    z = R.encode_frame(fr, ENC_DEFLATE)
+    assert z.encoding == ENC_DEFLATE and z.rgba == enc["scene_deflate_rgba"].tobytes()
+    assert z.depth == enc["scene_deflate_depth"].tobytes()
+    syn = R.encode_frame(Frame(width=16, height=16, rgba=enc["syn_rgba"], depth=enc["syn_depth"]), ENC_DEFLATE, 7.5)
+    assert syn.rgba == enc["syn_deflate_rgba"].tobytes() and syn.depth == enc["syn_deflate_depth"].tobytes()

@@ -40,3 +40,23 @@ def test_invalid_arguments_fail_loudly_without_gpu():
     rc = lib.nolf_compose(0, 10, None, None, 0.5, None, None, None)
     assert rc == _native.NOLF_EINVAL
     assert b"at least one frame" in lib.nolf_last_error()
+
+
+def test_deflate_matches_python_zlib():
+    """nolf_deflate (ENC_DEFLATE, protocol.py:265-267) == zlib.compress(x, 6)
+    byte for byte when the library's zlib is the interpreter's."""
+    import zlib
+    import numpy as np
+    from paper_2303_04086_b200 import render
+    from golden_util import load
+    lib = _native.lib()
+    if lib.nolf_zlib_version().decode() != zlib.ZLIB_RUNTIME_VERSION:
+        import pytest
+        pytest.skip("different zlib builds")
+    g = load("encode.npz")
+    for key in ("scene_rgba8", "scene_depth16", "syn_rgba8"):
+        raw = np.ascontiguousarray(g[key]).tobytes()
+        assert render.deflate(raw) == zlib.compress(raw, 6)
+    assert render.deflate(np.ascontiguousarray(g["scene_rgba8"]).tobytes()) == g["scene_deflate_rgba"].tobytes()
+    assert render.deflate(np.ascontiguousarray(g["scene_depth16"]).astype("<u2").tobytes()) == \
+        g["scene_deflate_depth"].tobytes()

@@ -23,7 +23,11 @@ def test_install_rebinds_every_call_site():
         orig = radfarm.farm.compose
         done = shim.install()
         try:
-            assert len(done) == 9
+            assert len(done) == 11
+            import radfarm.protocol
+            assert radfarm.protocol.encode_frame is render.encode_frame
+            assert radfarm.farm.encode_frame is render.encode_frame
+            assert render.TYPES["FrameData"] is radfarm.protocol.FrameData
             assert radfarm.renderer.render_rays is render.render_rays
             assert radfarm.lightfield.render_rays is render.render_rays
             assert radfarm.farm.render_range is render.render_range
