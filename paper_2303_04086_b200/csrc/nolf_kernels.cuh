@@ -503,6 +503,130 @@ __device__ __forceinline__ MarchOut march_p2(const DevAsset &A, const double oG[
   return r;
 }
 
+// march_p2 with warp-uniform PHASES.  The lanes of a warp march different
+// rays; in march_p2 every warp iteration executes the union of the paths its
+// lanes take (jump estimate + verification, occupied-sample addressing, the
+// trilinear + exp evaluation) -- nearly always all of them.  Here each lane
+// computes its current sample's cell, then the warp runs ONE path per
+// iteration: the jump path while any lane sits in an empty cell, otherwise
+// the occupied-sample path; the other lanes keep their state and recompute
+// the same sample next iteration.  The samples each ray visits, and so its
+// result, are exactly march_p2's (each lane's sequence of decisions is
+// unchanged; only the interleaving across lanes differs).  Warp-collective.
+__device__ __forceinline__ double grid_pos_rt(const double oG[3], const double dG[3], double t_mid, double G, int k,
+                                              bool noclip) {
+  const double v = __dadd_rn(oG[k], __dmul_rn(t_mid, dG[k]));
+  return noclip ? v : (v < 0.0 ? 0.0 : (v > G ? G : v));
+}
+
+__device__ __forceinline__ MarchOut march_p2s(const DevAsset &A, const double oG[3], const double dG[3],
+                                              const float invG[3], double t_near, double t_far, bool use_zmask,
+                                              int i_start, double t_end, bool active, bool noclip) {
+  MarchOut r;
+  r.alpha_c = 0.0;
+  r.t_hit = __longlong_as_double(0x7ff0000000000000ll);
+  r.samples = 0;
+  r.hit = false;
+  bool live = active && t_near < t_far;
+  const DevAtlas &at = A.den;
+  const double delta = A.step;
+  const int b = at.b, lr = at.lr;
+  const int Gi = b << lr;
+  const double G = (double)Gi;
+  const double t_lim = fmin(t_far, t_end);
+  double best_w = 0.0, trans = 1.0, alpha_c = 0.0, t_hit = r.t_hit;
+  int samples = 0;
+  int i = i_start;
+  double ti = (double)i_start + 0.5;          // i + 0.5, exact
+  for (;;) {
+    // this lane's current sample (lanes that are done carry no work)
+    const double t_mid = __dadd_rn(t_near, __dmul_rn(ti, delta));
+    if (live && !(t_mid < t_lim)) live = false;
+    double xg[3];
+    int gi[3], cell[3], dist = 0, ci = 0;
+    if (live) {
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        xg[k] = grid_pos_rt(oG, dG, t_mid, G, k, noclip);
+        gi[k] = floor_grid(xg[k]);
+        cell[k] = min(gi[k] >> lr, b - 1);
+      }
+      ci = (cell[0] * b + cell[1]) * b + cell[2];
+      dist = __ldg(at.dist + ci);
+    }
+    const bool want_jump = live && dist > 0;
+    const unsigned jumpers = __ballot_sync(0xffffffffu, want_jump);
+    if (!__any_sync(0xffffffffu, live)) break;
+    NOLF_STAT(7, 1);
+    if (jumpers) {             // ---- jump phase: only lanes in empty cells move
+      if (want_jump) {
+        NOLF_STAT(3, 1);
+        int lo_c[3], hi_c[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          lo_c[k] = max(cell[k] - (dist - 1), 0);
+          hi_c[k] = min(cell[k] + (dist - 1), b - 1);
+        }
+        float te = __int_as_float(0x7f800000);
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          const float ok = (float)oG[k];
+          if (invG[k] > 0.f && hi_c[k] < b - 1) te = fminf(te, ((float)((hi_c[k] + 1) << lr) - ok) * invG[k]);
+          else if (invG[k] < 0.f && lo_c[k] > 0) te = fminf(te, ((float)(lo_c[k] << lr) - ok) * invG[k]);
+        }
+        const float jf = floorf((fminf(te, (float)t_lim) - (float)t_near) * A.inv_step_f - 0.5f);
+        int j = jf > 2.0e9f ? 2000000000 : (int)jf;
+        int next = i + 1;
+        for (int attempt = 0; attempt < 2 && j > i; ++attempt, --j) {
+          const double tj = __dadd_rn(t_near, __dmul_rn((double)j + 0.5, delta));
+          bool inside = tj < t_lim;
+#pragma unroll
+          for (int k = 0; k < 3; ++k) {
+            const int cj = min(floor_grid(grid_pos_rt(oG, dG, tj, G, k, noclip)) >> lr, b - 1);
+            inside = inside && cj >= lo_c[k] && cj <= hi_c[k];
+          }
+          if (inside) { next = j + 1; break; }
+        }
+        ti = next == i + 1 ? ti + 1.0 : (double)next + 0.5;
+        i = next;
+      }
+      continue;
+    }
+    // ---- sample phase: every live lane is in an occupied cell
+    if (live) {
+      const int cid = __ldg(at.index + ci);
+      int base[3];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) base[k] = min(gi[k] - (cell[k] << lr), at.r - 1);   // gi == G: base r-1
+      ++samples;
+      const int bit = (((base[0] << lr) + base[1]) << lr) + base[2];
+      bool stop = false;
+      if (!(use_zmask && ((__ldg(at.zmask + (unsigned)(cid * at.zwords + (bit >> 5))) >> (bit & 31)) & 1u))) {
+        NOLF_STAT(6, 1);
+        double frac[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) frac[k] = gi[k] >= Gi ? 1.0 : frac_grid(xg[k]);
+        float s;
+        atlas_trilinear_at<1>(at, cid, base, frac, &s);
+        const double sigma = (double)s;
+        const double absorb = exp(__dmul_rn(-sigma, delta));
+        const double w = __dmul_rn(trans, __dsub_rn(1.0, absorb));
+        if (w > best_w) { best_w = w; t_hit = t_mid; }
+        alpha_c = __dadd_rn(alpha_c, w);
+        trans = __dmul_rn(trans, absorb);
+        stop = !(trans > t_stop_of(A));
+      }
+      if (stop) live = false;
+      else { ++i; ti += 1.0; }
+    }
+  }
+  r.alpha_c = alpha_c;
+  r.samples = samples;
+  r.hit = alpha_c > A.alpha_floor;
+  r.t_hit = r.hit ? t_hit : __longlong_as_double(0x7ff0000000000000ll);
+  return r;
+}
+
 #ifndef NOLF_MARCH_MINB
 #define NOLF_MARCH_MINB 8  // latency-bound: 50% occupancy beats the spills it costs (measured 4..8)
 #endif
@@ -790,7 +914,24 @@ __device__ __forceinline__ void march_chunk(const MarchArgs &args, unsigned chun
         else sp.t_near = tm;
       }
     }
-    if (boxhit && prepare_clip(A, o, d, inv, sp)) {
+    const bool go = boxhit && prepare_clip(A, o, d, inv, sp);
+#ifdef NOLF_MARCH_PHASED
+    float invf[3] = {0.f, 0.f, 0.f};
+    if (go) {
+      NOLF_STAT(2, 1);
+      invf[0] = (float)inv[0]; invf[1] = (float)inv[1]; invf[2] = (float)inv[2];
+      unit = to_grid_units(A, o, d, invf);
+    }
+    if (A.den.lr >= 0)         // warp-uniform (the instance is): phased, warp-collective march
+      mr = march_p2s(A, o, d, invf, sp.t_near, sp.t_far, args.use_zmask, sp.i_start, sp.t_end, go, sp.noclip);
+    else if (go)
+      mr = run_march(A, o, d, invf, sp, args.use_zmask);
+    if (go) {
+      samples_total += (unsigned)mr.samples;
+      hit = mr.hit;
+    }
+#else
+    if (go) {
       NOLF_STAT(2, 1);
       float invf[3] = {(float)inv[0], (float)inv[1], (float)inv[2]};
       unit = to_grid_units(A, o, d, invf);
@@ -798,6 +939,7 @@ __device__ __forceinline__ void march_chunk(const MarchArgs &args, unsigned chun
       samples_total += (unsigned)mr.samples;
       hit = mr.hit;
     }
+#endif
     if (args.out_hit) {        // march_rays outputs (MarchResult, lightfield.py:101-110)
       if (live) {
         args.out_hit[gid] = hit ? 1 : 0;
