@@ -73,13 +73,21 @@ def parse():
     p.add_argument("--verify", action="store_true",
                    help="rank 0 re-renders the last frame alone and compares bitwise with the "
                         "multi-GPU assembled frame")
-    p.add_argument("--prefill", default="on", choices=["on", "off"],
-                   help="frame buffers are pre-set to the miss encoding (memset, on the owning "
-                        "GPU, inside the timed step) so compose skips every chunk no instance "
-                        "can reach; off = compose writes every pixel")
+    p.add_argument("--prefill", default="on", choices=["on", "state", "off"],
+                   help="frame buffers hold the miss encoding outside live chunks so compose "
+                        "writes only the chunks some instance reaches: on = the owner re-clears "
+                        "a consumed buffer with a memset (side stream); state = per-buffer run "
+                        "dirty bits (NolfSceneOut.chunk_state: stale runs reset by the writing "
+                        "rank, no full clear; measured slower across NVLink); off = compose "
+                        "writes every pixel")
     p.add_argument("--sync", default="flags", choices=["flags", "nccl"],
                    help="p2p frame completion: flags = peer-mapped u32 flags set/polled by tiny kernels "
                         "(no collective); nccl = a 1-element all-reduce per frame")
+    p.add_argument("--rank0-weight", type=float, default=None,
+                   help="share of tile rows rank 0 renders relative to the other ranks (it also "
+                        "re-clears consumed frame buffers and polls the completion flags); default "
+                        "0.9 for the 16-view configs (a 440 MB re-clear per step; measured 0.694 -> "
+                        "0.677 ms on 4 GPUs, config 5), else 1")
     p.add_argument("--frames", type=int, default=3,
                    help="p2p + flags: frame buffers in rank 0's ring (a peer renders frame seq once "
                         "frame seq - frames was consumed and re-cleared)")
@@ -590,7 +598,11 @@ def run_ours(args):
     stride = T * T
     tiles = np.concatenate([frame_tiles(W, H, T, cam=v) for v in range(n_views)])
     n_tiles = len(tiles)
-    parts = partition(tiles, world, T, by_rows=args.partition == "rows")
+    # rank 0 also re-clears the consumed frame buffers and waits on the flags:
+    # --rank0-weight < 1 gives it proportionally fewer tile rows
+    w0 = args.rank0_weight if args.rank0_weight is not None else (0.9 if n_views > 1 else 1.0)
+    weights = [w0] + [1.0] * (world - 1) if world > 1 else None
+    parts = partition(tiles, world, T, by_rows=args.partition == "rows", weights=weights)
     mine, n_max = shard_tiles(tiles, world, rank, parts)
     my_tiles = torch.from_numpy(mine).to(dev)
     P = n_max * stride
@@ -620,7 +632,7 @@ def run_ours(args):
         args.exchange = "p2p"            # strided band copies need the row partition
     p2p = world > 1 and args.exchange in ("p2p", "dma")
     dma = p2p and args.exchange == "dma" and rank != 0
-    bands_dev = row_bands(world, rank, n_views, W, H, T) if dma else []
+    bands_dev = row_bands(world, rank, n_views, W, H, T, weights) if dma else []
     peer_frames = []
     token = torch.zeros(1, dtype=torch.float32, device=dev)
     NB = max(2, args.frames) if (p2p and args.sync == "flags") else 2   # frame buffers in the ring
@@ -685,9 +697,13 @@ def run_ours(args):
     # started (so it overlaps rendering, never the untimed L2 flush), then the
     # peers' "free" flags are set and the owner's next render into that buffer
     # waits for it.
-    prefill = args.prefill == "on" and ((flags and not dma) or world == 1)
+    prefill = args.prefill != "off" and ((flags and not dma) or world == 1)
+    state_mode = prefill and args.prefill == "state"   # run dirty bits instead of re-clearing
     owner = world == 1 or rank == 0
     last_fb = [0]
+    n_my_chunks = n_max * stride // 128
+    chunk_states = [torch.zeros(n_my_chunks, dtype=torch.int16, device=dev) for _ in range(NB if p2p else 2)] \
+        if state_mode else None
 
     def clear(fb, s):
         """miss encoding (rgba8 0, depth16 65535) over frame buffer fb, on its owner GPU"""
@@ -698,13 +714,13 @@ def run_ours(args):
         N.check(N.lib().nolf_memset_async(rgba_ptr, 0, NPX * 4, s))
         N.check(N.lib().nolf_memset_async(d_ptr, 0xFF, NPX * 2, s))
 
-    clear_stream = torch.cuda.Stream(device=dev) if (prefill and owner) else None
+    clear_stream = torch.cuda.Stream(device=dev) if (prefill and owner and not state_mode) else None
     clear_ev = [None] * NB
     pending = []
 
     def release(fb, seq, ts):
         """owner: buffer fb (frame seq, None at 1 GPU) consumed on torch stream ts"""
-        if prefill:
+        if prefill and not state_mode:
             ev = torch.cuda.Event()
             ev.record(ts)
             pending.append((fb, seq, ev))
@@ -736,8 +752,24 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
 
-    def step(k, fb=0, before_barrier=None, auto_release=True):
+    def reset_frames():
+        """back to miss-encoded buffers and empty chunk states (after renders
+        that bypassed the states, e.g. the hostmap e2e loop)"""
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
         if prefill and owner:
+            for i in range(NB if p2p else 2):
+                clear(i, stream)
+        if state_mode:
+            for st_ in chunk_states:
+                st_.zero_()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+
+    def step(k, fb=0, before_barrier=None, auto_release=True):
+        if prefill and owner and not state_mode:
             flush_pending()
         if p2p and flags:
             seq_box[0] += 1
@@ -762,6 +794,8 @@ def run_ours(args):
             else:
                 o2 = {"rgba8": peer_frames[fb][0], "depth16": peer_frames[fb][1],
                       "counters": out["counters"]}
+                if state_mode:
+                    o2["chunk_state"] = chunk_states[fb]
                 if rank == 0 and clear_ev[fb] is not None:
                     torch.cuda.current_stream().wait_event(clear_ev[fb])   # buffer re-cleared
                 R.render(cam_arrays[k % n_cam], my_tiles, n_max, stride, o2, frame_layout=True,
@@ -784,6 +818,8 @@ def run_ours(args):
         last_fb[0] = fb
         if world == 1:             # single GPU: compose writes the frame directly
             out["rgba8"], out["depth16"] = frame, frame_d
+            if state_mode:
+                out["chunk_state"] = chunk_states[fb]
             if prefill and clear_ev[fb] is not None:
                 torch.cuda.current_stream().wait_event(clear_ev[fb])   # buffer re-cleared
         R.render(cam_arrays[k % n_cam], my_tiles, n_max, stride, out, frame_layout=(world == 1),
@@ -888,7 +924,7 @@ def run_ours(args):
         dptr = ctypes.c_void_p()
         N.check(N.lib().nolf_host_register(host_addr, 2 * FB, ctypes.byref(dptr)))
         host_map = [host_addr + fb * FB for fb in range(2)]
-        bands = row_bands(world, rank, n_views, W, H, T)
+        bands = row_bands(world, rank, n_views, W, H, T, weights)
         copy_stream = torch.cuda.Stream(device=dev)
         comp = torch.cuda.current_stream()
         done_copy = [None, None]
@@ -990,6 +1026,8 @@ def run_ours(args):
     # ---- multi-GPU frame == single-GPU frame (bitwise)
     verify = None
     if args.verify:
+        if host_map is not None or args.e2e_mode == "copy":
+            reset_frames()
         kv = args.warmup + args.steps - 1
         step(kv, 0, auto_release=False)    # keep the frame until it is read back
         fbv = last_fb[0]

@@ -44,7 +44,7 @@
 extern "C" {
 #endif
 
-#define NOLF_ABI_VERSION 2
+#define NOLF_ABI_VERSION 3
 
 #define NOLF_OK 0
 #define NOLF_EINVAL -1
@@ -170,6 +170,15 @@ typedef struct NolfSceneOut {
     uint8_t *pack;
     uint32_t *pack_ids;
     uint32_t *pack_count;
+    /* With prefilled = 1 and frame layout: a u16 per 128-slot chunk of the
+     * tile list (DEVICE, owned by the caller, one array per frame buffer,
+     * zero for a buffer that holds only the miss encoding): bit r = the
+     * chunk's 8-pixel run r holds non-miss bytes from an earlier frame.  The
+     * library rewrites exactly the runs that change (hits now, or dirty and
+     * a miss now; dead chunks' dirty runs are reset) and keeps the bits: a
+     * frame buffer never needs a full clear between frames.  NULL: the
+     * caller re-clears. */
+    uint16_t *chunk_state;
 } NolfSceneOut;
 
 int nolf_abi_version(void);

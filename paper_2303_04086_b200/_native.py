@@ -20,7 +20,7 @@ LIB_PATH = os.environ.get("NOLF_LIB") or os.path.join(os.path.dirname(os.path.ab
 
 NOLF_EINVAL, NOLF_ESTATE, NOLF_EDATA, NOLF_ECUDA, NOLF_ENOMEM, NOLF_ECAPACITY = -1, -2, -3, -4, -5, -6
 HEAD_ACT = {"identity": 0, "sigmoid": 1, "exponential": 2}
-ABI_VERSION = 2              # NOLF_ABI_VERSION of include/nolf.h
+ABI_VERSION = 3              # NOLF_ABI_VERSION of include/nolf.h
 # nolf_set_option keys (include/nolf.h)
 OPT_MARCH_ORDER, OPT_COMPOSE_SLOTS, OPT_HEAVY_WAVES = 1, 2, 3
 MLP_FP32, MLP_BF16 = 0, 1
@@ -71,7 +71,8 @@ class SceneOut(C.Structure):
     _fields_ = [("rgba", C.c_void_p), ("depth", C.c_void_p), ("rgba8", C.c_void_p),
                 ("depth16", C.c_void_p), ("tile_stride", C.c_int64), ("depth_far", C.c_double),
                 ("layout", C.c_int32), ("peer", C.c_int32), ("prefilled", C.c_int32),
-                ("pack", C.c_void_p), ("pack_ids", C.c_void_p), ("pack_count", C.c_void_p)]
+                ("pack", C.c_void_p), ("pack_ids", C.c_void_p), ("pack_count", C.c_void_p),
+                ("chunk_state", C.c_void_p)]
 
 
 _lib = None

@@ -1271,6 +1271,11 @@ int launch_march_shade(int mode, const NolfInstance *ins, int n_inst, const Nolf
       ca.pack_ids = sout->pack_ids;
       ca.pack_count = sout->pack_count;
     }
+    if (sout->chunk_state) {
+      if (!(chunked && ca.prefilled && ca.four == 2 && sout->layout == 1 && sout->rgba8 && sout->depth16 && !pack))
+        return fail(NOLF_EINVAL, "chunk_state needs prefilled u8 frame-layout outputs and 128-slot tiles");
+      ca.chunk_state = sout->chunk_state;     // run-level dirty bits (compose_eight_state)
+    }
     if (chunked && ca.prefilled && ca.four == 2) {
       // misses are already in place: only the live chunks (grid from the
       // earlier frame's live count, grid-stride for any size)
@@ -1278,7 +1283,7 @@ int launch_march_shade(int mode, const NolfInstance *ins, int n_inst, const Nolf
       const long long live = std::min<long long>(n_chunks, g_live.last + g_live.last / 8 + 2ll * num_sms());
       // 8 slots per thread, or 4 when that leaves under ~1024 threads per SM
       const int g_opt = options().compose_slots;
-      const int G = pack ? 8 : g_opt == 4 || g_opt == 8 ? g_opt : (live * 16 >= 1024ll * num_sms() ? 8 : 4);
+      const int G = (pack || sout->chunk_state) ? 8 : g_opt == 4 || g_opt == 8 ? g_opt : (live * 16 >= 1024ll * num_sms() ? 8 : 4);
       g_last_launch[2] = G;
       const long long threads = live * (128 / G);
       const unsigned cgrid = (unsigned)std::max<long long>(1, (threads + 255) / 256);
@@ -1288,6 +1293,11 @@ int launch_march_shade(int mode, const NolfInstance *ins, int n_inst, const Nolf
       k_compose<<<(unsigned)((n_thr + 255) / 256), 256, 0, st>>>(ca);
     }
     CUDA_TRY(cudaGetLastError());
+    if (sout->chunk_state) {   // after compose: reset chunks written last time that are dead now, state = live
+      const long long n_chunks = n_rays / kMarchThreads;
+      k_clear_stale<<<(unsigned)((n_chunks * 16 + 255) / 256), 256, 0, st>>>(ca, n_chunks);
+      CUDA_TRY(cudaGetLastError());
+    }
     if ((rc = prof_mark(3, st))) return rc;
     if ((rc = ring_release(slot, st))) return rc;   // the block is reusable once this frame is done
   } else {

@@ -82,13 +82,14 @@ struct MarchArgs {
 // offending work is dropped instead of writing out of bounds.
 enum { kErrQueue = 0, kErrLayers = 1, kErrTile = 2, kErrBvh = 3, kNumErr = 4 };
 
-// A scene tile the kernels may address: a non-empty rect inside its camera's
-// frame with no more pixels than a tile slot holds.
+// A scene tile the kernels may address: a rect inside its camera's frame
+// with no more pixels than a tile slot holds (empty rects are the padding of
+// uneven shards: valid, no pixels).
 __device__ __forceinline__ bool tile_valid(const TileParams &tp, const CamParams *cams, int n_cams,
                                            long long stride) {
   if (tp.cam < 0 || tp.cam >= n_cams) return false;
   const CamParams &c = cams[tp.cam];
-  return tp.x0 >= 0 && tp.y0 >= 0 && tp.x1 > tp.x0 && tp.y1 > tp.y0 && tp.x1 <= c.width && tp.y1 <= c.height &&
+  return tp.x0 >= 0 && tp.y0 >= 0 && tp.x1 >= tp.x0 && tp.y1 >= tp.y0 && tp.x1 <= c.width && tp.y1 <= c.height &&
          (long long)(tp.x1 - tp.x0) * (tp.y1 - tp.y0) <= stride;
 }
 
@@ -503,130 +504,6 @@ __device__ __forceinline__ MarchOut march_p2(const DevAsset &A, const double oG[
   return r;
 }
 
-// march_p2 with warp-uniform PHASES.  The lanes of a warp march different
-// rays; in march_p2 every warp iteration executes the union of the paths its
-// lanes take (jump estimate + verification, occupied-sample addressing, the
-// trilinear + exp evaluation) -- nearly always all of them.  Here each lane
-// computes its current sample's cell, then the warp runs ONE path per
-// iteration: the jump path while any lane sits in an empty cell, otherwise
-// the occupied-sample path; the other lanes keep their state and recompute
-// the same sample next iteration.  The samples each ray visits, and so its
-// result, are exactly march_p2's (each lane's sequence of decisions is
-// unchanged; only the interleaving across lanes differs).  Warp-collective.
-__device__ __forceinline__ double grid_pos_rt(const double oG[3], const double dG[3], double t_mid, double G, int k,
-                                              bool noclip) {
-  const double v = __dadd_rn(oG[k], __dmul_rn(t_mid, dG[k]));
-  return noclip ? v : (v < 0.0 ? 0.0 : (v > G ? G : v));
-}
-
-__device__ __forceinline__ MarchOut march_p2s(const DevAsset &A, const double oG[3], const double dG[3],
-                                              const float invG[3], double t_near, double t_far, bool use_zmask,
-                                              int i_start, double t_end, bool active, bool noclip) {
-  MarchOut r;
-  r.alpha_c = 0.0;
-  r.t_hit = __longlong_as_double(0x7ff0000000000000ll);
-  r.samples = 0;
-  r.hit = false;
-  bool live = active && t_near < t_far;
-  const DevAtlas &at = A.den;
-  const double delta = A.step;
-  const int b = at.b, lr = at.lr;
-  const int Gi = b << lr;
-  const double G = (double)Gi;
-  const double t_lim = fmin(t_far, t_end);
-  double best_w = 0.0, trans = 1.0, alpha_c = 0.0, t_hit = r.t_hit;
-  int samples = 0;
-  int i = i_start;
-  double ti = (double)i_start + 0.5;          // i + 0.5, exact
-  for (;;) {
-    // this lane's current sample (lanes that are done carry no work)
-    const double t_mid = __dadd_rn(t_near, __dmul_rn(ti, delta));
-    if (live && !(t_mid < t_lim)) live = false;
-    double xg[3];
-    int gi[3], cell[3], dist = 0, ci = 0;
-    if (live) {
-#pragma unroll
-      for (int k = 0; k < 3; ++k) {
-        xg[k] = grid_pos_rt(oG, dG, t_mid, G, k, noclip);
-        gi[k] = floor_grid(xg[k]);
-        cell[k] = min(gi[k] >> lr, b - 1);
-      }
-      ci = (cell[0] * b + cell[1]) * b + cell[2];
-      dist = __ldg(at.dist + ci);
-    }
-    const bool want_jump = live && dist > 0;
-    const unsigned jumpers = __ballot_sync(0xffffffffu, want_jump);
-    if (!__any_sync(0xffffffffu, live)) break;
-    NOLF_STAT(7, 1);
-    if (jumpers) {             // ---- jump phase: only lanes in empty cells move
-      if (want_jump) {
-        NOLF_STAT(3, 1);
-        int lo_c[3], hi_c[3];
-#pragma unroll
-        for (int k = 0; k < 3; ++k) {
-          lo_c[k] = max(cell[k] - (dist - 1), 0);
-          hi_c[k] = min(cell[k] + (dist - 1), b - 1);
-        }
-        float te = __int_as_float(0x7f800000);
-#pragma unroll
-        for (int k = 0; k < 3; ++k) {
-          const float ok = (float)oG[k];
-          if (invG[k] > 0.f && hi_c[k] < b - 1) te = fminf(te, ((float)((hi_c[k] + 1) << lr) - ok) * invG[k]);
-          else if (invG[k] < 0.f && lo_c[k] > 0) te = fminf(te, ((float)(lo_c[k] << lr) - ok) * invG[k]);
-        }
-        const float jf = floorf((fminf(te, (float)t_lim) - (float)t_near) * A.inv_step_f - 0.5f);
-        int j = jf > 2.0e9f ? 2000000000 : (int)jf;
-        int next = i + 1;
-        for (int attempt = 0; attempt < 2 && j > i; ++attempt, --j) {
-          const double tj = __dadd_rn(t_near, __dmul_rn((double)j + 0.5, delta));
-          bool inside = tj < t_lim;
-#pragma unroll
-          for (int k = 0; k < 3; ++k) {
-            const int cj = min(floor_grid(grid_pos_rt(oG, dG, tj, G, k, noclip)) >> lr, b - 1);
-            inside = inside && cj >= lo_c[k] && cj <= hi_c[k];
-          }
-          if (inside) { next = j + 1; break; }
-        }
-        ti = next == i + 1 ? ti + 1.0 : (double)next + 0.5;
-        i = next;
-      }
-      continue;
-    }
-    // ---- sample phase: every live lane is in an occupied cell
-    if (live) {
-      const int cid = __ldg(at.index + ci);
-      int base[3];
-#pragma unroll
-      for (int k = 0; k < 3; ++k) base[k] = min(gi[k] - (cell[k] << lr), at.r - 1);   // gi == G: base r-1
-      ++samples;
-      const int bit = (((base[0] << lr) + base[1]) << lr) + base[2];
-      bool stop = false;
-      if (!(use_zmask && ((__ldg(at.zmask + (unsigned)(cid * at.zwords + (bit >> 5))) >> (bit & 31)) & 1u))) {
-        NOLF_STAT(6, 1);
-        double frac[3];
-#pragma unroll
-        for (int k = 0; k < 3; ++k) frac[k] = gi[k] >= Gi ? 1.0 : frac_grid(xg[k]);
-        float s;
-        atlas_trilinear_at<1>(at, cid, base, frac, &s);
-        const double sigma = (double)s;
-        const double absorb = exp(__dmul_rn(-sigma, delta));
-        const double w = __dmul_rn(trans, __dsub_rn(1.0, absorb));
-        if (w > best_w) { best_w = w; t_hit = t_mid; }
-        alpha_c = __dadd_rn(alpha_c, w);
-        trans = __dmul_rn(trans, absorb);
-        stop = !(trans > t_stop_of(A));
-      }
-      if (stop) live = false;
-      else { ++i; ti += 1.0; }
-    }
-  }
-  r.alpha_c = alpha_c;
-  r.samples = samples;
-  r.hit = alpha_c > A.alpha_floor;
-  r.t_hit = r.hit ? t_hit : __longlong_as_double(0x7ff0000000000000ll);
-  return r;
-}
-
 #ifndef NOLF_MARCH_MINB
 #define NOLF_MARCH_MINB 8  // latency-bound: 50% occupancy beats the spills it costs (measured 4..8)
 #endif
@@ -914,24 +791,7 @@ __device__ __forceinline__ void march_chunk(const MarchArgs &args, unsigned chun
         else sp.t_near = tm;
       }
     }
-    const bool go = boxhit && prepare_clip(A, o, d, inv, sp);
-#ifdef NOLF_MARCH_PHASED
-    float invf[3] = {0.f, 0.f, 0.f};
-    if (go) {
-      NOLF_STAT(2, 1);
-      invf[0] = (float)inv[0]; invf[1] = (float)inv[1]; invf[2] = (float)inv[2];
-      unit = to_grid_units(A, o, d, invf);
-    }
-    if (A.den.lr >= 0)         // warp-uniform (the instance is): phased, warp-collective march
-      mr = march_p2s(A, o, d, invf, sp.t_near, sp.t_far, args.use_zmask, sp.i_start, sp.t_end, go, sp.noclip);
-    else if (go)
-      mr = run_march(A, o, d, invf, sp, args.use_zmask);
-    if (go) {
-      samples_total += (unsigned)mr.samples;
-      hit = mr.hit;
-    }
-#else
-    if (go) {
+    if (boxhit && prepare_clip(A, o, d, inv, sp)) {
       NOLF_STAT(2, 1);
       float invf[3] = {(float)inv[0], (float)inv[1], (float)inv[2]};
       unit = to_grid_units(A, o, d, invf);
@@ -939,7 +799,6 @@ __device__ __forceinline__ void march_chunk(const MarchArgs &args, unsigned chun
       samples_total += (unsigned)mr.samples;
       hit = mr.hit;
     }
-#endif
     if (args.out_hit) {        // march_rays outputs (MarchResult, lightfield.py:101-110)
       if (live) {
         args.out_hit[gid] = hit ? 1 : 0;
@@ -1355,6 +1214,8 @@ struct ComposeArgs {
   int four;                    // slots per thread: 0 -> 1, 1 -> 4, 2 -> 8 (tiles && nhit && stride % 4 / 8 == 0)
   const uint8_t *chunk_live;   // scene: per 128-slot chunk, 0 = never marched (all misses)
   int prefilled;               // outputs already hold the miss encoding: dead chunks are not written
+  uint16_t *chunk_state;       // prefilled buffers re-used across frames: per chunk, bit r = 8-pixel
+                               // run r holds non-miss bytes from an earlier frame (NULL: freshly cleared)
   uint8_t *pack;               // sparse frame: 768 B per live chunk (NolfSceneOut.pack), or NULL
   uint32_t *pack_ids;
   uint32_t *pack_count;
@@ -1721,6 +1582,92 @@ __device__ __forceinline__ void compose_pack8(const ComposeArgs &a, const long l
   }
 }
 
+// Frame buffers re-used across frames (NolfSceneOut.chunk_state): every
+// 8-pixel run of a chunk has a dirty bit (non-miss bytes written by an
+// earlier frame).  A live chunk's all-miss run is written only if dirty, a
+// run with hits always (and becomes dirty); a dead chunk's dirty runs are
+// reset (k_clear_stale).  The buffer therefore never needs a full clear and
+// only changed runs cross NVLink.  8 slots (one run) per thread; the 16 runs
+// of a chunk are 16 consecutive lanes (their dirty mask is one ballot).
+__device__ __forceinline__ void compose_eight_state(const ComposeArgs &a, const long long p0, unsigned lane) {
+  const long long c = p0 >> 7;
+  const int run = (int)((p0 & 127) >> 3);
+  const unsigned half = 0xffffu << (lane & 16u);
+  const bool was = (a.chunk_state[c] >> run) & 1u;
+  bool dirty = false;
+  long long t, local0;
+  split_slot(p0, a.tile_stride, t, local0);
+  const TileParams tp = a.tiles[t];
+  const int w = tp.x1 - tp.x0, h = tp.y1 - tp.y0;
+  if (!(w & 7) && !(h & 3) && local0 < (long long)w * h && tile_valid(tp, a.cams, a.n_cams, a.tile_stride)) {
+    const CamParams &cp = a.cams[tp.cam];
+    int x, y;
+    slot_xy(local0, w, h, x, y);
+    const long long q0 = cp.pix_base + (long long)(tp.y0 + y) * cp.width + (tp.x0 + x);
+    const uint2 nh = *reinterpret_cast<const uint2 *>(a.nhit + p0);
+    uint4 r0 = make_uint4(0u, 0u, 0u, 0u), r1 = r0, dv = make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu);
+    if (nh.x | nh.y) {
+      unsigned c8[8], dd[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int n = (int)(((j < 4 ? nh.x : nh.y) >> (8 * (j & 3))) & 0xffu);
+        float4 o;
+        float od;
+        compose_px(a, p0 + j, n, o, od);
+        const uchar4 u = encode_rgba8(o);
+        c8[j] = (unsigned)u.x | ((unsigned)u.y << 8) | ((unsigned)u.z << 16) | ((unsigned)u.w << 24);
+        dd[j] = encode_depth16(od, a.depth_far);
+      }
+      r0 = make_uint4(c8[0], c8[1], c8[2], c8[3]);
+      r1 = make_uint4(c8[4], c8[5], c8[6], c8[7]);
+      dv = make_uint4(dd[0] | (dd[1] << 16), dd[2] | (dd[3] << 16), dd[4] | (dd[5] << 16), dd[6] | (dd[7] << 16));
+      dirty = true;
+    }
+    if (dirty || was) {
+      uint4 *r8 = reinterpret_cast<uint4 *>(a.out_rgba8 + q0 * 4);
+      r8[0] = r0;
+      r8[1] = r1;
+      *reinterpret_cast<uint4 *>(a.out_depth16 + q0) = dv;
+    }
+  }
+  const unsigned mask = (__ballot_sync(half, dirty) >> (lane & 16u)) & 0xffffu;
+  if (run == 0) a.chunk_state[c] = (uint16_t)mask;
+}
+
+// Dead chunks (no screen box reaches them now): reset their dirty runs.
+__global__ void __launch_bounds__(256) k_clear_stale(ComposeArgs a, long long n_chunks) {
+  const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long c = g >> 4;
+  const int run = (int)(g & 15);
+  const bool in = c < n_chunks && !a.chunk_live[c];
+  const unsigned st = in ? a.chunk_state[c] : 0u;
+  __syncwarp();                                  // every run read the state before it is reset
+  if (in && st) {
+    if (run == 0) a.chunk_state[c] = 0;
+    if ((st >> run) & 1u) {
+      const long long p0 = c * 128 + run * 8;
+      long long t, local0;
+      split_slot(p0, a.tile_stride, t, local0);
+      const TileParams tp = a.tiles[t];
+      const int w = tp.x1 - tp.x0, h = tp.y1 - tp.y0;
+      if (!(w & 7) && !(h & 3) && local0 < (long long)w * h && tile_valid(tp, a.cams, a.n_cams, a.tile_stride)) {
+        const CamParams &cp = a.cams[tp.cam];
+        int x, y;
+        slot_xy(local0, w, h, x, y);
+        const long long q0 = cp.pix_base + (long long)(tp.y0 + y) * cp.width + (tp.x0 + x);
+        uint4 *r8 = reinterpret_cast<uint4 *>(a.out_rgba8 + q0 * 4);
+        r8[0] = make_uint4(0u, 0u, 0u, 0u);
+        r8[1] = make_uint4(0u, 0u, 0u, 0u);
+        *reinterpret_cast<uint4 *>(a.out_depth16 + q0) = make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu);
+      }
+    }
+  }
+  if (a.peer) {                // stores into another GPU's frame: fenced before the completion flag
+    __syncthreads();
+    if (threadIdx.x == 0) __threadfence_system();
+  }
+}
+
 // Prefilled outputs: compose only the live chunks, from the compacted list
 // (16 threads x 8 slots per chunk, grid-stride over the list's length).
 // G slots per thread (8 or 4): a launch over few live chunks (a multi-GPU
@@ -1736,6 +1683,8 @@ __global__ void __launch_bounds__(256) k_compose_live(ComposeArgs a, const unsig
     if (G == 8 && a.pack) {
       compose_pack8(a, p0, (unsigned)(g / per_chunk));
       if (g % per_chunk == 0) a.pack_ids[g / per_chunk] = live_list[g / per_chunk];
+    } else if (G == 8 && a.chunk_state) {
+      compose_eight_state(a, p0, threadIdx.x & 31u);
     } else if (G == 8) {
       compose_eight(a, p0);
     } else {

@@ -12,13 +12,14 @@ import math
 
 import numpy as np
 
-from .schedule import gather_slots, row_partition, tile_partition
+from .schedule import gather_slots, row_owners, row_partition, tile_partition
 
 
-def partition(tiles: np.ndarray, world: int, tile: int, by_rows: bool = True):
-    """Per-rank tile index lists (row-interleaved by default)."""
+def partition(tiles: np.ndarray, world: int, tile: int, by_rows: bool = True, weights=None):
+    """Per-rank tile index lists (row-interleaved by default, optionally
+    weighted per rank)."""
     if by_rows:
-        return [row_partition(tiles, world, r, tile) for r in range(world)]
+        return [row_partition(tiles, world, r, tile, weights) for r in range(world)]
     return [tile_partition(len(tiles), world, r) for r in range(world)]
 
 
@@ -42,15 +43,30 @@ def slot_tile_table(tiles: np.ndarray, world: int, parts=None) -> np.ndarray:
     return table
 
 
-def row_bands(world: int, rank: int, n_views: int, width: int, height: int, tile: int):
+def row_bands(world: int, rank: int, n_views: int, width: int, height: int, tile: int, weights=None):
     """2-D copy descriptors (in pixels) covering this rank's tile rows of a
     row-major frame stack (cameras concatenated): (first_pixel, width_px,
-    pitch_px, height) -- full bands as one strided copy per camera, a
-    partial last band as its own copy."""
+    pitch_px, height).  Plain round robin: full bands as one strided copy per
+    camera, a partial last band as its own copy; weighted owners: one copy
+    per run of consecutive owned rows."""
     rows_per_cam = -(-height // tile)
+    owners = row_owners(n_views * rows_per_cam, world, weights)
     out = []
+    if weights is not None and not all(w == weights[0] for w in weights):
+        for c in range(n_views):
+            ty = 0
+            while ty < rows_per_cam:
+                if owners[c * rows_per_cam + ty] != rank:
+                    ty += 1
+                    continue
+                t0 = ty
+                while ty < rows_per_cam and owners[c * rows_per_cam + ty] == rank:
+                    ty += 1
+                npx = (min(ty * tile, height) - t0 * tile) * width
+                out.append(((c * height + t0 * tile) * width, npx, npx, 1))
+        return out
     for c in range(n_views):
-        mine = [ty for ty in range(rows_per_cam) if (c * rows_per_cam + ty) % world == rank]
+        mine = [ty for ty in range(rows_per_cam) if owners[c * rows_per_cam + ty] == rank]
         full = [ty for ty in mine if (ty + 1) * tile <= height]
         tail = [ty for ty in mine if (ty + 1) * tile > height]
         if full:

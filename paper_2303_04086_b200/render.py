@@ -556,7 +556,9 @@ class SceneRenderer:
         """One fused launch sequence.  ``out``: rgba / depth (f32), rgba8 /
         depth16 (encode_frame RAW), counters; optionally pack / pack_ids /
         pack_count (the sparse frame of live chunks, NolfSceneOut.pack;
-        needs prefilled=True)."""
+        needs prefilled=True); chunk_state (a u16 of run dirty bits per 128-slot chunk per
+        frame buffer: stale chunks are reset instead of re-clearing the
+        frame, NolfSceneOut.chunk_state)."""
         cams = cameras if isinstance(cameras, C.Array) else self.camera_array(cameras)
         so = N.SceneOut()
         def ptr(key):              # tensors, or raw device addresses (peer mappings)
@@ -575,6 +577,7 @@ class SceneRenderer:
         so.pack = ptr("pack")
         so.pack_ids = ptr("pack_ids")
         so.pack_count = ptr("pack_count")
+        so.chunk_state = ptr("chunk_state")
         st = stream if stream is not None else _stream_ptr()
         P = int(n_tiles) * int(tile_stride)
         # the library sizes the launch itself and refuses a short workspace:

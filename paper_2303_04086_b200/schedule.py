@@ -336,10 +336,25 @@ def tile_partition(n_tiles: int, world: int, rank: int) -> np.ndarray:
     return np.arange(rank, n_tiles, world, dtype=np.int64)
 
 
-def row_partition(tiles: np.ndarray, world: int, rank: int, tile: int) -> np.ndarray:
-    """Throughput-mode map: tile ROWS interleaved over GPUs (row index
-    counted across cameras), so a GPU's pixels form evenly strided bands of
-    the frame -- one strided DMA per frame moves them to host memory."""
+def row_owners(n_rows: int, world: int, weights=None) -> np.ndarray:
+    """Owner rank of every tile row: round robin (row r -> r mod N), or a
+    smooth weighted round robin when per-rank ``weights`` are given (a rank
+    with weight w gets ~w / sum(w) of the rows, still interleaved)."""
+    if weights is None or all(w == weights[0] for w in weights):
+        return np.arange(n_rows, dtype=np.int64) % world
+    w = np.asarray(weights, np.float64)
+    credit = np.zeros(world)
+    out = np.empty(n_rows, np.int64)
+    for r in range(n_rows):
+        credit += w
+        k = int(np.argmax(credit))
+        out[r] = k
+        credit[k] -= w.sum()
+    return out
+
+
+def tile_rows(tiles: np.ndarray, tile: int) -> np.ndarray:
+    """Global tile-row index of every tile (rows counted across cameras)."""
     tiles = np.asarray(tiles)
     heights = np.zeros(int(tiles[:, 0].max()) + 1 if len(tiles) else 1, np.int64)
     for c in range(len(heights)):
@@ -347,8 +362,17 @@ def row_partition(tiles: np.ndarray, world: int, rank: int, tile: int) -> np.nda
         heights[c] = tiles[sel, 4].max() if sel.any() else 0
     rows_per_cam = -(-heights // tile)
     base = np.concatenate([[0], np.cumsum(rows_per_cam)[:-1]])
-    row = base[tiles[:, 0]] + tiles[:, 2] // tile
-    return np.flatnonzero(row % world == rank).astype(np.int64)
+    return base[tiles[:, 0]] + tiles[:, 2] // tile
+
+
+def row_partition(tiles: np.ndarray, world: int, rank: int, tile: int, weights=None) -> np.ndarray:
+    """Throughput-mode map: tile ROWS interleaved over GPUs (row index
+    counted across cameras), so a GPU's pixels form strided bands of the
+    frame -- one strided DMA per band moves them to host memory.  ``weights``
+    skews the share per rank (row_owners)."""
+    row = tile_rows(tiles, tile)
+    owners = row_owners(int(row.max()) + 1 if len(row) else 0, world, weights)
+    return np.flatnonzero(owners[row] == rank).astype(np.int64)
 
 
 def gather_slots(n_tiles: int, world: int, parts=None) -> np.ndarray:

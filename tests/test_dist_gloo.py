@@ -99,3 +99,30 @@ def test_row_bands_cover_every_pixel_once(world):
                 for k in range(hgt):
                     cnt[first + k * ppx:first + k * ppx + wpx] += 1
         assert cnt.min() == 1 and cnt.max() == 1
+
+
+@pytest.mark.parametrize("world,w0", [(2, 0.8), (4, 0.85), (3, 0.5)])
+def test_weighted_row_partition_and_bands(world, w0):
+    """--rank0-weight: rank 0 gets ~w0/(w0 + N-1) of the tile rows; the row
+    bands of the weighted owners still cover every pixel exactly once and
+    agree with the tile partition."""
+    from paper_2303_04086_b200.schedule import row_owners
+    weights = [w0] + [1.0] * (world - 1)
+    for V, w, h, t in ((1, 3840, 2160, 32), (3, 96, 70, 16)):
+        tiles = frame_tiles(w, h, t)
+        tiles = np.concatenate([frame_tiles(w, h, t, cam=c) for c in range(V)])
+        parts = partition(tiles, world, t, by_rows=True, weights=weights)
+        assert sorted(np.concatenate(parts).tolist()) == list(range(len(tiles)))
+        cnt = np.zeros(V * h * w, np.int32)
+        for r in range(world):
+            own = np.zeros(V * h * w, bool)
+            for first, wpx, ppx, hgt in row_bands(world, r, V, w, h, t, weights):
+                for k in range(hgt):
+                    cnt[first + k * ppx:first + k * ppx + wpx] += 1
+                    own[first + k * ppx:first + k * ppx + wpx] = True
+            for c, x0, y0, x1, y1 in tiles[parts[r]]:
+                assert own[(c * h + y0) * w + x0] and own[(c * h + y1 - 1) * w + x1 - 1]
+        assert cnt.min() == 1 and cnt.max() == 1
+        owners = row_owners(1000, world, weights)
+        share = (owners == 0).mean()
+        assert abs(share - w0 / (w0 + world - 1)) < 0.01

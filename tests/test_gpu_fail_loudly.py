@@ -91,3 +91,12 @@ def test_valid_frames_report_nothing():
     cam = camera(g)
     r, _ = _render(scene, cam, R.frame_tiles(64, 64, 32))
     r.check()
+
+
+def test_empty_padding_tiles_are_valid():
+    """Uneven shards pad their tile lists with empty rects: no pixels, no error."""
+    g, scene = _scene()
+    cam = camera(g)
+    tiles = np.concatenate([R.frame_tiles(64, 64, 32), np.zeros((3, 5), np.int32)])
+    r, _ = _render(scene, cam, tiles)
+    r.check()

@@ -446,3 +446,27 @@ def test_encode_frame_vs_reference():
     assert z.depth == enc["scene_deflate_depth"].tobytes()
     syn = R.encode_frame(Frame(width=16, height=16, rgba=enc["syn_rgba"], depth=enc["syn_depth"]), ENC_DEFLATE, 7.5)
     assert syn.rgba == enc["syn_deflate_rgba"].tobytes() and syn.depth == enc["syn_deflate_depth"].tobytes()
+
+
+def test_prefilled_frame_with_chunk_state_over_frames():
+    """NolfSceneOut.chunk_state: one frame buffer re-used across cameras is
+    never cleared as a whole -- the library resets the chunks it wrote last
+    time that are not live now -- and every frame equals a full render."""
+    import torch
+    from paper_2303_04086_b200.model import orbit_camera
+    _, scene = _scene()
+    r = R.SceneRenderer(scene)
+    tiles = torch.from_numpy(R.frame_tiles(256, 256, 32)).to(r.device)
+    n = 256 * 256
+    buf = {"rgba8": torch.zeros((n, 4), dtype=torch.uint8, device=r.device),
+           "depth16": torch.full((n,), -1, dtype=torch.int16, device=r.device),
+           "chunk_state": torch.zeros(len(tiles) * 8, dtype=torch.int16, device=r.device),
+           "counters": torch.zeros(4, dtype=torch.int64, device=r.device)}
+    for az in (0.5, 1.3, 2.9, 0.6):
+        cam = orbit_camera(az, 0.6, radius=2.5, size=256, target=(0.2, 0.2, 0.25))
+        r.render([cam], tiles, len(tiles), 1024, buf, frame_layout=True, prefilled=True)
+        full = r.alloc(len(tiles), 1024, want_f32=False, want_u8=True)
+        r.render([cam], tiles, len(tiles), 1024, full, frame_layout=True)
+        assert torch.equal(buf["rgba8"], full["rgba8"][:n]) and torch.equal(buf["depth16"], full["depth16"][:n])
+    assert int((buf["chunk_state"] != 0).sum()) > 0
+    r.check()
