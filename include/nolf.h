@@ -329,6 +329,29 @@ int nolf_encode_frame(const float *rgba, const float *depth, int64_t n, double d
 int nolf_deflate(const void *src, size_t n, int32_t level, void *dst, size_t *dst_len);
 const char *nolf_zlib_version(void);
 
+/* Stage-2 training step (lightfield.train_light_field, lightfield.py:654-749,
+ * after the frozen march).  Trainable tensors live in one flat DEVICE f32
+ * buffer `params` in the reference layouts (W (out, in) row-major), at the
+ * float offsets `offsets` (HOST, NOLF_TRAIN_OFFSETS entries): psh features
+ * (m,F); specular W0,b0,W1,b1,W2,b2; diffuse W0,b0,W1,b1; hash-grid level
+ * features (rows_l, F) for l < 16.  `grads` (DEVICE f64, same layout) is
+ * ACCUMULATED (zero it first).  For n hit rays (p_h, alpha_c, object-space
+ * dirs; targets rgb (n,3) / alpha (n) f32; `batch` = rays in the batch b):
+ * shade_batch with the live diffuse network, the loss |c - rgb|^2 +
+ * (alpha - alpha_t)^2 (loss, pred = (c, alpha)), d = 2 err / b and
+ * shade_backward (MLP weight / bias gradients, psh_backward and
+ * hashgrid_backward scatters).  *nonfinite |= 1 on a non-finite loss. */
+#define NOLF_TRAIN_OFFSETS 27
+int nolf_train_shade(nolf_asset_t asset, const float *params, const int64_t *offsets, double *grads, int64_t n,
+                     const double *p_h, const double *alpha_c, const double *dirs, const float *rgb,
+                     const float *alpha_t, double batch, float *pred, double *loss, uint32_t *nonfinite,
+                     void *stream);
+/* adam_step (neural.py:162-177) on n DEVICE params with f64 gradients (used
+ * as f32), in the reference's f32 arithmetic; step = the group's step count
+ * after increment.  *nonfinite |= 2 on a non-finite gradient (TrainingError). */
+int nolf_adam(float *param, const double *grad, float *m, float *v, int64_t n, double lr, double beta1,
+              double beta2, double eps, int64_t step, uint32_t *nonfinite, void *stream);
+
 /* frames: rgba (K, P, 4) f32, depth (K, P) f32, all device pointers. */
 /* Host side of the sparse frame (NolfSceneOut.pack): writes the n packed
  * chunks (HOST copies of pack / pack_ids) into a row-major encode_frame RAW

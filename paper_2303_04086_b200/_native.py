@@ -116,6 +116,8 @@ def lib():
         "nolf_encode_frame": ([vp, vp, i64, dbl, vp, vp, vp], C.c_int),
         "nolf_deflate": ([vp, C.c_size_t, i32, vp, C.POINTER(C.c_size_t)], C.c_int),
         "nolf_zlib_version": ([], C.c_char_p),
+        "nolf_train_shade": ([vp, vp, vp, vp, i64, vp, vp, vp, vp, vp, dbl, vp, vp, vp, vp], C.c_int),
+        "nolf_adam": ([vp, vp, vp, vp, i64, dbl, dbl, dbl, dbl, i64, vp, vp], C.c_int),
         "nolf_host_scatter": ([vp, vp, C.c_uint32, vp, i32, i64, i32, i32, vp, vp, vp, vp, i32], C.c_int),
         "nolf_mlp_eval": ([vp, C.c_int, vp, i64, vp, vp], C.c_int),
         "nolf_device_alloc": ([C.c_size_t, C.POINTER(vp)], C.c_int),

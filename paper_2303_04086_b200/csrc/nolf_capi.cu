@@ -15,6 +15,7 @@
 #include "nolf_load.h"
 #include "nolf_shade_tc.cuh"
 #include "nolf_host.h"
+#include "nolf_train.cuh"
 
 using namespace nolf;
 
@@ -1923,5 +1924,56 @@ extern "C" int nolf_host_scatter(const uint8_t *pack, const uint32_t *ids, uint3
   if (rc) return fail(NOLF_EDATA, "sparse frame: tile of a packed chunk is not in the 8x4-block layout");
   memcpy(prev_ids, ids, sizeof(uint32_t) * n);
   *prev_n = n;
+  return 0;
+}
+
+// ---------------------------------------------------------------- stage-2 training step
+extern "C" int nolf_train_shade(nolf_asset_t asset, const float *params, const int64_t *offsets, double *grads,
+                                int64_t n, const double *p_h, const double *alpha_c, const double *dirs,
+                                const float *rgb, const float *alpha_t, double batch, float *pred, double *loss,
+                                uint32_t *nonfinite, void *stream) {
+  if (!asset || !params || !offsets || !grads || !nonfinite) return fail(NOLF_EINVAL, "null argument");
+  if (n < 0 || !(batch > 0.0)) return fail(NOLF_EINVAL, "bad batch");
+  if (n == 0) return 0;
+  if (!p_h || !alpha_c || !dirs || !rgb || !alpha_t || !pred || !loss) return fail(NOLF_EINVAL, "null buffer");
+  const DevAsset &H = asset->host;
+  if (H.fs.n_layers != 3 || (H.use_diffuse_color && (!H.fd.params || H.fd.n_layers != 2)))
+    return fail(NOLF_EINVAL, "training needs a 3-layer specular and a 2-layer diffuse network");
+  TrainArgs a{};
+  a.asset = asset->dev;
+  a.params = params;
+  a.grads = grads;
+  for (int i = 0; i < kTpCount; ++i) a.L.off[i] = offsets[i];
+  a.fs_in = H.fs.in;
+  a.fd_in = H.fd.params ? H.fd.in : 0;
+  a.p_h = p_h;
+  a.alpha_c = alpha_c;
+  a.dirs = dirs;
+  a.rgb = rgb;
+  a.alpha_t = alpha_t;
+  a.n = n;
+  a.batch = batch;
+  a.pred = pred;
+  a.loss = loss;
+  a.nonfinite = reinterpret_cast<unsigned *>(nonfinite);
+  const size_t smem = sizeof(double) * (size_t)train_smem(a.fs_in, a.fd_in).total;
+  CUDA_TRY(cudaFuncSetAttribute(k_train_shade, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k_train_shade<<<(unsigned)((n + 127) / 128), 128, smem, static_cast<cudaStream_t>(stream)>>>(a);
+  CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+extern "C" int nolf_adam(float *param, const double *grad, float *m, float *v, int64_t n, double lr, double beta1,
+                         double beta2, double eps, int64_t step, uint32_t *nonfinite, void *stream) {
+  if (!param || !grad || !m || !v || !nonfinite || n < 0 || step < 1) return fail(NOLF_EINVAL, "bad adam arguments");
+  if (n == 0) return 0;
+  // neural.py:167-177: c1 = 1 - beta1**t, c2 = 1 - beta2**t in f64; every
+  // scalar enters the f32 arithmetic rounded to f32 (numpy weak scalars)
+  const double c1 = 1.0 - pow(beta1, (double)step), c2 = 1.0 - pow(beta2, (double)step);
+  const long long blocks = std::min<long long>((n + 255) / 256, (long long)num_sms() * 16);
+  k_adam<<<(unsigned)blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      param, grad, m, v, n, (float)lr, (float)beta1, (float)beta2, (float)(1.0 - beta1), (float)(1.0 - beta2),
+      (float)c1, (float)c2, (float)eps, reinterpret_cast<unsigned *>(nonfinite));
+  CUDA_TRY(cudaGetLastError());
   return 0;
 }
