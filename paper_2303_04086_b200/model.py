@@ -207,6 +207,10 @@ class Mlp:
     def input_dim(self) -> int:
         return self.weights[0].shape[1]
 
+    def parameters(self) -> list:
+        """neural.Mlp.parameters (neural.py:65-66): weights then biases."""
+        return list(self.weights) + list(self.biases)
+
 
 @dataclass
 class LightFieldAsset:
