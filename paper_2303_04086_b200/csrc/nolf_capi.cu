@@ -687,6 +687,12 @@ int nolf_asset_create(const NolfAssetDesc *d, int device, nolf_asset_t *out) {
       for (int i = 0; i < in; ++i) put(0, o, i, d->specular.w[0][o * in + i]);
     for (int o = 0; o < 64; ++o)
       for (int i = 0; i < 64; ++i) put(kTcW0 / 2, o, i, d->specular.w[1][o * 64 + i]);
+    // W2 (4 x 64) as a 16-row operand (rows 4..15 zero): core matrix (g, c) at c*256 + g*128
+    for (int o = 0; o < 4; ++o)
+      for (int i = 0; i < 64; ++i) {
+        const size_t off = (size_t)(i >> 3) * 256 + (size_t)(o >> 3) * 128 + (o & 7) * 16 + (i & 7) * 2;
+        wt[(kTcW0 + kTcW1) / 2 + off / 2] = bf16(d->specular.w[2][o * 64 + i]);
+      }
     // the shader's shared-memory image after the bf16 weights: the fp32
     // block (b0, b1, W2 hidden-major [o][4], b2) and the PSH residue tables
     // when they fit, so one TMA bulk copy stages all of it
@@ -968,7 +974,7 @@ int run_shade(const DevInst *inst, const long long *qoff, int n_inst, const Work
     const int threads = 128 * kShadeTG;
     const int by_regs = 65536 / (((regs + 7) / 8 * 8) * threads);
     const int by_smem = (int)((227u * 1024u) / (smem + static_smem + 1024u));
-    const int by_tmem = 512 / (64 * kShadeTG);
+    const int by_tmem = 512 / (kTcCols * kShadeTG);
     const int per_sm = std::max(1, std::min(std::min(by_regs, by_smem), by_tmem));
     k_shade_tc<kShadeTG><<<num_sms() * per_sm, threads, smem, st>>>(sa);
   } else {

@@ -12,8 +12,9 @@
 //     one thread; tcgen05.commit arrives on an mbarrier; the 4 warps read
 //     their 32 TMEM lanes back with tcgen05.ld (bias + ReLU in fp32, H1
 //     re-quantised to bf16 as the next A operand).
-//   * Layer 2 [64->4] + heads + the c = c_d + t*c_s combine run in fp32 on
-//     CUDA cores in the epilogue (N=4 is too narrow for an MMA).
+//   * Layer 2 [64->4] is a third tcgen05.mma with W2 zero-padded to N = 16
+//     (TMEM columns 64..79); heads + the c = c_d + t*c_s combine run in fp32
+//     in the epilogue (-DNOLF_SHADE_L2_FP32: layer 2 on the CUDA cores).
 // Numerics: bf16 inputs/weights, fp32 accumulation -> north-star tolerance
 // 2/255 (lightfield.py:632-637 network, lightfield.py:291-336 combine).
 #pragma once
@@ -27,7 +28,13 @@ constexpr int kTcK0 = 32;                    // layer-0 K padded (inputs <= 32)
 constexpr uint32_t kTcA = 16384;             // A tile: 128 x 64 bf16
 constexpr uint32_t kTcW0 = 64 * kTcK0 * 2;   // 4 KB
 constexpr uint32_t kTcW1 = 64 * 64 * 2;      // 8 KB
-constexpr uint32_t kTcWBytes = kTcW0 + kTcW1;
+constexpr uint32_t kTcW2 = 16 * 64 * 2;      // 2 KB: W2 (4 x 64) zero-padded to N = 16 rows
+constexpr uint32_t kTcWBytes = kTcW0 + kTcW1 + kTcW2;
+#ifndef NOLF_SHADE_L2_FP32
+constexpr int kTcCols = 128;                 // TMEM columns per tile group: hidden (64) + layer 2 (16)
+#else
+constexpr int kTcCols = 64;
+#endif
 constexpr int kTcF32 = 64 + 64 + 4 * 64 + 4; // b0, b1, W2, b2
 #ifndef NOLF_TC_PHIMAX
 #define NOLF_TC_PHIMAX (64 * 1024)
@@ -100,6 +107,58 @@ __device__ __forceinline__ void tc_mlp_rows(uint8_t *A, const uint8_t *W, const 
   tc::mbar_wait(bar, phase);
   phase ^= 1;
   tc::tc_fence_after();
+#ifndef NOLF_SHADE_L2_FP32
+  // ---- layer 2 on the tensor cores too: H2 = relu(D + b1) re-quantised as
+  // the A operand, D2[128 x 16] = H2 * W2p^T (W2 zero-padded to 16 rows)
+#pragma unroll
+  for (int c4 = 0; c4 < 4; ++c4) {
+    uint32_t r[16];
+    tc::tmem_ld16(trow + 16 * c4, r);
+#pragma unroll
+    for (int hcol = 0; hcol < 2; ++hcol) {
+      const int c = 2 * c4 + hcol;
+      const float4 bA = tc::lds128(fpa + 256 + 32 * c), bB = tc::lds128(fpa + 256 + 32 * c + 16);
+      const float bb[8] = {bA.x, bA.y, bA.z, bA.w, bB.x, bB.y, bB.z, bB.w};
+      float v[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const float z = __uint_as_float(r[8 * hcol + e]) + bb[e];
+        v[e] = z > 0.f ? z : 0.f;
+      }
+      uint4 q;
+      q.x = tc::pack_bf16(v[0], v[1]);
+      q.y = tc::pack_bf16(v[2], v[3]);
+      q.z = tc::pack_bf16(v[4], v[5]);
+      q.w = tc::pack_bf16(v[6], v[7]);
+      tc::sts128(rowa + c * 2048, q);
+    }
+  }
+  tc::tc_fence_before();
+  tc::fence_async_smem();
+  tc::bar_sync(bar_id, 128);
+  if (gt == 0) {
+    tc::tc_fence_after();
+    constexpr uint32_t idesc2 = tc::idesc_bf16_f32(128, 16);
+    const uint32_t aW2 = aW1 + kTcW1;
+#pragma unroll
+    for (int s = 0; s < 4; ++s)
+      tc::umma_bf16(tmem + 64, tc::smem_desc(aA + s * 2 * 2048, 2048, 128), tc::smem_desc(aW2 + s * 2 * 256, 256, 128),
+                    idesc2, s > 0);
+    tc::umma_commit(bar);
+  }
+  tc::mbar_wait(bar, phase);
+  phase ^= 1;
+  tc::tc_fence_after();
+  uint32_t r4[4];
+  tc::tmem_ld4(trow + 64, r4);
+  tc::tc_fence_before();
+  const float4 b2 = tc::lds128(fpa + 1536);
+  out4[0] = __uint_as_float(r4[0]) + b2.x;
+  out4[1] = __uint_as_float(r4[1]) + b2.y;
+  out4[2] = __uint_as_float(r4[2]) + b2.z;
+  out4[3] = __uint_as_float(r4[3]) + b2.w;
+}
+#else
   // ---- layer 2 (fp32, CUDA cores): 64 -> 4, sequential in the hidden index;
   // W2 is staged hidden-major ([o][4]) so one 16 B load feeds the 4 outputs
   // b1 at fp + 64, W2 at fp + 128, b2 at fp + 384 (floats)
@@ -133,6 +192,7 @@ __device__ __forceinline__ void tc_mlp_rows(uint8_t *A, const uint8_t *W, const 
   out4[2] = acc[2] + b2.z;
   out4[3] = acc[3] + b2.w;
 }
+#endif
 
 // Write one bf16 input row (n values of x, zero padded to kTcK0) to A.
 __device__ __forceinline__ void tc_write_x(uint8_t *A, int gt, const float *x, int n) {
@@ -387,7 +447,7 @@ __global__ void __launch_bounds__(128 * TG, TG == 1 ? 4 : (TG == 2 ? 3 : 2)) k_s
   extern __shared__ uint8_t smem_raw[];
   const TcSmemPtrs S = tc_carve(smem_raw, TG);
   const int tid = threadIdx.x, warp = tid >> 5, g = tid >> 7, gt = tid & 127;
-  if (warp == 0) tc::tmem_alloc<64 * TG>(S.tmem_slot);
+  if (warp == 0) tc::tmem_alloc<kTcCols * TG>(S.tmem_slot);
   __shared__ DevAsset s_asset;
   __shared__ double s_scale;
   if (tid == 0) {
@@ -399,7 +459,7 @@ __global__ void __launch_bounds__(128 * TG, TG == 1 ? 4 : (TG == 2 ? 3 : 2)) k_s
   tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();
-  const uint32_t tmem_g = *S.tmem_slot + 64u * (uint32_t)g;
+  const uint32_t tmem_g = *S.tmem_slot + (uint32_t)kTcCols * (uint32_t)g;
   uint8_t *Ag = S.A + g * kTcA;
   uint32_t mma_phase = 0, tma_phase = 0;
   bool phi_smem = false, tab_smem = false;
@@ -447,7 +507,7 @@ __global__ void __launch_bounds__(128 * TG, TG == 1 ? 4 : (TG == 2 ? 3 : 2)) k_s
   }
   tc::tc_fence_before();
   __syncthreads();
-  if (warp == 0) tc::tmem_free<64 * TG>(*S.tmem_slot);
+  if (warp == 0) tc::tmem_free<kTcCols * TG>(*S.tmem_slot);
 }
 
 // The specular MLP alone on n input rows (numerics tests): X (n, in) f32 ->
@@ -458,7 +518,7 @@ __global__ void __launch_bounds__(kTcThreads) k_mlp_tc(const DevAsset *Ap, const
   const TcSmemPtrs S = tc_carve(smem_raw);
   const int tid = threadIdx.x, warp = tid >> 5;
   const DevAsset &A = *Ap;
-  if (warp == 0) tc::tmem_alloc<64>(S.tmem_slot);
+  if (warp == 0) tc::tmem_alloc<kTcCols>(S.tmem_slot);
   if (tid == 0) {
     tc::mbar_init(S.bar_mma, 1);
     tc::mbar_init(S.bar_tma, 1);
@@ -486,7 +546,7 @@ __global__ void __launch_bounds__(kTcThreads) k_mlp_tc(const DevAsset *Ap, const
   }
   tc::tc_fence_before();
   __syncthreads();
-  if (warp == 0) tc::tmem_free<64>(tmem);
+  if (warp == 0) tc::tmem_free<kTcCols>(tmem);
 }
 
 __global__ void __launch_bounds__(kShadeThreads) k_mlp_fp32(const DevAsset *Ap, const float *X, long long n,
