@@ -411,7 +411,7 @@ def workload_config(args, desc, W, H, n_assets):
 
 # ------------------------------------------------------------------ end to end (sparse frames)
 def run_e2e_sparse(args, R, N, cam_arrays, n_cam, mine, my_tiles, n_max, stride, W, H, n_views, world, rank,
-                   dev, out, scene):
+                   dev, out, scene, flush=None):
     """End to end through the public API, host wall clock: every step uploads
     its camera block, renders, packs ONLY the live chunks (the pixels any
     screen box reaches; the rest of the frame is the miss encoding), moves
@@ -428,14 +428,12 @@ def run_e2e_sparse(args, R, N, cam_arrays, n_cam, mine, my_tiles, n_max, stride,
     NPX = n_views * H * W
     tl = np.ascontiguousarray(mine, np.int32)
     NP = 3                              # pack buffers: render k+1 / copy k / scatter k-1
-    dpack = [torch.empty(n_chunks * 768, dtype=torch.uint8, device=dev) for _ in range(NP)]
-    dids = [torch.empty(n_chunks, dtype=torch.int32, device=dev) for _ in range(NP)]
-    hpack = [torch.empty(n_chunks * 768, dtype=torch.uint8, pin_memory=True) for _ in range(NP)]
-    hids = [torch.empty(n_chunks, dtype=torch.int32, pin_memory=True) for _ in range(NP)]
-    # live-chunk count written by the compose kernel straight into mapped host memory
-    cnt_host = np.zeros(NP, np.uint32)
-    cnt_dev = ctypes.c_void_p()
-    N.check(N.lib().nolf_host_register(cnt_host.ctypes.data, cnt_host.nbytes, ctypes.byref(cnt_dev)))
+    dpack = [torch.empty(n_chunks * 16 * 48, dtype=torch.uint8, device=dev) for _ in range(NP)]
+    dids = [torch.empty(n_chunks * 3, dtype=torch.int32, device=dev) for _ in range(NP)]
+    dcnt = [torch.zeros(2, dtype=torch.int32, device=dev) for _ in range(NP)]
+    hpack = [torch.empty(n_chunks * 16 * 48, dtype=torch.uint8, pin_memory=True) for _ in range(NP)]
+    hids = [torch.empty(n_chunks * 3, dtype=torch.int32, pin_memory=True) for _ in range(NP)]
+    hcnt = [torch.zeros(2, dtype=torch.int32, pin_memory=True) for _ in range(NP)]
     # the host frames (2, rotating): one shared block for all ranks
     FB = NPX * 6
     name = f"nolf_sparse_{os.environ.get('MASTER_PORT', 'solo')}_{os.environ.get('TORCHELASTIC_RUN_ID', os.getpid())}"
@@ -453,8 +451,7 @@ def run_e2e_sparse(args, R, N, cam_arrays, n_cam, mine, my_tiles, n_max, stride,
             hf[fb * FB + NPX * 4:(fb + 1) * FB] = 0xFF
     if world > 1:
         dist.barrier()
-    prev = [np.zeros(n_chunks, np.uint32) for _ in range(2)]
-    prev_n = [ctypes.c_uint32(0) for _ in range(2)]
+    dirty = [np.zeros(n_chunks, np.uint16) for _ in range(2)]     # per host frame: runs holding hits
     comp = torch.cuda.current_stream()
     copy_stream = torch.cuda.Stream(device=dev)
     ev_r = [torch.cuda.Event() for _ in range(NP)]
@@ -466,9 +463,11 @@ def run_e2e_sparse(args, R, N, cam_arrays, n_cam, mine, my_tiles, n_max, stride,
         b = k % NP
         if ev_c[b] is not None:
             comp.wait_event(ev_c[b])                 # pack buffer b copied out (step k-2)
-        o = {"pack": dpack[b], "pack_ids": dids[b], "pack_count": cnt_dev.value + 4 * b,
-             "counters": out["counters"]}
+        o = {"pack": dpack[b], "pack_ids": dids[b], "pack_count": dcnt[b], "counters": out["counters"]}
+        if flush is not None:
+            flush.fill_(k & 0xFF)                    # L2 evicted before every frame, inside the wall clock
         R.render(cam_arrays[k % n_cam], my_tiles, n_max, stride, o, frame_layout=True, prefilled=True)
+        hcnt[b].copy_(dcnt[b], non_blocking=True)    # 8 B: how much to download
         ev_r[b].record(comp)
 
     tm = {"wait_render": 0.0, "scatter": 0.0, "wait_copy": 0.0, "enqueue": 0.0}
@@ -478,16 +477,16 @@ def run_e2e_sparse(args, R, N, cam_arrays, n_cam, mine, my_tiles, n_max, stride,
         t = time.perf_counter()
         ev_r[b].synchronize()
         tm["wait_render"] += time.perf_counter() - t
-        n = int(cnt_host[b])
+        n, nr = (int(v) for v in hcnt[b])
         n_of[b] = n
         copy_stream.wait_event(ev_r[b])
         with torch.cuda.stream(copy_stream):
-            hpack[b][:n * 768].copy_(dpack[b][:n * 768], non_blocking=True)
-            hids[b][:n].copy_(dids[b][:n], non_blocking=True)
+            hpack[b][:nr * 48].copy_(dpack[b][:nr * 48], non_blocking=True)
+            hids[b][:3 * n].copy_(dids[b][:3 * n], non_blocking=True)
         ev = torch.cuda.Event()
         ev.record(copy_stream)
         ev_c[b] = ev
-        bytes_d2h[0] += n * 772 + 4
+        bytes_d2h[0] += nr * 48 + n * 12 + 8
 
     def scatter(k):                      # on the scatter thread
         b, f = k % NP, k % 2
@@ -496,8 +495,7 @@ def run_e2e_sparse(args, R, N, cam_arrays, n_cam, mine, my_tiles, n_max, stride,
         t1 = time.perf_counter()
         base = hf.ctypes.data + f * FB
         N.check(N.lib().nolf_host_scatter(hpack[b].data_ptr(), hids[b].data_ptr(), n_of[b], tl.ctypes.data,
-                                          len(tl), stride, W, H, base, base + NPX * 4, prev[f].ctypes.data,
-                                          ctypes.byref(prev_n[f]), 0))
+                                          len(tl), stride, W, H, base, base + NPX * 4, dirty[f].ctypes.data, 0))
         tm["wait_copy"] += t1 - t
         tm["scatter"] += time.perf_counter() - t1
 
@@ -542,11 +540,13 @@ def run_e2e_sparse(args, R, N, cam_arrays, n_cam, mine, my_tiles, n_max, stride,
            "h2d_bytes_per_step": int(N.lib().nolf_launch_param_bytes(len(scene), n_views)),
            "d2h_bytes_per_step": int(bytes_d2h[0] / args.steps),
            "timing": "host wall clock (perf_counter) from the first render to the last frame rebuilt in "
-                     "host memory, max over ranks",
-           "mode": ("sparse frame: compose packs the live 128-pixel chunks (768 B each), one DMA per step "
-                    "to pinned host memory, nolf_host_scatter rebuilds the full encode_frame RAW frame "
-                    "(rgba8 + u16 depth) in host memory on host threads (streaming stores; render k+1 / "
-                    "copy k / scatter k-1 pipelined, the scatter on its own host thread)"),
+                     "host memory, max over ranks; L2 flushed (256 MiB write) before every render, inside "
+                     "the timed window",
+           "mode": ("sparse frame: compose packs the non-miss 8-pixel runs of the live chunks (48 B "
+                    "each + a 12 B header per live chunk), one DMA per step to pinned host memory, "
+                    "nolf_host_scatter rebuilds the full encode_frame RAW frame (rgba8 + u16 depth) in "
+                    "host memory on host threads, touching only runs that change (render k+1 / copy k / "
+                    "scatter k-1 pipelined, the scatter on its own host thread)"),
            "full_frame_bytes": int(npix * 6),
            "host_us_per_step": {key: round(v / args.steps * 1e6, 1) for key, v in tm.items()},
            "host_threads": int(os.environ.get("NOLF_HOST_THREADS",
@@ -554,7 +554,6 @@ def run_e2e_sparse(args, R, N, cam_arrays, n_cam, mine, my_tiles, n_max, stride,
     last = (args.steps - 1) % 2
     frame_copy = torch.from_numpy(hf[last * FB:(last + 1) * FB].copy())
     worker.shutdown()
-    N.lib().nolf_host_unregister(cnt_host.ctypes.data)
     if world > 1:
         dist.barrier()
     del hf
@@ -900,7 +899,8 @@ def run_ours(args):
     sparse_host = None
     if not args.no_e2e and args.e2e_mode == "sparse":
         e2e, sparse_host, shm = run_e2e_sparse(args, R, N, cam_arrays, n_cam, mine, my_tiles, n_max, stride, W, H,
-                                               n_views, world, rank, dev, out, scene)
+                                               n_views, world, rank, dev, out, scene,
+                                               flush=None if args.no_flush else flush)
     elif not args.no_e2e and args.e2e_mode == "hostmap":
         # One shared page-locked host frame stack (double buffered) mapped by
         # every rank.  Each rank composes its tile rows into its own device

@@ -44,7 +44,7 @@
 extern "C" {
 #endif
 
-#define NOLF_ABI_VERSION 3
+#define NOLF_ABI_VERSION 4
 
 #define NOLF_OK 0
 #define NOLF_EINVAL -1
@@ -160,12 +160,14 @@ typedef struct NolfSceneOut {
                                           (u8/u16 outputs only; rgba/depth must be NULL) */
     /* Sparse frame (end-to-end delivery): with prefilled = 1, 128-slot-aligned
      * tiles in the 8x4-block layout (sides multiples of 8 x 4) and tile_stride
-     * a multiple of 128, the compose epilogue also packs every LIVE chunk (128
-     * consecutive slots some screen box reaches; all other pixels are misses):
-     * pack[i*768 ...] = the chunk's 128 encoded pixels in slot order (rgba8,
-     * 512 B) then their depth16 (256 B); pack_ids[i] = chunk id (slot / 128);
-     * *pack_count = number of packed chunks (may be host-mapped memory).  Only
-     * these bytes need to cross PCIe: nolf_host_scatter rebuilds the frame.
+     * a multiple of 128, the compose epilogue also packs the LIVE chunks (128
+     * consecutive slots some screen box reaches; every other pixel is a miss)
+     * run by run: each 8-pixel run that encodes to anything but the miss
+     * encoding goes to `pack` (48 B: 8 rgba8 then 8 depth16), and pack_ids
+     * holds per live chunk i {chunk id (slot / 128), mask of its packed runs,
+     * index of its first packed run}; pack_count[0] = live chunks,
+     * pack_count[1] = packed runs (may be host-mapped memory).  Only these
+     * bytes need to cross PCIe: nolf_host_scatter rebuilds the frame.
      * rgba8 / depth16 may then be NULL.  All three NULL: no pack. */
     uint8_t *pack;
     uint32_t *pack_ids;
@@ -353,18 +355,18 @@ int nolf_adam(float *param, const double *grad, float *m, float *v, int64_t n, d
               double beta2, double eps, int64_t step, uint32_t *nonfinite, void *stream);
 
 /* frames: rgba (K, P, 4) f32, depth (K, P) f32, all device pointers. */
-/* Host side of the sparse frame (NolfSceneOut.pack): writes the n packed
- * chunks (HOST copies of pack / pack_ids) into a row-major encode_frame RAW
- * frame in host memory (camera c at c*width*height; tiles = the HOST tile
- * list of the render, tile_stride as rendered) and resets to the miss
- * encoding (rgba 0, depth 65535) every chunk of prev_ids (the chunks written
- * into this frame buffer last time) that is not live now; prev_ids /
- * *prev_n are then updated to this frame's chunks (capacity: all chunks of
- * the tile list).  Runs on n_threads host threads (0: the library's pool
- * default).  A frame buffer starts as the miss encoding with *prev_n = 0. */
-int nolf_host_scatter(const uint8_t *pack, const uint32_t *ids, uint32_t n, const NolfTile *tiles, int32_t n_tiles,
+/* Host side of the sparse frame (NolfSceneOut.pack): writes the packed runs
+ * of the n live chunks (HOST copies of pack / pack_ids) into a row-major
+ * encode_frame RAW frame in host memory (camera c at c*width*height; tiles =
+ * the HOST tile list of the render, tile_stride as rendered).  `dirty`
+ * (HOST, one u16 per chunk of the tile list, zero for a buffer holding only
+ * the miss encoding) records which runs of this frame buffer hold non-miss
+ * bytes: runs that were dirty and are misses now are reset, the rest of the
+ * frame is never touched.  Runs on n_threads host threads (0: the pool
+ * default). */
+int nolf_host_scatter(const uint8_t *runs, const uint32_t *heads, uint32_t n, const NolfTile *tiles, int32_t n_tiles,
                       int64_t tile_stride, int32_t width, int32_t height, uint8_t *rgba8, uint16_t *depth16,
-                      uint32_t *prev_ids, uint32_t *prev_n, int32_t n_threads);
+                      uint16_t *dirty, int32_t n_threads);
 
 int nolf_compose(int32_t K, int64_t P, const float *rgba, const float *depth, double alpha_vis,
                  float *out_rgba, float *out_depth, void *stream);

@@ -20,7 +20,7 @@ LIB_PATH = os.environ.get("NOLF_LIB") or os.path.join(os.path.dirname(os.path.ab
 
 NOLF_EINVAL, NOLF_ESTATE, NOLF_EDATA, NOLF_ECUDA, NOLF_ENOMEM, NOLF_ECAPACITY = -1, -2, -3, -4, -5, -6
 HEAD_ACT = {"identity": 0, "sigmoid": 1, "exponential": 2}
-ABI_VERSION = 3              # NOLF_ABI_VERSION of include/nolf.h
+ABI_VERSION = 4              # NOLF_ABI_VERSION of include/nolf.h
 # nolf_set_option keys (include/nolf.h)
 OPT_MARCH_ORDER, OPT_COMPOSE_SLOTS, OPT_HEAVY_WAVES = 1, 2, 3
 MLP_FP32, MLP_BF16 = 0, 1
@@ -118,7 +118,7 @@ def lib():
         "nolf_zlib_version": ([], C.c_char_p),
         "nolf_train_shade": ([vp, vp, vp, vp, i64, vp, vp, vp, vp, vp, dbl, vp, vp, vp, vp], C.c_int),
         "nolf_adam": ([vp, vp, vp, vp, i64, dbl, dbl, dbl, dbl, i64, vp, vp], C.c_int),
-        "nolf_host_scatter": ([vp, vp, C.c_uint32, vp, i32, i64, i32, i32, vp, vp, vp, vp, i32], C.c_int),
+        "nolf_host_scatter": ([vp, vp, C.c_uint32, vp, i32, i64, i32, i32, vp, vp, vp, i32], C.c_int),
         "nolf_mlp_eval": ([vp, C.c_int, vp, i64, vp, vp], C.c_int),
         "nolf_device_alloc": ([C.c_size_t, C.POINTER(vp)], C.c_int),
         "nolf_device_free": ([vp], C.c_int),

@@ -1277,6 +1277,7 @@ int launch_march_shade(int mode, const NolfInstance *ins, int n_inst, const Nolf
       ca.pack = sout->pack;
       ca.pack_ids = sout->pack_ids;
       ca.pack_count = sout->pack_count;
+      CUDA_TRY(cudaMemsetAsync(sout->pack_count + 1, 0, sizeof(uint32_t), st));   // run allocator
     }
     if (sout->chunk_state) {
       if (!(chunked && ca.prefilled && ca.four == 2 && sout->layout == 1 && sout->rgba8 && sout->depth16 && !pack))
@@ -1914,22 +1915,23 @@ extern "C" int nolf_asset_load(const char *path, int device, nolf_asset_t *out, 
 }
 
 // ---------------------------------------------------------------- sparse frame, host side
-extern "C" int nolf_host_scatter(const uint8_t *pack, const uint32_t *ids, uint32_t n, const NolfTile *tiles,
+extern "C" int nolf_host_scatter(const uint8_t *runs, const uint32_t *heads, uint32_t n, const NolfTile *tiles,
                                  int32_t n_tiles, int64_t tile_stride, int32_t width, int32_t height, uint8_t *rgba8,
-                                 uint16_t *depth16, uint32_t *prev_ids, uint32_t *prev_n, int32_t n_threads) {
-  if ((n && (!pack || !ids)) || !tiles || n_tiles < 0 || tile_stride < 128 || tile_stride % 128 || width < 1 ||
-      height < 1 || !rgba8 || !depth16 || !prev_ids || !prev_n)
+                                 uint16_t *depth16, uint16_t *dirty, int32_t n_threads) {
+  if ((n && !heads) || !tiles || n_tiles < 0 || tile_stride < 128 || tile_stride % 128 || width < 1 || height < 1 ||
+      !rgba8 || !depth16 || !dirty)
     return fail(NOLF_EINVAL, "bad sparse frame arguments");
   const uint64_t n_chunks = (uint64_t)n_tiles * (uint64_t)(tile_stride / 128);
-  if (n > n_chunks || *prev_n > n_chunks) return fail(NOLF_EINVAL, "more chunks than the tile list holds");
-  for (uint32_t i = 0; i < n; ++i)
-    if (ids[i] >= n_chunks) return fail(NOLF_EDATA, "packed chunk id %u out of range", ids[i]);
-  nolf_host::ScatterJob job{pack, ids, n, tiles, n_tiles, tile_stride, width, height, rgba8, depth16,
-                           prev_ids, *prev_n};
-  const int rc = nolf_host::scatter(job, n_threads);
-  if (rc) return fail(NOLF_EDATA, "sparse frame: tile of a packed chunk is not in the 8x4-block layout");
-  memcpy(prev_ids, ids, sizeof(uint32_t) * n);
-  *prev_n = n;
+  uint64_t total_runs = 0;
+  for (uint32_t i = 0; i < n; ++i) {
+    if (heads[3 * i] >= n_chunks || heads[3 * i + 1] > 0xffffu)
+      return fail(NOLF_EDATA, "packed chunk %u: bad header", i);
+    total_runs = std::max<uint64_t>(total_runs, (uint64_t)heads[3 * i + 2] + __builtin_popcount(heads[3 * i + 1]));
+  }
+  if (total_runs && !runs) return fail(NOLF_EINVAL, "null run payload");
+  nolf_host::ScatterJob job{runs, heads, n, tiles, n_tiles, tile_stride, width, height, rgba8, depth16, dirty};
+  if (nolf_host::scatter(job, n_threads))
+    return fail(NOLF_EDATA, "sparse frame: tile of a packed chunk is not in the 8x4-block layout");
   return 0;
 }
 

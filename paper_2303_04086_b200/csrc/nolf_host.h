@@ -99,8 +99,8 @@ inline Pool &pool(int want) {
 }
 
 struct ScatterJob {
-  const uint8_t *pack;
-  const uint32_t *ids;
+  const uint8_t *runs;         // 48 B per packed run
+  const uint32_t *heads;       // per live chunk: {chunk id, run mask, first run}
   uint32_t n;
   const NolfTile *tiles;
   int32_t n_tiles;
@@ -108,8 +108,7 @@ struct ScatterJob {
   int32_t width, height;
   uint8_t *rgba8;
   uint16_t *depth16;
-  const uint32_t *prev_ids;
-  uint32_t prev_n;
+  uint16_t *dirty;             // per chunk of this frame buffer: runs holding non-miss bytes
 };
 
 // (x, y) of packed slot `local` in a w x h tile of 8x4 blocks (render.slot_xy).
@@ -119,25 +118,33 @@ inline void block_xy(int64_t local, int w, int &x, int &y) {
   y = (int)((blk / bx) * 4 + (l >> 3));
 }
 
-// Write (pack != null) or clear one chunk's 16 runs of 8 pixels.
-inline bool put_chunk(const ScatterJob &J, uint32_t id, const uint8_t *e) {
+// Write the runs of chunk `id`: bit r of `put` from payload run e + 48 * k
+// (k-th set bit), bit r of `clear` to the miss encoding.
+inline bool chunk_runs(const ScatterJob &J, uint32_t id, unsigned put, unsigned clear, const uint8_t *e) {
   const int64_t p0 = (int64_t)id * 128;
   const int64_t t = p0 / J.tile_stride, local0 = p0 % J.tile_stride;
   const NolfTile &tp = J.tiles[t];
   const int w = tp.x1 - tp.x0, h = tp.y1 - tp.y0;
   if ((w & 7) || (h & 3)) return false;
+  static const uint8_t kMiss8[32] = {}, kMiss16[16] = {0xFF, 0xFF, 0xFF, 0xFF, 0xFF, 0xFF, 0xFF, 0xFF,
+                                                        0xFF, 0xFF, 0xFF, 0xFF, 0xFF, 0xFF, 0xFF, 0xFF};
   const int64_t base = (int64_t)tp.cam * J.width * J.height;
+  const unsigned any = put | clear;
   for (int r = 0; r < 16; ++r) {
+    if (!((any >> r) & 1u)) continue;
     const int64_t local = local0 + 8 * r;
     if (local >= (int64_t)w * h) break;
     int x, y;
     block_xy(local, w, x, y);
     const int64_t q = base + (int64_t)(tp.y0 + y) * J.width + (tp.x0 + x);
-    static const uint8_t kMiss8[32] = {}, kMiss16[16] = {0xFF, 0xFF, 0xFF, 0xFF, 0xFF, 0xFF, 0xFF, 0xFF,
-                                                          0xFF, 0xFF, 0xFF, 0xFF, 0xFF, 0xFF, 0xFF, 0xFF};
-    const uint8_t *s8 = e ? e + 32 * r : kMiss8, *s16 = e ? e + 512 + 16 * r : kMiss16;
-    memcpy(J.rgba8 + 4 * q, s8, 32);
-    memcpy(J.depth16 + q, s16, 16);
+    if ((put >> r) & 1u) {
+      memcpy(J.rgba8 + 4 * q, e, 32);
+      memcpy(J.depth16 + q, e + 32, 16);
+      e += 48;
+    } else {
+      memcpy(J.rgba8 + 4 * q, kMiss8, 32);
+      memcpy(J.depth16 + q, kMiss16, 16);
+    }
   }
   return true;
 }
@@ -145,22 +152,29 @@ inline bool put_chunk(const ScatterJob &J, uint32_t id, const uint8_t *e) {
 inline int scatter(const ScatterJob &J, int n_threads) {
   Pool &P = pool(n_threads);
   const uint64_t n_chunks = (uint64_t)J.n_tiles * (uint64_t)(J.tile_stride / 128);
-  // chunks live now (bitmap): stale ones from last time are reset
+  // chunks live now (bitmap): dirty runs of the others are reset
   thread_local std::vector<uint64_t> live;
   live.assign((n_chunks + 63) / 64, 0ull);
-  for (uint32_t i = 0; i < J.n; ++i) live[J.ids[i] >> 6] |= 1ull << (J.ids[i] & 63);
+  for (uint32_t i = 0; i < J.n; ++i) live[J.heads[3 * i] >> 6] |= 1ull << (J.heads[3 * i] & 63);
   const std::vector<uint64_t> &lv = live;    // the caller's copy (workers have their own thread_locals)
   const int parts = P.size() * 4;
   std::atomic<int> bad{0};
   const std::function<void(int)> f = [&](int part) {
-    const uint64_t c0 = (uint64_t)J.prev_n * part / parts, c1 = (uint64_t)J.prev_n * (part + 1) / parts;
-    for (uint64_t i = c0; i < c1; ++i) {
-      const uint32_t id = J.prev_ids[i];
-      if (id < n_chunks && !((lv[id >> 6] >> (id & 63)) & 1ull) && !put_chunk(J, id, nullptr)) bad = 1;
-    }
+    // live chunks: packed runs written, dirty runs that are misses now reset
     const uint64_t a = (uint64_t)J.n * part / parts, b = (uint64_t)J.n * (part + 1) / parts;
-    for (uint64_t i = a; i < b; ++i)
-      if (!put_chunk(J, J.ids[i], J.pack + 768 * i)) bad = 1;
+    for (uint64_t i = a; i < b; ++i) {
+      const uint32_t id = J.heads[3 * i], mask = J.heads[3 * i + 1];
+      const unsigned clear = J.dirty[id] & ~mask;
+      if ((mask | clear) && !chunk_runs(J, id, mask, clear, J.runs + 48ull * J.heads[3 * i + 2])) bad = 1;
+      J.dirty[id] = (uint16_t)mask;
+    }
+    // chunks not live now: reset their dirty runs
+    const uint64_t c0 = n_chunks * part / parts, c1 = n_chunks * (part + 1) / parts;
+    for (uint64_t c = c0; c < c1; ++c) {
+      if (!J.dirty[c] || ((lv[c >> 6] >> (c & 63)) & 1ull)) continue;
+      if (!chunk_runs(J, (uint32_t)c, 0u, J.dirty[c], nullptr)) bad = 1;
+      J.dirty[c] = 0;
+    }
   };
   P.run(f, parts);
   return bad.load();

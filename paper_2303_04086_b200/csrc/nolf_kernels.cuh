@@ -1216,9 +1216,9 @@ struct ComposeArgs {
   int prefilled;               // outputs already hold the miss encoding: dead chunks are not written
   uint16_t *chunk_state;       // prefilled buffers re-used across frames: per chunk, bit r = 8-pixel
                                // run r holds non-miss bytes from an earlier frame (NULL: freshly cleared)
-  uint8_t *pack;               // sparse frame: 768 B per live chunk (NolfSceneOut.pack), or NULL
-  uint32_t *pack_ids;
-  uint32_t *pack_count;
+  uint8_t *pack;               // sparse frame (NolfSceneOut.pack): 48 B per non-miss 8-pixel run, or NULL
+  uint32_t *pack_ids;          // per live chunk: {chunk id, run mask, first run in pack}
+  uint32_t *pack_count;        // [0] live chunks, [1] runs in pack
   unsigned *errors;            // device error counters (kErrTile for tiles the pack cannot hold)
 };
 
@@ -1538,37 +1538,60 @@ __global__ void __launch_bounds__(256) k_compose(ComposeArgs a) {
   }                            // the completion collective that follows
 }
 
-// Sparse frame: 8 consecutive slots (one 8-pixel row of an 8x4 block) of
-// live chunk `idx` into its 768-byte pack entry (slot order), misses included;
-// the frame itself is written as compose_eight does (when given).
-__device__ __forceinline__ void compose_pack8(const ComposeArgs &a, const long long p0, const unsigned idx) {
+// Sparse frame: 8 consecutive slots (one 8-pixel run of an 8x4 block) of
+// live chunk `idx` (16 consecutive lanes hold the chunk's 16 runs).  Runs
+// that encode to anything but the miss encoding are packed (32 B rgba8 +
+// 16 B depth16, run order within the chunk, chunks in allocation order); the
+// chunk's header is {chunk id, mask of packed runs, index of its first run}.
+// The frame itself is written as compose_eight does (when given).
+__device__ __forceinline__ void compose_pack8(const ComposeArgs &a, const long long p0, const unsigned idx,
+                                              const unsigned chunk_id, const unsigned lane) {
   long long t, local0;
   split_slot(p0, a.tile_stride, t, local0);
   const TileParams tp = a.tiles[t];
   const int w = tp.x1 - tp.x0, h = tp.y1 - tp.y0;
-  if ((w & 7) || (h & 3)) {                 // no 8-pixel runs: cannot be packed
-    if ((local0 & 127) == 0) atomicAdd(a.errors + kErrTile, 1u);
-    return;
-  }
-  const uint2 nh = *reinterpret_cast<const uint2 *>(a.nhit + p0);
+  const bool blocks = !(w & 7) && !(h & 3);
+  if (!blocks && (local0 & 127) == 0) atomicAdd(a.errors + kErrTile, 1u);   // no 8-pixel runs: cannot be packed
   unsigned c8[8], dd[8];
+  bool nonmiss = false;
 #pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    const int n = local0 + j < (long long)w * h ? (int)(((j < 4 ? nh.x : nh.y) >> (8 * (j & 3))) & 0xffu) : 0;
-    float4 o;
-    float od;
-    compose_px(a, p0 + j, n, o, od);
-    const uchar4 u = encode_rgba8(o);
-    c8[j] = (unsigned)u.x | ((unsigned)u.y << 8) | ((unsigned)u.z << 16) | ((unsigned)u.w << 24);
-    dd[j] = encode_depth16(od, a.depth_far);
+  for (int j = 0; j < 8; ++j) { c8[j] = 0u; dd[j] = 0xffffu; }
+  if (blocks) {
+    const uint2 nh = *reinterpret_cast<const uint2 *>(a.nhit + p0);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int n = local0 + j < (long long)w * h ? (int)(((j < 4 ? nh.x : nh.y) >> (8 * (j & 3))) & 0xffu) : 0;
+      if (n == 0) continue;
+      float4 o;
+      float od;
+      compose_px(a, p0 + j, n, o, od);
+      const uchar4 u = encode_rgba8(o);
+      c8[j] = (unsigned)u.x | ((unsigned)u.y << 8) | ((unsigned)u.z << 16) | ((unsigned)u.w << 24);
+      dd[j] = encode_depth16(od, a.depth_far);
+      nonmiss = nonmiss || c8[j] != 0u || dd[j] != 0xffffu;
+    }
   }
-  const unsigned s = (unsigned)(p0 & 127);
-  uint8_t *e = a.pack + (size_t)idx * 768;
-  reinterpret_cast<uint4 *>(e + 4 * s)[0] = make_uint4(c8[0], c8[1], c8[2], c8[3]);
-  reinterpret_cast<uint4 *>(e + 4 * s)[1] = make_uint4(c8[4], c8[5], c8[6], c8[7]);
-  *reinterpret_cast<uint4 *>(e + 512 + 2 * s) =
-      make_uint4(dd[0] | (dd[1] << 16), dd[2] | (dd[3] << 16), dd[4] | (dd[5] << 16), dd[6] | (dd[7] << 16));
-  if (a.out_rgba8 && local0 < (long long)w * h && tile_valid(tp, a.cams, a.n_cams, a.tile_stride)) {
+  // run allocation for the chunk: one atomic per chunk (lane of run 0)
+  const unsigned half = 0xffffu << (lane & 16u);
+  const unsigned mask = (__ballot_sync(half, nonmiss) >> (lane & 16u)) & 0xffffu;
+  const int run = (int)((p0 & 127) >> 3);
+  unsigned first = 0;
+  if (run == 0) {
+    first = mask ? atomicAdd(a.pack_count + 1, (unsigned)__popc(mask)) : 0u;
+    a.pack_ids[3 * idx + 0] = chunk_id;
+    a.pack_ids[3 * idx + 1] = mask;
+    a.pack_ids[3 * idx + 2] = first;
+  }
+  first = __shfl_sync(half, first, (int)(lane & 16u));
+  if (nonmiss) {
+    uint8_t *e = a.pack + 48ull * (first + (unsigned)__popc(mask & ((1u << run) - 1u)));
+    reinterpret_cast<uint4 *>(e)[0] = make_uint4(c8[0], c8[1], c8[2], c8[3]);
+    reinterpret_cast<uint4 *>(e)[1] = make_uint4(c8[4], c8[5], c8[6], c8[7]);
+    reinterpret_cast<uint4 *>(e)[2] =
+        make_uint4(dd[0] | (dd[1] << 16), dd[2] | (dd[3] << 16), dd[4] | (dd[5] << 16), dd[6] | (dd[7] << 16));
+  }
+  if (a.out_rgba8 && blocks && local0 < (long long)w * h && tile_valid(tp, a.cams, a.n_cams, a.tile_stride) &&
+      (nonmiss || !a.prefilled)) {
     const CamParams &cp = a.cams[tp.cam];
     int x, y;
     slot_xy(local0, w, h, x, y);
@@ -1681,8 +1704,7 @@ __global__ void __launch_bounds__(256) k_compose_live(ComposeArgs a, const unsig
        g += (long long)gridDim.x * blockDim.x) {
     const long long p0 = (long long)live_list[g / per_chunk] * 128 + (g % per_chunk) * G;   // spatial list
     if (G == 8 && a.pack) {
-      compose_pack8(a, p0, (unsigned)(g / per_chunk));
-      if (g % per_chunk == 0) a.pack_ids[g / per_chunk] = live_list[g / per_chunk];
+      compose_pack8(a, p0, (unsigned)(g / per_chunk), live_list[g / per_chunk], threadIdx.x & 31u);
     } else if (G == 8 && a.chunk_state) {
       compose_eight_state(a, p0, threadIdx.x & 31u);
     } else if (G == 8) {
@@ -1691,7 +1713,7 @@ __global__ void __launch_bounds__(256) k_compose_live(ComposeArgs a, const unsig
       compose_four(a, p0);
     }
   }
-  if (a.pack_count && blockIdx.x == 0 && threadIdx.x == 0) *a.pack_count = count[0];
+  if (a.pack_count && blockIdx.x == 0 && threadIdx.x == 0) a.pack_count[0] = count[0];
   if (a.peer) {
     __syncthreads();
     if (threadIdx.x == 0) __threadfence_system();

@@ -335,10 +335,10 @@ def test_random_full_size_scene_matches_oracle(seed):
 
 @pytest.mark.parametrize("size", [(256, 256), (200, 136)])
 def test_sparse_frame_pack_and_host_scatter(size):
-    """NolfSceneOut.pack (only live chunks leave the GPU) + nolf_host_scatter
-    rebuild the encode_frame RAW frame on the host bit for bit, across two
-    frames (stale chunks of the first are reset to the miss encoding)."""
-    import ctypes as C
+    """NolfSceneOut.pack (only the non-miss 8-pixel runs of live chunks leave
+    the GPU) + nolf_host_scatter rebuild the encode_frame RAW frame on the
+    host bit for bit, across frames (runs written before and missed now are
+    reset)."""
     import torch
     from paper_2303_04086_b200 import _native as N
     from paper_2303_04086_b200.model import orbit_camera
@@ -350,26 +350,24 @@ def test_sparse_frame_pack_and_host_scatter(size):
     n_chunks = len(tiles) * 1024 // 128
     host8 = np.zeros((H, W, 4), np.uint8)
     host16 = np.full((H, W), 65535, np.uint16)
-    prev = np.zeros(n_chunks, np.uint32)
-    prev_n = C.c_uint32(0)
-    for az in (0.5, 1.7):
+    dirty = np.zeros(n_chunks, np.uint16)
+    for az in (0.5, 1.7, 1.75):
         cam = orbit_camera(az, 0.6, radius=2.5, width=W, height=H, target=(0.2, 0.2, 0.25))
-        dev = {"pack": torch.zeros(n_chunks * 768, dtype=torch.uint8, device=r.device),
-               "pack_ids": torch.zeros(n_chunks, dtype=torch.int32, device=r.device),
-               "pack_count": torch.zeros(1, dtype=torch.int32, device=r.device),
+        dev = {"pack": torch.zeros(n_chunks * 16 * 48, dtype=torch.uint8, device=r.device),
+               "pack_ids": torch.zeros(n_chunks * 3, dtype=torch.int32, device=r.device),
+               "pack_count": torch.zeros(2, dtype=torch.int32, device=r.device),
                "counters": torch.zeros(4, dtype=torch.int64, device=r.device)}
         r.render([cam], tiles_dev, len(tiles), 1024, dev, frame_layout=True, prefilled=True)
         ref = r.alloc(len(tiles), 1024, want_f32=False, want_u8=True)
         r.render([cam], tiles_dev, len(tiles), 1024, ref, frame_layout=True)
         r.check()
-        n = int(dev["pack_count"].item())
-        assert 0 < n < n_chunks
-        pack = dev["pack"][:n * 768].cpu().numpy()
-        ids = dev["pack_ids"][:n].cpu().numpy().astype(np.uint32)
+        n_live, n_runs = (int(v) for v in dev["pack_count"].cpu().numpy())
+        assert 0 < n_live < n_chunks and 0 < n_runs < 16 * n_live
+        runs = dev["pack"][:max(n_runs, 1) * 48].cpu().numpy()
+        heads = dev["pack_ids"][:n_live * 3].cpu().numpy().astype(np.uint32)
         tl = np.ascontiguousarray(tiles, np.int32)
-        N.check(N.lib().nolf_host_scatter(pack.ctypes.data, ids.ctypes.data, n, tl.ctypes.data, len(tl), 1024, W, H,
-                                          host8.ctypes.data, host16.ctypes.data, prev.ctypes.data,
-                                          C.byref(prev_n), 0))
+        N.check(N.lib().nolf_host_scatter(runs.ctypes.data, heads.ctypes.data, n_live, tl.ctypes.data, len(tl), 1024,
+                                          W, H, host8.ctypes.data, host16.ctypes.data, dirty.ctypes.data, 0))
         np.testing.assert_array_equal(host8.reshape(-1, 4), ref["rgba8"][:W * H].cpu().numpy())
         np.testing.assert_array_equal(host16.reshape(-1), ref["depth16"][:W * H].cpu().numpy().view(np.uint16))
 

@@ -26,7 +26,7 @@ def test_library_exports_every_declared_symbol():
     lib = _native.lib()
     missing = [n for n in declared() if not hasattr(lib, n)]
     assert not missing, missing
-    assert lib.nolf_abi_version() == _native.ABI_VERSION == 3
+    assert lib.nolf_abi_version() == _native.ABI_VERSION == 4
 
 
 def test_workspace_size_is_monotone():
