@@ -311,6 +311,10 @@ int nolf_ipc_close_handle(void *ptr);
 int nolf_flag_set(uint32_t *flag, uint32_t value, void *stream);
 int nolf_flag_wait(const uint32_t *flags, int32_t n, uint32_t value, uint32_t *timed_out, void *stream);
 int nolf_memcpy_async(void *dst, const void *src, size_t bytes, void *stream);
+/* n (<= 1024) u32 words by a one-warp kernel (plain stores, system fence):
+ * e.g. a render's pack_count into host-mapped memory without a copy-engine
+ * operation in the stream. */
+int nolf_store_u32(uint32_t *dst, const uint32_t *src, int32_t n, void *stream);
 int nolf_memset_async(void *dst, int32_t byte_value, size_t bytes, void *stream);
 int nolf_memcpy2d_async(void *dst, size_t dpitch, const void *src, size_t spitch, size_t width_bytes,
                         size_t height, void *stream);

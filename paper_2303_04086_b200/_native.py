@@ -129,6 +129,7 @@ def lib():
         "nolf_memset_async": ([vp, C.c_int32, C.c_size_t, vp], C.c_int),
         "nolf_flag_wait": ([vp, C.c_int32, C.c_uint32, vp, vp], C.c_int),
         "nolf_memcpy_async": ([vp, vp, C.c_size_t, vp], C.c_int),
+        "nolf_store_u32": ([vp, vp, i32, vp], C.c_int),
         "nolf_memcpy2d_async": ([vp, C.c_size_t, vp, C.c_size_t, C.c_size_t, C.c_size_t, vp], C.c_int),
         "nolf_host_register": ([vp, C.c_size_t, C.POINTER(vp)], C.c_int),
         "nolf_host_unregister": ([vp], C.c_int),

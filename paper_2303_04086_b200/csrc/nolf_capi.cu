@@ -1589,6 +1589,14 @@ int nolf_ipc_close_handle(void *ptr) {
   return 0;
 }
 
+int nolf_store_u32(uint32_t *dst, const uint32_t *src, int32_t n, void *stream) {
+  if (n < 0 || n > 1024 || (n && (!dst || !src))) return fail(NOLF_EINVAL, "bad store arguments");
+  if (n == 0) return 0;
+  k_store_u32<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(dst, src, n);
+  CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
 int nolf_memset_async(void *dst, int32_t byte_value, size_t bytes, void *stream) {
   if (bytes == 0) return 0;
   if (!dst) return fail(NOLF_EINVAL, "null buffer");

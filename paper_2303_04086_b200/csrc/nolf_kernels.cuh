@@ -1744,6 +1744,13 @@ __global__ void __launch_bounds__(256) k_unpack(const uint8_t *gathered, long lo
   depth16[dst] = reinterpret_cast<const uint16_t *>(base + (long long)n_per_rank * tile_stride * 4)[src];
 }
 
+// n words from device memory to (typically host-mapped) memory by plain
+// stores: no copy-engine operation in the stream.
+__global__ void k_store_u32(uint32_t *dst, const uint32_t *src, int n) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+  __threadfence_system();
+}
+
 // ---------------------------------------------------------------- cross-GPU flags
 __global__ void k_flag_set(uint32_t *flag, uint32_t value) {
   __threadfence_system();      // the stream's earlier (peer) stores become visible first
