@@ -844,6 +844,7 @@ struct Options {
   long long heavy_waves = 3;   // marcher launches below this many CTA waves go heaviest-chunk-first
   int march_order = 0;         // 0 auto, 1 spatial list, 2 heavy-first buckets
   int compose_slots = 0;       // live-chunk compose slots per thread: 0 auto, 4, 8
+  int march_split = 1;         // CTAs per live chunk in the chunked marcher: 1 or 2
   bool init = false;
 };
 thread_local Options g_opt;
@@ -852,6 +853,7 @@ Options &options() {
   if (!g_opt.init) {
     if (const char *e = getenv("NOLF_HEAVY_WAVES")) g_opt.heavy_waves = atoll(e);
     if (const char *e = getenv("NOLF_COMPOSE_G")) g_opt.compose_slots = atoi(e);
+    if (const char *e = getenv("NOLF_MARCH_SPLIT")) g_opt.march_split = atoi(e) == 2 ? 2 : 1;
     g_opt.init = true;
   }
   return g_opt;
@@ -1224,8 +1226,14 @@ int launch_march_shade(int mode, const NolfInstance *ins, int n_inst, const Nolf
     CUDA_TRY(cudaGetLastError());
     CUDA_TRY(cudaEventRecord(ax.ev_cull, st));   // the live count is final here
     const unsigned mgrid = (unsigned)std::max<long long>(1, std::min(n_chunks, want));
-    if (n_inst > 64) k_march_chunks<true><<<mgrid, kMarchThreads, 0, st>>>(ma);
-    else k_march_chunks<false><<<mgrid, kMarchThreads, 0, st>>>(ma);
+    if (opt.march_split == 2) {           // two 64-thread CTAs per chunk
+      if (n_inst > 64) k_march_chunks_half<true><<<2 * mgrid, kMarchThreads / 2, 0, st>>>(ma);
+      else k_march_chunks_half<false><<<2 * mgrid, kMarchThreads / 2, 0, st>>>(ma);
+    } else if (n_inst > 64) {
+      k_march_chunks<true><<<mgrid, kMarchThreads, 0, st>>>(ma);
+    } else {
+      k_march_chunks<false><<<mgrid, kMarchThreads, 0, st>>>(ma);
+    }
     if (!le.pending) {          // read the live count back on the side stream: shading never waits for it
       CUDA_TRY(cudaStreamWaitEvent(ax.s, ax.ev_cull, 0));
       CUDA_TRY(cudaMemcpyAsync(le.host, w.counts + n_inst, sizeof(unsigned), cudaMemcpyDeviceToHost, ax.s));
@@ -1456,6 +1464,10 @@ int nolf_set_option(int32_t key, int64_t value) {
     case NOLF_OPT_COMPOSE_SLOTS:
       if (value != 0 && value != 4 && value != 8) return fail(NOLF_EINVAL, "compose slots must be 0, 4 or 8");
       o.compose_slots = (int)value;
+      return 0;
+    case NOLF_OPT_MARCH_SPLIT:
+      if (value != 1 && value != 2) return fail(NOLF_EINVAL, "march split must be 1 or 2");
+      o.march_split = (int)value;
       return 0;
     case NOLF_OPT_HEAVY_WAVES:
       if (value < 0) return fail(NOLF_EINVAL, "heavy waves must be >= 0");

@@ -738,8 +738,8 @@ __device__ __forceinline__ HitRec hit_record(const DevAsset &A, const double o[3
 // GROUPS: more than 64 instances (candidate masks per group of 64); the
 // common case compiles without the group loop.
 template <int MODE, bool GROUPS = false>
-__device__ __forceinline__ void march_chunk(const MarchArgs &args, unsigned chunk, bool precull) {
-  const long long gid = (long long)chunk * kMarchThreads + threadIdx.x;
+__device__ __forceinline__ void march_chunk(const MarchArgs &args, unsigned chunk, bool precull, int sub = 0) {
+  const long long gid = (long long)chunk * kMarchThreads + (long long)sub * blockDim.x + threadIdx.x;
   const unsigned lane = threadIdx.x & 31;
   if (MODE == kModeScene && precull && cta_precull(args, gid)) return;
   bool valid = gid < args.n_rays;
@@ -919,6 +919,16 @@ __global__ void __launch_bounds__(kMarchThreads, NOLF_MARCH_MINB) k_march_chunks
     march_chunk<kModeScene, GROUPS>(args, chunk_at(args.chunks, args.n_chunks, args.list_stride, it, args.heavy_first),
                                     false);
   stat_cta_end();
+}
+
+// Each live chunk marched by two 64-thread CTAs (half the work per CTA: a
+// shorter tail for launches of few waves -- multi-GPU shards).
+template <bool GROUPS = false>
+__global__ void __launch_bounds__(kMarchThreads / 2, 2 * NOLF_MARCH_MINB) k_march_chunks_half(MarchArgs args) {
+  const unsigned n = *args.n_chunks;
+  for (unsigned it = blockIdx.x; it < 2 * n; it += gridDim.x)
+    march_chunk<kModeScene, GROUPS>(
+        args, chunk_at(args.chunks, args.n_chunks, args.list_stride, it >> 1, args.heavy_first), false, (int)(it & 1));
 }
 
 // ---------------------------------------------------------------- shading

@@ -468,3 +468,34 @@ def test_prefilled_frame_with_chunk_state_over_frames():
         assert torch.equal(buf["rgba8"], full["rgba8"][:n]) and torch.equal(buf["depth16"], full["depth16"][:n])
     assert int((buf["chunk_state"] != 0).sum()) > 0
     r.check()
+
+
+def test_multi_view_launch_vs_oracle():
+    """One launch over two cameras' tiles (the multi-user batches of BASELINE
+    configs 3 / 5) against the oracle's render_frame + compose of each
+    camera: depth bits and counters equal, rgba <= 1e-6 (fp32 MLP)."""
+    import torch
+    from paper_2303_04086_b200.model import orbit_camera
+    _, scene = _scene()
+    cams = [orbit_camera(0.5, 0.6, radius=2.5, size=64, target=(0.2, 0.2, 0.25)),
+            orbit_camera(2.6, -0.3, radius=2.0, size=64, target=(0.1, 0.3, 0.2))]
+    r = R.SceneRenderer(scene)
+    tiles = np.concatenate([R.frame_tiles(64, 64, 32, cam=c) for c in range(2)])
+    out = r.alloc(len(tiles), 1024, want_f32=True, want_u8=False)
+    r.render(cams, torch.from_numpy(tiles).to(r.device), len(tiles), 1024, out, frame_layout=True)
+    r.check()
+    got_rgba = out["rgba"][:2 * 4096].cpu().numpy().reshape(2, 64, 64, 4)
+    got_depth = out["depth"][:2 * 4096].cpu().numpy().reshape(2, 64, 64)
+    cnt = out["counters"].cpu().numpy()
+    from paper_2303_04086_b200.model import RenderCounters
+    oc = RenderCounters()
+    for c, cam in enumerate(cams):
+        rg, dp = [], []
+        for a, m in scene:
+            r_, d_ = O.render_rect(a, cam, (0, 0, 64, 64), oc, transform=m)
+            rg.append(r_)
+            dp.append(d_)
+        o_rgba, o_depth = O.compose(np.stack(rg), np.stack(dp))
+        assert np.array_equal(got_depth[c], o_depth)
+        assert np.abs(got_rgba[c] - o_rgba).max() <= 1e-6
+    assert (int(cnt[2]), int(cnt[3])) == (oc.hit_pixels, oc.march_samples)
