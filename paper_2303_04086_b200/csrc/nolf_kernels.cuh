@@ -781,7 +781,9 @@ __device__ __forceinline__ void march_chunk(const MarchArgs &args, unsigned chun
       boxhit = prepare_slab(I, A, args.raw_rays, ow, dw, o, d, inv, sp);
     }
     if (A.mesh.nodes) {        // mesh proxy (warp-uniform: k is): march from its first hit
-#ifdef NOLF_MESH_PER_THREAD
+#if defined(NOLF_MESH_TIMING_ONLY)   // diagnostic (wrong results): the march from the slab entry
+      const double tm = sp.t_near;
+#elif defined(NOLF_MESH_PER_THREAD)
       const double tm = boxhit ? mesh_first_hit(A.mesh, o, d, args.errors + kErrBvh) : -1.0;
 #else
       const double tm = mesh_first_hit_warp(A.mesh, o, d, boxhit, args.errors + kErrBvh);
