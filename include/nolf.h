@@ -259,7 +259,8 @@ int nolf_check_errors(void *stream);
  * when live 128-slot chunks were compacted and marched (k_cull_chunks +
  * k_march_chunks), info[1] = 1 heaviest-first / 0 spatial order, info[2] =
  * live-chunk compose slots per thread (4 / 8; 0 = full-frame k_compose),
- * info[3] = 1 bf16 tcgen05 shading (k_shade_tc) / 0 fp32 (k_shade). */
+ * info[3] = resident k_shade_tc CTAs per SM (bf16 tcgen05 shading; >= 1) /
+ * 0 fp32 (k_shade). */
 int nolf_last_launch(int32_t info[4]);
 
 /* Parity read-back (debug): while slots != NULL, every render call on the

@@ -361,7 +361,7 @@ int ensure_attrs() {            // function attributes are per device
     CUDA_TRY(cudaFuncSetAttribute(k_shade, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kShadeSmem));
     CUDA_TRY(cudaFuncSetAttribute(k_eval_diffuse, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kShadeSmem));
     CUDA_TRY(cudaFuncSetAttribute(k_shade_tc<kShadeTG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)tc_smem_bytes(kShadeTG, kTcPhiMax)));
+                                  (int)tc_smem_bytes(kShadeTG, kTcPhiMax, kTcTabMax * 4)));
     CUDA_TRY(cudaFuncSetAttribute(k_mlp_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTcSmem));
     CUDA_TRY(cudaFuncSetAttribute(k_mlp_fp32, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kShadeSmem));
     done = true;
@@ -424,7 +424,7 @@ int fill_inst(const NolfInstance *in, DevInst *out) {
 
 int run_shade(const DevInst *inst, const long long *qoff, int n_inst, const Workspace &w, int mode, float *rgba,
               float *depth, long long layer_stride, unsigned long long *counters, cudaStream_t st, bool use_tc,
-              uint32_t phi_smem_bytes);
+              uint32_t phi_smem_bytes, uint32_t tab_smem_bytes);
 
 }  // namespace
 
@@ -670,7 +670,7 @@ int nolf_asset_create(const NolfAssetDesc *d, int device, nolf_asset_t *out) {
   }
   // tensor-core tables: bf16 specular weights in the UMMA K-major layout
   // (core matrix (row group g, K chunk c) at c*(rows/8)*128 + g*128) + u16 Phi
-  if (d->specular.n_layers == 3 && d->specular.widths[0] <= kTcK0) {
+  if (d->specular.n_layers == 3 && d->specular.widths[0] <= kTcIn) {
     std::vector<uint16_t> wt(kTcWBytes / 2, 0);
     auto bf16 = [](float f) {
       uint32_t u;
@@ -678,36 +678,52 @@ int nolf_asset_create(const NolfAssetDesc *d, int device, nolf_asset_t *out) {
       u += 0x7FFFu + ((u >> 16) & 1u);            // round to nearest even
       return (uint16_t)(u >> 16);
     };
-    auto put = [&](size_t base_elems, int row, int k, float v) {
-      const size_t off = (size_t)(k >> 3) * (64 / 8) * 128 + (size_t)(row >> 3) * 128 + (row & 7) * 16 + (k & 7) * 2;
-      wt[base_elems + off / 2] = bf16(v);
+    auto bf16_f = [](uint16_t h) {
+      const uint32_t u = (uint32_t)h << 16;
+      float f;
+      memcpy(&f, &u, 4);
+      return f;
+    };
+    // element (row, k) of a K-major operand with `rows` rows at base_elems
+    auto put = [&](size_t base_elems, int rows, int row, int k, uint16_t v) {
+      const size_t off = (size_t)(k >> 3) * (rows / 8) * 128 + (size_t)(row >> 3) * 128 + (row & 7) * 16 + (k & 7) * 2;
+      wt[base_elems + off / 2] = v;
+    };
+    // an fp32 bias as bf16 hi + lo in K columns (k, k+1)
+    auto put_bias = [&](size_t base_elems, int rows, int row, int k, float b) {
+      const uint16_t hi = bf16(b);
+      put(base_elems, rows, row, k, hi);
+      put(base_elems, rows, row, k + 1, bf16(b - bf16_f(hi)));
     };
     const int in = d->specular.widths[0];
-    for (int o = 0; o < 64; ++o)
-      for (int i = 0; i < in; ++i) put(0, o, i, d->specular.w[0][o * in + i]);
-    for (int o = 0; o < 64; ++o)
-      for (int i = 0; i < 64; ++i) put(kTcW0 / 2, o, i, d->specular.w[1][o * 64 + i]);
-    // W2 (4 x 64) as a 16-row operand (rows 4..15 zero): core matrix (g, c) at c*256 + g*128
-    for (int o = 0; o < 4; ++o)
-      for (int i = 0; i < 64; ++i) {
-        const size_t off = (size_t)(i >> 3) * 256 + (size_t)(o >> 3) * 128 + (o & 7) * 16 + (i & 7) * 2;
-        wt[(kTcW0 + kTcW1) / 2 + off / 2] = bf16(d->specular.w[2][o * 64 + i]);
-      }
-    // the shader's shared-memory image after the bf16 weights: the fp32
-    // block (b0, b1, W2 hidden-major [o][4], b2) and the PSH residue tables
-    // when they fit, so one TMA bulk copy stages all of it
+    const size_t e_w1 = kOffW1 / 2, e_w2 = kOffW2 / 2, e_w1b = kOffW1b / 2, e_w2b = kOffW2b / 2,
+                 e_one = kOffOne / 2;
+    for (int o = 0; o < 64; ++o) {
+      for (int i = 0; i < in; ++i) put(0, 64, o, i, bf16(d->specular.w[0][o * in + i]));
+      put_bias(0, 64, o, kTcIn, d->specular.b[0][o]);
+      for (int i = 0; i < 64; ++i) put(e_w1, 64, o, i, bf16(d->specular.w[1][o * 64 + i]));
+      put_bias(e_w1b, 64, o, 0, d->specular.b[1][o]);
+    }
+    // W2 (4 x 64) as a 16-row operand (rows 4..15 zero)
+    for (int o = 0; o < 4; ++o) {
+      for (int i = 0; i < 64; ++i) put(e_w2, 16, o, i, bf16(d->specular.w[2][o * 64 + i]));
+      put_bias(e_w2b, 16, o, 0, d->specular.b[2][o]);
+    }
+    // the broadcast ones operand: one core matrix of rows {1, 1, 0 ...}
+    for (int r = 0; r < 8; ++r) wt[e_one + r * 8] = wt[e_one + r * 8 + 1] = bf16(1.0f);
+    // the shader's shared-memory image after the bf16 weights: [the fp32
+    // block (W2 hidden-major [o][4], b2) for -DNOLF_SHADE_L2_FP32 builds] and
+    // the PSH residue tables when they fit, so one TMA bulk copy stages all of it
     const int nt = 6 * (H.N + 1);
-    const size_t tab_bytes = nt <= (int)kTcTabMax ? ((size_t)nt * 4 + 15) / 16 * 16 : 0;
+    const size_t tab_bytes = tc_tab_bytes(H.N);
     std::vector<uint8_t> img(kTcWBytes + kTcF32 * 4 + tab_bytes, 0);
     memcpy(img.data(), wt.data(), kTcWBytes);
-    std::vector<float> fpb(kTcF32, 0.f);
-    for (int q = 0; q < kTcF32; ++q) {
-      if (q < 64) fpb[q] = d->specular.b[0][q];
-      else if (q < 128) fpb[q] = d->specular.b[1][q - 64];
-      else if (q < 128 + 256) fpb[q] = d->specular.w[2][((q - 128) & 3) * 64 + ((q - 128) >> 2)];
-      else fpb[q] = d->specular.b[2][q - 384];
+    if (kTcF32) {
+      std::vector<float> fpb((size_t)std::max(kTcF32, 1), 0.f);
+      for (int q = 128; q < kTcF32; ++q)
+        fpb[q] = q < 128 + 256 ? d->specular.w[2][((q - 128) & 3) * 64 + ((q - 128) >> 2)] : d->specular.b[2][q - 384];
+      memcpy(img.data() + kTcWBytes, fpb.data(), (size_t)kTcF32 * 4);
     }
-    memcpy(img.data() + kTcWBytes, fpb.data(), kTcF32 * 4);
     if (tab_bytes) {
       std::vector<uint32_t> tab((size_t)nt);
       const int s1 = H.N + 1;
@@ -807,7 +823,7 @@ int nolf_asset_set_mlp_mode(nolf_asset_t a, int mode) {
   if (!a) return fail(NOLF_EINVAL, "null asset");
   if (mode != NOLF_MLP_FP32 && mode != NOLF_MLP_BF16) return fail(NOLF_EINVAL, "unknown MLP mode %d", mode);
   if (mode == NOLF_MLP_BF16) {
-    if (!a->host.tc_w) return fail(NOLF_EINVAL, "bf16 tensor-core MLP needs a 3-layer specular net with <= 32 inputs");
+    if (!a->host.tc_w) return fail(NOLF_EINVAL, "bf16 tensor-core MLP needs a 3-layer specular net with <= 30 inputs");
     if (a->host.use_diffuse_color && !a->host.has_dif)
       return fail(NOLF_EINVAL, "bf16 tensor-core shading needs a baked diffuse atlas (live diffuse runs in fp32)");
   }
@@ -944,7 +960,7 @@ thread_local long long g_dbg_rows = 0;
 
 int run_shade(const DevInst *inst, const long long *qoff, int n_inst, const Workspace &w, int mode, float *rgba,
               float *depth, long long layer_stride, unsigned long long *counters, cudaStream_t st, bool use_tc,
-              uint32_t phi_smem_bytes) {
+              uint32_t phi_smem_bytes, uint32_t tab_smem_bytes) {
   ShadeArgs sa{};
   sa.dbg_slots = g_dbg_slots;
   sa.dbg_rows = g_dbg_rows;
@@ -959,10 +975,11 @@ int run_shade(const DevInst *inst, const long long *qoff, int n_inst, const Work
   sa.layer_stride = layer_stride;
   sa.counters = counters;
   if (use_tc) {
+    sa.tab_bytes = tab_smem_bytes;
     // dynamic smem sized to the largest Phi the launch stages (not the 64 KB
     // worst case) so more CTAs fit per SM
     sa.tile_order = 1;               // blocked tile ranges per CTA
-    const size_t smem = tc_smem_bytes(kShadeTG, phi_smem_bytes);
+    const size_t smem = tc_smem_bytes(kShadeTG, phi_smem_bytes, sa.tab_bytes);
     // resident CTAs per SM from registers and shared memory (TMEM: 64
     // columns per tile group, never the limit here)
     static int regs = 0;
@@ -978,6 +995,7 @@ int run_shade(const DevInst *inst, const long long *qoff, int n_inst, const Work
     const int by_smem = (int)((227u * 1024u) / (smem + static_smem + 1024u));
     const int by_tmem = 512 / (kTcCols * kShadeTG);
     const int per_sm = std::max(1, std::min(std::min(by_regs, by_smem), by_tmem));
+    g_last_launch[3] = per_sm;
     k_shade_tc<kShadeTG><<<num_sms() * per_sm, threads, smem, st>>>(sa);
   } else {
     k_shade<<<num_sms() * 3, kShadeThreads, kShadeSmem, st>>>(sa);
@@ -1137,12 +1155,13 @@ int launch_march_shade(int mode, const NolfInstance *ins, int n_inst, const Nolf
   ParamBlock hb = param_view(hraw, PL), db = param_view(draw, PL);
   ParamBlock *hp = &hb, *dp = &db;
   bool use_tc = true;
-  uint32_t phi_smem = 0;
+  uint32_t phi_smem = 0, tab_smem = 0;
   for (int k = 0; k < n_inst; ++k) {
     if ((rc = fill_inst(ins + k, hp->inst + k))) return rc;
     const DevAsset &H = ins[k].asset->host;
     use_tc = use_tc && H.mlp_mode == NOLF_MLP_BF16;
     if (H.phi16 && H.phi16_bytes <= kTcPhiMax) phi_smem = std::max(phi_smem, H.phi16_bytes);
+    tab_smem = std::max(tab_smem, tc_tab_bytes(H.N));
   }
   for (int c = 0; c < n_cams; ++c) hp->cams[c] = hcams[(size_t)c];
   *hp->rect = rect;
@@ -1245,7 +1264,7 @@ int launch_march_shade(int mode, const NolfInstance *ins, int n_inst, const Nolf
   if ((rc = prof_mark(1, st))) return rc;
   if (mode == kModeScene) {
     if ((rc = run_shade(dp->inst, dp->qoff, n_inst, w, mode, w.lrgba, w.ldepth, w.P, counters, st, use_tc,
-                        phi_smem)))
+                        phi_smem, tab_smem)))
       return rc;
     if ((rc = prof_mark(2, st))) return rc;
     ComposeArgs ca{};
@@ -1317,7 +1336,7 @@ int launch_march_shade(int mode, const NolfInstance *ins, int n_inst, const Nolf
     if ((rc = prof_mark(3, st))) return rc;
     if ((rc = ring_release(slot, st))) return rc;   // the block is reusable once this frame is done
   } else {
-    if ((rc = run_shade(dp->inst, dp->qoff, n_inst, w, mode, rgba, depth, 0, counters, st, use_tc, phi_smem)))
+    if ((rc = run_shade(dp->inst, dp->qoff, n_inst, w, mode, rgba, depth, 0, counters, st, use_tc, phi_smem, tab_smem)))
       return rc;
     if ((rc = prof_mark(2, st))) return rc;
     if ((rc = prof_mark(3, st))) return rc;

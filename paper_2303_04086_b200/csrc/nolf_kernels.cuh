@@ -948,6 +948,7 @@ struct ShadeArgs {
   unsigned long long *counters;
   uint32_t *dbg_slots;         // debug (nolf_debug_psh_slots): 8 PSH slots per output row, or NULL
   long long dbg_rows;          // rows dbg_slots holds
+  uint32_t tab_bytes;          // bf16 shader: largest staged residue table of the launch's assets
 };
 
 constexpr int kShadeThreads = 128;

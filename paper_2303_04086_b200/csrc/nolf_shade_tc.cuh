@@ -24,24 +24,67 @@
 namespace nolf {
 
 constexpr int kTcThreads = 128;
-constexpr int kTcK0 = 32;                    // layer-0 K padded (inputs <= 32)
+constexpr int kTcK0 = 32;                    // layer-0 K padded (inputs <= kTcIn)
+constexpr int kTcIn = kTcK0 - 2;             // K columns 30, 31: constant 1 (layer-0 bias hi / lo)
 constexpr uint32_t kTcA = 16384;             // A tile: 128 x 64 bf16
-constexpr uint32_t kTcW0 = 64 * kTcK0 * 2;   // 4 KB
+constexpr uint32_t kTcW0 = 64 * kTcK0 * 2;   // 4 KB (bias hi / lo in K columns 30, 31)
 constexpr uint32_t kTcW1 = 64 * 64 * 2;      // 8 KB
 constexpr uint32_t kTcW2 = 16 * 64 * 2;      // 2 KB: W2 (4 x 64) zero-padded to N = 16 rows
-constexpr uint32_t kTcWBytes = kTcW0 + kTcW1 + kTcW2;
+// Biases of layers 1 and 2 as one more K=16 MMA step each: A = a broadcast
+// "ones" operand (every row {1, 1, 0 x 6}: one 128 B core matrix re-read for
+// all row groups, SBO = 0; its second K chunk is a zero core matrix -- the
+// zero-padded rows 8..15 of W2, LBO = 256), B = one K chunk holding (bias hi,
+// bias lo) per output row (its second K chunk aliases the first, LBO = 0, and
+// meets the zeros of A).  hi + lo = the fp32 bias to 2^-17 relative.
+// Image layout (byte offsets; one TMA bulk copy):
+constexpr uint32_t kTcW1b = 64 * 8 * 2;      // 1 KB
+constexpr uint32_t kTcW2b = 16 * 8 * 2;      // 256 B
+constexpr uint32_t kOffW1 = kTcW0;
+constexpr uint32_t kOffOne = kOffW1 + kTcW1;
+constexpr uint32_t kOffW2 = kOffOne + 128;
+constexpr uint32_t kOffW1b = kOffW2 + kTcW2;
+constexpr uint32_t kOffW2b = kOffW1b + kTcW1b;
+constexpr uint32_t kTcWBytes = kOffW2b + kTcW2b;
+constexpr uint32_t kOneLbo = kOffW2 + 128 - kOffOne;   // -> W2 row group 1 of K chunk 0: zeros
 #ifndef NOLF_SHADE_L2_FP32
 constexpr int kTcCols = 128;                 // TMEM columns per tile group: hidden (64) + layer 2 (16)
+constexpr int kTcF32 = 0;                    // no fp32 block staged
 #else
 constexpr int kTcCols = 64;
+constexpr int kTcF32 = 64 + 64 + 4 * 64 + 4; // (b0, b1 unused: folded), W2 hidden-major, b2
 #endif
-constexpr int kTcF32 = 64 + 64 + 4 * 64 + 4; // b0, b1, W2, b2
 #ifndef NOLF_TC_PHIMAX
 #define NOLF_TC_PHIMAX (64 * 1024)
 #endif
 constexpr uint32_t kTcPhiMax = NOLF_TC_PHIMAX;   // Phi bytes staged in smem
 constexpr uint32_t kTcTabMax = 776;          // residue tables 6*(N+1) for N <= 128 (16-B multiple)
-constexpr uint32_t kTcSmem = 1024 + kTcA + kTcWBytes + kTcF32 * 4 + kTcTabMax * 4 + 64 + kTcPhiMax;
+constexpr uint32_t kTcAlign = 16;            // SWIZZLE_NONE operands, TMA bulk copies and mbarriers need <= 16 B
+
+// Residue-table bytes of an asset's shared-memory image (0: read from global).
+__host__ __device__ constexpr uint32_t tc_tab_bytes(int N) {
+  return 6 * (N + 1) <= (int)kTcTabMax ? (uint32_t)(6 * (N + 1) * 4 + 15) / 16 * 16 : 0u;
+}
+
+// ReLU of this thread's 64 TMEM accumulator columns, re-quantised to bf16
+// into its row of the K-major A tile (16 columns per TMEM load, one cvt per
+// pair).
+__device__ __forceinline__ void tc_relu_store(uint32_t trow, uint32_t rowa) {
+#pragma unroll
+  for (int c4 = 0; c4 < 4; ++c4) {
+    uint32_t r[16];
+    tc::tmem_ld16(trow + 16 * c4, r);
+#pragma unroll
+    for (int hcol = 0; hcol < 2; ++hcol) {
+      const uint32_t *v = r + 8 * hcol;
+      uint4 q;
+      q.x = tc::pack_bf16_relu(v[0], v[1]);
+      q.y = tc::pack_bf16_relu(v[2], v[3]);
+      q.z = tc::pack_bf16_relu(v[4], v[5]);
+      q.w = tc::pack_bf16_relu(v[6], v[7]);
+      tc::sts128(rowa + (2 * c4 + hcol) * 2048, q);
+    }
+  }
+}
 
 // Two layers on tcgen05 for the 128 rows already written to A (layer-0 input,
 // bf16, K-major) by one 128-thread tile group (named barrier `bar_id`,
@@ -50,7 +93,8 @@ constexpr uint32_t kTcSmem = 1024 + kTcA + kTcWBytes + kTcF32 * 4 + kTcTabMax * 
 // hidden layer never occupies more than 16 registers.
 __device__ __forceinline__ void tc_mlp_rows(uint8_t *A, const uint8_t *W, const float *fp, uint32_t tmem,
                                             uint64_t *bar, uint32_t &phase, int gt, int bar_id, float out4[4]) {
-  const uint32_t aA = tc::smem_u32(A), aW0 = tc::smem_u32(W), aW1 = aW0 + kTcW0;
+  const uint32_t aA = tc::smem_u32(A), aW0 = tc::smem_u32(W), aW1 = aW0 + kOffW1;
+  const uint32_t aW1b = aW0 + kOffW1b, aW2b = aW0 + kOffW2b, aOne = aW0 + kOffOne;
   constexpr uint32_t idesc = tc::idesc_bf16_f32(128, 64);
   const uint32_t trow = tmem + ((uint32_t)((gt >> 5) * 32) << 16);   // this warp's TMEM lane quadrant
   // ---- layer 0: D = X[128x32] * W0[64x32]^T
@@ -67,83 +111,42 @@ __device__ __forceinline__ void tc_mlp_rows(uint8_t *A, const uint8_t *W, const 
   tc::mbar_wait(bar, phase);
   phase ^= 1;
   tc::tc_fence_after();
-  // bias + ReLU, re-quantised as the layer-1 A operand (K=64), 16 columns at a time
-  const uint32_t rowa = aA + (gt >> 3) * 128 + (gt & 7) * 16, fpa = tc::smem_u32(fp);
-#pragma unroll
-  for (int c4 = 0; c4 < 4; ++c4) {
-    uint32_t r[16];
-    tc::tmem_ld16(trow + 16 * c4, r);
-#pragma unroll
-    for (int hcol = 0; hcol < 2; ++hcol) {
-      const int c = 2 * c4 + hcol;
-      const float4 bA = tc::lds128(fpa + 32 * c), bB = tc::lds128(fpa + 32 * c + 16);
-      const float bb[8] = {bA.x, bA.y, bA.z, bA.w, bB.x, bB.y, bB.z, bB.w};
-      float v[8];
-#pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        const float z = __uint_as_float(r[8 * hcol + e]) + bb[e];
-        v[e] = z > 0.f ? z : 0.f;
-      }
-      uint4 q;
-      q.x = tc::pack_bf16(v[0], v[1]);
-      q.y = tc::pack_bf16(v[2], v[3]);
-      q.z = tc::pack_bf16(v[4], v[5]);
-      q.w = tc::pack_bf16(v[6], v[7]);
-      tc::sts128(rowa + c * 2048, q);
-    }
-  }
+  // ReLU (bias already in the accumulator), re-quantised as the layer-1 A
+  // operand (K=64), 16 columns at a time
+  const uint32_t rowa = aA + (gt >> 3) * 128 + (gt & 7) * 16;
+  tc_relu_store(trow, rowa);
   tc::tc_fence_before();
   tc::fence_async_smem();
   tc::bar_sync(bar_id, 128);
-  // ---- layer 1: D = H1[128x64] * W1[64x64]^T (reuses the TMEM columns)
+  // ---- layer 1: D = H1[128x64] * W1[64x64]^T + 1 * b1 (reuses the TMEM columns)
   if (gt == 0) {
     tc::tc_fence_after();
 #pragma unroll
     for (int s = 0; s < 4; ++s)
       tc::umma_bf16(tmem, tc::smem_desc(aA + s * 2 * 2048, 2048, 128), tc::smem_desc(aW1 + s * 2 * 1024, 1024, 128),
                     idesc, s > 0);
+    tc::umma_bf16(tmem, tc::smem_desc(aOne, kOneLbo, 0), tc::smem_desc(aW1b, 0, 128), idesc, 1);
     tc::umma_commit(bar);
   }
   tc::mbar_wait(bar, phase);
   phase ^= 1;
   tc::tc_fence_after();
 #ifndef NOLF_SHADE_L2_FP32
-  // ---- layer 2 on the tensor cores too: H2 = relu(D + b1) re-quantised as
-  // the A operand, D2[128 x 16] = H2 * W2p^T (W2 zero-padded to 16 rows)
-#pragma unroll
-  for (int c4 = 0; c4 < 4; ++c4) {
-    uint32_t r[16];
-    tc::tmem_ld16(trow + 16 * c4, r);
-#pragma unroll
-    for (int hcol = 0; hcol < 2; ++hcol) {
-      const int c = 2 * c4 + hcol;
-      const float4 bA = tc::lds128(fpa + 256 + 32 * c), bB = tc::lds128(fpa + 256 + 32 * c + 16);
-      const float bb[8] = {bA.x, bA.y, bA.z, bA.w, bB.x, bB.y, bB.z, bB.w};
-      float v[8];
-#pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        const float z = __uint_as_float(r[8 * hcol + e]) + bb[e];
-        v[e] = z > 0.f ? z : 0.f;
-      }
-      uint4 q;
-      q.x = tc::pack_bf16(v[0], v[1]);
-      q.y = tc::pack_bf16(v[2], v[3]);
-      q.z = tc::pack_bf16(v[4], v[5]);
-      q.w = tc::pack_bf16(v[6], v[7]);
-      tc::sts128(rowa + c * 2048, q);
-    }
-  }
+  // ---- layer 2 on the tensor cores too: H2 = relu(D) re-quantised as the A
+  // operand, D2[128 x 16] = H2 * W2p^T + 1 * b2 (W2 zero-padded to 16 rows)
+  tc_relu_store(trow, rowa);
   tc::tc_fence_before();
   tc::fence_async_smem();
   tc::bar_sync(bar_id, 128);
   if (gt == 0) {
     tc::tc_fence_after();
     constexpr uint32_t idesc2 = tc::idesc_bf16_f32(128, 16);
-    const uint32_t aW2 = aW1 + kTcW1;
+    const uint32_t aW2 = aW0 + kOffW2;
 #pragma unroll
     for (int s = 0; s < 4; ++s)
       tc::umma_bf16(tmem + 64, tc::smem_desc(aA + s * 2 * 2048, 2048, 128), tc::smem_desc(aW2 + s * 2 * 256, 256, 128),
                     idesc2, s > 0);
+    tc::umma_bf16(tmem + 64, tc::smem_desc(aOne, kOneLbo, 0), tc::smem_desc(aW2b, 0, 128), idesc2, 1);
     tc::umma_commit(bar);
   }
   tc::mbar_wait(bar, phase);
@@ -152,16 +155,14 @@ __device__ __forceinline__ void tc_mlp_rows(uint8_t *A, const uint8_t *W, const 
   uint32_t r4[4];
   tc::tmem_ld4(trow + 64, r4);
   tc::tc_fence_before();
-  const float4 b2 = tc::lds128(fpa + 1536);
-  out4[0] = __uint_as_float(r4[0]) + b2.x;
-  out4[1] = __uint_as_float(r4[1]) + b2.y;
-  out4[2] = __uint_as_float(r4[2]) + b2.z;
-  out4[3] = __uint_as_float(r4[3]) + b2.w;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) out4[j] = __uint_as_float(r4[j]);
 }
 #else
   // ---- layer 2 (fp32, CUDA cores): 64 -> 4, sequential in the hidden index;
   // W2 is staged hidden-major ([o][4]) so one 16 B load feeds the 4 outputs
-  // b1 at fp + 64, W2 at fp + 128, b2 at fp + 384 (floats)
+  // W2 at fp + 128, b2 at fp + 384 (floats; b1 is folded into the MMA)
+  const uint32_t fpa = tc::smem_u32(fp);
   float acc[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
   for (int c4 = 0; c4 < 4; ++c4) {
@@ -170,12 +171,10 @@ __device__ __forceinline__ void tc_mlp_rows(uint8_t *A, const uint8_t *W, const 
 #pragma unroll
     for (int q4 = 0; q4 < 4; ++q4) {
       const int o4 = 4 * c4 + q4;
-      const float4 bv = tc::lds128(fpa + 256 + 16 * o4);
-      const float bb[4] = {bv.x, bv.y, bv.z, bv.w};
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         const int o = 4 * o4 + e;
-        float z = __uint_as_float(r[4 * q4 + e]) + bb[e];
+        float z = __uint_as_float(r[4 * q4 + e]);
         z = z > 0.f ? z : 0.f;
         const float4 wv = tc::lds128(fpa + 512 + 16 * o);
         acc[0] = fmaf(z, wv.x, acc[0]);
@@ -194,14 +193,15 @@ __device__ __forceinline__ void tc_mlp_rows(uint8_t *A, const uint8_t *W, const 
 }
 #endif
 
-// Write one bf16 input row (n values of x, zero padded to kTcK0) to A.
+// Write one bf16 input row (n <= kTcIn values of x, zero padded; columns
+// kTcIn.. = 1, the layer-0 bias inputs) to A.
 __device__ __forceinline__ void tc_write_x(uint8_t *A, int gt, const float *x, int n) {
   const uint32_t rowa = tc::smem_u32(A) + (gt >> 3) * 128 + (gt & 7) * 16;
 #pragma unroll
   for (int c = 0; c < kTcK0 / 8; ++c) {
     float v[8];
 #pragma unroll
-    for (int e = 0; e < 8; ++e) v[e] = (8 * c + e < n) ? x[8 * c + e] : 0.f;
+    for (int e = 0; e < 8; ++e) v[e] = 8 * c + e >= kTcIn ? 1.f : ((8 * c + e < n) ? x[8 * c + e] : 0.f);
     uint4 q;
     q.x = tc::pack_bf16(v[0], v[1]);
     q.y = tc::pack_bf16(v[2], v[3]);
@@ -220,19 +220,24 @@ struct TcSmemPtrs {
   uint8_t *phi;
 };
 
-// Shared-memory carve-up for `groups` 128-thread tile groups (1 KB aligned).
-__host__ __device__ constexpr uint32_t tc_smem_bytes(int groups, uint32_t phi_bytes) {
-  return 1024 + groups * kTcA + kTcWBytes + kTcF32 * 4 + kTcTabMax * 4 + 64 + phi_bytes;
+// Shared-memory carve-up for `groups` 128-thread tile groups: the operand
+// tiles, then the asset image (bf16 weights, bias chunks, ones operand,
+// [fp32 block], residue tables of up to tab_bytes) exactly as the host laid
+// it out for one bulk copy, the barriers and Phi.
+__host__ __device__ constexpr uint32_t tc_smem_bytes(int groups, uint32_t phi_bytes, uint32_t tab_bytes) {
+  return kTcAlign + groups * kTcA + kTcWBytes + kTcF32 * 4 + tab_bytes + 64 + phi_bytes;
 }
+constexpr uint32_t kTcSmem = tc_smem_bytes(1, kTcPhiMax, kTcTabMax * 4);
 
-__device__ __forceinline__ TcSmemPtrs tc_carve(uint8_t *raw, int groups = 1) {
-  uint8_t *base = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
+__device__ __forceinline__ TcSmemPtrs tc_carve(uint8_t *raw, int groups, uint32_t tab_bytes) {
+  uint8_t *base = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(raw) + kTcAlign - 1) &
+                                              ~uintptr_t(kTcAlign - 1));
   TcSmemPtrs p;
   p.A = base;
   p.W = p.A + groups * kTcA;
   p.fp = reinterpret_cast<float *>(p.W + kTcWBytes);
   p.tab = reinterpret_cast<uint32_t *>(p.fp + kTcF32);
-  p.bar_mma = reinterpret_cast<uint64_t *>(p.tab + kTcTabMax);
+  p.bar_mma = reinterpret_cast<uint64_t *>(reinterpret_cast<uint8_t *>(p.tab) + tab_bytes);
   p.bar_tma = p.bar_mma + groups;
   p.tmem_slot = reinterpret_cast<uint32_t *>(p.bar_tma + 1);
   p.phi = reinterpret_cast<uint8_t *>(p.bar_mma) + 64;
@@ -354,6 +359,18 @@ __device__ __forceinline__ void tc_gather_inputs(const DevAsset &A, const TcSmem
   if (A.refine_opacity) x[F + 16] = (float)clampd(rec.alpha_c, 1e-4, 1.0 - 1e-4);
 }
 
+// Heads of the bf16 path (its inputs already carry bf16 rounding; the
+// 2/255 budget dwarfs the ~2 ulp of the fast exp / reciprocal / log).
+#ifdef NOLF_SHADE_EXACT_ACT
+__device__ __forceinline__ float tc_sigmoid(float z) { return sigmoidf_np(z); }
+__device__ __forceinline__ float tc_exp(float z) { return expf(z); }
+__device__ __forceinline__ float tc_log(float z) { return logf(z); }
+#else
+__device__ __forceinline__ float tc_sigmoid(float z) { return __frcp_rn(1.0f + __expf(-z)); }
+__device__ __forceinline__ float tc_exp(float z) { return __expf(z); }
+__device__ __forceinline__ float tc_log(float z) { return __logf(z); }
+#endif
+
 // Shading of one 128-hit tile by one tile group (group thread gt owns row
 // gt): gather -> bf16 operand tile -> two tcgen05 layers -> fp32 layer 2,
 // heads and the combine (lightfield.py:267-336, 446-455).  Only the values
@@ -362,9 +379,8 @@ template <int TG>
 __device__ __forceinline__ void tc_shade_tile(const ShadeArgs &args, const DevAsset &A, const TcSmemPtrs &S,
                                               uint8_t *Ag, uint32_t tmem_g, uint64_t *bar_g, uint32_t &mma_phase,
                                               int gt, int bar_id, bool tab_smem, bool phi_smem, double scale,
-                                              const HitRec *recs, long long r, unsigned cnt,
+                                              const HitRec &rec, bool valid, const HitRec *next, HitRec &nxt,
                                               unsigned long long &n_fs) {
-  const bool valid = r < cnt;
   float cd0 = 0.f, cd1 = 0.f, cd2 = 0.f, tint = 1.f, aterm = 0.f, dep = 0.f;
   long long orow = 0;
   {
@@ -372,7 +388,6 @@ __device__ __forceinline__ void tc_shade_tile(const ShadeArgs &args, const DevAs
 #pragma unroll
     for (int q = 0; q < kTcK0; ++q) x[q] = 0.f;
     if (valid) {
-      const HitRec rec = recs[r];
       orow = args.mode == kModeScene ? (long long)rec.ordinal * args.layer_stride + rec.out_idx
                                      : (long long)rec.out_idx;
       uint32_t *dbg = (args.dbg_slots && orow < args.dbg_rows) ? args.dbg_slots + 8 * orow : nullptr;
@@ -398,24 +413,26 @@ __device__ __forceinline__ void tc_shade_tile(const ShadeArgs &args, const DevAs
         aterm = (float)clampd(rec.alpha_c, 0.0, 1.0);
       } else if (A.refine_opacity) {
         const float ac = (float)clampd(rec.alpha_c, 1e-4, 1.0 - 1e-4);
-        aterm = logf(ac / (1.0f - ac));
+        aterm = tc_log(__fdividef(ac, 1.0f - ac));
       }
       dep = (float)__ddiv_rn(rec.t_obj, scale);
       ++n_fs;
     }
-    tc_write_x(Ag, gt, x, kTcK0);   // unused inputs are 0 (W0 is zero-padded too)
+    tc_write_x(Ag, gt, x, kTcIn);   // unused inputs are 0 (W0 is zero-padded too)
   }
+  // the next tile's record, in flight across this tile's MMA chain
+  if (next) nxt = *next;
   float z4[4];
   tc_mlp_rows(Ag, S.W, S.fp, tmem_g, bar_g, mma_phase, gt, bar_id, z4);
   if (valid) {
     float fs_out[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j)
-      fs_out[j] = A.fs.act[j] == 0 ? z4[j] : (A.fs.act[j] == 1 ? sigmoidf_np(z4[j]) : expf(z4[j]));
+      fs_out[j] = A.fs.act[j] == 0 ? z4[j] : (A.fs.act[j] == 1 ? tc_sigmoid(z4[j]) : tc_exp(z4[j]));
     float alpha;
     if (!A.use_opacity) alpha = aterm;
-    else if (A.refine_opacity) alpha = sigmoidf_np(fs_out[3] + aterm);
-    else alpha = sigmoidf_np(fs_out[3]);
+    else if (A.refine_opacity) alpha = tc_sigmoid(fs_out[3] + aterm);
+    else alpha = tc_sigmoid(fs_out[3]);
     float4 o;
     o.x = fminf(fmaxf(fmaf(tint, fs_out[0], cd0), 0.f), 1.f);
     o.y = fminf(fmaxf(fmaf(tint, fs_out[1], cd1), 0.f), 1.f);
@@ -445,7 +462,7 @@ constexpr int kShadeTG = NOLF_SHADE_TG;
 template <int TG>
 __global__ void __launch_bounds__(128 * TG, TG == 1 ? 4 : (TG == 2 ? 3 : 2)) k_shade_tc(ShadeArgs args) {
   extern __shared__ uint8_t smem_raw[];
-  const TcSmemPtrs S = tc_carve(smem_raw, TG);
+  const TcSmemPtrs S = tc_carve(smem_raw, TG, args.tab_bytes);
   const int tid = threadIdx.x, warp = tid >> 5, g = tid >> 7, gt = tid & 127;
   if (warp == 0) tc::tmem_alloc<kTcCols * TG>(S.tmem_slot);
   __shared__ DevAsset s_asset;
@@ -490,13 +507,19 @@ __global__ void __launch_bounds__(128 * TG, TG == 1 ? 4 : (TG == 2 ? 3 : 2)) k_s
     __syncthreads();
     const DevAsset &A = s_asset;
     tc_stage_asset(A, S, tma_phase, tid, phi_smem);
-    tab_smem = 6 * (A.N + 1) <= (int)kTcTabMax;
+    tab_smem = tc_tab_bytes(A.N) != 0;   // the launch sized the carve for it
     __syncthreads();
     const HitRec *recs = args.queue + args.qoff[k];
     const double scale = s_scale;
-    for (long long q = g; q < n_here; q += TG)
+    long long r = (first + g) * 128 + gt;
+    HitRec cur, nxt;
+    if (g < n_here && r < cnt) cur = recs[r];
+    for (long long q = g; q < n_here; q += TG, r += 128 * TG) {
+      const bool has_next = q + TG < n_here && r + 128 * TG < cnt;
       tc_shade_tile<TG>(args, A, S, Ag, tmem_g, S.bar_mma + g, mma_phase, gt, 1 + g, tab_smem, phi_smem, scale,
-                        recs, (first + q) * 128 + gt, cnt, n_fs);
+                        cur, r < cnt, has_next ? recs + r + 128 * TG : nullptr, nxt, n_fs);
+      cur = nxt;
+    }
   }
   const unsigned lane = tid & 31;
 #pragma unroll
@@ -515,7 +538,7 @@ __global__ void __launch_bounds__(128 * TG, TG == 1 ? 4 : (TG == 2 ? 3 : 2)) k_s
 // CUDA-core routine (mode FP32).
 __global__ void __launch_bounds__(kTcThreads) k_mlp_tc(const DevAsset *Ap, const float *X, long long n, float *out) {
   extern __shared__ uint8_t smem_raw[];
-  const TcSmemPtrs S = tc_carve(smem_raw);
+  const TcSmemPtrs S = tc_carve(smem_raw, 1, kTcTabMax * 4);
   const int tid = threadIdx.x, warp = tid >> 5;
   const DevAsset &A = *Ap;
   if (warp == 0) tc::tmem_alloc<kTcCols>(S.tmem_slot);

@@ -189,6 +189,14 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
   return *reinterpret_cast<uint32_t *>(&h);
 }
+// bf16x2 of (relu(a), relu(b)) in one cvt (a in the low half, like
+// pack_bf16): rounding is monotone and sign-preserving, so this equals
+// pack_bf16(max(a, 0), max(b, 0)) up to the sign of zero.
+__device__ __forceinline__ uint32_t pack_bf16_relu(uint32_t a, uint32_t b) {
+  uint32_t d;
+  asm("cvt.rn.relu.bf16x2.f32 %0, %1, %2;" : "=r"(d) : "f"(__uint_as_float(b)), "f"(__uint_as_float(a)));
+  return d;
+}
 
 }  // namespace tc
 }  // namespace nolf

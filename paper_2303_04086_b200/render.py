@@ -250,7 +250,8 @@ def last_launch() -> dict:
     info = (C.c_int32 * 4)()
     N.check(N.lib().nolf_last_launch(info))
     return {"chunked": bool(info[0]), "march_order": "heavy-first" if info[1] else "spatial",
-            "compose_slots": int(info[2]), "shade": "k_shade_tc (bf16)" if info[3] else "k_shade (fp32)"}
+            "compose_slots": int(info[2]), "shade": "k_shade_tc (bf16)" if info[3] else "k_shade (fp32)",
+            "shade_ctas_per_sm": int(info[3])}
 
 
 class debug_psh_slots:
