@@ -887,6 +887,8 @@ def run_ours(args):
         rank_kernel_ms = [[round(float(v), 4) for v in x.tolist()] for x in allk]
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     t_max = float(t.item())
+    from paper_2303_04086_b200 import render as RM
+    launch = RM.last_launch()          # the variants the timed steps launched
     cnt = out["counters"].cpu().numpy().astype(np.float64) / args.steps
     if os.environ.get("NOLF_STATS_DUMP") and hasattr(N.lib(), "nolf_stats_read"):
         import ctypes                # diagnostic build (-DNOLF_STATS): march work counters
@@ -1171,7 +1173,7 @@ def run_ours(args):
             "random-init networks)", "config": workload_config(args, desc, W, H, len(scene)),
             "e2e": e2e, "gpu_launches": launches_per_step * args.steps,
             "gpu_launches_per_step": launches_per_step, "roofline": roof, "cpu_baseline": cpu,
-            "clocks": csum, "verify": verify,
+            "clocks": csum, "verify": verify, "launch": launch,
             "rank_kernel_ms": {"fields": ["k_march", "k_shade", "k_compose", "sm_mhz", "host_enqueue_ms"],
                                "ranks": rank_kernel_ms},
             "per_frame": {"march_samples": S, "hits": Hh, "pixels": npix},

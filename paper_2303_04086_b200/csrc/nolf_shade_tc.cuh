@@ -380,7 +380,7 @@ __device__ __forceinline__ void tc_shade_tile(const ShadeArgs &args, const DevAs
                                               uint8_t *Ag, uint32_t tmem_g, uint64_t *bar_g, uint32_t &mma_phase,
                                               int gt, int bar_id, bool tab_smem, bool phi_smem, double scale,
                                               const HitRec &rec, bool valid, const HitRec *next, HitRec &nxt,
-                                              unsigned long long &n_fs) {
+                                              bool std_heads, unsigned long long &n_fs) {
   float cd0 = 0.f, cd1 = 0.f, cd2 = 0.f, tint = 1.f, aterm = 0.f, dep = 0.f;
   long long orow = 0;
   {
@@ -426,9 +426,15 @@ __device__ __forceinline__ void tc_shade_tile(const ShadeArgs &args, const DevAs
   tc_mlp_rows(Ag, S.W, S.fp, tmem_g, bar_g, mma_phase, gt, bar_id, z4);
   if (valid) {
     float fs_out[4];
+    if (std_heads) {             // the reference's (sigmoid x 3, identity) head (lightfield.py:635)
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
-      fs_out[j] = A.fs.act[j] == 0 ? z4[j] : (A.fs.act[j] == 1 ? tc_sigmoid(z4[j]) : tc_exp(z4[j]));
+      for (int j = 0; j < 3; ++j) fs_out[j] = tc_sigmoid(z4[j]);
+      fs_out[3] = z4[3];
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        fs_out[j] = A.fs.act[j] == 0 ? z4[j] : (A.fs.act[j] == 1 ? tc_sigmoid(z4[j]) : tc_exp(z4[j]));
+    }
     float alpha;
     if (!A.use_opacity) alpha = aterm;
     else if (A.refine_opacity) alpha = tc_sigmoid(fs_out[3] + aterm);
@@ -481,20 +487,33 @@ __global__ void __launch_bounds__(128 * TG, TG == 1 ? 4 : (TG == 2 ? 3 : 2)) k_s
   uint32_t mma_phase = 0, tma_phase = 0;
   bool phi_smem = false, tab_smem = false;
   unsigned long long n_fs = 0;
+  const unsigned lane = tid & 31;
+  // hits of instance q (its queue may have overflowed: capped), read by the
+  // lanes of every warp in chunks of 32 instances and shared by shuffles
+  auto inst_hits = [&](int q) -> unsigned {
+    return q < args.n_inst ? (unsigned)min((long long)args.counts[q], args.qoff[q + 1] - args.qoff[q]) : 0u;
+  };
   long long total_tiles = 0;
-  for (int q = 0; q < args.n_inst; ++q)
-    total_tiles += (min((long long)args.counts[q], args.qoff[q + 1] - args.qoff[q]) + 127) / 128;
+  for (int b0 = 0; b0 < args.n_inst; b0 += 32)
+    total_tiles += __reduce_add_sync(0xffffffffu, (inst_hits(b0 + (int)lane) + 127u) / 128u);
   const long long tile_lo = total_tiles * blockIdx.x / gridDim.x;
   const long long tile_hi = total_tiles * (blockIdx.x + 1) / gridDim.x;
   // walk the instances overlapping [tile_lo, tile_hi)
   long long t_skip = tile_lo, left = tile_hi - tile_lo;
+  unsigned lane_hits = 0;
   for (int k = 0; k < args.n_inst && left > 0; ++k) {
-    const unsigned cnt = (unsigned)min((long long)args.counts[k], args.qoff[k + 1] - args.qoff[k]);
+    if ((k & 31) == 0) lane_hits = inst_hits(k + (int)lane);
+    const unsigned cnt = __shfl_sync(0xffffffffu, lane_hits, k & 31);
     const long long nt = (cnt + 127) / 128;
     if (t_skip >= nt) { t_skip -= nt; continue; }
     const long long first = t_skip, n_here = min(nt - first, left);
     t_skip = 0;
     left -= n_here;
+    // this group's first record, in flight while the tables are staged
+    const HitRec *recs = args.queue + args.qoff[k];
+    long long r = (first + g) * 128 + gt;
+    HitRec cur, nxt;
+    if (g < n_here && r < cnt) cur = recs[r];
     // the instance's asset record and tables, once per CTA (record as shared
     // memory: the tile loop's field reads never miss a gather-thrashed L1)
     __syncthreads();
@@ -509,19 +528,16 @@ __global__ void __launch_bounds__(128 * TG, TG == 1 ? 4 : (TG == 2 ? 3 : 2)) k_s
     tc_stage_asset(A, S, tma_phase, tid, phi_smem);
     tab_smem = tc_tab_bytes(A.N) != 0;   // the launch sized the carve for it
     __syncthreads();
-    const HitRec *recs = args.queue + args.qoff[k];
     const double scale = s_scale;
-    long long r = (first + g) * 128 + gt;
-    HitRec cur, nxt;
-    if (g < n_here && r < cnt) cur = recs[r];
+    const bool std_heads = A.fs.act[0] == NOLF_HEAD_SIGMOID && A.fs.act[1] == NOLF_HEAD_SIGMOID &&
+                           A.fs.act[2] == NOLF_HEAD_SIGMOID && A.fs.act[3] == NOLF_HEAD_IDENTITY;
     for (long long q = g; q < n_here; q += TG, r += 128 * TG) {
       const bool has_next = q + TG < n_here && r + 128 * TG < cnt;
       tc_shade_tile<TG>(args, A, S, Ag, tmem_g, S.bar_mma + g, mma_phase, gt, 1 + g, tab_smem, phi_smem, scale,
-                        cur, r < cnt, has_next ? recs + r + 128 * TG : nullptr, nxt, n_fs);
+                        cur, r < cnt, has_next ? recs + r + 128 * TG : nullptr, nxt, std_heads, n_fs);
       cur = nxt;
     }
   }
-  const unsigned lane = tid & 31;
 #pragma unroll
   for (int off = 16; off; off >>= 1) n_fs += __shfl_xor_sync(0xffffffffu, n_fs, off);
   if (lane == 0 && n_fs) {
