@@ -191,6 +191,10 @@ struct BvhBuilder {
       }
   }
   // writes the subtree over order[first, first+count) into nodes[slot]
+#ifndef NOLF_BVH_LEAF
+#define NOLF_BVH_LEAF 4
+#endif
+  static constexpr int kBvhLeaf = NOLF_BVH_LEAF;   // triangles per leaf at most
   void build(int slot, int first, int count) {
     double lo[3], hi[3];
     bounds(first, count, lo, hi);
@@ -200,7 +204,7 @@ struct BvhBuilder {
       n.lo[k] = nextafterf((float)(lo[k] - pad), -INFINITY);
       n.hi[k] = nextafterf((float)(hi[k] + pad), INFINITY);
     }
-    if (count <= 4) {
+    if (count <= kBvhLeaf) {
       n.first = first;
       n.count = count;
       nodes[(size_t)slot] = n;
