@@ -88,6 +88,12 @@ def parse():
                         "re-clears consumed frame buffers and polls the completion flags); default "
                         "0.9 for the 16-view configs (a 440 MB re-clear per step; measured 0.694 -> "
                         "0.677 ms on 4 GPUs, config 5), else 1")
+    p.add_argument("--march-order", default="auto", choices=["auto", "spatial", "heavy"],
+                   help="live-chunk order of the marcher (NOLF_OPT_MARCH_ORDER): auto = heaviest first "
+                        "for launches of a few CTA waves (multi-GPU shards), spatial otherwise")
+    p.add_argument("--chunk-cost", type=int, default=1, choices=[0, 1],
+                   help="heaviest-first buckets from the previous frame's measured per-chunk march "
+                        "durations (1) or from candidate-instance counts (0)")
     p.add_argument("--frames", type=int, default=3,
                    help="p2p + flags: frame buffers in rank 0's ring (a peer renders frame seq once "
                         "frame seq - frames was consumed and re-cleared)")
@@ -596,6 +602,9 @@ def run_ours(args):
     scene, views, W, H, desc = workload(args)
     n_views = len(views(0))
     R = SceneRenderer(scene)
+    from paper_2303_04086_b200 import render as RM
+    RM.set_option(N.OPT_MARCH_ORDER, {"auto": 0, "spatial": 1, "heavy": 2}[args.march_order])
+    RM.set_option(N.OPT_CHUNK_COST, args.chunk_cost)
     if args.mlp == "bf16":
         R.mlp_mode(N.MLP_BF16)
     T = args.tile

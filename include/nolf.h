@@ -243,6 +243,8 @@ int nolf_eval_diffuse(nolf_asset_t asset, const double *points, int64_t n, float
 #define NOLF_OPT_COMPOSE_SLOTS 2  /* live-chunk compose slots per thread: 0 auto, 4 or 8 */
 #define NOLF_OPT_HEAVY_WAVES 3    /* auto order: heaviest-first below this many CTA waves (3) */
 #define NOLF_OPT_MARCH_SPLIT 4    /* CTAs per live 128-slot chunk in the marcher: 1 (128 threads) or 2 (64) */
+#define NOLF_OPT_CHUNK_COST 5     /* heaviest-first order: 1 by the previous frame's measured per-chunk
+                                     marcher durations (default), 0 by candidate-instance counts */
 int nolf_set_option(int32_t key, int64_t value);
 
 /* Device-side failures fail loudly.  The kernels count (never silently

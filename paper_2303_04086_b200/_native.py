@@ -22,7 +22,7 @@ NOLF_EINVAL, NOLF_ESTATE, NOLF_EDATA, NOLF_ECUDA, NOLF_ENOMEM, NOLF_ECAPACITY = 
 HEAD_ACT = {"identity": 0, "sigmoid": 1, "exponential": 2}
 ABI_VERSION = 4              # NOLF_ABI_VERSION of include/nolf.h
 # nolf_set_option keys (include/nolf.h)
-OPT_MARCH_ORDER, OPT_COMPOSE_SLOTS, OPT_HEAVY_WAVES, OPT_MARCH_SPLIT = 1, 2, 3, 4
+OPT_MARCH_ORDER, OPT_COMPOSE_SLOTS, OPT_HEAVY_WAVES, OPT_MARCH_SPLIT, OPT_CHUNK_COST = 1, 2, 3, 4, 5
 MLP_FP32, MLP_BF16 = 0, 1
 
 

@@ -379,6 +379,7 @@ struct Workspace {
   unsigned int *counts;        // per-instance hit counts, then [n_inst]: live chunks, [n_inst+1]: fetch
   unsigned int *chunk_list;    // scene: live 128-slot chunks
   uint8_t *chunk_live;
+  unsigned *chunk_cost;        // last frame's per-chunk CTA durations (fixed offset: persists across frames)
   HitRec *queue;
   uint8_t *nhit;
   float *lrgba, *ldepth;
@@ -399,6 +400,7 @@ size_t ws_layout(int n_inst, long long queue_recs, int layers, long long P, char
   const size_t n_chunks = (size_t)((P > 0 ? P : 1) + 127) / 128;
   char *chunk_list = take(sizeof(unsigned) * n_chunks * kChunkBuckets);
   char *chunk_live = take(n_chunks);
+  char *chunk_cost = take(sizeof(unsigned) * n_chunks);
   char *queue = take(sizeof(HitRec) * (size_t)(queue_recs > 0 ? queue_recs : 1));
   char *nhit = take(layers > 0 ? n : 1);
   char *lrgba = take(sizeof(float) * 4 * n * (size_t)layers);
@@ -407,6 +409,7 @@ size_t ws_layout(int n_inst, long long queue_recs, int layers, long long P, char
     w->counts = reinterpret_cast<unsigned *>(counts);
     w->chunk_list = reinterpret_cast<unsigned *>(chunk_list);
     w->chunk_live = reinterpret_cast<uint8_t *>(chunk_live);
+    w->chunk_cost = reinterpret_cast<unsigned *>(chunk_cost);
     w->queue = reinterpret_cast<HitRec *>(queue);
     w->nhit = reinterpret_cast<uint8_t *>(nhit);
     w->lrgba = reinterpret_cast<float *>(lrgba);
@@ -865,6 +868,8 @@ struct Options {
   int march_order = 0;         // 0 auto, 1 spatial list, 2 heavy-first buckets
   int compose_slots = 0;       // live-chunk compose slots per thread: 0 auto, 4, 8
   int march_split = 1;         // CTAs per live chunk in the chunked marcher: 1 or 2
+  int chunk_cost = 1;          // heavy-first buckets: 1 last frame's CTA durations, 0 candidate counts
+  long long cost_waves = 96;   // auto order: duration-ordered heaviest-first below this many CTA waves
   bool init = false;
 };
 thread_local Options g_opt;
@@ -874,6 +879,8 @@ Options &options() {
     if (const char *e = getenv("NOLF_HEAVY_WAVES")) g_opt.heavy_waves = atoll(e);
     if (const char *e = getenv("NOLF_COMPOSE_G")) g_opt.compose_slots = atoi(e);
     if (const char *e = getenv("NOLF_MARCH_SPLIT")) g_opt.march_split = atoi(e) == 2 ? 2 : 1;
+    if (const char *e = getenv("NOLF_CHUNK_COST")) g_opt.chunk_cost = atoi(e) ? 1 : 0;
+    if (const char *e = getenv("NOLF_COST_WAVES")) g_opt.cost_waves = atoll(e);
     g_opt.init = true;
   }
   return g_opt;
@@ -1241,9 +1248,17 @@ int launch_march_shade(int mode, const NolfInstance *ins, int n_inst, const Nolf
     // a launch of only a few waves is bounded by its heaviest CTAs: start them
     // first (NOLF_OPT_MARCH_ORDER forces either order)
     const Options &opt = options();
+    // auto: heaviest first by the previous frame's measured chunk durations
+    // below cost_waves CTA waves (longer launches keep the spatial order's
+    // cache locality: measured on 16 single-asset 4K views), or by candidate
+    // counts below heavy_waves
+    const long long wave = (long long)NOLF_MARCH_MINB * num_sms();
     ma.heavy_first = opt.march_order == 1 ? 0 : opt.march_order == 2 ? 1
-                   : (le.last < opt.heavy_waves * NOLF_MARCH_MINB * num_sms() ? 1 : 0);
+                   : ((opt.chunk_cost && le.last < opt.cost_waves * wave) || le.last < opt.heavy_waves * wave ? 1 : 0);
     g_last_launch[1] = ma.heavy_first;
+    // heavy-first buckets from the previous frame's measured CTA durations
+    // (frames of a session are coherent; the first one uses candidate counts)
+    ma.chunk_cost = ma.heavy_first && opt.chunk_cost ? w.chunk_cost : nullptr;
     k_cull_chunks<<<(unsigned)((n_chunks + 127) / 128), 128, 0, st>>>(ma, n_chunks, w.chunk_live, w.chunk_list,
                                                                       w.counts + n_inst);
     CUDA_TRY(cudaGetLastError());
@@ -1495,6 +1510,10 @@ int nolf_set_option(int32_t key, int64_t value) {
     case NOLF_OPT_HEAVY_WAVES:
       if (value < 0) return fail(NOLF_EINVAL, "heavy waves must be >= 0");
       o.heavy_waves = value;
+      return 0;
+    case NOLF_OPT_CHUNK_COST:
+      if (value != 0 && value != 1) return fail(NOLF_EINVAL, "chunk cost must be 0 or 1");
+      o.chunk_cost = (int)value;
       return 0;
     default:
       return fail(NOLF_EINVAL, "unknown option %d", key);

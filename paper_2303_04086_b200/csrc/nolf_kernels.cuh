@@ -69,6 +69,8 @@ struct MarchArgs {
   unsigned *fetch;
   long long list_stride;
   int heavy_first;             // walk the buckets (most candidates first) instead of the spatial list
+  unsigned *chunk_cost;        // per chunk: the CTA's duration (clock cycles) in the last frame that marched
+                               // it, or 0 -- the heavy-first buckets of the next frame (null: candidate counts)
   int max_layers;              // scene mode: compose layers per pixel slot in the workspace
   unsigned *errors;            // sticky device error counters (kErr*), never NULL
 };
@@ -93,7 +95,13 @@ __device__ __forceinline__ bool tile_valid(const TileParams &tp, const CamParams
          (long long)(tp.x1 - tp.x0) * (tp.y1 - tp.y0) <= stride;
 }
 
-constexpr int kChunkBuckets = 8;   // candidate-count buckets (the last one: >= 7 instances)
+#ifndef NOLF_CHUNK_BUCKETS
+#define NOLF_CHUNK_BUCKETS 8
+#endif
+// heavy-first buckets of live chunks (1 .. kChunkBuckets-1; the list keeps one
+// region per bucket): the previous frame's CTA duration class, else the
+// candidate-instance count (the last bucket: >= kChunkBuckets-1 instances)
+constexpr int kChunkBuckets = NOLF_CHUNK_BUCKETS;
 
 // it-th live chunk: spatial order (list region 0, best cache locality) or
 // heavy-first (most candidate instances first, so the longest CTAs start
@@ -890,6 +898,7 @@ __global__ void __launch_bounds__(128) k_cull_chunks(MarchArgs args, long long n
     }
     chunk_live[c] = live ? 1 : 0;
   }
+  const unsigned prev_cost = (c < n_chunks && args.chunk_cost) ? args.chunk_cost[c] : 0u;
   const unsigned lane = threadIdx.x & 31;
   const unsigned ballot = __ballot_sync(0xffffffffu, live);
   if (ballot) {
@@ -897,8 +906,18 @@ __global__ void __launch_bounds__(128) k_cull_chunks(MarchArgs args, long long n
     if (lane == __ffs(ballot) - 1) sbase = atomicAdd(count, (unsigned)__popc(ballot));
     sbase = __shfl_sync(0xffffffffu, sbase, __ffs(ballot) - 1);
     if (live) list[sbase + __popc(ballot & ((1u << lane) - 1u))] = (unsigned)c;
-    if (live && args.heavy_first) {   // and this chunk's candidate-count bucket (regions 1..)
-      const int b = min(ncand, kChunkBuckets - 1);
+    if (live && args.heavy_first) {   // and this chunk's bucket (regions 1..): heaviest last frame first
+      int b = min(ncand, kChunkBuckets - 1);
+      if (args.chunk_cost) {
+        const unsigned cyc = prev_cost;
+        // CTA duration classes (0: never marched -> candidate count): octaves
+        // [2^12, 2^13) -> 1 ... with 8 buckets, half octaves from 2^12 with 16
+        if (cyc) {
+          const int msb = 31 - __clz((int)min(cyc, 0x7fffffffu));
+          const int cls = kChunkBuckets >= 16 ? 2 * msb + (int)((cyc >> max(msb - 1, 0)) & 1u) - 23 : msb - 11;
+          b = min(max(cls, 1), kChunkBuckets - 1);
+        }
+      }
       const unsigned peers = __match_any_sync(ballot, b);
       const int leader = __ffs(peers) - 1;
       unsigned base = 0;
@@ -907,6 +926,7 @@ __global__ void __launch_bounds__(128) k_cull_chunks(MarchArgs args, long long n
       list[(long long)b * n_chunks + base + __popc(peers & ((1u << lane) - 1u))] = (unsigned)c;
     }
   }
+  if (prev_cost) args.chunk_cost[c] = 0u;   // this frame's marcher records afresh
 }
 
 // Scene marcher over the compacted live chunks: one CTA per list entry.  The
@@ -917,9 +937,13 @@ template <bool GROUPS = false>
 __global__ void __launch_bounds__(kMarchThreads, NOLF_MARCH_MINB) k_march_chunks(MarchArgs args) {
   const unsigned n = *args.n_chunks;
   stat_cta_start();
-  for (unsigned it = blockIdx.x; it < n; it += gridDim.x)   // normally one pass: the grid is sized
-    march_chunk<kModeScene, GROUPS>(args, chunk_at(args.chunks, args.n_chunks, args.list_stride, it, args.heavy_first),
-                                    false);
+  for (unsigned it = blockIdx.x; it < n; it += gridDim.x) {  // normally one pass: the grid is sized
+    const long long t0 = clock64();
+    const unsigned chunk = chunk_at(args.chunks, args.n_chunks, args.list_stride, it, args.heavy_first);
+    march_chunk<kModeScene, GROUPS>(args, chunk, false);
+    if (args.chunk_cost && (threadIdx.x & 31) == 0)         // the CTA's duration = its slowest warp's
+      atomicMax(args.chunk_cost + chunk, (unsigned)min(clock64() - t0, 0x7fffffffll) | 1u);
+  }
   stat_cta_end();
 }
 
