@@ -1746,6 +1746,12 @@ extern "C" int nolf_stats_cta(unsigned long long *start, unsigned long long *end
   cudaMemcpyToSymbol(nolf::g_cta_end, z, sizeof(z));
   return (int)cudaGetLastError();
 }
+extern "C" int nolf_stats_work(unsigned *out, int n) {   // g_cta_work[0..n) (then zeroed)
+  cudaMemcpyFromSymbol(out, nolf::g_cta_work, sizeof(unsigned) * 4 * n);
+  static unsigned z[4 << 20];
+  cudaMemcpyToSymbol(nolf::g_cta_work, z, sizeof(z));
+  return (int)cudaGetLastError();
+}
 extern "C" int nolf_stats_read(unsigned long long *out, int reset) {
   cudaMemcpyFromSymbol(out, nolf::g_stats, sizeof(unsigned long long) * 16);
   if (reset) {

@@ -188,6 +188,11 @@ __device__ __forceinline__ bool samples_inside_unit(const double o[3], const dou
 #ifdef NOLF_STATS   // diagnostic build only: march work counters (-DNOLF_STATS_CTR) / CTA spans
 __device__ unsigned long long g_stats[16];
 __device__ unsigned long long g_cta_start[1 << 20], g_cta_end[1 << 20];
+__device__ unsigned g_cta_work[1 << 20][4];   // per CTA: warp-instance passes, max lane iterations
+                                               // of one march, max lane iterations over all, max instances
+#define NOLF_ITER(x) (x)
+#else
+#define NOLF_ITER(x) ((void)0)
 #endif
 #if defined(NOLF_STATS) && defined(NOLF_STATS_CTR)
 #define NOLF_STAT(k, v) atomicAdd(&g_stats[k], (unsigned long long)(v))
@@ -252,6 +257,9 @@ struct MarchOut {
   double alpha_c, t_hit;
   long long samples;
   bool hit;
+#ifdef NOLF_STATS
+  unsigned iters;
+#endif
 };
 
 template <bool CLIP, bool POW2>
@@ -424,7 +432,11 @@ __device__ __forceinline__ MarchOut march_p2(const DevAsset &A, const double oG[
   int samples = 0;
   int i = i_start;
   double ti = (double)i_start + 0.5;          // i + 0.5, exact
+#ifdef NOLF_STATS
+  unsigned iters_cta = 0;
+#endif
   for (;;) {
+    NOLF_ITER(++iters_cta);
     const double t_mid = __dadd_rn(t_near, __dmul_rn(ti, delta));
     if (!(t_mid < t_lim)) break;
     NOLF_STAT(7, 1);
@@ -505,6 +517,10 @@ __device__ __forceinline__ MarchOut march_p2(const DevAsset &A, const double oG[
     ++i;
     ti += 1.0;
   }
+#ifdef NOLF_STATS
+  atomicMax(&g_cta_work[blockIdx.x & ((1 << 20) - 1)][1], iters_cta);
+  r.iters = iters_cta;
+#endif
   r.alpha_c = alpha_c;
   r.samples = samples;
   r.hit = alpha_c > A.alpha_floor;
@@ -761,6 +777,9 @@ __device__ __forceinline__ void march_chunk(const MarchArgs &args, unsigned chun
   }
   unsigned samples_total = 0;  // per lane (< 2^32: at most n_inst * samples per ray)
   unsigned ordinal = 0;
+#ifdef NOLF_STATS
+  unsigned st_iters = 0, st_inst = 0, st_pass = 0;
+#endif
   // candidates OR-ed over the warp so the instance loop below is
   // warp-uniform (ascending = scene order, so layer ordinals match); in
   // groups of 64 instances
@@ -781,6 +800,7 @@ __device__ __forceinline__ void march_chunk(const MarchArgs &args, unsigned chun
     MarchOut mr{0.0, __longlong_as_double(0x7ff0000000000000ll), 0, false};
     const bool live = (lane_mask >> kb) & 1ull;
     if (lane == 0) NOLF_STAT(8, 1);
+    NOLF_ITER(++st_pass);
     bool boxhit = false;
     if (live) {
       NOLF_STAT(0, 1);
@@ -807,6 +827,10 @@ __device__ __forceinline__ void march_chunk(const MarchArgs &args, unsigned chun
       unit = to_grid_units(A, o, d, invf);
       mr = run_march(A, o, d, invf, sp, args.use_zmask);
       samples_total += (unsigned)mr.samples;
+#ifdef NOLF_STATS
+      st_iters += mr.iters;
+      ++st_inst;
+#endif
       hit = mr.hit;
     }
     if (args.out_hit) {        // march_rays outputs (MarchResult, lightfield.py:101-110)
@@ -846,6 +870,14 @@ __device__ __forceinline__ void march_chunk(const MarchArgs &args, unsigned chun
   }
   }  // instance groups
   if (MODE == kModeScene && valid) args.nhit[gid] = (uint8_t)ordinal;
+#ifdef NOLF_STATS
+  {
+    unsigned *w = g_cta_work[blockIdx.x & ((1 << 20) - 1)];
+    if (lane == 0) atomicAdd(w + 0, st_pass);
+    atomicMax(w + 2, st_iters);
+    atomicMax(w + 3, st_inst);
+  }
+#endif
   // march_samples counter (lightfield.py:430-431)
   const unsigned warp_samples = __reduce_add_sync(0xffffffffu, samples_total);
   if (lane == 0 && warp_samples && args.counters) atomicAdd(args.counters + 3, (unsigned long long)warp_samples);
