@@ -469,16 +469,23 @@ def run_e2e_sparse(args, R, N, cam_arrays, n_cam, mine, my_tiles, n_max, stride,
     n_of = [0] * NP
     bytes_d2h = [0]
 
+    ev_dev = []                          # (start, end) device events of every render (diagnostic)
+
     def render(k):
         b = k % NP
         if ev_c[b] is not None:
             comp.wait_event(ev_c[b])                 # pack buffer b copied out (step k-2)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e0.record(comp)
         o = {"pack": dpack[b], "pack_ids": dids[b], "pack_count": dcnt[b], "counters": out["counters"]}
         if flush is not None:
-            flush.fill_(k & 0xFF)                    # L2 evicted before every frame, inside the wall clock
+            flush.fill_(k & 0x7F)                    # L2 evicted before every frame, inside the wall clock
         R.render(cam_arrays[k % n_cam], my_tiles, n_max, stride, o, frame_layout=True, prefilled=True)
         N.check(N.lib().nolf_store_u32(hcnt_dev.value + 8 * b, dcnt[b].data_ptr(), 2, comp.cuda_stream))
         ev_r[b].record(comp)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e1.record(comp)
+        ev_dev.append((e0, e1))
 
     tm = {"wait_render": 0.0, "scatter": 0.0, "wait_copy": 0.0, "enqueue": 0.0}
 
@@ -538,10 +545,19 @@ def run_e2e_sparse(args, R, N, cam_arrays, n_cam, mine, my_tiles, n_max, stride,
     bytes_d2h[0] = 0
     for key in tm:
         tm[key] = 0.0
+    ev_dev.clear()
+    N.check(N.lib().nolf_profile(1))
     t0 = time.perf_counter()
     run(args.steps)
     el = time.perf_counter() - t0
     torch.cuda.synchronize()
+    kms = (ctypes.c_float * 3)()
+    n_prof = N.lib().nolf_profile_read(kms)
+    N.check(N.lib().nolf_profile(0))
+    e2e_kernel_us = [round(1e3 * float(v) / max(n_prof, 1), 1) for v in kms[:3]]
+    dev_us = 1e3 * float(np.mean([a.elapsed_time(b) for a, b in ev_dev])) if ev_dev else None
+    gap_us = (1e3 * float(np.mean([ev_dev[i][1].elapsed_time(ev_dev[i + 1][0]) for i in range(len(ev_dev) - 1)]))
+              if len(ev_dev) > 1 else None)
     te = torch.tensor([el], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
@@ -559,6 +575,10 @@ def run_e2e_sparse(args, R, N, cam_arrays, n_cam, mine, my_tiles, n_max, stride,
                     "scatter k-1 pipelined, the scatter on its own host thread)"),
            "full_frame_bytes": int(npix * 6),
            "host_us_per_step": {key: round(v / args.steps * 1e6, 1) for key, v in tm.items()},
+           "device_us_per_step": {"render": round(dev_us, 1) if dev_us is not None else None,
+                                  "gap_between_renders": round(gap_us, 1) if gap_us is not None else None,
+                                  "k_march": e2e_kernel_us[0], "k_shade": e2e_kernel_us[1],
+                                  "k_compose": e2e_kernel_us[2]},
            "host_threads": int(os.environ.get("NOLF_HOST_THREADS",
                                               max(1, os.cpu_count() // (2 * int(os.environ.get("LOCAL_WORLD_SIZE", "1"))))))}
     last = (args.steps - 1) % 2
@@ -633,7 +653,11 @@ def run_ours(args):
     NPX = n_views * H * W
     frames = [(torch.empty((NPX, 4), dtype=torch.uint8, device=dev),
                torch.empty((NPX,), dtype=torch.int16, device=dev)) for _ in range(2)]
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    # 256 MiB (2x the 126 MB L2) written as int32: 16 B vector stores, ~7 TB/s
+    # (a uint8 fill runs at half that rate)
+    flush = torch.empty(64 << 20, dtype=torch.int32, device=dev)
+    if os.environ.get("NOLF_FLUSH_U8"):             # diagnostic: the byte-wise fill
+        flush = flush.view(torch.uint8)
     n_cam = args.warmup + args.steps + 4
     cam_arrays = [R.camera_array(views(k)) for k in range(n_cam)]
     R.reserve(cam_arrays, n_max * stride)
@@ -870,7 +894,7 @@ def run_ours(args):
     # each step is bracketed by device events, the L2 flush sits between them
     for k in range(args.steps):
         if not args.no_flush:
-            flush.fill_(k & 0xFF)                          # evict L2 (untimed)
+            flush.fill_(k & 0x7F)                          # evict L2 (untimed)
         ev[k][0].record()
         step(args.warmup + k, k % 2)
         ev[k][1].record()
