@@ -12,6 +12,6 @@ case $STEPS in *a*) for c in 1 2 3 5; do timeout 400 python bench.py --config $c
 case $STEPS in *r*) timeout 400 python bench.py --impl reference --steps 20 --warmup 5 > gpurun_out/${P}_bench_ref.json 2> gpurun_out/${P}_bench_ref.err;; esac
 case $STEPS in *n*)
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/${P}_launches.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/${P}_ncu_launch.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k "regex:^k_(cull_chunks|march_chunks|shade_tc|compose_live)" -c 4 -o gpurun_out/${P}_cfg4 python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/${P}_ncu_full.log 2>&1;;
+timeout 900 ncu --set full --clock-control none --import-source on -k "regex:^k_(cull_chunks|march_chunks|shade_tc|compose_live)" -s 12 -c 4 -o gpurun_out/${P}_cfg4 python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/${P}_ncu_full.log 2>&1;;
 esac
 tail -5 gpurun_out/${P}_pytest_gpu.log; tail -2 gpurun_out/${P}_smoke.log; cat gpurun_out/${P}_bench_cfg4.json | head -c 3000
