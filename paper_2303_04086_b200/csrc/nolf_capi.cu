@@ -9,6 +9,7 @@
 #include <cstring>
 #include <string>
 #include <vector>
+#include <functional>
 
 #include "../../include/nolf.h"
 #include "nolf_kernels.cuh"
@@ -240,6 +241,7 @@ int upload_mesh(NolfAsset *A, const NolfAssetDesc &d, DevMesh *out) {
   out->nodes = nullptr;
   out->tri = nullptr;
   out->n_tri = 0;
+  out->nodes4 = nullptr;
   if (d.mesh_n_triangles <= 0) return 0;
   if (!d.mesh_vertices || !d.mesh_triangles || d.mesh_n_vertices <= 0)
     return fail(NOLF_EINVAL, "mesh proxy: missing arrays");
@@ -285,6 +287,56 @@ int upload_mesh(NolfAsset *A, const NolfAssetDesc &d, DevMesh *out) {
     }
     if (depth > 28) return fail(NOLF_EINVAL, "mesh proxy: BVH depth %d exceeds the traversal stack", depth);
   }
+  // the same tree collapsed 4-wide for the warp walk: each 4-wide node takes
+  // the binary node's children, then repeatedly the children of its largest
+  // inner child, up to 4 slots (leaves stay leaves)
+  std::vector<Bvh4Node> n4;
+  int depth4 = 0;
+  std::function<int(int, int)> collapse = [&](int b, int lvl) -> int {
+    depth4 = std::max(depth4, lvl);
+    const int idx = (int)n4.size();
+    n4.push_back(Bvh4Node{});
+    std::vector<int> kids;
+    if (B.nodes[(size_t)b].count > 0) kids.push_back(b);    // a leaf root
+    else kids = {B.nodes[(size_t)b].first, B.nodes[(size_t)b].first + 1};
+    auto area = [&](int k) {
+      const BvhNode &c = B.nodes[(size_t)k];
+      const double ex = c.hi[0] - c.lo[0], ey = c.hi[1] - c.lo[1], ez = c.hi[2] - c.lo[2];
+      return ex * ey + ey * ez + ez * ex;
+    };
+    while (kids.size() < 4) {
+      int bi = -1;
+      for (int i = 0; i < (int)kids.size(); ++i)
+        if (B.nodes[(size_t)kids[i]].count == 0 && (bi < 0 || area(kids[i]) > area(kids[bi]))) bi = i;
+      if (bi < 0) break;
+      const int k = kids[(size_t)bi];
+      kids.erase(kids.begin() + bi);
+      kids.push_back(B.nodes[(size_t)k].first);
+      kids.push_back(B.nodes[(size_t)k].first + 1);
+    }
+    Bvh4Node nn{};
+    for (int j = 0; j < 4; ++j) {
+      for (int a = 0; a < 3; ++a) nn.lo[a][j] = nn.hi[a][j] = 0.f;
+      nn.child[j] = -1;
+      nn.count[j] = -1;
+    }
+    for (int j = 0; j < (int)kids.size(); ++j) {
+      const BvhNode c = B.nodes[(size_t)kids[(size_t)j]];
+      for (int a = 0; a < 3; ++a) { nn.lo[a][j] = c.lo[a]; nn.hi[a][j] = c.hi[a]; }
+      if (c.count > 0) {
+        nn.child[j] = c.first;
+        nn.count[j] = c.count;
+      } else {
+        nn.child[j] = collapse(kids[(size_t)j], lvl + 1);
+        nn.count[j] = 0;
+      }
+    }
+    n4[(size_t)idx] = nn;
+    return idx;
+  };
+  collapse(0, 0);
+  if (3 * (depth4 + 1) + 1 > kMesh4Stack)
+    return fail(NOLF_EINVAL, "mesh proxy: 4-wide BVH depth %d exceeds the traversal stack", depth4);
   std::vector<double> tri(9ull * nt);
   for (int i = 0; i < nt; ++i)
     for (int v = 0; v < 3; ++v)
@@ -295,6 +347,9 @@ int upload_mesh(NolfAsset *A, const NolfAssetDesc &d, DevMesh *out) {
   int rc;
   if ((rc = A->upload(B.nodes.data(), B.nodes.size(), &nd))) return rc;
   if ((rc = A->upload(tri.data(), tri.size(), &tp))) return rc;
+  Bvh4Node *nd4;
+  if ((rc = A->upload(n4.data(), n4.size(), &nd4))) return rc;
+  out->nodes4 = nd4;
   out->nodes = nd;
   out->tri = tp;
   out->n_tri = nt;

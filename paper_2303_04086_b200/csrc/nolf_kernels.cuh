@@ -813,8 +813,10 @@ __device__ __forceinline__ void march_chunk(const MarchArgs &args, unsigned chun
       const double tm = sp.t_near;
 #elif defined(NOLF_MESH_PER_THREAD)
       const double tm = boxhit ? mesh_first_hit(A.mesh, o, d, args.errors + kErrBvh) : -1.0;
-#else
+#elif defined(NOLF_MESH_BINARY)
       const double tm = mesh_first_hit_warp(A.mesh, o, d, boxhit, args.errors + kErrBvh);
+#else
+      const double tm = mesh_first_hit_warp4(A.mesh, o, d, boxhit, args.errors + kErrBvh);
 #endif
       if (boxhit) {
         if (tm < 0.0) boxhit = false;
