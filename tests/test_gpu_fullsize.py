@@ -158,3 +158,47 @@ def test_zodiac_encoded_frame_timed_variants(zodiac, mode, order, slots):
     lsb = int(np.abs(r8.astype(np.int32) - e8.astype(np.int32)).max())
     assert lsb <= (1 if mode == "fp32" else 3), f"rgba8 off by {lsb} LSB"
     assert int(cnt[3]) == int(g["counters"][3])
+
+
+def test_zodiac_chunk_order_from_previous_frames_is_exact(zodiac):
+    """The bench's default launch: from the second frame on, the live chunks
+    are marched heaviest-first by the previous frame's measured durations
+    (NOLF_OPT_CHUNK_COST).  Over a moving camera every frame must equal the
+    spatial-order render bit for bit (order changes which CTA runs when,
+    never what a pixel computes), and the first frame must equal the
+    reference frame as above."""
+    import torch
+    sys.path.insert(0, ROOT)
+    import bench
+    scene, g = zodiac
+    R.set_mlp_mode("bf16")
+    try:
+        r = R.SceneRenderer(scene)
+        r_sp = R.SceneRenderer(scene)
+        W, H = 3840, 2160
+        tiles = torch.from_numpy(R.frame_tiles(W, H, 32)).to(r.device)
+        npx = W * H
+
+        def frame(rr, cam, order):
+            R.set_option(N.OPT_MARCH_ORDER, order)
+            out = {"rgba8": torch.zeros((npx, 4), dtype=torch.uint8, device=rr.device),
+                   "depth16": torch.full((npx,), -1, dtype=torch.int16, device=rr.device),
+                   "counters": torch.zeros(4, dtype=torch.int64, device=rr.device)}
+            rr.render([cam], tiles, len(tiles), 1024, out, frame_layout=True, prefilled=True)
+            launch = R.last_launch()
+            return out, launch
+
+        seen_cost_order = False
+        for k in range(4):
+            cam = bench.camera_for_step(k, W, H)
+            a, la = frame(r, cam, 0)               # auto: heaviest first by the last frame's durations
+            b, lb = frame(r_sp, cam, 1)            # spatial order
+            assert lb["march_order"] == "spatial"
+            seen_cost_order |= la["march_order"] == "heavy-first" and k > 0
+            assert torch.equal(a["rgba8"], b["rgba8"]) and torch.equal(a["depth16"], b["depth16"]), k
+            assert torch.equal(a["counters"], b["counters"]), k
+        assert seen_cost_order
+        r.check()
+    finally:
+        R.set_mlp_mode("fp32")
+        R.set_option(N.OPT_MARCH_ORDER, 0)

@@ -60,3 +60,17 @@ def test_deflate_matches_python_zlib():
     assert render.deflate(np.ascontiguousarray(g["scene_rgba8"]).tobytes()) == g["scene_deflate_rgba"].tobytes()
     assert render.deflate(np.ascontiguousarray(g["scene_depth16"]).astype("<u2").tobytes()) == \
         g["scene_deflate_depth"].tobytes()
+
+
+def test_launch_options_are_validated_without_gpu():
+    lib = _native.lib()
+    for key, good, bad in ((_native.OPT_MARCH_ORDER, 2, 3), (_native.OPT_COMPOSE_SLOTS, 8, 5),
+                           (_native.OPT_MARCH_SPLIT, 2, 3), (_native.OPT_CHUNK_COST, 0, 2),
+                           (_native.OPT_HEAVY_WAVES, 3, -1)):
+        assert lib.nolf_set_option(key, good) == 0
+        assert lib.nolf_set_option(key, bad) == _native.NOLF_EINVAL
+    assert lib.nolf_set_option(99, 0) == _native.NOLF_EINVAL
+    # back to the defaults (options are per thread)
+    for key, v in ((_native.OPT_MARCH_ORDER, 0), (_native.OPT_COMPOSE_SLOTS, 0), (_native.OPT_MARCH_SPLIT, 1),
+                   (_native.OPT_CHUNK_COST, 1), (_native.OPT_HEAVY_WAVES, 3)):
+        assert lib.nolf_set_option(key, v) == 0
