@@ -126,12 +126,40 @@ int upload_atlas(NolfAsset *A, const NolfAtlasDesc &d, int channels, DevAtlas *o
   }
   std::vector<uint8_t> dist((size_t)ncell);
   for (int64_t i = 0; i < ncell; ++i) dist[(size_t)i] = (uint8_t)std::min(f[(size_t)i], 255);
+  // octant fields: r_o(c) = 0 when c is occupied, else 1 + the minimum of r_o
+  // over the 7 neighbours c + e_S (S a nonempty subset of the axes, stepping
+  // in the octant's direction; outside the grid counts as unbounded): the
+  // cube of r_o(c) cells per axis anchored at c in that direction is empty
+  std::vector<uint8_t> odist(8 * (size_t)ncell);
+  for (int o = 0; o < 8; ++o) {
+    const int sx = (o & 1) ? -1 : 1, sy = (o & 2) ? -1 : 1, sz = (o & 4) ? -1 : 1;
+    uint8_t *r8 = odist.data() + (size_t)o * ncell;
+    for (int ix = 0; ix < b; ++ix)
+      for (int iy = 0; iy < b; ++iy)
+        for (int iz = 0; iz < b; ++iz) {
+          const int x = sx > 0 ? b - 1 - ix : ix, y = sy > 0 ? b - 1 - iy : iy, z = sz > 0 ? b - 1 - iz : iz;
+          int m = 255;
+          if (d.index[at3(x, y, z)] != -1) {
+            m = -1;
+          } else {
+            for (int S = 1; S < 8; ++S) {
+              const int nx = x + ((S & 1) ? sx : 0), ny = y + ((S & 2) ? sy : 0), nz = z + ((S & 4) ? sz : 0);
+              if (nx < 0 || ny < 0 || nz < 0 || nx >= b || ny >= b || nz >= b) continue;
+              m = std::min(m, (int)r8[at3(nx, ny, nz)]);
+            }
+          }
+          r8[at3(x, y, z)] = (uint8_t)std::min(m + 1, 255);
+        }
+  }
   int32_t *idx;
   uint8_t *mac;
   float *cubes;
   int rc;
   if ((rc = A->upload(d.index, (size_t)ncell, &idx))) return rc;
   if ((rc = A->upload(dist.data(), dist.size(), &mac))) return rc;
+  uint8_t *omac;
+  if ((rc = A->upload(odist.data(), odist.size(), &omac))) return rc;
+  out->odist = omac;
   const size_t nc = (size_t)d.n_cubes * s * s * s * channels;
   if (nc == 0) {               // keep a valid pointer for empty atlases
     float z4[4] = {0, 0, 0, 0};

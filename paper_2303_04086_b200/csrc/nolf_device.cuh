@@ -21,6 +21,9 @@ struct DevAtlas {              // CubeAtlas (atlas.py:25-51)
   const float *cubes;          // n * s^3 * C
   const uint8_t *dist;         // b^3: Chebyshev distance (cells) to the nearest
                                // occupied cell, 0 = occupied, capped at 255
+  const uint8_t *odist;        // 8 x b^3 (octant-major): edge (cells) of the largest empty cube
+                               // anchored at the cell and extending in the octant's direction
+                               // (octant bit k set: axis k negative); 0 = occupied, capped at 255
   const uint32_t *zmask;       // per cube, r^3 bits: sub-voxel whose 8 corners are all 0
   int zwords;                  // 32-bit words per cube
   int lr;                      // log2(r) when b and r are both powers of two, else -1

@@ -432,6 +432,15 @@ __device__ __forceinline__ MarchOut march_p2(const DevAsset &A, const double oG[
   int samples = 0;
   int i = i_start;
   double ti = (double)i_start + 0.5;          // i + 0.5, exact
+#ifdef NOLF_CHEB_DIST
+  const uint8_t *dfield = at.dist;           // symmetric (Chebyshev) empty boxes
+#else
+  // empty cubes anchored at the cell in the ray's direction of travel: the
+  // samples between here and the box exit only move forward, so they stay
+  // inside it (no room is spent behind the ray)
+  const int oct = (dG[0] < 0.0 ? 1 : 0) | (dG[1] < 0.0 ? 2 : 0) | (dG[2] < 0.0 ? 4 : 0);
+  const uint8_t *dfield = at.odist + (size_t)oct * (size_t)(b * b * b);
+#endif
 #ifdef NOLF_STATS
   unsigned iters_cta = 0;
 #endif
@@ -455,14 +464,20 @@ __device__ __forceinline__ MarchOut march_p2(const DevAsset &A, const double oG[
       cell[k] = min(gi[k] >> lr, b - 1);
     }
     const int ci = (cell[0] * b + cell[1]) * b + cell[2];
-    const int dist = __ldg(at.dist + ci);
-    if (dist > 0) {            // every cell within Chebyshev radius dist-1 is empty: jump (verified)
+    const int dist = __ldg(dfield + ci);
+    if (dist > 0) {            // every cell of the empty box around / ahead of this one: jump (verified)
       NOLF_STAT(3, 1);
       int lo_c[3], hi_c[3];
 #pragma unroll
       for (int k = 0; k < 3; ++k) {
+#ifdef NOLF_CHEB_DIST
         lo_c[k] = max(cell[k] - (dist - 1), 0);
         hi_c[k] = min(cell[k] + (dist - 1), b - 1);
+#else
+        const bool neg = (oct >> k) & 1;
+        lo_c[k] = neg ? max(cell[k] - (dist - 1), 0) : cell[k];
+        hi_c[k] = neg ? cell[k] : min(cell[k] + (dist - 1), b - 1);
+#endif
       }
       // fp32 estimate of the last sample before the empty box's exit
       float te = __int_as_float(0x7f800000);
