@@ -329,6 +329,22 @@ __device__ __forceinline__ void atlas_query4_f(const DevAtlas &at, int cid, cons
   out[0] = a0; out[1] = a1; out[2] = a2; out[3] = a3;
 }
 
+// L2 prefetch of the 8 corners atlas_query4_f(at, ., x) will read (4-channel atlas).
+__device__ __forceinline__ void atlas_prefetch4(const DevAtlas &at, const double x[3]) {
+  const int cid = atlas_cell_id(at, x);
+  if (cid < 0) return;
+  int base[3];
+  double frac[3];
+  atlas_subvoxel(at, x, base, frac);
+  const int s = at.s;
+  const float *cube = at.cubes + (size_t)cid * (size_t)(s * s * s * 4);
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const float *p = cube + (((base[0] + (c & 1)) * s + (base[1] + ((c >> 1) & 1))) * s + (base[2] + ((c >> 2) & 1))) * 4;
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+  }
+}
+
 template <int C>
 __device__ __forceinline__ void atlas_query(const DevAtlas &at, const double x[3], float out[C]) {
   const int cid = atlas_cell_id(at, x);

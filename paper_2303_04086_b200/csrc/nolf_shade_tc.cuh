@@ -91,8 +91,14 @@ __device__ __forceinline__ void tc_relu_store(uint32_t trow, uint32_t rowa) {
 // group thread gt, TMEM columns [tmem, tmem+64)); returns this thread's 4
 // pre-head outputs (fp32).  TMEM is read back 16 columns at a time so the
 // hidden layer never occupies more than 16 registers.
+struct NoHook {
+  __device__ __forceinline__ void operator()() const {}
+};
+
+template <class Hook = NoHook>
 __device__ __forceinline__ void tc_mlp_rows(uint8_t *A, const uint8_t *W, const float *fp, uint32_t tmem,
-                                            uint64_t *bar, uint32_t &phase, int gt, int bar_id, float out4[4]) {
+                                            uint64_t *bar, uint32_t &phase, int gt, int bar_id, float out4[4],
+                                            const Hook &while_mma = Hook()) {
   const uint32_t aA = tc::smem_u32(A), aW0 = tc::smem_u32(W), aW1 = aW0 + kOffW1;
   const uint32_t aW1b = aW0 + kOffW1b, aW2b = aW0 + kOffW2b, aOne = aW0 + kOffOne;
   constexpr uint32_t idesc = tc::idesc_bf16_f32(128, 64);
@@ -108,6 +114,7 @@ __device__ __forceinline__ void tc_mlp_rows(uint8_t *A, const uint8_t *W, const 
                     idesc, s > 0);
     tc::umma_commit(bar);
   }
+  while_mma();                 // independent work while layer 0 runs
   tc::mbar_wait(bar, phase);
   phase ^= 1;
   tc::tc_fence_after();
@@ -423,7 +430,15 @@ __device__ __forceinline__ void tc_shade_tile(const ShadeArgs &args, const DevAs
   // the next tile's record, in flight across this tile's MMA chain
   if (next) nxt = *next;
   float z4[4];
+#ifdef NOLF_SHADE_PREFETCH_DIF
+  // and its diffuse-atlas corners pulled into L2 while layer 0 runs
+  auto prefetch = [&]() {
+    if (next && A.use_diffuse_color && A.has_dif) atlas_prefetch4(A.dif, nxt.p);
+  };
+  tc_mlp_rows(Ag, S.W, S.fp, tmem_g, bar_g, mma_phase, gt, bar_id, z4, prefetch);
+#else
   tc_mlp_rows(Ag, S.W, S.fp, tmem_g, bar_g, mma_phase, gt, bar_id, z4);
+#endif
   if (valid) {
     float fs_out[4];
     if (std_heads) {             // the reference's (sigmoid x 3, identity) head (lightfield.py:635)
