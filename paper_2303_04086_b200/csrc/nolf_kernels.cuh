@@ -917,6 +917,10 @@ __global__ void __launch_bounds__(128) k_cull_chunks(MarchArgs args, long long n
   const long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   bool live = false;
   int ncand = 0;
+  // the previous frame's duration of this chunk: when known it is the bucket,
+  // and any one candidate instance makes the chunk live
+  const unsigned prev_cost = (c < n_chunks && args.chunk_cost) ? args.chunk_cost[c] : 0u;
+  const bool count_all = args.heavy_first && !prev_cost;
   if (c < n_chunks) {
     long long t, local0;
     split_slot(c * kMarchThreads, args.tile_stride, t, local0);
@@ -929,6 +933,15 @@ __global__ void __launch_bounds__(128) k_cull_chunks(MarchArgs args, long long n
       // positions at every 8x4-block start/end (row-major tiles: the rows)
       const long long l1 = min(local0 + kMarchThreads, (long long)w * h) - 1;
       int xa = INT_MAX, xb = INT_MIN, ya = INT_MAX, yb = INT_MIN;
+      const int nb = w >> 3;                    // 8x4 blocks per block row
+      const long long blk0 = local0 >> 5;
+      if ((w & 7) == 0 && (h & 3) == 0 && l1 == local0 + kMarchThreads - 1 && (blk0 % nb) + 3 < nb) {
+        // 4 whole blocks in one block row (32-wide tiles: every chunk)
+        xa = (int)(blk0 % nb) * 8;
+        xb = xa + 31;
+        ya = (int)(blk0 / nb) * 4;
+        yb = ya + 3;
+      } else
       for (long long l = local0; l <= l1; l += 32) {
         int x, y;
         slot_xy(min(l, l1), w, h, x, y);
@@ -941,13 +954,12 @@ __global__ void __launch_bounds__(128) k_cull_chunks(MarchArgs args, long long n
       for (int k = 0; k < args.n_inst; ++k) {   // count them only when the buckets are used
         const ScreenBox bb = args.cull[k * args.n_cams + tp.cam];
         ncand += (bb.x0 <= bb.x1 && bb.x0 <= xb && bb.x1 >= xa && bb.y0 <= yb && bb.y1 >= ya) ? 1 : 0;
-        if (ncand && !args.heavy_first) break;
+        if (ncand && !count_all) break;
       }
       live = ncand > 0;
     }
     chunk_live[c] = live ? 1 : 0;
   }
-  const unsigned prev_cost = (c < n_chunks && args.chunk_cost) ? args.chunk_cost[c] : 0u;
   const unsigned lane = threadIdx.x & 31;
   const unsigned ballot = __ballot_sync(0xffffffffu, live);
   if (ballot) {
