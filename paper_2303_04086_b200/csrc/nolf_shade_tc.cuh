@@ -373,7 +373,11 @@ __device__ __forceinline__ float tc_sigmoid(float z) { return sigmoidf_np(z); }
 __device__ __forceinline__ float tc_exp(float z) { return expf(z); }
 __device__ __forceinline__ float tc_log(float z) { return logf(z); }
 #else
-__device__ __forceinline__ float tc_sigmoid(float z) { return __frcp_rn(1.0f + __expf(-z)); }
+__device__ __forceinline__ float tc_sigmoid(float z) {   // 1 / (1 + e^-z): MUFU ex2 + rcp (rcp(inf) = 0)
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(1.0f + __expf(-z)));
+  return r;
+}
 __device__ __forceinline__ float tc_exp(float z) { return __expf(z); }
 __device__ __forceinline__ float tc_log(float z) { return __logf(z); }
 #endif
