@@ -94,6 +94,10 @@ def parse():
     p.add_argument("--chunk-cost", type=int, default=1, choices=[0, 1],
                    help="heaviest-first buckets from the previous frame's measured per-chunk march "
                         "durations (1) or from candidate-instance counts (0)")
+    p.add_argument("--split", type=int, default=1, choices=[1, 2],
+                   help="2: each rank renders its tiles as two interleaved halves on two streams (two "
+                        "renderers, two workspaces) so one half's shading / compose overlaps the other's "
+                        "march tail")
     p.add_argument("--frames", type=int, default=3,
                    help="p2p + flags: frame buffers in rank 0's ring (a peer renders frame seq once "
                         "frame seq - frames was consumed and re-cleared)")
@@ -661,6 +665,28 @@ def run_ours(args):
     n_cam = args.warmup + args.steps + 4
     cam_arrays = [R.camera_array(views(k)) for k in range(n_cam)]
     R.reserve(cam_arrays, n_max * stride)
+    split = None
+    if args.split == 2:                  # two interleaved halves of this rank's tiles, two streams
+        halves = [np.ascontiguousarray(mine[0::2]), np.ascontiguousarray(mine[1::2])]
+        R2 = SceneRenderer(scene)
+        if args.mlp == "bf16":
+            R2.mlp_mode(N.MLP_BF16)
+        R2.reserve(cam_arrays, len(halves[1]) * stride)
+        split = {"tiles": [torch.from_numpy(h).to(dev) for h in halves], "n": [len(h) for h in halves],
+                 "side": torch.cuda.Stream(device=dev), "R": [R, R2]}
+
+    def render_tiles(cams, o, **kw):
+        """This rank's tiles: one render, or (--split 2) two halves on two streams."""
+        if split is None:
+            R.render(cams, my_tiles, n_max, stride, o, **kw)
+            return
+        main = torch.cuda.current_stream()
+        side = split["side"]
+        side.wait_stream(main)
+        split["R"][0].render(cams, split["tiles"][0], split["n"][0], stride, o, **kw)
+        with torch.cuda.stream(side):
+            split["R"][1].render(cams, split["tiles"][1], split["n"][1], stride, o, stream=side.cuda_stream, **kw)
+        main.wait_stream(side)
     stream = torch.cuda.current_stream().cuda_stream
 
     # ---- p2p frame composer: rank 0 owns the frame buffers, every rank maps
@@ -835,8 +861,7 @@ def run_ours(args):
                     o2["chunk_state"] = chunk_states[fb]
                 if rank == 0 and clear_ev[fb] is not None:
                     torch.cuda.current_stream().wait_event(clear_ev[fb])   # buffer re-cleared
-                R.render(cam_arrays[k % n_cam], my_tiles, n_max, stride, o2, frame_layout=True,
-                         peer=(rank != 0), prefilled=prefill)
+                render_tiles(cam_arrays[k % n_cam], o2, frame_layout=True, peer=(rank != 0), prefilled=prefill)
             if flags:
                 if rank != 0:
                     N.check(N.lib().nolf_flag_set(done_remote + 4 * rank, seq, stream))
@@ -859,8 +884,10 @@ def run_ours(args):
                 out["chunk_state"] = chunk_states[fb]
             if prefill and clear_ev[fb] is not None:
                 torch.cuda.current_stream().wait_event(clear_ev[fb])   # buffer re-cleared
-        R.render(cam_arrays[k % n_cam], my_tiles, n_max, stride, out, frame_layout=(world == 1),
-                 prefilled=(world == 1 and prefill))
+        if world == 1:
+            render_tiles(cam_arrays[k % n_cam], out, frame_layout=True, prefilled=prefill)
+        else:
+            R.render(cam_arrays[k % n_cam], my_tiles, n_max, stride, out, frame_layout=False, prefilled=False)
         if world == 1 and auto_release:
             release(fb, None, torch.cuda.current_stream())
         if world > 1:
