@@ -1574,8 +1574,13 @@ __device__ __forceinline__ void compose_four(const ComposeArgs &a, const long lo
 // tile they are one 8-pixel row of a block, i.e. 32 contiguous rgba8 bytes
 // and 16 depth16 bytes of the frame -> two 16 B + one 16 B stores, one 8 B
 // layer-count load; anything else goes through the 4-slot path twice.
+// known_live: the caller walks the live-chunk list (no chunk_live loads);
+// the layer counts are then loaded before the tile record, not after it
+template <bool known_live = false>
 __device__ __forceinline__ void compose_eight(const ComposeArgs &a, const long long p0) {
-  if (a.prefilled && a.chunk_live && !a.chunk_live[p0 >> 7]) return;   // misses already in place
+  if (!known_live && a.prefilled && a.chunk_live && !a.chunk_live[p0 >> 7]) return;   // misses already in place
+  uint2 nh_early = make_uint2(0u, 0u);
+  if (known_live) nh_early = *reinterpret_cast<const uint2 *>(a.nhit + p0);
   long long t, local0;
   split_slot(p0, a.tile_stride, t, local0);
   const TileParams tp = a.tiles[t];
@@ -1587,8 +1592,11 @@ __device__ __forceinline__ void compose_eight(const ComposeArgs &a, const long l
     slot_xy(local0, w, h, x, y);
     const long long q0 = cp.pix_base + (long long)(tp.y0 + y) * cp.width + (tp.x0 + x);
     if ((q0 & 7) == 0) {
-      const bool live = !a.chunk_live || a.chunk_live[p0 >> 7];
-      const uint2 nh = live ? *reinterpret_cast<const uint2 *>(a.nhit + p0) : make_uint2(0u, 0u);
+      uint2 nh = nh_early;
+      if (!known_live) {
+        const bool live = !a.chunk_live || a.chunk_live[p0 >> 7];
+        nh = live ? *reinterpret_cast<const uint2 *>(a.nhit + p0) : make_uint2(0u, 0u);
+      }
       uint4 *r8 = reinterpret_cast<uint4 *>(a.out_rgba8 + q0 * 4);
       uint4 *d16 = reinterpret_cast<uint4 *>(a.out_depth16 + q0);
       if ((nh.x | nh.y) == 0) {                 // eight misses
@@ -1806,7 +1814,7 @@ __global__ void __launch_bounds__(256) k_compose_live(ComposeArgs a, const unsig
     } else if (G == 8 && a.chunk_state) {
       compose_eight_state(a, p0, threadIdx.x & 31u);
     } else if (G == 8) {
-      compose_eight(a, p0);
+      compose_eight<true>(a, p0);
     } else {
       compose_four(a, p0);
     }
