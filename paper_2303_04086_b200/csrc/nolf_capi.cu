@@ -514,7 +514,7 @@ int fill_inst(const NolfInstance *in, DevInst *out) {
 
 int run_shade(const DevInst *inst, const long long *qoff, int n_inst, const Workspace &w, int mode, float *rgba,
               float *depth, long long layer_stride, unsigned long long *counters, cudaStream_t st, bool use_tc,
-              uint32_t phi_smem_bytes, uint32_t tab_smem_bytes);
+              uint32_t phi_smem_bytes, uint32_t tab_smem_bytes, long long max_recs = -1);
 
 }  // namespace
 
@@ -1054,7 +1054,7 @@ thread_local long long g_dbg_rows = 0;
 
 int run_shade(const DevInst *inst, const long long *qoff, int n_inst, const Workspace &w, int mode, float *rgba,
               float *depth, long long layer_stride, unsigned long long *counters, cudaStream_t st, bool use_tc,
-              uint32_t phi_smem_bytes, uint32_t tab_smem_bytes) {
+              uint32_t phi_smem_bytes, uint32_t tab_smem_bytes, long long max_recs) {
   ShadeArgs sa{};
   sa.dbg_slots = g_dbg_slots;
   sa.dbg_rows = g_dbg_rows;
@@ -1090,9 +1090,15 @@ int run_shade(const DevInst *inst, const long long *qoff, int n_inst, const Work
     const int by_tmem = 512 / (kTcCols * kShadeTG);
     const int per_sm = std::max(1, std::min(std::min(by_regs, by_smem), by_tmem));
     g_last_launch[3] = per_sm;
-    k_shade_tc<kShadeTG><<<num_sms() * per_sm, threads, smem, st>>>(sa);
+    // no more CTAs than 128-hit tiles the queues can hold (small launches:
+    // a farm worker's 32x32 tile needs at most 8 per instance)
+    long long grid = (long long)num_sms() * per_sm;
+    if (max_recs >= 0) grid = std::max(1ll, std::min(grid, (max_recs + 127) / 128 + n_inst));
+    k_shade_tc<kShadeTG><<<(unsigned)grid, threads, smem, st>>>(sa);
   } else {
-    k_shade<<<num_sms() * 3, kShadeThreads, kShadeSmem, st>>>(sa);
+    long long grid = (long long)num_sms() * 3;
+    if (max_recs >= 0) grid = std::max(1ll, std::min(grid, (max_recs + kShadeThreads - 1) / kShadeThreads));
+    k_shade<<<(unsigned)grid, kShadeThreads, kShadeSmem, st>>>(sa);
   }
   CUDA_TRY(cudaGetLastError());
   return 0;
@@ -1366,7 +1372,7 @@ int launch_march_shade(int mode, const NolfInstance *ins, int n_inst, const Nolf
   if ((rc = prof_mark(1, st))) return rc;
   if (mode == kModeScene) {
     if ((rc = run_shade(dp->inst, dp->qoff, n_inst, w, mode, w.lrgba, w.ldepth, w.P, counters, st, use_tc,
-                        phi_smem, tab_smem)))
+                        phi_smem, tab_smem, pl.qoff[(size_t)n_inst])))
       return rc;
     if ((rc = prof_mark(2, st))) return rc;
     ComposeArgs ca{};
@@ -1438,7 +1444,8 @@ int launch_march_shade(int mode, const NolfInstance *ins, int n_inst, const Nolf
     if ((rc = prof_mark(3, st))) return rc;
     if ((rc = ring_release(slot, st))) return rc;   // the block is reusable once this frame is done
   } else {
-    if ((rc = run_shade(dp->inst, dp->qoff, n_inst, w, mode, rgba, depth, 0, counters, st, use_tc, phi_smem, tab_smem)))
+    if ((rc = run_shade(dp->inst, dp->qoff, n_inst, w, mode, rgba, depth, 0, counters, st, use_tc, phi_smem, tab_smem,
+                        pl.qoff[(size_t)n_inst])))
       return rc;
     if ((rc = prof_mark(2, st))) return rc;
     if ((rc = prof_mark(3, st))) return rc;

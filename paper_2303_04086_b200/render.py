@@ -19,6 +19,7 @@ the reference's own tests mutate in place); ``invalidate()`` drops it.
 from __future__ import annotations
 
 import ctypes as C
+import threading
 import time
 import zlib
 from collections import OrderedDict
@@ -207,10 +208,20 @@ def workspace(nbytes: int):
     return cur
 
 
+_XFORM = {}          # o2w bytes -> (w2o, scale): the per-call inverse / scale check, memoised
+
+
 def _instance(asset, transform=None) -> N.Instance:
     o2w = np.asarray(asset.object_to_world if transform is None else transform, np.float64)
-    w2o = np.linalg.inv(o2w)                      # lightfield.py:408
-    scale = uniform_scale_of(w2o)                 # lightfield.py:409
+    key = o2w.tobytes()
+    hit = _XFORM.get(key)
+    if hit is None:
+        w2o = np.linalg.inv(o2w)                  # lightfield.py:408
+        scale = uniform_scale_of(w2o)             # lightfield.py:409 (raises for non-uniform scales)
+        if len(_XFORM) > 4096:
+            _XFORM.clear()
+        hit = _XFORM[key] = (w2o, scale)
+    w2o, scale = hit
     dev = device_asset(asset)
     dev.set_mlp_mode(_MLP_MODE if dev.bf16_ok else N.MLP_FP32)
     inst = N.Instance()
@@ -361,6 +372,9 @@ def render_ray(asset, ray, counters=None):
     return rgba[0], float(depth[0])
 
 
+_RANGE_BUFS = {}
+
+
 def render_range(asset, ray_range, counters=None):
     """Render a RayRange rectangle -> (Tile, instr); renderer.py:63-93."""
     t = torch()
@@ -371,19 +385,36 @@ def render_range(asset, ray_range, counters=None):
     x0, y0, x1, y1 = ray_range.x0, ray_range.y0, ray_range.x1, ray_range.y1
     h, w = y1 - y0, x1 - x0
     dev = _device()
-    rgba = t.empty((h, w, 4), dtype=t.float32, device=dev)
-    depth = t.empty((h, w), dtype=t.float32, device=dev)
-    cnt = t.zeros(4, dtype=t.int64, device=dev)
+    # per-shape device outputs and one pinned host staging block, reused by
+    # every call of this shape (a farm worker's light tiles are all 32x32):
+    # one launch, three async copies and one synchronisation per call
+    key = (threading.get_ident(), dev.index, h, w)
+    bufs = _RANGE_BUFS.get(key)
+    if bufs is None:
+        host = t.empty(32 + h * w * 5 * 4, dtype=t.uint8, pin_memory=True)   # [counters | rgba | depth]
+        bufs = (t.empty((h, w, 4), dtype=t.float32, device=dev), t.empty((h, w), dtype=t.float32, device=dev),
+                t.zeros(4, dtype=t.int64, device=dev), host,
+                host[32:32 + h * w * 16].view(t.float32).view(h, w, 4),
+                host[32 + h * w * 16:].view(t.float32).view(h, w), host[:32].view(t.int64))
+        _RANGE_BUFS[key] = bufs
+    rgba, depth, cnt, _, h_rgba, h_depth, h_cnt = bufs
+    cnt.zero_()
     ws = workspace(int(N.lib().nolf_workspace_bytes(1, h * w)))
     cs = N.camera_struct(cam)
     N.check(N.lib().nolf_render_rect(C.byref(inst), C.byref(cs), x0, y0, x1, y1, rgba.data_ptr(),
                                      depth.data_ptr(), cnt.data_ptr(), ws.data_ptr(), ws.numel(),
                                      _stream_ptr()))
-    tile = TYPES["Tile"](x0=x0, y0=y0, rgba=rgba.cpu().numpy(), depth=depth.cpu().numpy())
-    check_device_errors()
-    c = cnt.cpu().numpy()
+    h_rgba.copy_(rgba, non_blocking=True)
+    h_depth.copy_(depth, non_blocking=True)
+    h_cnt.copy_(cnt, non_blocking=True)
+    check_device_errors()                 # synchronises the stream: the copies have landed
+    tile = TYPES["Tile"](x0=x0, y0=y0, rgba=h_rgba.numpy().copy(), depth=h_depth.numpy().copy())
+    c = h_cnt.numpy()
     before_fs, before_hits = counters.fs_evals, counters.hit_pixels
-    _merge(counters, cnt)
+    counters.fs_evals += int(c[0])
+    counters.fd_evals += int(c[1])
+    counters.hit_pixels += int(c[2])
+    counters.march_samples += int(c[3])
     instr = {"wall_time_s": time.perf_counter() - start, "rays": int(h * w),
              "hits": counters.hit_pixels - before_hits, "fs_evals": counters.fs_evals - before_fs}
     del c
