@@ -323,9 +323,22 @@ def render_rays(asset, origins, dirs, counters=None):
     N.check(N.lib().nolf_render_rays(C.byref(inst), o.data_ptr(), 0 if shared else 1, d.data_ptr(), n,
                                      rgba.data_ptr(), depth.data_ptr(), cnt.data_ptr(), ws.data_ptr(),
                                      ws.numel(), _stream_ptr()))
-    out = rgba.cpu().numpy(), depth.cpu().numpy()
-    check_device_errors()
-    _merge(counters, cnt)
+    # one pinned staging block [counters | rgba | depth]: async copies, one sync
+    host = _staging(32 + n * 20)
+    h_cnt = host[:32].view(t.int64)
+    h_rgba = host[32:32 + n * 16].view(t.float32).view(n, 4)
+    h_depth = host[32 + n * 16:32 + n * 20].view(t.float32)
+    h_cnt.copy_(cnt, non_blocking=True)
+    h_rgba.copy_(rgba, non_blocking=True)
+    h_depth.copy_(depth, non_blocking=True)
+    check_device_errors()                 # synchronises the stream: the copies have landed
+    out = h_rgba.numpy().copy(), h_depth.numpy().copy()
+    if counters is not None:
+        c = h_cnt.numpy()
+        counters.fs_evals += int(c[0])
+        counters.fd_evals += int(c[1])
+        counters.hit_pixels += int(c[2])
+        counters.march_samples += int(c[3])
     return out
 
 
@@ -373,6 +386,18 @@ def render_ray(asset, ray, counters=None):
 
 
 _RANGE_BUFS = {}
+_STAGING = {}
+
+
+def _staging(nbytes: int):
+    """A pinned host block of at least nbytes for this thread (grown, reused)."""
+    t = torch()
+    key = threading.get_ident()
+    cur = _STAGING.get(key)
+    if cur is None or cur.numel() < nbytes:
+        cur = t.empty(max(int(nbytes), 1 << 16) * 2, dtype=t.uint8, pin_memory=True)
+        _STAGING[key] = cur
+    return cur
 
 
 def render_range(asset, ray_range, counters=None):
