@@ -373,10 +373,20 @@ def march_rays(asset, origins, dirs) -> MarchResult:
         N.check(N.lib().nolf_march_rays(device_asset(asset).handle, o.data_ptr(), 1, d.data_ptr(), n,
                                         hit.data_ptr(), t_hit.data_ptr(), alpha.data_ptr(), samples.data_ptr(),
                                         p_h.data_ptr(), None, 0, _stream_ptr()))
-    res = MarchResult(hit.cpu().numpy().astype(bool), t_hit.cpu().numpy(), alpha.cpu().numpy(),
-                      samples.cpu().numpy(), p_h.cpu().numpy())
-    check_device_errors()
-    return res
+    # one pinned staging block [t_hit | alpha | samples | p_h | hit]: async copies, one sync
+    host = _staging(n * (8 + 8 + 8 + 24 + 1) + 64)
+    views = []
+    off = 0
+    for src, dt, shape in ((t_hit, t.float64, (n,)), (alpha, t.float64, (n,)), (samples, t.int64, (n,)),
+                           (p_h, t.float64, (n, 3)), (hit, t.uint8, (n,))):
+        nb = src.numel() * src.element_size()
+        v = host[off:off + nb].view(dt).view(*shape)
+        v.copy_(src, non_blocking=True)
+        views.append(v)
+        off += nb
+    check_device_errors()                 # synchronises the stream: the copies have landed
+    h_t, h_a, h_s, h_p, h_h = (v.numpy().copy() for v in views)
+    return MarchResult(h_h.astype(bool), h_t, h_a, h_s, h_p)
 
 
 def render_ray(asset, ray, counters=None):
