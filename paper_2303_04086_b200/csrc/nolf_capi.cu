@@ -2122,7 +2122,7 @@ extern "C" int nolf_train_shade(nolf_asset_t asset, const float *params, const i
   a.pred = pred;
   a.loss = loss;
   a.nonfinite = reinterpret_cast<unsigned *>(nonfinite);
-  const size_t smem = sizeof(double) * (size_t)train_smem(a.fs_in, a.fd_in).total;
+  const size_t smem = sizeof(float) * 2 * 128 * kHid;     // the staged per-layer vectors
   CUDA_TRY(cudaFuncSetAttribute(k_train_shade, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   k_train_shade<<<(unsigned)((n + 127) / 128), 128, smem, static_cast<cudaStream_t>(stream)>>>(a);
   CUDA_TRY(cudaGetLastError());

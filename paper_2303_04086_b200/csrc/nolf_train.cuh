@@ -95,14 +95,24 @@ __device__ __forceinline__ float dense_row(const float *W, const float *b, int o
 __device__ __forceinline__ double sigmoid_d(double z) { return sigmoid_np(z); }
 
 __global__ void __launch_bounds__(128) k_train_shade(TrainArgs a) {
-  extern __shared__ double sg[];
+  // Weight gradients are per-CTA matrix products over its 128 rays: each
+  // layer stages every ray's upstream vector and input activations in shared
+  // memory, then thread t sums (double) g[r][o] * (double) in[r][i] over the
+  // rays for its weights (f64, as the reference's f64 accumulation) and adds
+  // one value per weight to the global gradient -- no per-ray atomics.
+  extern __shared__ float stage[];               // [128][kHid] upstream | [128][kHid] inputs
   const int fs_in = a.fs_in, fd_in = a.fd_in;
   const TrainSmem S = train_smem(fs_in, fd_in);
-  for (int i = threadIdx.x; i < S.total; i += blockDim.x) sg[i] = 0.0;
-  __syncthreads();
   const DevAsset &A = *a.asset;
   const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (r < a.n) {
+  const bool valid = r < a.n;
+  const bool dif = A.use_diffuse_color;          // uniform
+  // per-ray vectors kept for the staged reductions (zero for padding rays)
+  float x[kInp], h1[kHid], h2[kHid], g2[4] = {0.f, 0.f, 0.f, 0.f}, g1[kHid], g0[kHid];
+  float ed[kInp], hd[kHid], gd[4] = {0.f, 0.f, 0.f, 0.f}, gd0[kHid];
+  for (int i = 0; i < kInp; ++i) { x[i] = 0.f; ed[i] = 0.f; }
+  for (int o = 0; o < kHid; ++o) { h1[o] = h2[o] = g1[o] = g0[o] = hd[o] = gd0[o] = 0.f; }
+  if (valid) {
     const float *P = a.params;
     const double p[3] = {a.p_h[3 * r], a.p_h[3 * r + 1], a.p_h[3 * r + 2]};
     const double dv[3] = {a.dirs[3 * r], a.dirs[3 * r + 1], a.dirs[3 * r + 2]};
@@ -119,7 +129,6 @@ __global__ void __launch_bounds__(128) k_train_shade(TrainArgs a) {
                           base[2] + ((c >> 2) & 1));
       for (int f = 0; f < F; ++f) es[f] = __dadd_rn(es[f], __dmul_rn((double)feat[(size_t)slots[c] * F + f], w8[c]));
     }
-    float x[kInp];
     int nin = 0;
     for (int f = 0; f < F; ++f) x[nin++] = (float)es[f];
     double sh[16];
@@ -130,7 +139,7 @@ __global__ void __launch_bounds__(128) k_train_shade(TrainArgs a) {
     // ---- specular MLP [in -> 64 -> 64 -> 4] (neural.py:89-108), f32
     const float *W0 = P + a.L.off[kTpFsW0], *B0 = P + a.L.off[kTpFsB0], *W1 = P + a.L.off[kTpFsW1],
                 *B1 = P + a.L.off[kTpFsB1], *W2 = P + a.L.off[kTpFsW2], *B2 = P + a.L.off[kTpFsB2];
-    float h1[kHid], h2[kHid], zs[4], fs[4];
+    float zs[4], fs[4];
     for (int o = 0; o < kHid; ++o) h1[o] = fmaxf(dense_row(W0, B0, o, fs_in, x), 0.f);
     for (int o = 0; o < kHid; ++o) h2[o] = fmaxf(dense_row(W1, B1, o, kHid, h1), 0.f);
     for (int j = 0; j < 4; ++j) {
@@ -144,12 +153,11 @@ __global__ void __launch_bounds__(128) k_train_shade(TrainArgs a) {
     else if (A.refine_opacity) alpha = sigmoid_d(z + log(ac / (1.0 - ac)));
     else alpha = sigmoid_d(z);
     // ---- live diffuse: hash grid (encoding.py:467-478) + diffuse MLP
-    float ed[kInp], hd[kHid], fd[4] = {0.f, 0.f, 0.f, 1.f};
+    float fd[4] = {0.f, 0.f, 0.f, 1.f};
     int led = 0;
     int hb[kMaxLevels][3];
     double hw[kMaxLevels][8];
     long long hidx[kMaxLevels][8];
-    const bool dif = A.use_diffuse_color;
     if (dif) {
       for (int l = 0; l < A.hg_levels; ++l) {
         base_weights(p, A.hg_res[l], hb[l], hw[l]);
@@ -214,42 +222,30 @@ __global__ void __launch_bounds__(128) k_train_shade(TrainArgs a) {
     // specular: upstream (f32, neural.py:119) through the heads
     float up[4] = {(float)__dmul_rn(dcpre[0], t), (float)__dmul_rn(dcpre[1], t), (float)__dmul_rn(dcpre[2], t),
                    (float)dz};
-    float g2[4];
     for (int j = 0; j < 4; ++j)
       g2[j] = A.fs.act[j] == 0 ? up[j] : (A.fs.act[j] == 1 ? up[j] * fs[j] * (1.0f - fs[j]) : up[j] * fs[j]);
-    // layer 2
+    // layer 2 -> dh2
     float dh2[kHid];
     for (int o = 0; o < kHid; ++o) dh2[o] = 0.f;
-    for (int j = 0; j < 4; ++j) {
-      atomicAdd(&sg[S.fs_b2 + j], (double)g2[j]);
-      for (int o = 0; o < kHid; ++o) {
-        atomicAdd(&sg[S.fs_w2 + j * kHid + o], (double)g2[j] * (double)h2[o]);
-        dh2[o] = fmaf(g2[j], W2[j * kHid + o], dh2[o]);
-      }
-    }
-    // layer 1
+    for (int j = 0; j < 4; ++j)
+      for (int o = 0; o < kHid; ++o) dh2[o] = fmaf(g2[j], W2[j * kHid + o], dh2[o]);
+    // layer 1 -> dh1
     float dh1[kHid];
     for (int i = 0; i < kHid; ++i) dh1[i] = 0.f;
     for (int o = 0; o < kHid; ++o) {
       const float g = h2[o] > 0.f ? dh2[o] : 0.f;
+      g1[o] = g;
       if (g == 0.f) continue;
-      atomicAdd(&sg[S.fs_b1 + o], (double)g);
-      for (int i = 0; i < kHid; ++i) {
-        atomicAdd(&sg[S.fs_w1 + o * kHid + i], (double)g * (double)h1[i]);
-        dh1[i] = fmaf(g, W1[o * kHid + i], dh1[i]);
-      }
+      for (int i = 0; i < kHid; ++i) dh1[i] = fmaf(g, W1[o * kHid + i], dh1[i]);
     }
     // layer 0 -> input gradient
     float dx[kInp];
     for (int i = 0; i < fs_in; ++i) dx[i] = 0.f;
     for (int o = 0; o < kHid; ++o) {
       const float g = h1[o] > 0.f ? dh1[o] : 0.f;
+      g0[o] = g;
       if (g == 0.f) continue;
-      atomicAdd(&sg[S.fs_b0 + o], (double)g);
-      for (int i = 0; i < fs_in; ++i) {
-        atomicAdd(&sg[S.fs_w0 + o * fs_in + i], (double)g * (double)x[i]);
-        dx[i] = fmaf(g, W0[o * fs_in + i], dx[i]);
-      }
+      for (int i = 0; i < fs_in; ++i) dx[i] = fmaf(g, W0[o * fs_in + i], dx[i]);
     }
     // psh_backward: trilinear weight x upstream, scattered (f64)
     double *gfeat = a.grads + a.L.off[kTpPsh];
@@ -262,29 +258,20 @@ __global__ void __launch_bounds__(128) k_train_shade(TrainArgs a) {
       if (A.use_tint)
         for (int k = 0; k < 3; ++k) dt = __dadd_rn(dt, __dmul_rn(dcpre[k], cs[k]));
       const float upd[4] = {(float)dcpre[0], (float)dcpre[1], (float)dcpre[2], (float)dt};
-      float gd[4];
       for (int j = 0; j < 4; ++j)
         gd[j] = A.fd.act[j] == 0 ? upd[j] : (A.fd.act[j] == 1 ? upd[j] * fd[j] * (1.0f - fd[j]) : upd[j] * fd[j]);
       const float *V0 = P + a.L.off[kTpFdW0], *V1 = P + a.L.off[kTpFdW1];
       float dhd[kHid];
       for (int o = 0; o < kHid; ++o) dhd[o] = 0.f;
-      for (int j = 0; j < 4; ++j) {
-        atomicAdd(&sg[S.fd_b1 + j], (double)gd[j]);
-        for (int o = 0; o < kHid; ++o) {
-          atomicAdd(&sg[S.fd_w1 + j * kHid + o], (double)gd[j] * (double)hd[o]);
-          dhd[o] = fmaf(gd[j], V1[j * kHid + o], dhd[o]);
-        }
-      }
+      for (int j = 0; j < 4; ++j)
+        for (int o = 0; o < kHid; ++o) dhd[o] = fmaf(gd[j], V1[j * kHid + o], dhd[o]);
       float ded[kInp];
       for (int i = 0; i < fd_in; ++i) ded[i] = 0.f;
       for (int o = 0; o < kHid; ++o) {
         const float g = hd[o] > 0.f ? dhd[o] : 0.f;
+        gd0[o] = g;
         if (g == 0.f) continue;
-        atomicAdd(&sg[S.fd_b0 + o], (double)g);
-        for (int i = 0; i < fd_in; ++i) {
-          atomicAdd(&sg[S.fd_w0 + o * fd_in + i], (double)g * (double)ed[i]);
-          ded[i] = fmaf(g, V0[o * fd_in + i], ded[i]);
-        }
+        for (int i = 0; i < fd_in; ++i) ded[i] = fmaf(g, V0[o * fd_in + i], ded[i]);
       }
       // hashgrid_backward (encoding.py:481-489)
       for (int l = 0; l < A.hg_levels; ++l) {
@@ -297,9 +284,36 @@ __global__ void __launch_bounds__(128) k_train_shade(TrainArgs a) {
       }
     }
   }
-  __syncthreads();
-  for (int i = threadIdx.x; i < S.total; i += blockDim.x)
-    if (sg[i] != 0.0) atomicAdd(a.grads + train_goff(a, S, i), sg[i]);
+  // ---- weight gradients, one layer at a time (all threads: uniform)
+  float *G = stage, *IN = stage + 128 * kHid;
+  const int t = threadIdx.x;
+  // dW[o][i] = sum_r G[r][o] * IN[r][i] and db[o] = sum_r G[r][o] over the
+  // CTA's rays; w_off / b_off: the blocks' offsets in the TrainSmem layout
+  auto layer = [&](const float *g, int O, const float *in, int I, int w_off, int b_off) {
+    __syncthreads();
+    for (int o = 0; o < O; ++o) G[t * kHid + o] = g[o];
+    for (int i = 0; i < I; ++i) IN[t * kHid + i] = in[i];
+    __syncthreads();
+    for (int w = t; w < O * I + O; w += 128) {
+      double acc = 0.0;
+      if (w < O * I) {
+        const int o = w / I, i = w % I;
+        for (int q = 0; q < 128; ++q) acc = __dadd_rn(acc, __dmul_rn((double)G[q * kHid + o], (double)IN[q * kHid + i]));
+        if (acc != 0.0) atomicAdd(a.grads + train_goff(a, S, w_off + w), acc);
+      } else {
+        const int o = w - O * I;
+        for (int q = 0; q < 128; ++q) acc = __dadd_rn(acc, (double)G[q * kHid + o]);
+        if (acc != 0.0) atomicAdd(a.grads + train_goff(a, S, b_off + o), acc);
+      }
+    }
+  };
+  layer(g2, 4, h2, kHid, S.fs_w2, S.fs_b2);
+  layer(g1, kHid, h1, kHid, S.fs_w1, S.fs_b1);
+  layer(g0, kHid, x, fs_in, S.fs_w0, S.fs_b0);
+  if (dif) {
+    layer(gd, 4, hd, kHid, S.fd_w1, S.fd_b1);
+    layer(gd0, kHid, ed, fd_in, S.fd_w0, S.fd_b0);
+  }
 }
 
 // adam_step (neural.py:162-177) on one parameter group, in the reference's
