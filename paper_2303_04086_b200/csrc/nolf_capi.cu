@@ -191,6 +191,14 @@ int upload_atlas(NolfAsset *A, const NolfAtlasDesc &d, int channels, DevAtlas *o
   out->index = idx;
   out->dist = mac;
   out->cubes = cubes;
+  out->cubes16 = nullptr;
+  if (channels == 4 && nc > 0) {   // fp16 copy for the bf16 shading path (round to nearest)
+    std::vector<uint16_t> h(nc);
+    for (size_t i = 0; i < nc; ++i) h[i] = __half_as_ushort(__float2half_rn(d.cubes[i]));
+    uint16_t *hp;
+    if ((rc = A->upload(h.data(), h.size(), &hp))) return rc;
+    out->cubes16 = reinterpret_cast<const uint2 *>(hp);
+  }
   out->zmask = zmp;
   out->zwords = words;
   auto pow2 = [](int v) { return v > 0 && (v & (v - 1)) == 0; };

@@ -6,6 +6,7 @@
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
+#include <cuda_fp16.h>
 
 #include "nolf_mesh.cuh"
 
@@ -21,6 +22,8 @@ struct DevAtlas {              // CubeAtlas (atlas.py:25-51)
   const float *cubes;          // n * s^3 * C
   const uint8_t *dist;         // b^3: Chebyshev distance (cells) to the nearest
                                // occupied cell, 0 = occupied, capped at 255
+  const uint2 *cubes16;        // C == 4 atlases: the cubes again as fp16 (4 halves per corner) for the
+                               // bf16 shading path's diffuse term (null: use cubes)
   const uint8_t *odist;        // 8 x b^3 (octant-major): edge (cells) of the largest empty cube
                                // anchored at the cell and extending in the octant's direction
                                // (octant bit k set: axis k negative); 0 = occupied, capped at 255
@@ -309,12 +312,26 @@ __device__ __forceinline__ void atlas_query4_f(const DevAtlas &at, int cid, cons
   double frac[3];
   atlas_subvoxel(at, x, base, frac);
   const int s = at.s;
-  const float *cube = at.cubes + (size_t)cid * (size_t)(s * s * s * 4);
   float4 q[8];
+  if (at.cubes16) {            // fp16 corners: half the bytes per gather (|err| <= 2^-11 relative)
+    const uint2 *cube = at.cubes16 + (size_t)cid * (size_t)(s * s * s);
+    uint2 h[8];
 #pragma unroll
-  for (int c = 0; c < 8; ++c)
-    q[c] = __ldg(reinterpret_cast<const float4 *>(
-        cube + (((base[0] + (c & 1)) * s + (base[1] + ((c >> 1) & 1))) * s + (base[2] + ((c >> 2) & 1))) * 4));
+    for (int c = 0; c < 8; ++c)
+      h[c] = __ldg(cube + (((base[0] + (c & 1)) * s + (base[1] + ((c >> 1) & 1))) * s + (base[2] + ((c >> 2) & 1))));
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const float2 lo = __half22float2(*reinterpret_cast<const __half2 *>(&h[c].x));
+      const float2 hi = __half22float2(*reinterpret_cast<const __half2 *>(&h[c].y));
+      q[c] = make_float4(lo.x, lo.y, hi.x, hi.y);
+    }
+  } else {
+    const float *cube = at.cubes + (size_t)cid * (size_t)(s * s * s * 4);
+#pragma unroll
+    for (int c = 0; c < 8; ++c)
+      q[c] = __ldg(reinterpret_cast<const float4 *>(
+          cube + (((base[0] + (c & 1)) * s + (base[1] + ((c >> 1) & 1))) * s + (base[2] + ((c >> 2) & 1))) * 4));
+  }
   const float f0 = (float)frac[0], f1 = (float)frac[1], f2 = (float)frac[2];
   const float g0 = 1.0f - f0, g1 = 1.0f - f1, g2 = 1.0f - f2;
   float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
