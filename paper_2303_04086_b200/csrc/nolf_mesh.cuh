@@ -296,17 +296,20 @@ __device__ __forceinline__ double mesh_first_hit_warp4(const DevMesh &M, const d
       if (lane == 0) atomicAdd(err_overflow, 1u);
       continue;
     }
-    // push the reached children farthest first (selection by key, 4 slots)
-    unsigned done = 0;
+    // push the reached children farthest first: a 5-exchange sorting network
+    // on (key, slot), descending (warp-uniform), then the entries in order
+    int slot[4] = {0, 1, 2, 3};
+    auto cx = [&](int p, int q) {
+      if (key[p] < key[q]) {
+        const unsigned tk = key[p]; key[p] = key[q]; key[q] = tk;
+        const int ts = slot[p]; slot[p] = slot[q]; slot[q] = ts;
+      }
+    };
+    cx(0, 1); cx(2, 3); cx(0, 2); cx(1, 3); cx(1, 2);
 #pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      int jm = -1;
-      unsigned km = 0;
-#pragma unroll
-      for (int j = 0; j < 4; ++j)
-        if (!((done >> j) & 1u) && key[j] != none && (jm < 0 || key[j] >= km)) { jm = j; km = key[j]; }
-      if (jm < 0) break;
-      done |= 1u << jm;
+    for (int q = 0; q < 4; ++q) {
+      if (key[q] == none) continue;          // +inf sorts first: nobody reaches it
+      const int jm = slot[q];
       if (lane == 0) stack[sp] = n.count[jm] > 0 ? -(4 * e + jm) - 1 : n.child[jm];
       ++sp;
     }
