@@ -1013,9 +1013,13 @@ __global__ void __launch_bounds__(kMarchThreads, NOLF_MARCH_MINB) k_march_chunks
 template <bool GROUPS = false>
 __global__ void __launch_bounds__(kMarchThreads / 2, 2 * NOLF_MARCH_MINB) k_march_chunks_half(MarchArgs args) {
   const unsigned n = *args.n_chunks;
-  for (unsigned it = blockIdx.x; it < 2 * n; it += gridDim.x)
-    march_chunk<kModeScene, GROUPS>(
-        args, chunk_at(args.chunks, args.n_chunks, args.list_stride, it >> 1, args.heavy_first), false, (int)(it & 1));
+  for (unsigned it = blockIdx.x; it < 2 * n; it += gridDim.x) {
+    const long long t0 = clock64();
+    const unsigned chunk = chunk_at(args.chunks, args.n_chunks, args.list_stride, it >> 1, args.heavy_first);
+    march_chunk<kModeScene, GROUPS>(args, chunk, false, (int)(it & 1));
+    if (args.chunk_cost && (threadIdx.x & 31) == 0)         // the chunk's duration = its slowest half's
+      atomicMax(args.chunk_cost + chunk, (unsigned)min(clock64() - t0, 0x7fffffffll) | 1u);
+  }
 }
 
 // ---------------------------------------------------------------- shading
