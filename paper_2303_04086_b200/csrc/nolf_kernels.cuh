@@ -455,14 +455,22 @@ __device__ __forceinline__ MarchOut march_p2(const DevAsset &A, const double oG[
       if ((threadIdx.x & 31) == (unsigned)(__ffs(am) - 1)) { NOLF_STAT(9, 1); NOLF_STAT(10, __popc(am)); }
     }
 #endif
-    double xg[3];
     int gi[3], cell[3];
+#ifdef NOLF_KEEP_XG
+    double xg[3];
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
       xg[k] = grid_pos<CLIP>(oG, dG, t_mid, G, k);
       gi[k] = floor_grid(xg[k]);
       cell[k] = min(gi[k] >> lr, b - 1);
     }
+#else
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      gi[k] = floor_grid(grid_pos<CLIP>(oG, dG, t_mid, G, k));
+      cell[k] = min(gi[k] >> lr, b - 1);
+    }
+#endif
     const int ci = (cell[0] * b + cell[1]) * b + cell[2];
     const int dist = __ldg(dfield + ci);
     if (dist > 0) {            // every cell of the empty box around / ahead of this one: jump (verified)
@@ -510,7 +518,13 @@ __device__ __forceinline__ MarchOut march_p2(const DevAsset &A, const double oG[
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
       base[k] = gi[k] - (cell[k] << lr);
+#ifdef NOLF_KEEP_XG
       frac[k] = frac_grid(xg[k]);
+#else
+      // the position again (cheaper than keeping three doubles live across
+      // the distance-field load: they were spilled every iteration)
+      frac[k] = frac_grid(grid_pos<CLIP>(oG, dG, t_mid, G, k));
+#endif
       if (gi[k] >= Gi) { base[k] = rr - 1; frac[k] = 1.0; }   // pos == 1.0 (clipped to the far face)
     }
     ++samples;
