@@ -522,8 +522,13 @@ __device__ __forceinline__ MarchOut march_p2(const DevAsset &A, const double oG[
       frac[k] = frac_grid(xg[k]);
 #else
       // the position again (cheaper than keeping three doubles live across
-      // the distance-field load: they were spilled every iteration)
-      frac[k] = frac_grid(grid_pos<CLIP>(oG, dG, t_mid, G, k));
+      // the distance-field load: they were spilled every iteration); the
+      // volatile asm keeps the compiler from merging it with the first one
+      double v;
+      asm volatile("{\n\t.reg .f64 m;\n\tmul.rn.f64 m, %1, %2;\n\tadd.rn.f64 %0, %3, m;\n\t}"
+                   : "=d"(v) : "d"(t_mid), "d"(dG[k]), "d"(oG[k]));
+      if (CLIP) v = v < 0.0 ? 0.0 : (v > G ? G : v);
+      frac[k] = frac_grid(v);
 #endif
       if (gi[k] >= Gi) { base[k] = rr - 1; frac[k] = 1.0; }   // pos == 1.0 (clipped to the far face)
     }
