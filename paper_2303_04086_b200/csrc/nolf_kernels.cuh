@@ -424,7 +424,7 @@ __device__ __forceinline__ MarchOut march_p2(const DevAsset &A, const double oG[
   if (!(t_near < t_far)) return r;
   const DevAtlas &at = A.den;
   const double delta = A.step;
-  const int b = at.b, lr = at.lr, rr = at.r;
+  const int b = at.b, lr = at.lr;
   const int Gi = b << lr;
   const double G = (double)Gi;
   const double t_lim = fmin(t_far, t_end);
@@ -530,13 +530,14 @@ __device__ __forceinline__ MarchOut march_p2(const DevAsset &A, const double oG[
       if (CLIP) v = v < 0.0 ? 0.0 : (v > G ? G : v);
       frac[k] = frac_grid(v);
 #endif
-      if (gi[k] >= Gi) { base[k] = rr - 1; frac[k] = 1.0; }   // pos == 1.0 (clipped to the far face)
+      if (gi[k] >= Gi) { base[k] = (1 << lr) - 1; frac[k] = 1.0; }   // pos == 1.0 (clipped to the far face)
     }
     ++samples;
     const int bit = (((base[0] << lr) + base[1]) << lr) + base[2];
     // sub-voxel whose 8 corner densities are all 0: sigma = +0 exactly, so
     // absorb = exp(-0) = 1, w = 0 -- only the active-sample count changes
-    if (!(use_zmask && ((__ldg(at.zmask + (unsigned)(cid * at.zwords + (bit >> 5))) >> (bit & 31)) & 1u))) {
+    // (every uploaded atlas has its zero mask: use_zmask only matters for the general-grid march)
+    if (!((__ldg(at.zmask + (unsigned)(cid * at.zwords + (bit >> 5))) >> (bit & 31)) & 1u)) {
       NOLF_STAT(6, 1);
       float s;
       atlas_trilinear_at<1>(at, cid, base, frac, &s);
