@@ -492,8 +492,16 @@ __device__ __forceinline__ MarchOut march_p2(const DevAsset &A, const double oG[
 #pragma unroll
       for (int k = 0; k < 3; ++k) {
         const float ok = (float)oG[k];
-        if (invG[k] > 0.f && hi_c[k] < b - 1) te = fminf(te, ((float)((hi_c[k] + 1) << lr) - ok) * invG[k]);
-        else if (invG[k] < 0.f && lo_c[k] > 0) te = fminf(te, ((float)(lo_c[k] << lr) - ok) * invG[k]);
+#ifdef NOLF_INVG_REG
+        const float ig = invG[k];
+#else
+        // an estimate only (the jump is verified): 1/dG from the MUFU instead
+        // of three floats held across the whole march
+        float ig;
+        asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(ig) : "f"((float)dG[k]));
+#endif
+        if (ig > 0.f && hi_c[k] < b - 1) te = fminf(te, ((float)((hi_c[k] + 1) << lr) - ok) * ig);
+        else if (ig < 0.f && lo_c[k] > 0) te = fminf(te, ((float)(lo_c[k] << lr) - ok) * ig);
       }
       const float jf = floorf((fminf(te, (float)t_lim) - (float)t_near) * A.inv_step_f - 0.5f);
       int j = jf > 2.0e9f ? 2000000000 : (int)jf;
